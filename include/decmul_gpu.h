@@ -1,0 +1,126 @@
+/* decmul_gpu.h — C ABI of the B200 decimal multiplier (libdecmul_gpu.so).
+ *
+ * The drop-in boundary for the hot path of the reference decimal multiplier
+ * (arXiv 2011.11524, reference tree proj/). Plain pointers and sizes only; the
+ * C++ header include/decmul/decimal.hpp re-exposes the reference's own C++ API
+ * (DecimalNumber, MultiplyOptions, OperandTooLarge, multiply, ...) on top of it.
+ * Every entry point cites the reference interface it replaces.
+ *
+ * Conventions
+ *  - Every call returns an int status (DECMUL_OK or one DECMUL_E* code); the
+ *    message of the last failure on a context is decmul_gpu_last_error(ctx).
+ *    Codes map one-to-one onto the reference's exception types so a C++
+ *    wrapper rethrows the same type with the same text.
+ *  - Buffers are caller-owned. "d_" parameters are device pointers on the
+ *    context's GPU; all others are host pointers.
+ *  - A context is internally locked: one context may be shared by threads
+ *    (calls serialise), or use one context per thread — matching the
+ *    reference's reentrant multiply and its single plan-cache
+ *    mutex (conv.cpp:311-322).
+ */
+#ifndef DECMUL_GPU_H
+#define DECMUL_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  DECMUL_OK = 0,
+  DECMUL_EINVAL = 1,    /* std::invalid_argument (decimal.cpp:30-34, :104; conv.cpp:221-238, :274-295) */
+  DECMUL_ETOOLARGE = 2, /* decmul::OperandTooLarge (decimal.hpp:20-22; decimal.cpp:96, :99) */
+  DECMUL_ECORRUPT = 3,  /* std::runtime_error: analytic bound violated (decimal.cpp:174-180) */
+  DECMUL_ELOGIC = 4,    /* std::logic_error: internal self-check (primes.cpp:87,92; decimal.cpp:144) */
+  DECMUL_ECUDA = 5,     /* CUDA runtime failure */
+  DECMUL_ENOMEM = 6,    /* device or host allocation failure */
+  DECMUL_ESPACE = 7     /* caller's output buffer too small */
+};
+
+typedef struct decmul_gpu_ctx decmul_gpu_ctx;
+
+typedef struct {
+  unsigned base_exp;  /* lambda: limb base 10^lambda */
+  size_t length;      /* transform length N (2^k or 3 * 2^k) */
+  uint64_t p1, p2;    /* prime pair used (the reference pair unless N > 3 * 2^24) */
+  int large_pair;     /* 1 when the reference pair cannot hold N (reference: OperandTooLarge) */
+  int one_cta;        /* 1 when the whole product runs inside one CTA */
+} decmul_gpu_plan_info;
+
+/* ---- context ---- */
+int decmul_gpu_create(decmul_gpu_ctx** ctx, int device);
+void decmul_gpu_destroy(decmul_gpu_ctx* ctx);
+const char* decmul_gpu_last_error(const decmul_gpu_ctx* ctx); /* ctx may be NULL (create failures) */
+int decmul_gpu_device_count(int* count);
+
+/* ---- planning: decimal.cpp:54-100 (select_base_and_length, smallest_supported_length) ---- */
+int decmul_gpu_select_base_and_length(size_t digits_x, size_t digits_y, uint64_t p1, uint64_t p2,
+                                      unsigned forced_base_exp, unsigned* base_exp, size_t* length);
+int decmul_gpu_smallest_supported_length(size_t need, uint64_t p1, uint64_t p2, size_t* length);
+int decmul_gpu_plan(decmul_gpu_ctx* ctx, size_t digits_x, size_t digits_y, unsigned forced_base_exp,
+                    decmul_gpu_plan_info* info);
+
+/* ---- multiply: decmul::multiply, decimal.hpp:176-177 / decimal.cpp:191-216 ----
+ * x, y: most-significant-first ASCII digits (the DecimalNumber text, decimal.hpp:26-38).
+ * out receives the product digits (cap >= nx + ny); *out_len its length.
+ * alias != 0 is the reference's &x == &y squaring path (decimal.cpp:198); equal texts
+ * are detected as squaring too. forced_base_exp = MultiplyOptions::forced_base_exp. */
+int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
+                        size_t cap, size_t* out_len, unsigned forced_base_exp, int alias);
+
+/* Device-resident variant: digits in and out stay in HBM. stream = cudaStream_t (NULL = the
+ * context's stream). If out_len is NULL the call is asynchronous (no host sync; read the
+ * length later with decmul_gpu_result_length after synchronising the stream). */
+int decmul_gpu_multiply_device(decmul_gpu_ctx* ctx, const char* d_x, size_t nx, const char* d_y, size_t ny,
+                               char* d_out, size_t cap, size_t* out_len, unsigned forced_base_exp, int squaring,
+                               void* stream);
+int decmul_gpu_result_length(decmul_gpu_ctx* ctx, size_t* out_len);
+
+/* Batch of `count` independent products of uniform sizes (operand i at xs + i * x_stride,
+ * product i at outs + i * out_stride, out_stride >= nx + ny). One CTA per product when the
+ * transform fits shared memory. The reference runs products one multiply() at a time. */
+int decmul_gpu_multiply_batch(decmul_gpu_ctx* ctx, size_t count, const char* xs, size_t x_stride, size_t nx,
+                              const char* ys, size_t y_stride, size_t ny, char* outs, size_t out_stride,
+                              size_t* out_lens);
+int decmul_gpu_multiply_batch_device(decmul_gpu_ctx* ctx, size_t count, const char* d_xs, size_t x_stride,
+                                     size_t nx, const char* d_ys, size_t y_stride, size_t ny, char* d_outs,
+                                     size_t out_stride, unsigned long long* d_lens, void* stream);
+
+/* ---- parity hooks on host arrays (conv.hpp:59-71) ----
+ * p must be one of the supported primes (the reference pair or the large pair); n = 2^k or
+ * 3 * 2^k dividing p - 1. forward_transform output follows the reference's documented storage
+ * order for its default plan (conv.hpp:19-24); inverse_transform consumes that order. */
+int decmul_gpu_convolve_mod_p(decmul_gpu_ctx* ctx, uint64_t p, size_t n, const uint64_t* x, size_t nx,
+                              const uint64_t* y, size_t ny, uint64_t* out);
+int decmul_gpu_forward_transform(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint64_t* a);
+int decmul_gpu_inverse_transform(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint64_t* a);
+int decmul_gpu_pointwise_product(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint64_t* a, const uint64_t* b);
+
+/* ---- stage hooks ----
+ * pack: decimal.cpp:102-118. recover_decimal: crt2 over the two residue vectors
+ * (decimal.cpp:148-152, :209-211), recover_digits (:154-189) and to_decimal (:120-134);
+ * digits_sum = digit count of x plus digit count of y (bounds the product length). */
+int decmul_gpu_pack(decmul_gpu_ctx* ctx, const char* digits, size_t nd, unsigned base_exp, uint64_t* limbs,
+                    size_t cap, size_t* nlimbs);
+int decmul_gpu_recover_decimal(decmul_gpu_ctx* ctx, const uint64_t* r1, const uint64_t* r2, size_t n, uint64_t p1,
+                               uint64_t p2, unsigned base_exp, size_t min_limbs, size_t digits_sum, char* out,
+                               size_t cap, size_t* out_len);
+
+/* ---- in-place transposition: transpose.hpp:11-24 ---- */
+int decmul_gpu_transpose_square_sub(decmul_gpu_ctx* ctx, uint64_t* a, size_t n, size_t stride);
+int decmul_gpu_transpose_n_x_2n(decmul_gpu_ctx* ctx, uint64_t* a, size_t n);
+int decmul_gpu_transpose_2n_x_n(decmul_gpu_ctx* ctx, uint64_t* a, size_t n);
+
+/* ---- introspection ---- */
+typedef struct {
+  int last_launches;       /* kernels launched by the last product */
+  size_t table_bytes;      /* device bytes held by cached twiddle tables */
+} decmul_gpu_stats;
+int decmul_gpu_get_stats(decmul_gpu_ctx* ctx, decmul_gpu_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DECMUL_GPU_H */

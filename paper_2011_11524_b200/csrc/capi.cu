@@ -1,0 +1,218 @@
+// extern "C" implementation of include/decmul_gpu.h over dmg::Engine.
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "../../include/decmul_gpu.h"
+#include "engine.hpp"
+
+struct decmul_gpu_ctx {
+  std::unique_ptr<dmg::Engine> eng;
+  std::mutex mu;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+template <class F>
+int guarded(decmul_gpu_ctx* ctx, F&& f) {
+  std::string msg;
+  int rc = DECMUL_OK;
+  try {
+    f();
+    return DECMUL_OK;
+  } catch (const dmg::OperandTooLarge& e) {
+    rc = DECMUL_ETOOLARGE;
+    msg = e.what();
+  } catch (const std::invalid_argument& e) {
+    rc = DECMUL_EINVAL;
+    msg = e.what();
+  } catch (const std::length_error& e) {
+    rc = DECMUL_ESPACE;
+    msg = e.what();
+  } catch (const dmg::CudaError& e) {
+    msg = e.what();
+    rc = msg.find("out of memory") != std::string::npos ? DECMUL_ENOMEM : DECMUL_ECUDA;
+  } catch (const std::bad_alloc& e) {
+    rc = DECMUL_ENOMEM;
+    msg = e.what();
+  } catch (const std::logic_error& e) {
+    rc = DECMUL_ELOGIC;
+    msg = e.what();
+  } catch (const std::runtime_error& e) {
+    rc = DECMUL_ECORRUPT;
+    msg = e.what();
+  } catch (const std::exception& e) {
+    rc = DECMUL_ECUDA;
+    msg = e.what();
+  }
+  if (ctx)
+    ctx->err = msg;
+  else
+    g_create_err = msg;
+  return rc;
+}
+
+#define LOCKED(ctx, ...)                                     \
+  do {                                                       \
+    if (!(ctx)) return DECMUL_EINVAL;                        \
+    std::lock_guard<std::mutex> lock_((ctx)->mu);            \
+    return guarded((ctx), [&] { __VA_ARGS__; });             \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+int decmul_gpu_create(decmul_gpu_ctx** ctx, int device) {
+  if (!ctx) return DECMUL_EINVAL;
+  *ctx = nullptr;
+  return guarded(nullptr, [&] {
+    auto c = std::make_unique<decmul_gpu_ctx>();
+    c->eng = std::make_unique<dmg::Engine>(device);
+    *ctx = c.release();
+  });
+}
+
+void decmul_gpu_destroy(decmul_gpu_ctx* ctx) { delete ctx; }
+
+const char* decmul_gpu_last_error(const decmul_gpu_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+int decmul_gpu_device_count(int* count) {
+  return guarded(nullptr, [&] { dmg::cuda_check(cudaGetDeviceCount(count), "cudaGetDeviceCount"); });
+}
+
+int decmul_gpu_select_base_and_length(size_t dx, size_t dy, uint64_t p1, uint64_t p2, unsigned forced,
+                                      unsigned* base_exp, size_t* length) {
+  return guarded(nullptr, [&] {
+    dmg::BasePlan bp = dmg::select_base_and_length(dx, dy, p1 ? p1 : dmg::kP1, p1 ? p2 : dmg::kP2, forced);
+    *base_exp = bp.base_exp;
+    *length = bp.length;
+  });
+}
+
+int decmul_gpu_smallest_supported_length(size_t need, uint64_t p1, uint64_t p2, size_t* length) {
+  return guarded(nullptr, [&] {
+    *length = dmg::smallest_supported_length(need, p1 ? p1 : dmg::kP1, p1 ? p2 : dmg::kP2);
+  });
+}
+
+int decmul_gpu_plan(decmul_gpu_ctx* ctx, size_t dx, size_t dy, unsigned forced, decmul_gpu_plan_info* info) {
+  LOCKED(ctx, {
+    dmg::ProductPlan pp = ctx->eng->plan_product(dx, dy, forced);
+    info->base_exp = pp.base_exp;
+    info->length = pp.N;
+    info->p1 = pp.p1;
+    info->p2 = pp.p2;
+    info->large_pair = pp.large_pair ? 1 : 0;
+    const int three = pp.N % 3 == 0;
+    const size_t c = three ? pp.N / 3 : pp.N;
+    info->one_cta = __builtin_ctzll(c) <= dmg::small_max_logc(three) ? 1 : 0;
+  });
+}
+
+int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
+                        size_t cap, size_t* out_len, unsigned forced, int alias) {
+  LOCKED(ctx, {
+    if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
+    const bool xz = nx == 1 && x[0] == '0', yz = ny == 1 && y[0] == '0';
+    if (xz || yz) {  // decimal.cpp:193, after DecimalNumber::parse validated both texts
+      for (size_t i = 0; i < nx; ++i)
+        if (x[i] < '0' || x[i] > '9') throw std::invalid_argument("decimal: non-digit character");
+      for (size_t i = 0; i < ny; ++i)
+        if (y[i] < '0' || y[i] > '9') throw std::invalid_argument("decimal: non-digit character");
+      if ((nx > 1 && x[0] == '0') || (ny > 1 && y[0] == '0')) throw std::invalid_argument("decimal: leading zero");
+      if (cap < 1) throw std::length_error("multiply: output buffer too small");
+      out[0] = '0';
+      *out_len = 1;
+      return;
+    }
+    *out_len = ctx->eng->multiply_host(x, nx, y, ny, out, cap, forced, alias != 0);
+  });
+}
+
+int decmul_gpu_multiply_device(decmul_gpu_ctx* ctx, const char* d_x, size_t nx, const char* d_y, size_t ny,
+                               char* d_out, size_t cap, size_t* out_len, unsigned forced, int squaring,
+                               void* stream) {
+  LOCKED(ctx, {
+    const bool sq = squaring != 0 || (d_x == d_y && nx == ny);
+    const size_t len = ctx->eng->multiply_device(d_x, nx, d_y, ny, d_out, cap, forced, sq,
+                                                 static_cast<cudaStream_t>(stream), out_len != nullptr);
+    if (out_len) *out_len = len;
+  });
+}
+
+int decmul_gpu_result_length(decmul_gpu_ctx* ctx, size_t* out_len) {
+  LOCKED(ctx, {
+    *out_len = ctx->eng->result_length();
+  });
+}
+
+int decmul_gpu_multiply_batch(decmul_gpu_ctx* ctx, size_t count, const char* xs, size_t x_stride, size_t nx,
+                              const char* ys, size_t y_stride, size_t ny, char* outs, size_t out_stride,
+                              size_t* out_lens) {
+  LOCKED(ctx, ctx->eng->multiply_batch_host(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, out_lens));
+}
+
+int decmul_gpu_multiply_batch_device(decmul_gpu_ctx* ctx, size_t count, const char* d_xs, size_t x_stride,
+                                     size_t nx, const char* d_ys, size_t y_stride, size_t ny, char* d_outs,
+                                     size_t out_stride, unsigned long long* d_lens, void* stream) {
+  LOCKED(ctx, ctx->eng->multiply_batch_device(count, d_xs, x_stride, nx, d_ys, y_stride, ny, d_outs, out_stride,
+                                               d_lens, static_cast<cudaStream_t>(stream)));
+}
+
+int decmul_gpu_convolve_mod_p(decmul_gpu_ctx* ctx, uint64_t p, size_t n, const uint64_t* x, size_t nx,
+                              const uint64_t* y, size_t ny, uint64_t* out) {
+  LOCKED(ctx, ctx->eng->convolve_mod_p(p, n, reinterpret_cast<const dmg::u64*>(x), nx,
+                                       reinterpret_cast<const dmg::u64*>(y), ny, reinterpret_cast<dmg::u64*>(out)));
+}
+
+int decmul_gpu_forward_transform(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint64_t* a) {
+  LOCKED(ctx, ctx->eng->forward_transform(p, n, reinterpret_cast<dmg::u64*>(a)));
+}
+
+int decmul_gpu_inverse_transform(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint64_t* a) {
+  LOCKED(ctx, ctx->eng->inverse_transform(p, n, reinterpret_cast<dmg::u64*>(a)));
+}
+
+int decmul_gpu_pointwise_product(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint64_t* a, const uint64_t* b) {
+  LOCKED(ctx, ctx->eng->pointwise_product(p, n, reinterpret_cast<dmg::u64*>(a), reinterpret_cast<const dmg::u64*>(b)));
+}
+
+int decmul_gpu_pack(decmul_gpu_ctx* ctx, const char* digits, size_t nd, unsigned base_exp, uint64_t* limbs,
+                    size_t cap, size_t* nlimbs) {
+  LOCKED(ctx, *nlimbs = ctx->eng->pack(digits, nd, base_exp, reinterpret_cast<dmg::u64*>(limbs), cap));
+}
+
+int decmul_gpu_recover_decimal(decmul_gpu_ctx* ctx, const uint64_t* r1, const uint64_t* r2, size_t n, uint64_t p1,
+                               uint64_t p2, unsigned base_exp, size_t min_limbs, size_t digits_sum, char* out,
+                               size_t cap, size_t* out_len) {
+  LOCKED(ctx, *out_len = ctx->eng->recover_decimal(reinterpret_cast<const dmg::u64*>(r1),
+                                                   reinterpret_cast<const dmg::u64*>(r2), n, p1, p2, base_exp,
+                                                   min_limbs, digits_sum, out, cap));
+}
+
+int decmul_gpu_transpose_square_sub(decmul_gpu_ctx* ctx, uint64_t* a, size_t n, size_t stride) {
+  LOCKED(ctx, ctx->eng->transpose(0, reinterpret_cast<dmg::u64*>(a), n, stride));
+}
+int decmul_gpu_transpose_n_x_2n(decmul_gpu_ctx* ctx, uint64_t* a, size_t n) {
+  LOCKED(ctx, ctx->eng->transpose(1, reinterpret_cast<dmg::u64*>(a), n, 2 * n));
+}
+int decmul_gpu_transpose_2n_x_n(decmul_gpu_ctx* ctx, uint64_t* a, size_t n) {
+  LOCKED(ctx, ctx->eng->transpose(2, reinterpret_cast<dmg::u64*>(a), n, n));
+}
+
+int decmul_gpu_get_stats(decmul_gpu_ctx* ctx, decmul_gpu_stats* out) {
+  LOCKED(ctx, {
+    out->last_launches = ctx->eng->last_launches();
+    out->table_bytes = ctx->eng->table_bytes();
+  });
+}
+
+}  // extern "C"

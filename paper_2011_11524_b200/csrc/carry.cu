@@ -1,0 +1,170 @@
+// Decimal recovery for one large product: CRT + digit split + chunk maps,
+// chunk-carry scan + top-limb detection, then carry application fused with the
+// ASCII formatting (reference recover_digits decimal.cpp:154-189 and
+// to_decimal decimal.cpp:120-134).
+#include "carry.cuh"
+#include "kernels.cuh"
+
+namespace dmg {
+
+namespace {
+
+constexpr int CH = kCarryChunk;
+constexpr int NT = kCarryThreads;
+constexpr int PER = CH / NT;  // limbs per thread
+
+__device__ __forceinline__ void coeff_digits(const CarryArgs& a, long long i, u64& d0, u64& d1, u64& d2) {
+  d0 = d1 = d2 = 0;
+  if (i < 0 || (unsigned long long)i >= a.n) return;
+  u64 lo, hi;
+  crt2(a.z1[i], a.z2[i], a.p1, a.p2, a.p2_prime, a.r_tilde, lo, hi);
+  if (above_cap(lo, hi, a.coeff_cap_lo, a.coeff_cap_hi)) atomicOr(a.err, kErrCoeffBound);
+  split3(a.div, lo, hi, d0, d1, d2);
+}
+
+// Phase 1: s_k for the chunk's limbs and the chunk's composed transfer map.
+__global__ void __launch_bounds__(NT) k_carry_split(CarryArgs a) {
+  __shared__ u64 d1s[CH + 2], d2s[CH + 2];
+  __shared__ unsigned wsm[NT / 32 + 1];
+  const unsigned long long k0 = (unsigned long long)blockIdx.x * CH;
+  const unsigned long long K = a.n + 2;
+  u64 d0r[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int loc = threadIdx.x * PER + j;
+    u64 d0, d1, d2;
+    coeff_digits(a, (long long)(k0 + loc), d0, d1, d2);
+    d0r[j] = d0;
+    d1s[loc + 2] = d1;
+    d2s[loc + 2] = d2;
+  }
+  if (threadIdx.x < 2) {
+    u64 d0, d1, d2;
+    coeff_digits(a, (long long)k0 - 2 + threadIdx.x, d0, d1, d2);
+    d1s[threadIdx.x] = d1;
+    d2s[threadIdx.x] = d2;
+  }
+  __syncthreads();
+  unsigned agg = kIdentityMap;
+  const u64 B = a.div.base;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int loc = threadIdx.x * PER + j;
+    const unsigned long long k = k0 + loc;
+    if (k >= K) break;
+    const u64 s = d0r[j] + d1s[loc + 1] + d2s[loc];
+    a.s[k] = s;
+    agg = map_compose(limb_map(s, B), agg);
+  }
+  unsigned total;
+  block_scan_maps<NT>(agg, wsm, &total);
+  if (threadIdx.x == 0) a.maps[blockIdx.x] = total;
+}
+
+// Phase 2 (one block): exclusive scan of chunk maps -> chunk carry-ins (stored in
+// place), then the top limb, its digit count and the output length.
+__global__ void __launch_bounds__(1024) k_carry_scan(CarryArgs a, unsigned nchunks) {
+  __shared__ unsigned wsm[1024 / 32 + 1];
+  __shared__ u64 zc[2];
+  const unsigned per = (nchunks + 1023) / 1024;
+  const unsigned c0 = threadIdx.x * per;
+  unsigned agg = kIdentityMap;
+  for (unsigned c = c0; c < c0 + per && c < nchunks; ++c) agg = map_compose(a.maps[c], agg);
+  unsigned pre = block_scan_maps<1024>(agg, wsm, nullptr);
+  unsigned carry = map_apply(pre, 0);
+  for (unsigned c = c0; c < c0 + per && c < nchunks; ++c) {
+    const unsigned m = a.maps[c];
+    a.maps[c] = carry;  // chunk carry-in
+    carry = map_apply(m, carry);
+  }
+  __syncthreads();
+  __threadfence_block();
+  // z at the two candidate top limbs: carry-in of the chunk, then the maps of
+  // the limbs before the candidate inside its chunk.
+  const u64 B = a.div.base;
+  for (int t = 0; t < 2; ++t) {
+    const unsigned long long k = a.top_candidates[t];
+    const unsigned long long cs = k / CH * CH;
+    unsigned m = kIdentityMap;
+    const unsigned long long len = k - cs;  // ordered contiguous segments, one per thread
+    const unsigned long long seg = (len + 1023) / 1024;
+    const unsigned long long j0 = cs + threadIdx.x * seg;
+    for (unsigned long long j = j0; j < j0 + seg && j < k; ++j) m = map_compose(limb_map(a.s[j], B), m);
+    const unsigned before = block_scan_maps<1024>(m, wsm, &m);
+    (void)before;
+    if (threadIdx.x == 0) {
+      const unsigned cin = a.maps[k / CH];
+      const unsigned c = map_apply(m, cin);
+      u64 v = a.s[k] + c;
+      v -= (v >= B ? B : 0);
+      v -= (v >= B ? B : 0);
+      zc[t] = v;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long top;
+    u64 z;
+    if (zc[1] != 0) {
+      top = a.top_candidates[1];
+      z = zc[1];
+    } else if (zc[0] != 0) {
+      top = a.top_candidates[0];
+      z = zc[0];
+    } else {
+      top = 0;
+      z = 0;
+    }
+    const unsigned len = decimal_len(z);
+    a.meta[0] = top;
+    a.meta[1] = len;
+    a.meta[2] = len + top * a.base_exp;
+  }
+}
+
+// Phase 3: apply carries and print each limb at its place in the output string.
+__global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
+  __shared__ unsigned wsm[NT / 32 + 1];
+  const unsigned long long k0 = (unsigned long long)blockIdx.x * CH + threadIdx.x * PER;
+  const unsigned long long K = a.n + 2;
+  const u64 B = a.div.base;
+  u64 s[PER];
+  unsigned agg = kIdentityMap;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const unsigned long long k = k0 + j;
+    s[j] = k < K ? a.s[k] : 0;
+    agg = map_compose(limb_map(s[j], B), agg);
+  }
+  const unsigned pre = block_scan_maps<NT>(agg, wsm, nullptr);
+  unsigned c = map_apply(pre, a.maps[blockIdx.x]);
+  const unsigned long long top = a.meta[0];
+  const unsigned top_len = unsigned(a.meta[1]);
+  const unsigned be = a.base_exp;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const unsigned long long k = k0 + j;
+    u64 v = s[j] + c;
+    unsigned q = 0;
+    if (v >= B) { v -= B; ++q; }
+    if (v >= B) { v -= B; ++q; }
+    c = q;
+    if (k > top) continue;
+    if (k == top)
+      write_digits(a.out, v, top_len);
+    else
+      write_digits(a.out + top_len + (top - 1 - k) * be, v, be);
+  }
+}
+
+}  // namespace
+
+void launch_carry(const CarryArgs& a, cudaStream_t st) {
+  const unsigned long long K = a.n + 2;
+  const unsigned nchunks = unsigned((K + CH - 1) / CH);
+  k_carry_split<<<nchunks, NT, 0, st>>>(a);
+  k_carry_scan<<<1, 1024, 0, st>>>(a, nchunks);
+  k_carry_emit<<<nchunks, NT, 0, st>>>(a);
+}
+
+}  // namespace dmg

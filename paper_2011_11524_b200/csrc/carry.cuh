@@ -1,0 +1,112 @@
+// Device helpers for decimal recovery: CRT (reference decimal.cpp:136-152),
+// base-B digit split, and the parallel form of the reference's sequential carry
+// recurrence (decimal.cpp:154-189).
+//
+// Parallel carry: every coefficient c_i < p1 p2 < 2^126 < B^3 splits into three
+// base-B digits (d0, d1, d2). The product's value is sum_k s_k B^k with
+// s_k = d0[k] + d1[k-1] + d2[k-2] <= 3(B-1), so a carry entering limb k is in
+// {0, 1, 2} and leaves in {0, 1, 2}. Each limb is a map {0,1,2} -> {0,1,2}
+// (6 bits: output for input c at bits [2c, 2c+1]); maps compose associatively,
+// so the carries are an ordered scan over maps.
+#pragma once
+#include "modarith.cuh"
+
+namespace dmg {
+
+constexpr unsigned kIdentityMap = 0x24u;  // c -> c
+
+__device__ __forceinline__ unsigned map_apply(unsigned m, unsigned c) { return (m >> (2 * c)) & 3u; }
+// later o earlier
+__device__ __forceinline__ unsigned map_compose(unsigned later, unsigned earlier) {
+  return map_apply(later, earlier & 3u) | (map_apply(later, (earlier >> 2) & 3u) << 2) |
+         (map_apply(later, (earlier >> 4) & 3u) << 4);
+}
+__device__ __forceinline__ unsigned limb_map(u64 s, u64 B) {
+  unsigned m = 0;
+#pragma unroll
+  for (unsigned c = 0; c < 3; ++c) {
+    const u64 v = s + c;
+    m |= (unsigned(v >= B) + unsigned(v >= 2 * B)) << (2 * c);
+  }
+  return m;
+}
+
+// m = a1 + p1 * REDC_{p2}(r~, (a2 - a1) mod p2) < p1 p2.
+__device__ __forceinline__ void crt2(u64 a1, u64 a2, u64 p1, u64 p2, u64 p2p, u64 r_tilde, u64& lo, u64& hi) {
+  const u64 diff = mod_sub(a2, a1, p2);
+  const u64 q = mont_mul(r_tilde, diff, p2, p2p);
+  const u64 l = p1 * q;
+  hi = __umul64hi(p1, q);
+  lo = l + a1;
+  hi += lo < l ? 1ull : 0ull;
+}
+
+// c = d0 + d1 B + d2 B^2 (each < B).
+__device__ __forceinline__ void split3(const DivB& d, u64 lo, u64 hi, u64& d0, u64& d1, u64& d2) {
+  u64 qlo, qhi, q2lo, q2hi;
+  d0 = divmod_base(d, lo, hi, qlo, qhi);
+  d1 = divmod_base(d, qlo, qhi, q2lo, q2hi);
+  d2 = q2lo;
+}
+
+__device__ __forceinline__ bool above_cap(u64 lo, u64 hi, u64 cap_lo, u64 cap_hi) {
+  return hi > cap_hi || (hi == cap_hi && lo > cap_lo);
+}
+
+__device__ __forceinline__ unsigned decimal_len(u64 v) {
+  unsigned n = 1;
+  while (v >= 10) {
+    v /= 10;
+    ++n;
+  }
+  return n;
+}
+
+// Write the `len` least-significant decimal digits of v (zero padded) to out[0..len).
+__device__ __forceinline__ void write_digits(char* out, u64 v, unsigned len) {
+  // split at 10^9 so the digit loop runs on 32-bit values
+  unsigned lo = unsigned(v % 1000000000ull);
+  unsigned hi = unsigned(v / 1000000000ull);
+  int pos = int(len) - 1;
+  for (int k = 0; k < 9 && pos >= 0; ++k, --pos) {
+    out[pos] = char('0' + lo % 10u);
+    lo /= 10u;
+  }
+  for (; pos >= 0; --pos) {
+    out[pos] = char('0' + hi % 10u);
+    hi /= 10u;
+  }
+}
+
+// Exclusive ordered scan of maps across a block of NT threads (NT multiple of 32).
+// Returns the composition of all earlier threads' maps; *total gets the block composition.
+template <int NT>
+__device__ __forceinline__ unsigned block_scan_maps(unsigned m, unsigned* smem_warp, unsigned* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned inc = m;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned o = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc = map_compose(inc, o);
+  }
+  unsigned exc = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) exc = kIdentityMap;
+  if (lane == 31) smem_warp[wid] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned acc = kIdentityMap;
+    for (int w = 0; w < NT / 32; ++w) {
+      const unsigned t = smem_warp[w];
+      smem_warp[w] = acc;  // exclusive prefix of warp w
+      acc = map_compose(t, acc);
+    }
+    smem_warp[NT / 32] = acc;
+  }
+  __syncthreads();
+  const unsigned pre = map_compose(exc, smem_warp[wid]);
+  if (total) *total = smem_warp[NT / 32];
+  __syncthreads();
+  return pre;
+}
+
+}  // namespace dmg

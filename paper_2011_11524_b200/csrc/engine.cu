@@ -1,0 +1,854 @@
+// Host orchestration for the device multiplier. See engine.hpp.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+
+namespace dmg {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+TwPair shoup_pair(const HostField& F, u64 w) { return TwPair{w, F.shoup(w)}; }
+
+u64 recip_of(u64 d) {  // reference make_div_by_const (decimal.hpp:93-104), for a normalized divisor
+  return u64(~(u128)0 / d - ((u128)1 << 64));
+}
+
+DivB div_for(u64 base) {
+  DivB d;
+  d.base = base;
+  d.shift = __builtin_clzll(base);
+  d.d_norm = base << d.shift;
+  d.recip = recip_of(d.d_norm);
+  return d;
+}
+
+int bitrev_h(std::size_t x, int bits) {
+  std::size_t r = 0;
+  for (int i = 0; i < bits; ++i) {
+    r = (r << 1) | (x & 1);
+    x >>= 1;
+  }
+  return int(r);
+}
+
+// The reference's storage -> spectrum map for its default plan (conv.hpp:19-24,
+// build_conv_plan threshold 2^15; checked by test_conv.cpp:18-32).
+std::size_t ref_order_of(std::size_t n, std::size_t k) {
+  if (n <= 1) return 0;
+  if (n % 3 == 0) {
+    const std::size_t c = n / 3;
+    return k / c + 3 * ref_order_of(c, k % c);
+  }
+  const int lg = __builtin_ctzll(n);
+  if (n <= (std::size_t(1) << 15)) return std::size_t(bitrev_h(k, lg));
+  const std::size_t n1 = std::size_t(1) << (lg / 2), n2 = n / n1;
+  const std::size_t i = k / n2, j = k % n2;
+  return i + n1 * std::size_t(bitrev_h(j, __builtin_ctzll(n2)));
+}
+
+std::vector<int> split_log(int k, int maxlog) {
+  std::vector<int> parts;
+  if (k <= 0) return parts;
+  const int m = (k + maxlog - 1) / maxlog;
+  for (int i = 0; i < m; ++i) parts.push_back(k / m + (i < k % m ? 1 : 0));
+  return parts;
+}
+
+template <class T>
+void upload(DevBuf<T>& b, const std::vector<T>& v, cudaStream_t st) {
+  b.ensure(std::max<std::size_t>(v.size(), 1));
+  if (!v.empty())
+    cuda_check(cudaMemcpyAsync(b.ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
+}
+
+__host__ u64 padded_len(const PrimePlan& pl) {
+  std::size_t n = std::max<std::size_t>(pl.N, 1);
+  if (pl.last_pow2) {
+    const std::size_t blk = std::size_t(pl.passes.back()->R) * kTileW;
+    n = (n + blk - 1) / blk * blk;
+  }
+  return n;
+}
+
+}  // namespace
+
+std::size_t PrimePlan::position_of(std::size_t spec) const {
+  std::size_t pos = 0, rem = spec;
+  for (const auto& ps : passes) {
+    const std::size_t f = rem % ps->R;
+    rem /= ps->R;
+    const std::size_t r = ps->radix3 ? f : std::size_t(bitrev_h(f, ps->logR));
+    pos += r * ps->S;
+  }
+  return pos;
+}
+
+Engine::Engine(int device) : device_(device) {
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  err_.ensure(1);
+  meta_.ensure(4);
+  cuda_check(cudaMemsetAsync(err_.ptr, 0, sizeof(unsigned), stream_), "memset");
+}
+
+Engine::~Engine() {
+  cudaStreamSynchronize(stream_);
+  plans_.clear();
+  cudaStreamDestroy(stream_);
+}
+
+const PrimePlan& Engine::prime_plan(u64 p, std::size_t N) {
+  std::lock_guard<std::mutex> lock(mu_);
+  auto key = std::make_pair(p, N);
+  auto it = plans_.find(key);
+  if (it != plans_.end()) return *it->second;
+  auto pl = std::make_unique<PrimePlan>();
+  HostField F(p);
+  pl->p = p;
+  pl->pp = F.pp;
+  pl->N = N;
+  pl->three = (N % 3 == 0) ? 1 : 0;
+  const std::size_t c = pl->three ? N / 3 : N;
+  if (N == 0 || (c & (c - 1))) throw std::invalid_argument("build_conv_plan: length must be 2^k or 3*2^k");
+  if (N > 1 && (p - 1) % N) throw std::invalid_argument("build_conv_plan: length does not divide p-1");
+  pl->k = __builtin_ctzll(c);
+  pl->xi = N > 1 ? F.root_of_unity(N) : 1;
+  pl->conv_scale = F.mul(F.r, F.inv(N % p));
+  pl->final_scale = shoup_pair(F, pl->conv_scale);
+  if (pl->three) {
+    pl->lam = shoup_pair(F, F.pow(pl->xi, N / 3));
+    pl->lam_inv = shoup_pair(F, F.pow(pl->xi, 2 * (N / 3)));
+  }
+  build_passes(*pl);
+  build_small_tables(*pl);
+  cuda_check(cudaStreamSynchronize(stream_), "plan build");
+  auto* raw = pl.get();
+  plans_.emplace(key, std::move(pl));
+  return *raw;
+}
+
+void Engine::build_passes(PrimePlan& pl) {
+  HostField F(pl.p);
+  const u64 recip = recip_of(pl.p << __builtin_clzll(pl.p));
+  std::vector<std::pair<bool, int>> spec;  // (radix3, logR)
+  if (pl.three) spec.push_back({true, 0});
+  for (int lg : split_log(pl.k, kMaxPassLog)) spec.push_back({false, lg});
+  std::size_t done = 1;
+  int last_table = -1;
+  for (std::size_t i = 0; i < spec.size(); ++i) {
+    auto ps = std::make_unique<PassPlan>();
+    ps->radix3 = spec[i].first;
+    ps->logR = spec[i].second;
+    ps->R = ps->radix3 ? 3 : (1 << ps->logR);
+    done *= std::size_t(ps->R);
+    ps->S = pl.N / done;
+    ps->logS = ps->S ? __builtin_ctzll(ps->S) : 0;
+    if (ps->radix3 || ps->S > 1) last_table = int(i);
+    pl.passes.push_back(std::move(ps));
+  }
+  for (std::size_t i = 0; i < pl.passes.size(); ++i) {
+    PassPlan& ps = *pl.passes[i];
+    const std::size_t M = std::size_t(ps.R) * ps.S;
+    const u64 wM = F.pow(pl.xi, pl.N / M);
+    if (ps.radix3 || ps.S > 1) {
+      const std::size_t cnt = std::size_t(ps.R) * ps.S;
+      ps.tw_fwd.ensure(cnt);
+      ps.tw_inv.ensure(cnt);
+      const u64 scale = int(i) == last_table ? pl.conv_scale : 1;
+      launch_gen_pass_table(ps.tw_fwd.ptr, F.to_mont(wM), F.to_mont(1), ps.R, ps.logR, ps.S, pl.p, recip, stream_);
+      launch_gen_pass_table(ps.tw_inv.ptr, F.to_mont(F.inv(wM)), F.to_mont(scale), ps.R, ps.logR, ps.S, pl.p, recip,
+                            stream_);
+      cuda_check(cudaGetLastError(), "gen table");
+    }
+    if (!ps.radix3) {
+      const u64 wR = F.pow(pl.xi, pl.N / std::size_t(ps.R)), wRi = F.inv(wR);
+      std::vector<TwPair> tf(std::max(ps.R / 2, 1)), ti(std::max(ps.R / 2, 1));
+      u64 a = 1, b = 1;
+      for (int j = 0; j < ps.R / 2; ++j) {
+        tf[j] = shoup_pair(F, a);
+        ti[j] = shoup_pair(F, b);
+        a = F.mul(a, wR);
+        b = F.mul(b, wRi);
+      }
+      upload(ps.dft_fwd, tf, stream_);
+      upload(ps.dft_inv, ti, stream_);
+      cuda_check(cudaStreamSynchronize(stream_), "table upload");
+    }
+  }
+  pl.last_pow2 = !pl.passes.empty() && !pl.passes.back()->radix3;
+  if (last_table < 0) {
+    // no table carries the convolution scale: the last inverse kernel applies final_scale
+  }
+}
+
+void Engine::build_small_tables(PrimePlan& pl) {
+  const int maxlog = small_max_logc(pl.three);
+  if (pl.k > maxlog) return;
+  HostField F(pl.p);
+  const std::size_t c = std::size_t(1) << pl.k;
+  const u64 wc = F.pow(pl.xi, pl.N / c), wci = F.inv(wc);
+  std::vector<TwPair> tf(std::max<std::size_t>(c / 2, 1)), ti(std::max<std::size_t>(c / 2, 1));
+  u64 a = 1, b = 1;
+  for (std::size_t j = 0; j < c / 2; ++j) {
+    tf[j] = shoup_pair(F, a);
+    ti[j] = shoup_pair(F, b);
+    a = F.mul(a, wc);
+    b = F.mul(b, wci);
+  }
+  upload(pl.small_fwd, tf, stream_);
+  upload(pl.small_inv, ti, stream_);
+  if (pl.three) {
+    std::vector<TwPair> r3f(3 * c), r3i(3 * c);
+    const u64 xin = F.inv(pl.xi);
+    for (int f = 0; f < 3; ++f) {
+      const u64 sf = F.pow(pl.xi, f), sfi = F.pow(xin, f);
+      u64 w = 1, wi = pl.conv_scale;
+      for (std::size_t s = 0; s < c; ++s) {
+        r3f[f * c + s] = shoup_pair(F, w);
+        r3i[f * c + s] = shoup_pair(F, wi);
+        w = F.mul(w, sf);
+        wi = F.mul(wi, sfi);
+      }
+    }
+    upload(pl.r3_fwd, r3f, stream_);
+    upload(pl.r3_inv, r3i, stream_);
+  }
+  cuda_check(cudaStreamSynchronize(stream_), "small tables");
+  pl.small_ok = true;
+}
+
+std::size_t Engine::table_bytes() const {
+  std::size_t b = 0;
+  for (const auto& kv : plans_)
+    for (const auto& ps : kv.second->passes)
+      b += (ps->tw_fwd.n + ps->tw_inv.n + ps->dft_fwd.n + ps->dft_inv.n) * sizeof(TwPair);
+  return b;
+}
+
+ProductPlan Engine::plan_product(std::size_t dx, std::size_t dy, unsigned forced) const {
+  PairChoice pc = choose_pair(dx, dy, forced, /*allow_large=*/true);
+  ProductPlan pp;
+  pp.dx = dx;
+  pp.dy = dy;
+  pp.base_exp = pc.bp.base_exp;
+  pp.N = pc.bp.length;
+  pp.p1 = pc.p1;
+  pp.p2 = pc.p2;
+  pp.large_pair = pc.large_pair;
+  return pp;
+}
+
+void Engine::transform_forward(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2],
+                               bool include_last, cudaStream_t st) {
+  const std::size_t m = pl[0]->passes.size();
+  for (std::size_t i = 0; i < m; ++i) {
+    if (i + 1 == m && !include_last) break;
+    const bool first = i == 0;
+    if (pl[0]->passes[i]->radix3) {
+      Radix3Args a{};
+      for (int q = 0; q < np; ++q) {
+        a.src[q] = first ? src[q] : dst[q];
+        a.dst[q] = dst[q];
+        a.tw[q] = pl[q]->passes[i]->tw_fwd.ptr;
+        a.p[q] = pl[q]->p;
+        a.lam[q] = pl[q]->lam;
+      }
+      a.S = pl[0]->passes[i]->S;
+      launch_radix3(false, a, np, st);
+    } else {
+      PassArgs a{};
+      const PassPlan& P = *pl[0]->passes[i];
+      for (int q = 0; q < np; ++q) {
+        const PassPlan& Pq = *pl[q]->passes[i];
+        a.src[q] = first ? src[q] : dst[q];
+        a.dst[q] = dst[q];
+        a.dft_fwd[q] = Pq.dft_fwd.ptr;
+        a.dft_inv[q] = Pq.dft_inv.ptr;
+        a.pass_tw[q] = Pq.S > 1 ? Pq.tw_fwd.ptr : nullptr;
+        a.p[q] = pl[q]->p;
+        a.pp[q] = pl[q]->pp;
+      }
+      a.S = P.S;
+      a.logS = P.logS;
+      launch_pass_fwd(P.logR, a, pl[0]->N / std::size_t(P.R), np, st);
+    }
+    ++launches_;
+  }
+}
+
+void Engine::transform_fused_last(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
+                                  cudaStream_t st) {
+  const std::size_t m = pl[0]->passes.size();
+  const PassPlan& P = *pl[0]->passes[m - 1];
+  bool any_table = false;
+  for (const auto& ps : pl[0]->passes) any_table |= ps->radix3 || ps->S > 1;
+  PassArgs a{};
+  for (int q = 0; q < np; ++q) {
+    const PassPlan& Pq = *pl[q]->passes[m - 1];
+    a.src[q] = data[q];
+    a.dst[q] = data[q];
+    a.other[q] = other ? other[q] : nullptr;
+    a.dft_fwd[q] = Pq.dft_fwd.ptr;
+    a.dft_inv[q] = Pq.dft_inv.ptr;
+    a.pass_tw[q] = nullptr;
+    a.final_scale[q] = pl[q]->final_scale;
+    a.p[q] = pl[q]->p;
+    a.pp[q] = pl[q]->pp;
+  }
+  a.S = 1;
+  a.logS = 0;
+  a.has_final_scale = any_table ? 0 : 1;
+  launch_pass_fused(P.logR, a, pl[0]->N / std::size_t(P.R), np, st);
+  ++launches_;
+}
+
+void Engine::transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2], bool skip_last,
+                               cudaStream_t st) {
+  const std::size_t m = pl[0]->passes.size();
+  bool any_table = false;
+  for (const auto& ps : pl[0]->passes) any_table |= ps->radix3 || ps->S > 1;
+  for (std::size_t ii = m; ii-- > 0;) {
+    if (ii + 1 == m && skip_last) continue;
+    if (pl[0]->passes[ii]->radix3) {
+      Radix3Args a{};
+      for (int q = 0; q < np; ++q) {
+        a.src[q] = data[q];
+        a.dst[q] = data[q];
+        a.tw[q] = pl[q]->passes[ii]->tw_inv.ptr;
+        a.p[q] = pl[q]->p;
+        a.lam[q] = pl[q]->lam_inv;
+      }
+      a.S = pl[0]->passes[ii]->S;
+      launch_radix3(true, a, np, st);
+    } else {
+      PassArgs a{};
+      const PassPlan& P = *pl[0]->passes[ii];
+      for (int q = 0; q < np; ++q) {
+        const PassPlan& Pq = *pl[q]->passes[ii];
+        a.src[q] = data[q];
+        a.dst[q] = data[q];
+        a.dft_fwd[q] = Pq.dft_fwd.ptr;
+        a.dft_inv[q] = Pq.dft_inv.ptr;
+        a.pass_tw[q] = Pq.S > 1 ? Pq.tw_inv.ptr : nullptr;
+        a.final_scale[q] = pl[q]->final_scale;
+        a.p[q] = pl[q]->p;
+        a.pp[q] = pl[q]->pp;
+      }
+      a.S = P.S;
+      a.logS = P.logS;
+      a.has_final_scale = (!any_table && ii == 0) ? 1 : 0;
+      launch_pass_inv(P.logR, a, pl[0]->N / std::size_t(P.R), np, st);
+    }
+    ++launches_;
+  }
+}
+
+void Engine::check_err(cudaStream_t st) {
+  unsigned e = 0;
+  cuda_check(cudaMemcpyAsync(&e, err_.ptr, sizeof e, cudaMemcpyDeviceToHost, st), "err readback");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  if (e) cuda_check(cudaMemsetAsync(err_.ptr, 0, sizeof(unsigned), st), "memset");
+  if (e & kErrBadDigit) throw std::invalid_argument("decimal: non-digit character");
+  if (e & kErrLeadingZero) throw std::invalid_argument("decimal: leading zero");
+  if (e & kErrCoeffBound)
+    throw CorruptionError("recover_digits: coefficient exceeds analytic bound (upstream corruption)");
+  if (e & kErrCarryBound) throw CorruptionError("recover_digits: carry exceeds analytic bound (upstream corruption)");
+}
+
+namespace {
+
+struct CrtConsts {
+  u64 p2_prime, r_tilde;
+};
+CrtConsts crt_consts(u64 p1, u64 p2) {  // make_crt_ctx, decimal.cpp:136-146
+  if (p1 >= p2) throw std::invalid_argument("make_crt_ctx: requires p1 < p2");
+  HostField F2(p2);
+  return {F2.pp, F2.to_mont(F2.inv(p1 % p2))};
+}
+
+void coeff_cap(unsigned be, std::size_t min_limbs, u64& lo, u64& hi) {
+  const u128 top = pow10u(be) - 1, unit = top * top;
+  const u128 cap = (u128)min_limbs <= ~(u128)0 / unit ? unit * min_limbs : ~(u128)0;
+  lo = u64(cap);
+  hi = u64(cap >> 64);
+}
+
+}  // namespace
+
+void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, bool squaring, char* dout,
+                         cudaStream_t st) {
+  const PrimePlan& P1 = prime_plan(pp.p1, pp.N);
+  const PrimePlan& P2 = prime_plan(pp.p2, pp.N);
+  const unsigned be = pp.base_exp;
+  const std::size_t lx = (pp.dx + be - 1) / be, ly = (pp.dy + be - 1) / be;
+  const CrtConsts cc = crt_consts(pp.p1, pp.p2);
+  const DivB div = div_for(pow10u(be));
+  u64 cap_lo, cap_hi;
+  coeff_cap(be, std::min(lx, ly), cap_lo, cap_hi);
+  launches_ = 0;
+
+  if (P1.small_ok && P2.small_ok) {
+    SmallArgs a{};
+    a.xs = dx;
+    a.ys = squaring ? dx : dy;
+    a.x_stride = a.y_stride = 0;
+    a.nx = pp.dx;
+    a.ny = pp.dy;
+    a.outs = dout;
+    a.out_stride = 0;
+    lens_.ensure(1);
+    a.out_lens = lens_.ptr;
+    a.count = 1;
+    a.base_exp = be;
+    a.logc = P1.k;
+    a.three = P1.three;
+    const PrimePlan* pls[2] = {&P1, &P2};
+    for (int q = 0; q < 2; ++q) {
+      a.p[q] = pls[q]->p;
+      a.pp[q] = pls[q]->pp;
+      a.dft_fwd[q] = pls[q]->small_fwd.ptr;
+      a.dft_inv[q] = pls[q]->small_inv.ptr;
+      a.r3_fwd[q] = pls[q]->r3_fwd.ptr;
+      a.r3_inv[q] = pls[q]->r3_inv.ptr;
+      a.lam[q] = pls[q]->lam;
+      a.lam_inv[q] = pls[q]->lam_inv;
+      a.scale[q] = pls[q]->final_scale;
+    }
+    a.p2_prime = cc.p2_prime;
+    a.r_tilde = cc.r_tilde;
+    a.div = div;
+    a.coeff_cap_lo = cap_lo;
+    a.coeff_cap_hi = cap_hi;
+    a.err = err_.ptr;
+    a.squaring = squaring ? 1 : 0;
+    if (!launch_small(a, st)) throw CudaError("small kernel launch failed");
+    cuda_check(cudaGetLastError(), "small kernel");
+    cuda_check(cudaMemcpyAsync(meta_.ptr + 2, lens_.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st),
+               "meta");
+    launches_ = 1;
+    return;
+  }
+
+  const std::size_t npad = padded_len(P1);
+  for (int q = 0; q < 2; ++q) {
+    X_[q].ensure(npad);
+    if (!squaring) Y_[q].ensure(npad);
+  }
+  Px_.ensure(npad);
+  if (!squaring) Py_.ensure(npad);
+  const std::size_t K = pp.N + 2;
+  const std::size_t nchunks = (K + kCarryChunk - 1) / kCarryChunk;
+  S_.ensure(nchunks * kCarryChunk);
+  maps_.ensure(nchunks);
+
+  launch_pack(dx, pp.dx, be, Px_.ptr, npad, err_.ptr, st);
+  ++launches_;
+  if (!squaring) {
+    launch_pack(dy, pp.dy, be, Py_.ptr, npad, err_.ptr, st);
+    ++launches_;
+  }
+  const PrimePlan* pl[2] = {&P1, &P2};
+  u64* Z[2];
+  if (squaring) {
+    const u64* src[2] = {Px_.ptr, Px_.ptr};
+    u64* X[2] = {X_[0].ptr, X_[1].ptr};
+    transform_forward(pl, 2, src, X, !P1.last_pow2, st);
+    if (P1.last_pow2) {
+      transform_fused_last(pl, 2, X, nullptr, st);
+    } else {
+      for (int q = 0; q < 2; ++q) launch_pointwise(X[q], X[q], pp.N, pl[q]->p, pl[q]->pp, st);
+      launches_ += 2;
+    }
+    transform_inverse(pl, 2, X, P1.last_pow2, st);
+    Z[0] = X[0];
+    Z[1] = X[1];
+  } else {
+    const u64* sx[2] = {Px_.ptr, Px_.ptr};
+    const u64* sy[2] = {Py_.ptr, Py_.ptr};
+    u64* X[2] = {X_[0].ptr, X_[1].ptr};
+    u64* Y[2] = {Y_[0].ptr, Y_[1].ptr};
+    transform_forward(pl, 2, sx, X, true, st);
+    transform_forward(pl, 2, sy, Y, !P1.last_pow2, st);
+    if (P1.last_pow2) {
+      const u64* oth[2] = {X[0], X[1]};
+      transform_fused_last(pl, 2, Y, oth, st);
+    } else {
+      for (int q = 0; q < 2; ++q) launch_pointwise(Y[q], X[q], pp.N, pl[q]->p, pl[q]->pp, st);
+      launches_ += 2;
+    }
+    transform_inverse(pl, 2, Y, P1.last_pow2, st);
+    Z[0] = Y[0];
+    Z[1] = Y[1];
+  }
+  if (P1.passes.empty()) {  // N == 1: no kernel carried the convolution scale
+    for (int q = 0; q < 2; ++q) {
+      HostField F(pl[q]->p);
+      launch_mont_scale(Z[q], 1, F.to_mont(pl[q]->conv_scale), pl[q]->p, pl[q]->pp, st);
+    }
+  }
+  CarryArgs c{};
+  c.z1 = Z[0];
+  c.z2 = Z[1];
+  c.n = pp.N;
+  c.p1 = pp.p1;
+  c.p2 = pp.p2;
+  c.p2_prime = cc.p2_prime;
+  c.r_tilde = cc.r_tilde;
+  c.div = div;
+  c.coeff_cap_lo = cap_lo;
+  c.coeff_cap_hi = cap_hi;
+  c.base_exp = be;
+  c.s = S_.ptr;
+  c.maps = maps_.ptr;
+  c.err = err_.ptr;
+  const unsigned long long dsum = pp.dx + pp.dy;
+  c.top_candidates[0] = dsum >= 2 ? (dsum - 2) / be : 0;
+  c.top_candidates[1] = (dsum - 1) / be;
+  c.meta = meta_.ptr;
+  c.out = dout;
+  launch_carry(c, st);
+  launches_ += 3;
+  cuda_check(cudaGetLastError(), "product kernels");
+}
+
+std::size_t Engine::multiply_device(const char* dx, std::size_t nx, const char* dy, std::size_t ny, char* dout,
+                                    std::size_t cap, unsigned forced, bool squaring, cudaStream_t st, bool sync) {
+  if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
+  if (!st) st = stream_;
+  if (nx == 1 || ny == 1) {  // zero short-circuit (decimal.cpp:193), before any size checks
+    char a = 0, b = 0;
+    if (nx == 1) cuda_check(cudaMemcpy(&a, dx, 1, cudaMemcpyDeviceToHost), "zero check");
+    if (ny == 1) cuda_check(cudaMemcpy(&b, dy, 1, cudaMemcpyDeviceToHost), "zero check");
+    if (a == '0' || b == '0') {
+      if (cap < 1) throw std::length_error("multiply: output buffer too small");
+      cuda_check(cudaMemcpyAsync(dout, "0", 1, cudaMemcpyHostToDevice, st), "zero");
+      if (sync) cuda_check(cudaStreamSynchronize(st), "sync");
+      return 1;
+    }
+  }
+  const ProductPlan pp = plan_product(nx, ny, forced);
+  if (cap < nx + ny) throw std::length_error("multiply: output buffer too small");
+  run_product(pp, dx, squaring ? dx : dy, squaring, dout, st);
+  if (!sync) return 0;
+  unsigned long long len = 0;
+  cuda_check(cudaMemcpyAsync(&len, meta_.ptr + 2, sizeof len, cudaMemcpyDeviceToHost, st), "len");
+  check_err(st);
+  return std::size_t(len);
+}
+
+std::size_t Engine::result_length() {
+  unsigned long long len = 0;
+  cuda_check(cudaMemcpyAsync(&len, meta_.ptr + 2, sizeof len, cudaMemcpyDeviceToHost, stream_), "len");
+  check_err(stream_);
+  return std::size_t(len);
+}
+
+std::size_t Engine::multiply_host(const char* x, std::size_t nx, const char* y, std::size_t ny, char* out,
+                                  std::size_t cap, unsigned forced, bool alias) {
+  if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
+  const bool squaring = alias || (nx == ny && (x == y || std::memcmp(x, y, nx) == 0));
+  din_x_.ensure(nx);
+  cuda_check(cudaMemcpyAsync(din_x_.ptr, x, nx, cudaMemcpyHostToDevice, stream_), "h2d");
+  if (!squaring) {
+    din_y_.ensure(ny);
+    cuda_check(cudaMemcpyAsync(din_y_.ptr, y, ny, cudaMemcpyHostToDevice, stream_), "h2d");
+  }
+  dout_.ensure(nx + ny);
+  const std::size_t len = multiply_device(din_x_.ptr, nx, squaring ? din_x_.ptr : din_y_.ptr, squaring ? nx : ny,
+                                          dout_.ptr, nx + ny, forced, squaring, stream_, true);
+  if (len > cap) throw std::length_error("multiply: output buffer too small");
+  cuda_check(cudaMemcpyAsync(out, dout_.ptr, len, cudaMemcpyDeviceToHost, stream_), "d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  return len;
+}
+
+void Engine::multiply_batch_device(std::size_t count, const char* dxs, std::size_t x_stride, std::size_t nx,
+                                   const char* dys, std::size_t y_stride, std::size_t ny, char* douts,
+                                   std::size_t out_stride, unsigned long long* dlens, cudaStream_t st) {
+  if (!st) st = stream_;
+  if (count == 0) return;
+  if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
+  if (out_stride < nx + ny) throw std::length_error("multiply_batch: output stride too small");
+  const ProductPlan pp = plan_product(nx, ny, 0);
+  const PrimePlan& P1 = prime_plan(pp.p1, pp.N);
+  const PrimePlan& P2 = prime_plan(pp.p2, pp.N);
+  if (!(P1.small_ok && P2.small_ok)) {
+    // large products: one after another through the pass engine
+    for (std::size_t i = 0; i < count; ++i) {
+      run_product(pp, dxs + i * x_stride, dys + i * y_stride, false, douts + i * out_stride, st);
+      cuda_check(cudaMemcpyAsync(dlens + i, meta_.ptr + 2, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st),
+                 "len");
+    }
+    return;
+  }
+  const unsigned be = pp.base_exp;
+  const std::size_t lx = (nx + be - 1) / be, ly = (ny + be - 1) / be;
+  const CrtConsts cc = crt_consts(pp.p1, pp.p2);
+  SmallArgs a{};
+  a.xs = dxs;
+  a.ys = dys;
+  a.x_stride = x_stride;
+  a.y_stride = y_stride;
+  a.nx = nx;
+  a.ny = ny;
+  a.outs = douts;
+  a.out_stride = out_stride;
+  a.out_lens = dlens;
+  a.base_exp = be;
+  a.logc = P1.k;
+  a.three = P1.three;
+  const PrimePlan* pls[2] = {&P1, &P2};
+  for (int q = 0; q < 2; ++q) {
+    a.p[q] = pls[q]->p;
+    a.pp[q] = pls[q]->pp;
+    a.dft_fwd[q] = pls[q]->small_fwd.ptr;
+    a.dft_inv[q] = pls[q]->small_inv.ptr;
+    a.r3_fwd[q] = pls[q]->r3_fwd.ptr;
+    a.r3_inv[q] = pls[q]->r3_inv.ptr;
+    a.lam[q] = pls[q]->lam;
+    a.lam_inv[q] = pls[q]->lam_inv;
+    a.scale[q] = pls[q]->final_scale;
+  }
+  a.p2_prime = cc.p2_prime;
+  a.r_tilde = cc.r_tilde;
+  a.div = div_for(pow10u(be));
+  coeff_cap(be, std::min(lx, ly), a.coeff_cap_lo, a.coeff_cap_hi);
+  a.err = err_.ptr;
+  a.squaring = 0;
+  const std::size_t maxgrid = 1u << 30;
+  for (std::size_t off = 0; off < count; off += maxgrid) {
+    SmallArgs b = a;
+    b.count = unsigned(std::min(maxgrid, count - off));
+    b.xs = dxs + off * x_stride;
+    b.ys = dys + off * y_stride;
+    b.outs = douts + off * out_stride;
+    b.out_lens = dlens + off;
+    if (!launch_small(b, st)) throw CudaError("small kernel launch failed");
+  }
+  launches_ = 1;
+  cuda_check(cudaGetLastError(), "batch kernel");
+}
+
+void Engine::multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
+                                 const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
+                                 std::size_t out_stride, std::size_t* lens) {
+  if (count == 0) return;
+  const std::size_t xb = (count - 1) * x_stride + nx, yb = (count - 1) * y_stride + ny;
+  const std::size_t ob = count * out_stride;
+  din_x_.ensure(xb);
+  din_y_.ensure(yb);
+  dout_.ensure(ob);
+  lens_.ensure(count);
+  cuda_check(cudaMemcpyAsync(din_x_.ptr, xs, xb, cudaMemcpyHostToDevice, stream_), "h2d");
+  cuda_check(cudaMemcpyAsync(din_y_.ptr, ys, yb, cudaMemcpyHostToDevice, stream_), "h2d");
+  multiply_batch_device(count, din_x_.ptr, x_stride, nx, din_y_.ptr, y_stride, ny, dout_.ptr, out_stride,
+                        lens_.ptr, stream_);
+  std::vector<unsigned long long> l(count);
+  cuda_check(cudaMemcpyAsync(l.data(), lens_.ptr, count * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_),
+             "d2h");
+  cuda_check(cudaMemcpyAsync(outs, dout_.ptr, ob, cudaMemcpyDeviceToHost, stream_), "d2h");
+  check_err(stream_);
+  for (std::size_t i = 0; i < count; ++i) lens[i] = std::size_t(l[i]);
+}
+
+// ---------------- parity hooks ----------------
+
+void Engine::convolve_mod_p(u64 p, std::size_t n, const u64* x, std::size_t nx, const u64* y, std::size_t ny,
+                            u64* out) {
+  if (nx > n || ny > n) throw std::invalid_argument("convolve_mod_p: input longer than plan length");
+  const PrimePlan& P = prime_plan(p, n);
+  const bool squaring = x == y && nx == ny;
+  const std::size_t npad = padded_len(P);
+  X_[0].ensure(npad);
+  Y_[0].ensure(npad);
+  cudaStream_t st = stream_;
+  cuda_check(cudaMemsetAsync(X_[0].ptr, 0, npad * 8, st), "memset");
+  cuda_check(cudaMemcpyAsync(X_[0].ptr, x, nx * 8, cudaMemcpyHostToDevice, st), "h2d");
+  if (!squaring) {
+    cuda_check(cudaMemsetAsync(Y_[0].ptr, 0, npad * 8, st), "memset");
+    cuda_check(cudaMemcpyAsync(Y_[0].ptr, y, ny * 8, cudaMemcpyHostToDevice, st), "h2d");
+  }
+  const PrimePlan* pl[2] = {&P, &P};
+  u64* X[2] = {X_[0].ptr, nullptr};
+  u64* Y[2] = {Y_[0].ptr, nullptr};
+  const u64* sx[2] = {X_[0].ptr, nullptr};
+  const u64* sy[2] = {Y_[0].ptr, nullptr};
+  u64* Z = nullptr;
+  if (squaring) {
+    transform_forward(pl, 1, sx, X, !P.last_pow2, st);
+    if (P.last_pow2)
+      transform_fused_last(pl, 1, X, nullptr, st);
+    else
+      launch_pointwise(X[0], X[0], n, p, P.pp, st);
+    transform_inverse(pl, 1, X, P.last_pow2, st);
+    Z = X[0];
+  } else {
+    transform_forward(pl, 1, sx, X, true, st);
+    transform_forward(pl, 1, sy, Y, !P.last_pow2, st);
+    if (P.last_pow2) {
+      const u64* oth[2] = {X[0], nullptr};
+      transform_fused_last(pl, 1, Y, oth, st);
+    } else {
+      launch_pointwise(Y[0], X[0], n, p, P.pp, st);
+    }
+    transform_inverse(pl, 1, Y, P.last_pow2, st);
+    Z = Y[0];
+  }
+  if (P.passes.empty()) {
+    HostField F(p);
+    launch_mont_scale(Z, 1, F.to_mont(P.conv_scale), p, P.pp, st);
+  }
+  cuda_check(cudaGetLastError(), "convolve");
+  cuda_check(cudaMemcpyAsync(out, Z, n * 8, cudaMemcpyDeviceToHost, st), "d2h");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+void Engine::forward_transform(u64 p, std::size_t n, u64* a) {
+  const PrimePlan& P = prime_plan(p, n);
+  const std::size_t npad = padded_len(P);
+  X_[0].ensure(npad);
+  Y_[0].ensure(npad);
+  cudaStream_t st = stream_;
+  cuda_check(cudaMemcpyAsync(X_[0].ptr, a, n * 8, cudaMemcpyHostToDevice, st), "h2d");
+  const PrimePlan* pl[2] = {&P, &P};
+  u64* X[2] = {X_[0].ptr, nullptr};
+  const u64* sx[2] = {X_[0].ptr, nullptr};
+  transform_forward(pl, 1, sx, X, true, st);
+  std::vector<unsigned long long> map(n);
+  for (std::size_t k = 0; k < n; ++k) map[k] = P.position_of(ref_order_of(n, k));
+  DevBuf<unsigned long long> dmap;
+  upload(dmap, map, st);
+  launch_gather(X_[0].ptr, Y_[0].ptr, dmap.ptr, n, st);
+  cuda_check(cudaGetLastError(), "forward");
+  cuda_check(cudaMemcpyAsync(a, Y_[0].ptr, n * 8, cudaMemcpyDeviceToHost, st), "d2h");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+void Engine::inverse_transform(u64 p, std::size_t n, u64* a) {
+  const PrimePlan& P = prime_plan(p, n);
+  const std::size_t npad = padded_len(P);
+  X_[0].ensure(npad);
+  Y_[0].ensure(npad);
+  cudaStream_t st = stream_;
+  cuda_check(cudaMemcpyAsync(Y_[0].ptr, a, n * 8, cudaMemcpyHostToDevice, st), "h2d");
+  // inverse of the forward gather: position_of(ref_order_of(k)) <- a[k]
+  std::vector<unsigned long long> map(n);
+  for (std::size_t k = 0; k < n; ++k) map[P.position_of(ref_order_of(n, k))] = k;
+  DevBuf<unsigned long long> dmap;
+  upload(dmap, map, st);
+  launch_gather(Y_[0].ptr, X_[0].ptr, dmap.ptr, n, st);
+  const PrimePlan* pl[2] = {&P, &P};
+  u64* X[2] = {X_[0].ptr, nullptr};
+  transform_inverse(pl, 1, X, false, st);
+  HostField F(p);
+  // the inverse carries R N^-1 (the convolution fold); one REDC against 1 leaves N^-1
+  if (P.passes.empty()) launch_mont_scale(X_[0].ptr, 1, F.to_mont(P.conv_scale), p, P.pp, st);
+  launch_mont_scale(X_[0].ptr, n, 1, p, P.pp, st);
+  cuda_check(cudaGetLastError(), "inverse");
+  cuda_check(cudaMemcpyAsync(a, X_[0].ptr, n * 8, cudaMemcpyDeviceToHost, st), "d2h");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+void Engine::pointwise_product(u64 p, std::size_t n, u64* a, const u64* b) {
+  HostField F(p);
+  X_[0].ensure(std::max<std::size_t>(n, 1));
+  Y_[0].ensure(std::max<std::size_t>(n, 1));
+  cudaStream_t st = stream_;
+  cuda_check(cudaMemcpyAsync(X_[0].ptr, a, n * 8, cudaMemcpyHostToDevice, st), "h2d");
+  cuda_check(cudaMemcpyAsync(Y_[0].ptr, b, n * 8, cudaMemcpyHostToDevice, st), "h2d");
+  launch_pointwise(X_[0].ptr, Y_[0].ptr, n, p, F.pp, st);
+  cuda_check(cudaGetLastError(), "pointwise");
+  cuda_check(cudaMemcpyAsync(a, X_[0].ptr, n * 8, cudaMemcpyDeviceToHost, st), "d2h");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+std::size_t Engine::pack(const char* digits, std::size_t nd, unsigned be, u64* limbs, std::size_t cap) {
+  if (be < 1 || be > 17) throw std::invalid_argument("pack: unsupported base");
+  if (nd == 0) throw std::invalid_argument("decimal: empty string");
+  const std::size_t nl = (nd + be - 1) / be;
+  if (nl > cap) throw std::length_error("pack: output buffer too small");
+  din_x_.ensure(nd);
+  Px_.ensure(nl);
+  cuda_check(cudaMemcpyAsync(din_x_.ptr, digits, nd, cudaMemcpyHostToDevice, stream_), "h2d");
+  launch_pack(din_x_.ptr, nd, be, Px_.ptr, nl, err_.ptr, stream_);
+  cuda_check(cudaMemcpyAsync(limbs, Px_.ptr, nl * 8, cudaMemcpyDeviceToHost, stream_), "d2h");
+  check_err(stream_);
+  return nl;
+}
+
+std::size_t Engine::recover_decimal(const u64* r1, const u64* r2, std::size_t n, u64 p1, u64 p2, unsigned be,
+                                    std::size_t min_limbs, std::size_t dsum, char* out, std::size_t cap) {
+  if (be < 14 || be > 17) throw std::invalid_argument("recover_digits: base out of range");
+  if (min_limbs < 1) throw std::invalid_argument("recover_digits: min_limbs must be >= 1");
+  const CrtConsts cc = crt_consts(p1, p2);
+  X_[0].ensure(n);
+  X_[1].ensure(n);
+  const std::size_t K = n + 2, nchunks = (K + kCarryChunk - 1) / kCarryChunk;
+  S_.ensure(nchunks * kCarryChunk);
+  maps_.ensure(nchunks);
+  dout_.ensure(std::max<std::size_t>(dsum, 1) + 64);
+  cudaStream_t st = stream_;
+  cuda_check(cudaMemcpyAsync(X_[0].ptr, r1, n * 8, cudaMemcpyHostToDevice, st), "h2d");
+  cuda_check(cudaMemcpyAsync(X_[1].ptr, r2, n * 8, cudaMemcpyHostToDevice, st), "h2d");
+  CarryArgs c{};
+  c.z1 = X_[0].ptr;
+  c.z2 = X_[1].ptr;
+  c.n = n;
+  c.p1 = p1;
+  c.p2 = p2;
+  c.p2_prime = cc.p2_prime;
+  c.r_tilde = cc.r_tilde;
+  c.div = div_for(pow10u(be));
+  coeff_cap(be, min_limbs, c.coeff_cap_lo, c.coeff_cap_hi);
+  c.base_exp = be;
+  c.s = S_.ptr;
+  c.maps = maps_.ptr;
+  c.err = err_.ptr;
+  c.top_candidates[0] = dsum >= 2 ? (dsum - 2) / be : 0;
+  c.top_candidates[1] = (dsum - 1) / be;
+  c.meta = meta_.ptr;
+  c.out = dout_.ptr;
+  launch_carry(c, st);
+  cuda_check(cudaGetLastError(), "carry");
+  unsigned long long len = 0;
+  cuda_check(cudaMemcpyAsync(&len, meta_.ptr + 2, sizeof len, cudaMemcpyDeviceToHost, st), "len");
+  check_err(st);
+  if (len > cap) throw std::length_error("recover: output buffer too small");
+  cuda_check(cudaMemcpy(out, dout_.ptr, len, cudaMemcpyDeviceToHost), "d2h");
+  return std::size_t(len);
+}
+
+void Engine::transpose(int kind, u64* a, std::size_t n, std::size_t stride) {
+  std::size_t total;
+  if (kind == 0)
+    total = n ? (n - 1) * stride + n : 0;
+  else
+    total = 2 * n * n;
+  if (total == 0) return;
+  X_[0].ensure(total);
+  X_[1].ensure(total);
+  cudaStream_t st = stream_;
+  cuda_check(cudaMemcpyAsync(X_[0].ptr, a, total * 8, cudaMemcpyHostToDevice, st), "h2d");
+  if (kind == 0) {
+    launch_transpose_square_sub(X_[0].ptr, n, stride, st);
+  } else if (kind == 1) {  // n x 2n -> 2n x n: rho per row, then both square halves (transpose.cpp:43-47)
+    launch_rho(X_[0].ptr, X_[1].ptr, n, false, st);
+    launch_transpose_square_sub(X_[0].ptr, n, 2 * n, st);
+    launch_transpose_square_sub(X_[0].ptr + n, n, 2 * n, st);
+  } else {  // 2n x n -> n x 2n (transpose.cpp:49-53)
+    launch_transpose_square_sub(X_[0].ptr, n, 2 * n, st);
+    launch_transpose_square_sub(X_[0].ptr + n, n, 2 * n, st);
+    launch_rho(X_[0].ptr, X_[1].ptr, n, true, st);
+  }
+  cuda_check(cudaGetLastError(), "transpose");
+  cuda_check(cudaMemcpyAsync(a, X_[0].ptr, total * 8, cudaMemcpyDeviceToHost, st), "d2h");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+}  // namespace dmg

@@ -1,0 +1,155 @@
+// Host orchestration of the device pipeline: per-(prime, length) transform
+// plans with device-resident twiddle tables, workspace management, and the
+// multiply / batch / parity-hook entry points used by the C ABI (capi.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "hostmath.hpp"
+#include "kernels.cuh"
+
+namespace dmg {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CorruptionError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (ptr) cudaFree(ptr);
+  }
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    n = 0;
+    cuda_check(cudaMalloc(&ptr, count * sizeof(T) + 16), "cudaMalloc");
+    n = count;
+  }
+};
+
+struct PassPlan {
+  bool radix3 = false;
+  int logR = 0, R = 0;
+  unsigned long long S = 0;
+  int logS = 0;
+  DevBuf<TwPair> tw_fwd, tw_inv;    // R x S inter-pass twiddles (S > 1) / 3 x S for radix-3
+  DevBuf<TwPair> dft_fwd, dft_inv;  // omega_R^{+-k}, k < R/2
+};
+
+// Transform plan for one prime and one length N = 2^k or 3*2^k (root chosen
+// exactly as the reference does: primitive_root_of_unity(N), primes.cpp:99-112).
+struct PrimePlan {
+  u64 p = 0, pp = 0;
+  std::size_t N = 0;
+  int three = 0, k = 0;
+  u64 xi = 0;          // plain primitive N-th root
+  u64 conv_scale = 0;  // R N^-1 mod p: undoes N (unscaled inverse) and R^-1 (pointwise REDC)
+  TwPair final_scale{};  // Shoup pair of conv_scale (used when no pass table carries it)
+  TwPair lam{}, lam_inv{};
+  std::vector<std::unique_ptr<PassPlan>> passes;  // pass 0 first
+  bool last_pow2 = false;  // last pass is a power-of-two pass with S == 1 (fusable)
+  // one-CTA kernel tables (N small): row length c = N / 3^three
+  DevBuf<TwPair> small_fwd, small_inv, r3_fwd, r3_inv;
+  bool small_ok = false;
+
+  // position of spectrum index f in this plan's forward output, and inverse.
+  std::size_t position_of(std::size_t spec) const;
+};
+
+struct ProductPlan {
+  std::size_t dx = 0, dy = 0;
+  unsigned base_exp = 0;
+  std::size_t N = 0;
+  u64 p1 = 0, p2 = 0;
+  bool large_pair = false;
+};
+
+class Engine {
+ public:
+  explicit Engine(int device);
+  ~Engine();
+
+  int device() const { return device_; }
+  cudaStream_t stream() const { return stream_; }
+
+  ProductPlan plan_product(std::size_t dx, std::size_t dy, unsigned forced_base_exp) const;
+
+  // Host strings -> host string (reference decmul::multiply semantics).
+  std::size_t multiply_host(const char* x, std::size_t nx, const char* y, std::size_t ny, char* out,
+                            std::size_t cap, unsigned forced_base_exp, bool alias);
+  // Device digits -> device digits; stream-ordered; *out_len written (host) after sync.
+  std::size_t multiply_device(const char* dx, std::size_t nx, const char* dy, std::size_t ny, char* dout,
+                              std::size_t cap, unsigned forced_base_exp, bool squaring, cudaStream_t st,
+                              bool sync);
+  // Uniform-size batch (config 2 shape), device buffers.
+  void multiply_batch_device(std::size_t count, const char* dxs, std::size_t x_stride, std::size_t nx,
+                             const char* dys, std::size_t y_stride, std::size_t ny, char* douts,
+                             std::size_t out_stride, unsigned long long* dlens, cudaStream_t st);
+  void multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
+                           const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
+                           std::size_t out_stride, std::size_t* lens);
+
+  // Parity hooks (reference conv.hpp:59-71), host arrays, one prime.
+  void convolve_mod_p(u64 p, std::size_t n, const u64* x, std::size_t nx, const u64* y, std::size_t ny,
+                      u64* out);
+  void forward_transform(u64 p, std::size_t n, u64* a);  // reference storage order (conv.hpp:19-24)
+  void inverse_transform(u64 p, std::size_t n, u64* a);
+  void pointwise_product(u64 p, std::size_t n, u64* a, const u64* b);
+  // Stage hooks on the device path (decimal.cpp pack / crt2 + recover_digits + to_decimal).
+  std::size_t pack(const char* digits, std::size_t nd, unsigned base_exp, u64* limbs, std::size_t cap);
+  std::size_t recover_decimal(const u64* r1, const u64* r2, std::size_t n, u64 p1, u64 p2, unsigned base_exp,
+                              std::size_t min_limbs, std::size_t dsum, char* out, std::size_t cap);
+  // In-place transposes (reference transpose.cpp) of a host matrix through the device.
+  void transpose(int kind, u64* a, std::size_t n, std::size_t stride);
+
+  const PrimePlan& prime_plan(u64 p, std::size_t N);
+  // Length of the last product (after its stream was synchronised); raises its errors.
+  std::size_t result_length();
+
+  // bytes of device tables currently held by plans
+  std::size_t table_bytes() const;
+
+  // Launch count of the last product (for the bench's gpu_launches claim).
+  int last_launches() const { return launches_; }
+
+ private:
+  void build_passes(PrimePlan& pl);
+  void build_small_tables(PrimePlan& pl);
+  void run_product(const ProductPlan& pp, const char* dx, const char* dy, bool squaring, char* dout,
+                   cudaStream_t st);
+  void transform_forward(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2],
+                         bool include_last, cudaStream_t st);
+  void transform_fused_last(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
+                            cudaStream_t st);
+  void transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2], bool skip_last, cudaStream_t st);
+  void check_err(cudaStream_t st);
+
+  int device_ = 0;
+  cudaStream_t stream_ = nullptr;
+  std::mutex mu_;
+  std::map<std::pair<u64, std::size_t>, std::unique_ptr<PrimePlan>> plans_;
+  DevBuf<u64> X_[2], Y_[2], Px_, Py_, S_;
+  DevBuf<unsigned> maps_, err_;
+  DevBuf<unsigned long long> meta_, lens_;
+  DevBuf<char> din_x_, din_y_, dout_;
+  int launches_ = 0;
+};
+
+}  // namespace dmg

@@ -1,0 +1,116 @@
+// Kernel parameter blocks and launch helpers shared by kernels.cu and engine.cu.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "modarith.cuh"
+
+namespace dmg {
+
+constexpr int kTileLogW = 4;  // 16 columns per pass tile: one 128 B row segment per tile row
+constexpr int kTileW = 1 << kTileLogW;
+constexpr int kPassThreads = 256;
+constexpr int kMaxPassLog = 9;  // radix of one pass <= 512 (64 KiB tile)
+
+// Error bits raised by kernels (device flag, read by the host after a product).
+enum : unsigned {
+  kErrBadDigit = 1u,
+  kErrLeadingZero = 2u,
+  kErrCoeffBound = 4u,
+  kErrCarryBound = 8u,
+};
+
+// One pass of a multi-pass transform over both primes (blockIdx.y = prime).
+struct PassArgs {
+  const u64* src[2];       // input (may equal dst; pass 0 of an operand reads the shared packed limbs)
+  u64* dst[2];             // output
+  const u64* other[2];     // fused pass: the other operand's spectrum (nullptr = square)
+  const TwPair* dft_fwd[2];  // omega_R^k, k < R/2
+  const TwPair* dft_inv[2];  // omega_R^-k, k < R/2
+  const TwPair* pass_tw[2];  // T[f][s] = omega_M^{+-f s} (* scale), R x S; nullptr when S == 1
+  TwPair final_scale[2];   // fused single-pass transforms: (c, c') applied after the inverse
+  u64 p[2], pp[2];
+  unsigned long long S;    // column stride (elements)
+  int logS;
+  int has_final_scale;
+};
+
+struct Radix3Args {
+  const u64* src[2];
+  u64* dst[2];
+  const TwPair* tw[2];  // 3 x S table: omega_N^{+-f s} (* scale on inverse)
+  u64 p[2];
+  TwPair lam[2];        // omega_3 (forward) or omega_3^-1 (inverse)
+  unsigned long long S;
+};
+
+// Launchers (kernels.cu).
+void launch_pass_fwd(int logR, const PassArgs& a, unsigned long long ncols, int nprimes, cudaStream_t st);
+void launch_pass_inv(int logR, const PassArgs& a, unsigned long long ncols, int nprimes, cudaStream_t st);
+void launch_pass_fused(int logR, const PassArgs& a, unsigned long long ncols, int nprimes, cudaStream_t st);
+void launch_radix3(bool inverse, const Radix3Args& a, int nprimes, cudaStream_t st);
+
+void launch_gen_pass_table(TwPair* out, u64 root_m, u64 scale, int R, int logR, unsigned long long S, u64 p,
+                           u64 recip, cudaStream_t st);
+void launch_pack(const char* digits, unsigned long long nd, unsigned base_exp, u64* limbs,
+                 unsigned long long nlimbs_total, unsigned* err, cudaStream_t st);
+void launch_pointwise(u64* a, const u64* b, unsigned long long n, u64 p, u64 pp, cudaStream_t st);
+void launch_mont_scale(u64* a, unsigned long long n, u64 factor, u64 p, u64 pp, cudaStream_t st);
+void launch_gather(const u64* src, u64* dst, const unsigned long long* map, unsigned long long n, cudaStream_t st);
+
+// Carry pipeline (decimal recovery).
+struct CarryArgs {
+  const u64* z1;        // residues mod p1, natural order, N
+  const u64* z2;        // residues mod p2
+  unsigned long long n;  // N coefficients; limbs k in [0, n + 2)
+  u64 p1, p2, p2_prime, r_tilde;  // CRT (reference decimal.cpp:136-152)
+  DivB div;
+  u64 coeff_cap_lo, coeff_cap_hi;  // (B-1)^2 * min_limbs
+  unsigned base_exp;
+  u64* s;               // n + 2 digit sums s_k < 3B
+  unsigned* maps;       // per-chunk transfer maps / carry-ins
+  unsigned* err;
+  unsigned long long top_candidates[2];
+  unsigned long long* meta;  // [0] top limb index, [1] top digit count, [2] output length
+  char* out;
+};
+constexpr int kCarryChunk = 2048;
+constexpr int kCarryThreads = 256;
+void launch_carry(const CarryArgs& a, cudaStream_t st);
+
+// One-CTA-per-product batch kernel (small transforms).
+struct SmallArgs {
+  const char* xs;               // count operands, x digits at xs + i * x_stride
+  const char* ys;
+  unsigned long long x_stride, y_stride, nx, ny;
+  char* outs;                   // outputs at outs + i * out_stride
+  unsigned long long out_stride;
+  unsigned long long* out_lens; // per product
+  unsigned count;
+  unsigned base_exp;
+  int logc;                     // power-of-two part: row length c = 2^logc
+  int three;                    // N = 3 c if set, else N = c
+  u64 p[2], pp[2];
+  const TwPair* dft_fwd[2];     // omega_c^k, k < c/2
+  const TwPair* dft_inv[2];
+  const TwPair* r3_fwd[2];      // 3 x c: omega_N^{f s}
+  const TwPair* r3_inv[2];      // 3 x c: omega_N^{-f s} * scale
+  TwPair lam[2], lam_inv[2];
+  TwPair scale[2];              // used when !three
+  u64 p2_prime, r_tilde;
+  DivB div;
+  u64 coeff_cap_lo, coeff_cap_hi;
+  unsigned* err;
+  int squaring;
+};
+bool launch_small(const SmallArgs& a, cudaStream_t st);
+int small_max_logc(int three);
+
+// In-place transposes (reference transpose.cpp) on device memory.
+void launch_transpose_square_sub(u64* a, unsigned long long n, unsigned long long stride, cudaStream_t st);
+// rho per row of 2n words (n rows), through scratch (>= 2 n^2 words); inverse = unpermute_rho.
+void launch_rho(u64* a, u64* scratch, unsigned long long n, bool inverse, cudaStream_t st);
+
+}  // namespace dmg

@@ -1,0 +1,118 @@
+// 63-bit prime-field arithmetic for sm_100a, built on 32-bit IMAD chains.
+//
+// Values are plain residues in [0, p); p < 2^63 (reference montgomery.hpp:9-17,
+// words.hpp:29-78). Two multiplication forms are used:
+//  * Shoup: x * w mod p for a fixed factor w with precomputed
+//    w' = floor(w 2^64 / p). One high product, two low products. Used for
+//    every root-of-unity factor (tables hold (w, w') pairs).
+//  * Montgomery REDC (R = 2^64), reference montgomery.hpp:26-39, for
+//    data x data products (pointwise spectra, CRT inner product).
+// Both produce canonical [0, p) results, so every transform value is the same
+// field element the reference computes (its tables hold Montgomery forms, whose
+// REDC against plain data yields plain products — ntt.hpp:14-19).
+#pragma once
+#include <cstdint>
+
+namespace dmg {
+
+typedef unsigned long long u64;
+
+struct TwPair {  // Shoup form of one root-of-unity factor
+  u64 w, wp;
+};
+
+__device__ __forceinline__ u64 mod_add(u64 a, u64 b, u64 p) {
+  u64 s = a + b;
+  return s >= p ? s - p : s;
+}
+__device__ __forceinline__ u64 mod_sub(u64 a, u64 b, u64 p) {
+  u64 d = a - b;
+  return a >= b ? d : d + p;
+}
+
+// x in [0, 2^64), w < p: returns x w mod p in [0, p).
+__device__ __forceinline__ u64 shoup_mul(u64 x, u64 w, u64 wp, u64 p) {
+  u64 q = __umul64hi(x, wp);
+  u64 r = x * w - q * p;  // exact, r < 2p
+  return r >= p ? r - p : r;
+}
+__device__ __forceinline__ u64 shoup_mul(u64 x, TwPair t, u64 p) { return shoup_mul(x, t.w, t.wp, p); }
+
+// REDC(a b) = a b 2^-64 mod p for a b < p 2^64 (one operand may lie in [0, 2p)).
+__device__ __forceinline__ u64 mont_mul(u64 a, u64 b, u64 p, u64 pp) {
+  u64 lo = a * b, hi = __umul64hi(a, b);
+  u64 m = lo * pp;
+  // lo + lo(m p) == 0 mod 2^64: the carry out of the low word is (lo != 0).
+  u64 r = hi + __umul64hi(m, p) + (lo != 0 ? 1ull : 0ull);
+  return r >= p ? r - p : r;
+}
+
+// Gentleman-Sande butterfly (reference ntt.cpp:42-47): (u + v, (u - v) w).
+__device__ __forceinline__ void bfly_dif(u64& u, u64& v, TwPair t, u64 p) {
+  u64 a = mod_add(u, v, p);
+  v = shoup_mul(u - v + p, t, p);  // u - v + p in [1, 2p)
+  u = a;
+}
+__device__ __forceinline__ void bfly_dif1(u64& u, u64& v, u64 p) {  // factor 1 (j = 0 peel)
+  u64 a = mod_add(u, v, p);
+  v = mod_sub(u, v, p);
+  u = a;
+}
+// Cooley-Tukey butterfly (reference ntt.cpp:65-70): (u + v w, u - v w).
+__device__ __forceinline__ void bfly_dit(u64& u, u64& v, TwPair t, u64 p) {
+  u64 w = shoup_mul(v, t, p);
+  v = mod_sub(u, w, p);
+  u = mod_add(u, w, p);
+}
+__device__ __forceinline__ void bfly_dit1(u64& u, u64& v, u64 p) {
+  u64 w = v;
+  v = mod_sub(u, w, p);
+  u = mod_add(u, w, p);
+}
+
+// ---- two-word division by the constant limb base B = 10^lambda ----
+// Restates the reciprocal scheme of reference decimal.hpp:93-146 (make_div_by_const,
+// udiv_2by1, divmod_base) for the device.
+struct DivB {
+  u64 base, d_norm, recip;
+  unsigned shift;
+};
+
+__device__ __forceinline__ void udiv_2by1(u64 u1, u64 u0, u64 d, u64 v, u64& q, u64& r) {
+  // t = v u1 + (u1 + 1) 2^64 + u0
+  u64 tlo = v * u1, thi = __umul64hi(v, u1);
+  u64 q0 = tlo + u0;
+  u64 q1 = thi + u1 + 1 + (q0 < tlo ? 1ull : 0ull);
+  u64 rr = u0 - q1 * d;
+  if (rr > q0) {
+    --q1;
+    rr += d;
+  }
+  if (rr >= d) {
+    ++q1;
+    rr -= d;
+  }
+  q = q1;
+  r = rr;
+}
+
+// (hi 2^64 + lo) = q B + r with q returned as (qhi, qlo). Requires the quotient to fit two words.
+__device__ __forceinline__ u64 divmod_base(const DivB& d, u64 lo, u64 hi, u64& qlo, u64& qhi) {
+  const unsigned sh = d.shift;
+  u64 n0, n1, n2;
+  if (sh == 0) {
+    n0 = lo;
+    n1 = hi;
+    n2 = 0;
+  } else {
+    n0 = lo << sh;
+    n1 = (hi << sh) | (lo >> (64 - sh));
+    n2 = hi >> (64 - sh);
+  }
+  u64 rmid, rlo;
+  udiv_2by1(n2, n1, d.d_norm, d.recip, qhi, rmid);
+  udiv_2by1(rmid, n0, d.d_norm, d.recip, qlo, rlo);
+  return rlo >> sh;
+}
+
+}  // namespace dmg

@@ -1,0 +1,267 @@
+// One product per CTA, end to end in shared memory: pack -> forward transforms
+// (both primes, both operands) -> pointwise REDC -> inverse -> CRT -> carry
+// scan -> ASCII. HBM sees only the digits in and the digits out.
+//
+// Replaces, for transform lengths that fit one SM (N <= 3 * 2^10 or 2^11), the
+// whole reference multiply (decimal.cpp:191-216): pack :102-118, the
+// three-row / direct convolution conv.cpp:149-166, :292-309, crt2 :148-152,
+// recover_digits :154-189 and to_decimal :120-134.
+#include "carry.cuh"
+#include "kernels.cuh"
+#include "ntt_tile.cuh"
+
+namespace dmg {
+
+namespace {
+
+constexpr int NT = 256;
+
+struct SmallField {
+  u64 p0, p1;
+  const TwPair* t0;
+  const TwPair* t1;
+  int nr;  // rows per array
+  __device__ __forceinline__ int q(int w) const { return (w / nr) & 1; }
+  __device__ __forceinline__ u64 p(int w) const { return q(w) ? p1 : p0; }
+  __device__ __forceinline__ const TwPair* tw(int w) const { return q(w) ? t1 : t0; }
+};
+
+template <int LOGC, int THREE, int SQ>
+struct SmallCfg {
+  static constexpr int C = 1 << LOGC;
+  static constexpr int NR = THREE ? 3 : 1;
+  static constexpr int N = NR * C;
+  static constexpr int NOPER = SQ ? 1 : 2;
+  static constexpr int W = 2 * NOPER * NR;          // columns (rows of length C) in the forward tile
+  static constexpr int NARR = 2 * NOPER < 3 ? 3 : 2 * NOPER;  // arrays of N words (3 needed for digits)
+  static constexpr int KL = N + 2;                  // limbs after carry
+  static constexpr int KPT = (KL + NT - 1) / NT;    // limbs per thread
+  static constexpr int TBL = C / 2 > 0 ? C / 2 : 1;
+  static constexpr size_t smem = size_t(NARR) * N * 8 + 4 * size_t(TBL) * 16;
+};
+
+// arrays: 0 = X mod p1, 1 = X mod p2, 2 = Y mod p1, 3 = Y mod p2 (each N words).
+template <int LOGC, int THREE, int SQ>
+__global__ void __launch_bounds__(NT) k_small(SmallArgs a) {
+  using Cfg = SmallCfg<LOGC, THREE, SQ>;
+  constexpr int C = Cfg::C, N = Cfg::N, NR = Cfg::NR;
+  extern __shared__ u64 sm[];
+  TwPair* tf0 = reinterpret_cast<TwPair*>(sm + Cfg::NARR * N);
+  TwPair* tf1 = tf0 + Cfg::TBL;
+  TwPair* ti0 = tf1 + Cfg::TBL;
+  TwPair* ti1 = ti0 + Cfg::TBL;
+  __shared__ unsigned wsm[NT / 32 + 1];
+  __shared__ unsigned long long meta[3];
+  const int tid = threadIdx.x;
+  const unsigned prod = blockIdx.x;
+  const unsigned be = a.base_exp;
+  const u64 p0 = a.p[0], p1 = a.p[1];
+
+  for (int i = tid; i < C / 2; i += NT) {
+    tf0[i] = a.dft_fwd[0][i];
+    tf1[i] = a.dft_fwd[1][i];
+    ti0[i] = a.dft_inv[0][i];
+    ti1[i] = a.dft_inv[1][i];
+  }
+  // ---- pack (decimal.cpp:102-118) ----
+  for (int o = 0; o < Cfg::NOPER; ++o) {
+    const char* d = o ? a.ys + prod * a.y_stride : a.xs + prod * a.x_stride;
+    const unsigned long long nd = o ? a.ny : a.nx;
+    const long long nl = (long long)((nd + be - 1) / be);
+    unsigned bad = 0;
+    for (int t = tid; t < N; t += NT) {
+      u64 limb = 0;
+      if (t < nl) {
+        const long long end = (long long)nd - (long long)t * be;
+        const long long begin = end > (long long)be ? end - (long long)be : 0;
+        for (long long i = begin; i < end; ++i) {
+          const unsigned c = (unsigned char)d[i] - '0';
+          bad |= c > 9;
+          limb = limb * 10 + c;
+        }
+      }
+      sm[(2 * o) * N + t] = limb;
+      sm[(2 * o + 1) * N + t] = limb;
+    }
+    if (bad) atomicOr(a.err, kErrBadDigit);
+    if (tid == 0 && nd > 1 && d[0] == '0') atomicOr(a.err, kErrLeadingZero);
+  }
+  __syncthreads();
+  // ---- forward: radix-3 columns (conv.cpp:109-125), then rows ----
+  if constexpr (THREE) {
+    for (int i = tid; i < 2 * Cfg::NOPER * C; i += NT) {
+      const int arr = i / C, s = i % C, q = arr & 1;
+      const u64 p = q ? p1 : p0;
+      u64* x = sm + arr * N;
+      const TwPair* T = a.r3_fwd[q];
+      const u64 x0 = x[s], x1 = x[C + s], x2 = x[2 * C + s];
+      const u64 t = shoup_mul(mod_sub(x1, x2, p), a.lam[q], p);
+      x[s] = mod_add(mod_add(x0, x1, p), x2, p);
+      x[C + s] = shoup_mul(mod_add(mod_sub(x0, x2, p), t, p), T[C + s], p);
+      x[2 * C + s] = shoup_mul(mod_sub(mod_sub(x0, x1, p), t, p), T[2 * C + s], p);
+    }
+    __syncthreads();
+  }
+  tile_dif<LOGC, Cfg::W>(sm, ContigColumns<LOGC>(), SmallField{p0, p1, tf0, tf1, NR}, tid, NT);
+  // ---- pointwise REDC (conv.cpp:205-208); squaring reuses X ----
+  for (int i = tid; i < 2 * N; i += NT) {
+    const int q = i / N;
+    const u64 v = sm[i];
+    sm[i] = mont_mul(v, SQ ? v : sm[2 * N + i], q ? p1 : p0, a.pp[q]);
+  }
+  __syncthreads();
+  tile_dit<LOGC, 2 * NR>(sm, ContigColumns<LOGC>(), SmallField{p0, p1, ti0, ti1, NR}, tid, NT);
+  if constexpr (THREE) {
+    for (int i = tid; i < 2 * C; i += NT) {
+      const int q = i / C, s = i % C;
+      const u64 p = q ? p1 : p0;
+      u64* x = sm + q * N;
+      const TwPair* T = a.r3_inv[q];
+      const u64 y0 = shoup_mul(x[s], T[s], p);
+      const u64 y1 = shoup_mul(x[C + s], T[C + s], p);
+      const u64 y2 = shoup_mul(x[2 * C + s], T[2 * C + s], p);
+      const u64 t = shoup_mul(mod_sub(y1, y2, p), a.lam_inv[q], p);
+      x[s] = mod_add(mod_add(y0, y1, p), y2, p);
+      x[C + s] = mod_add(mod_sub(y0, y2, p), t, p);
+      x[2 * C + s] = mod_sub(mod_sub(y0, y1, p), t, p);
+    }
+  } else {
+    for (int i = tid; i < 2 * N; i += NT) {
+      const int q = i / N;
+      sm[i] = shoup_mul(sm[i], a.scale[q], q ? p1 : p0);
+    }
+  }
+  __syncthreads();
+  // ---- CRT + digit split (decimal.cpp:148-152, bounds :174-180) ----
+  u64* D0 = sm;
+  u64* D1 = sm + N;
+  u64* D2 = sm + 2 * N;
+  for (int i = tid; i < N; i += NT) {
+    u64 lo, hi, d0, d1, d2;
+    crt2(D0[i], D1[i], p0, p1, a.pp[1], a.r_tilde, lo, hi);
+    if (above_cap(lo, hi, a.coeff_cap_lo, a.coeff_cap_hi)) atomicOr(a.err, kErrCoeffBound);
+    split3(a.div, lo, hi, d0, d1, d2);
+    D0[i] = d0;
+    D1[i] = d1;
+    D2[i] = d2;
+  }
+  __syncthreads();
+  // ---- carry scan over limbs k < N + 2 ----
+  const u64 B = a.div.base;
+  u64 s[Cfg::KPT];
+  unsigned agg = kIdentityMap;
+  const int k0 = tid * Cfg::KPT;
+#pragma unroll
+  for (int j = 0; j < Cfg::KPT; ++j) {
+    const int k = k0 + j;
+    u64 v = 0;
+    if (k < Cfg::KL) {
+      if (k < N) v += D0[k];
+      if (k >= 1 && k - 1 < N) v += D1[k - 1];
+      if (k >= 2 && k - 2 < N) v += D2[k - 2];
+    }
+    s[j] = v;
+    agg = map_compose(limb_map(v, B), agg);
+  }
+  const unsigned pre = block_scan_maps<NT>(agg, wsm, nullptr);  // ends with a barrier
+  unsigned c = map_apply(pre, 0);
+  u64* Z = sm;  // D arrays are dead after the barrier inside the scan
+#pragma unroll
+  for (int j = 0; j < Cfg::KPT; ++j) {
+    const int k = k0 + j;
+    u64 v = s[j] + c;
+    unsigned q = 0;
+    if (v >= B) { v -= B; ++q; }
+    if (v >= B) { v -= B; ++q; }
+    c = q;
+    if (k < Cfg::KL) Z[k] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned long long dsum = a.nx + a.ny;
+    const unsigned long long chi = (dsum - 1) / be, clo = dsum >= 2 ? (dsum - 2) / be : 0;
+    unsigned long long top = 0;
+    u64 z = 0;
+    if (chi < (unsigned long long)Cfg::KL && Z[chi] != 0) {
+      top = chi;
+      z = Z[chi];
+    } else if (clo < (unsigned long long)Cfg::KL && Z[clo] != 0) {
+      top = clo;
+      z = Z[clo];
+    }
+    const unsigned len = decimal_len(z);
+    meta[0] = top;
+    meta[1] = len;
+    meta[2] = len + top * be;
+    a.out_lens[prod] = meta[2];
+  }
+  __syncthreads();
+  const unsigned long long top = meta[0];
+  const unsigned top_len = unsigned(meta[1]);
+  char* out = a.outs + prod * a.out_stride;
+  for (int k = tid; k <= (int)top; k += NT) {
+    const u64 v = Z[k];
+    if ((unsigned long long)k == top)
+      write_digits(out, v, top_len);
+    else
+      write_digits(out + top_len + (top - 1 - k) * be, v, be);
+  }
+}
+
+template <int LOGC, int THREE, int SQ>
+bool run_small(const SmallArgs& a, cudaStream_t st) {
+  using Cfg = SmallCfg<LOGC, THREE, SQ>;
+  static bool done = false;
+  if (!done) {
+    if (cudaFuncSetAttribute((const void*)k_small<LOGC, THREE, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(Cfg::smem)) != cudaSuccess)
+      return false;
+    done = true;
+  }
+  k_small<LOGC, THREE, SQ><<<a.count, NT, Cfg::smem, st>>>(a);
+  return true;
+}
+
+template <int LOGC, int THREE>
+bool run_small_sq(const SmallArgs& a, cudaStream_t st) {
+  return a.squaring ? run_small<LOGC, THREE, 1>(a, st) : run_small<LOGC, THREE, 0>(a, st);
+}
+
+}  // namespace
+
+int small_max_logc(int three) { return three ? 10 : 11; }
+
+bool launch_small(const SmallArgs& a, cudaStream_t st) {
+  if (a.three) {
+    switch (a.logc) {
+      case 0: return run_small_sq<0, 1>(a, st);
+      case 1: return run_small_sq<1, 1>(a, st);
+      case 2: return run_small_sq<2, 1>(a, st);
+      case 3: return run_small_sq<3, 1>(a, st);
+      case 4: return run_small_sq<4, 1>(a, st);
+      case 5: return run_small_sq<5, 1>(a, st);
+      case 6: return run_small_sq<6, 1>(a, st);
+      case 7: return run_small_sq<7, 1>(a, st);
+      case 8: return run_small_sq<8, 1>(a, st);
+      case 9: return run_small_sq<9, 1>(a, st);
+      case 10: return run_small_sq<10, 1>(a, st);
+      default: return false;
+    }
+  }
+  switch (a.logc) {
+    case 1: return run_small_sq<1, 0>(a, st);
+    case 2: return run_small_sq<2, 0>(a, st);
+    case 3: return run_small_sq<3, 0>(a, st);
+    case 4: return run_small_sq<4, 0>(a, st);
+    case 5: return run_small_sq<5, 0>(a, st);
+    case 6: return run_small_sq<6, 0>(a, st);
+    case 7: return run_small_sq<7, 0>(a, st);
+    case 8: return run_small_sq<8, 0>(a, st);
+    case 9: return run_small_sq<9, 0>(a, st);
+    case 10: return run_small_sq<10, 0>(a, st);
+    case 11: return run_small_sq<11, 0>(a, st);
+    default: return false;
+  }
+}
+
+}  // namespace dmg
