@@ -1,0 +1,394 @@
+#!/usr/bin/env python3
+"""Benchmark: decimal digits multiplied per second on B200 (BASELINE.json metric).
+
+Default workload (config 2 of BASELINE.json, the contract's configs[1]): a batch
+of 4096 independent products of two 10,000-digit integers, uniform digits with a
+nonzero leading digit, pair k seeded (2k, 2k+1). One "step" = the whole batch.
+Under torchrun every rank runs its own 4096-product batch (pair seeds offset by
+rank): weak scaling, no data-path collective (the products are independent).
+
+  value : device-resident throughput — digits already in HBM, products written
+          to HBM; CUDA events on the launching stream around each step, L2
+          flushed between steps; max over ranks.
+  e2e   : the same metric through the public host API (decmul_gpu_multiply_batch)
+          from pinned host buffers: H2D of the step's digits and D2H of the
+          products inside the timed region.
+  --impl reference : the reference's own CPU implementation (oracle/_ref, the
+          unmodified reference sources compiled by oracle/Makefile) on all host
+          threads over the same batch; rank 0 only.
+
+Other configs (--config 1|3|4): one product per step (1e6 x 1e6, 1e8 x 1e8,
+2e9 x 1e9 digits), same reporting.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+CONFIGS = {
+    1: dict(workload="single product 1e6 x 1e6 digits (BASELINE config 1)", count=1, nx=10**6, ny=10**6, mode=0),
+    2: dict(workload="batch of 4096 products of 1e4 x 1e4 digits (BASELINE config 2)", count=4096, nx=10**4,
+            ny=10**4, mode=0),
+    3: dict(workload="single product 1e8 x 1e8 digits, uniform (BASELINE config 3)", count=1, nx=10**8, ny=10**8,
+            mode=0),
+    33: dict(workload="single product 1e8 x 1e8 digits, all nines (BASELINE config 3, squaring half)", count=1,
+             nx=10**8, ny=10**8, mode=1),
+    4: dict(workload="single product 2e9 x 1e9 digits (BASELINE config 4)", count=1, nx=2 * 10**9, ny=10**9,
+            mode=0),
+}
+PEAKS_FILE = os.path.join(HERE, "MEASURED_PEAKS.json")
+
+
+def modmuls_per_product(n: int, squaring: bool) -> int:
+    """Algorithmic modular multiplications per product:
+    T(2^k) = (N/2) k (+ N twiddles if six-step), T(3c) = 8c + 3 T(c);
+    M = 2 (3 T(N) + N) + N, squaring 2 (2 T(N) + N) + N."""
+    def T(m: int) -> int:
+        if m % 3 == 0:
+            return 8 * (m // 3) + 3 * T(m // 3)
+        k = m.bit_length() - 1
+        return (m // 2) * k + (m if m > (1 << 15) else 0)
+    return 2 * ((2 if squaring else 3) * T(n) + n) + n
+
+
+def hbm_bytes_per_product(n: int, nx: int, ny: int, one_cta: bool, squaring: bool) -> int:
+    """Algorithmic HBM bytes: 192 N (128 N squaring) for two primes x
+    (2 or 3) transforms x 2 passes x 16 B, plus digit I/O 2 (dx + dy); one-CTA
+    products move only their digits."""
+    io = 2 * (nx + ny)
+    if one_cta:
+        return io
+    return (128 if squaring else 192) * n + io
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the GPU is busy."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.proc = None
+        self.device = device
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = []
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6 and parts[0].isdigit():
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        smax = max(int(r[1]) for r in rows)
+        busy = [int(r[0]) for r in rows if int(r[0]) > 0.5 * smax] or [int(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows)}
+
+
+def load_peaks() -> dict:
+    try:
+        with open(PEAKS_FILE) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+def ncu_traffic(config: int):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    path = os.path.join(HERE, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(str(config), {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------------------------
+# reference arm
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    import oracle
+
+    ref = oracle.ref()
+    from paper_2011_11524_b200 import inputs
+
+    threads = os.cpu_count() or 1
+    count = cfg["count"]
+    xs = [inputs.gen_digits(2 * k, cfg["nx"], cfg["mode"]) for k in range(count)]
+    ys = [inputs.gen_digits(2 * k + 1, cfg["ny"], cfg["mode"]) for k in range(count)]
+    if cfg["mode"] == 1:
+        ys = [None] * count
+
+    def step():
+        if count == 1:
+            ref.multiply(xs[0], ys[0])
+        else:
+            ref.multiply_batch(xs, ys, threads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    digits = (cfg["nx"] + cfg["ny"]) * count
+    value = digits / dt
+    cores = threads if count > 1 else 1
+    line = {
+        "impl": "reference", "metric": "decimal digits multiplied/sec", "value": value, "unit": "digits/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded splitmix64 digits, SURVEY §8(d))",
+        "config": {"workload": cfg["workload"], "products": count, "digits_x": cfg["nx"], "digits_y": cfg["ny"]},
+        "cpu_baseline": {"value": value, "unit": "digits/s", "cores": cores, "kind": "reference",
+                         "sample": f"full workload per step ({count} product(s)) on {cores} host thread(s); "
+                                   "reference proj/src compiled unmodified (-O3 -DNDEBUG)"},
+        "e2e": {"value": value, "unit": "digits/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg) -> dict:
+    """Reference CPU path on a bounded sample of the workload (rank 0, N=1)."""
+    import oracle
+    from paper_2011_11524_b200 import inputs
+
+    ref = oracle.ref()
+    threads = os.cpu_count() or 1
+    if cfg["count"] > 1:
+        n = min(cfg["count"], 2048)
+        xs = [inputs.gen_digits(2 * k, cfg["nx"]) for k in range(n)]
+        ys = [inputs.gen_digits(2 * k + 1, cfg["ny"]) for k in range(n)]
+        ref.multiply_batch(xs[:threads], ys[:threads], threads)  # warm
+        t0 = time.perf_counter()
+        ref.multiply_batch(xs, ys, threads)
+        dt = time.perf_counter() - t0
+        return {"value": n * (cfg["nx"] + cfg["ny"]) / dt, "unit": "digits/s", "cores": threads, "kind": "reference",
+                "sample": f"{n} of the {cfg['count']} products, {threads} threads, one multiply() per product"}
+    nx = min(cfg["nx"], 10**7)
+    ny = min(cfg["ny"], 10**7)
+    x = inputs.gen_digits(0, nx, cfg["mode"])
+    y = None if cfg["mode"] == 1 else inputs.gen_digits(1, ny)
+    ref.multiply(x[: 10**4], None if y is None else y[: 10**4])
+    t0 = time.perf_counter()
+    ref.multiply(x, y)
+    dt = time.perf_counter() - t0
+    return {"value": (nx + ny) / dt, "unit": "digits/s", "cores": 1, "kind": "reference",
+            "sample": f"one {nx} x {ny}-digit product (1 thread; the reference has no intra-product parallelism)"
+                      + ("" if nx == cfg["nx"] else "; smaller than the workload, throughput grows ~1/log N")}
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm
+
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import paper_2011_11524_b200 as dm
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = dm.Context(local_rank)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    count, nx, ny, mode = cfg["count"], cfg["nx"], cfg["ny"], cfg["mode"]
+    squaring = mode == 1
+    plan = ctx.plan(nx, ny)
+    base = rank * count  # weak scaling: each rank its own products
+
+    xs = torch.empty(count * nx, dtype=torch.uint8, device=dev)
+    ys = torch.empty(count * ny, dtype=torch.uint8, device=dev)
+    out_stride = nx + ny
+    outs = torch.empty(count * out_stride, dtype=torch.uint8, device=dev)
+    lens = torch.zeros(count, dtype=torch.int64, device=dev)
+    ctx.generate_digits(xs.data_ptr(), nx, 2 * base, count=count, seed_step=2, mode=mode, stream=sptr)
+    ctx.generate_digits(ys.data_ptr(), ny, 2 * base + 1, count=count, seed_step=2, mode=mode, stream=sptr)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        if count > 1:
+            ctx.multiply_batch_device(count, xs.data_ptr(), nx, ys.data_ptr(), ny, outs.data_ptr(), out_stride,
+                                      lens.data_ptr(), stream=sptr)
+        else:
+            ctx.multiply_device(xs.data_ptr(), nx, xs.data_ptr() if squaring else ys.data_ptr(), ny,
+                                outs.data_ptr(), out_stride, stream=sptr, squaring=squaring, sync=False)
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    step()  # plans and tables (cold)
+    torch.cuda.synchronize()
+    # warmup: W steps, and at least ~1 s of load so the clock sampler sees the busy GPU
+    t_end = time.perf_counter() + 1.0
+    w = 0
+    while w < args.warmup or time.perf_counter() < t_end:
+        step()
+        w += 1
+        if w % 16 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for e0, e1 in evs:
+        flush.zero_()
+        e0.record(stream)
+        step()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    total_ms = sum(step_ms)
+    launches_per_step = ctx.stats()["last_launches"]
+    clk = clocks.stop()
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # correctness spot check of the last step's outputs (product lengths)
+    ok_len = True
+    if count > 1:
+        ln = lens.cpu()
+        ok_len = bool(((ln == nx + ny) | (ln == nx + ny - 1)).all())
+
+    # ---- e2e through the public host API (pinned host buffers) ----
+    e2e = None
+    if count > 1:
+        hx = torch.empty(count * nx, dtype=torch.uint8, pin_memory=True)
+        hy = torch.empty(count * ny, dtype=torch.uint8, pin_memory=True)
+        hx.copy_(xs)
+        hy.copy_(ys)
+        ho = torch.empty(count * out_stride, dtype=torch.uint8, pin_memory=True)
+        hl = torch.zeros(count, dtype=torch.int64)
+        call = lambda: ctx.multiply_batch_ptr(count, hx.data_ptr(), nx, hy.data_ptr(), ny, ho.data_ptr(),  # noqa
+                                              out_stride, hl.data_ptr())
+        h2d = count * (nx + ny)
+        d2h = count * out_stride + count * 8
+    else:
+        hx = torch.empty(nx, dtype=torch.uint8, pin_memory=True)
+        hx.copy_(xs)
+        hy = None
+        if not squaring:
+            hy = torch.empty(ny, dtype=torch.uint8, pin_memory=True)
+            hy.copy_(ys)
+        ho = torch.empty(out_stride, dtype=torch.uint8, pin_memory=True)
+        import ctypes as C
+        olen = C.c_size_t()
+
+        def call():
+            ctx._call("decmul_gpu_multiply", C.c_void_p(hx.data_ptr()), C.c_size_t(nx),
+                      C.c_void_p((hx if squaring else hy).data_ptr()), C.c_size_t(ny), C.c_void_p(ho.data_ptr()),
+                      C.c_size_t(out_stride), C.byref(olen), C.c_uint(0), C.c_int(int(squaring)))
+        h2d = nx + (0 if squaring else ny)
+        d2h = nx + ny
+    call()
+    for _ in range(max(1, args.warmup // 2)):
+        call()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        call()
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    if dist:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    digits_step = count * (nx + ny)
+    e2e = {"value": world * digits_step * args.steps / (e2e_ms * 1e-3), "unit": "digits/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    # ---- roofline: integer pipe (modmuls) and HBM, for the dominant kernel ----
+    rmm = ctx.measure_modmul_rate(0)
+    peaks = load_peaks()
+    n = plan["length"]
+    mm = modmuls_per_product(n, squaring) * count
+    byt = hbm_bytes_per_product(n, nx, ny, plan["one_cta"], squaring) * count
+    step_s = total_ms / args.steps * 1e-3
+    ach_mm = mm / step_s
+    ach_bw = byt / step_s / 1e9
+    roofline = {
+        "bound": "int", "unit": "Gmodmul/s", "achieved": ach_mm / 1e9, "peak": rmm / 1e9, "frac": ach_mm / rmm,
+        "traffic": ncu_traffic(args.config),
+        "algorithmic": {"modmuls_per_step": mm, "hbm_bytes_per_step": byt},
+        "peak_source": "live Shoup modmul micro-kernel on all SMs (decmul_gpu_measure_modmul_rate)",
+        "hbm": {"achieved": ach_bw, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                "frac": ach_bw / peaks.get("hbm_gbs", 6650.0),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("fallback") else "fallback"},
+        "kernel": "k_small (one CTA per product)" if plan["one_cta"] else "multi-pass NTT (k_pass_*)",
+    }
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    value = world * digits_step * args.steps / (total_ms * 1e-3)
+    line = {
+        "metric": "decimal digits multiplied/sec", "value": value, "unit": "digits/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded splitmix64 digits generated in HBM, SURVEY §8(d))",
+        "config": {"workload": cfg["workload"], "products_per_gpu": count, "digits_x": nx, "digits_y": ny,
+                   "base_exp": plan["base_exp"], "transform_length": n, "prime_pair": [plan["p1"], plan["p2"]],
+                   "parallelism": f"batch split, {world} GPU(s)" if count > 1 else "replicas",
+                   "l2": "flushed (512 MiB write) before every timed step; per-step CUDA events"},
+        "e2e": e2e, "roofline": roofline, "gpu_launches": launches_per_step * args.steps, "clocks": clk,
+        "outputs_ok": ok_len,
+    }
+    if world == 1:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.impl == "reference" else 1)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+    else:
+        run_ours(args, cfg, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

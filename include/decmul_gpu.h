@@ -113,7 +113,16 @@ int decmul_gpu_transpose_square_sub(decmul_gpu_ctx* ctx, uint64_t* a, size_t n, 
 int decmul_gpu_transpose_n_x_2n(decmul_gpu_ctx* ctx, uint64_t* a, size_t n);
 int decmul_gpu_transpose_2n_x_n(decmul_gpu_ctx* ctx, uint64_t* a, size_t n);
 
+/* ---- workload generation (not in the reference: its bench_mul draws digits on the host,
+ * bench.cpp:107-116). Seeded counter-based splitmix64 digits written in place in HBM:
+ * operand j (seed seed0 + j * seed_step) gets n digits at d_out + j * stride; mode 0 uniform
+ * with a nonzero leading digit, mode 1 all nines. Bit-identical to the host generator. ---- */
+int decmul_gpu_generate_digits(decmul_gpu_ctx* ctx, uint64_t seed0, uint64_t seed_step, size_t count, size_t n,
+                               size_t stride, int mode, char* d_out, void* stream);
+
 /* ---- introspection ---- */
+/* Integer-pipe roofline denominator: measured modmul/s on this GPU (variant 0 Shoup, 1 Montgomery). */
+int decmul_gpu_measure_modmul_rate(decmul_gpu_ctx* ctx, int variant, double* modmul_per_s);
 typedef struct {
   int last_launches;       /* kernels launched by the last product */
   size_t table_bytes;      /* device bytes held by cached twiddle tables */

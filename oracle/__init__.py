@@ -252,6 +252,20 @@ class Port(_Lib):
         self.fn("gen_digits", None)(C.c_uint64(seed), C.c_int(mode), C.c_size_t(n), buf)
         return buf.raw[:n]
 
+    def dif_forward_root(self, p, a, root):
+        a = _u64(a).copy()
+        self.check(self.fn("dif_forward_root")(C.c_uint64(p), C.c_size_t(a.size), C.c_uint64(root), _ptr(a)))
+        return a
+
+    def ntt_plan_root(self, p, n, root):
+        fwd = np.zeros(max(n - 1, 1), np.uint64)
+        inv = np.zeros(max(n - 1, 1), np.uint64)
+        self.check(self.fn("ntt_plan_root")(C.c_uint64(p), C.c_size_t(n), C.c_uint64(root), _ptr(fwd), _ptr(inv)))
+        return fwd[: n - 1], inv[: n - 1]
+
+    def residue_mod(self, s: bytes, q: int) -> int:
+        return self.fn("residue_mod", C.c_uint64)(s, C.c_size_t(len(s)), C.c_uint64(q))
+
     def gen_residues(self, seed: int, n: int, p: int):
         out = np.zeros(n, np.uint64)
         self.fn("gen_residues", None)(C.c_uint64(seed), C.c_size_t(n), C.c_uint64(p), _ptr(out))

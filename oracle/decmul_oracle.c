@@ -49,9 +49,8 @@ static int make_ctx(u64 p, mctx* c) {
 /* mont_reduce, montgomery.hpp:26-34: a < p 2^64 -> a R^-1 mod p. */
 static u64 mreduce(const mctx* c, u128 a) {
   u64 m = (u64)a * c->pp;
-  u128 t = a + (u128)m * c->p; /* may wrap past 2^128 only if a >= p 2^64 */
+  u128 t = a + (u128)m * c->p; /* < 2^128 for legal inputs a < p 2^64; low word is 0 */
   u64 hi = (u64)(t >> 64);
-  if (t < a) hi += 0; /* unreachable for legal inputs; kept explicit */
   return hi >= c->p ? hi - c->p : hi;
 }
 static u64 redc(const mctx* c, u64 x, u64 y) { return mreduce(c, (u128)x * y); }   /* :36-39 */
@@ -843,6 +842,27 @@ int or_schoolbook_multiply(const char* x, size_t nx, const char* y, size_t ny, c
   return rc;
 }
 
+/* ---------------- size-independent fingerprints (SURVEY §8(c) fast checks) ---------------- */
+
+/* The decimal value of s[0..n) modulo q (Horner over 18-digit chunks). Used to
+ * check z == x y (mod q) for products too large for the quadratic oracle. */
+u64 or_residue_mod(const char* s, size_t n, u64 q) {
+  u64 acc = 0;
+  size_t i = 0, head = n % 18;
+  const u64 p18 = 1000000000000000000ull % q;
+  if (head) {
+    u64 v = 0;
+    for (; i < head; ++i) v = v * 10 + (u64)(s[i] - '0');
+    acc = v % q;
+  }
+  for (; i < n; i += 18) {
+    u64 v = 0;
+    for (size_t j = 0; j < 18; ++j) v = v * 10 + (u64)(s[i + j] - '0');
+    acc = (u64)(((u128)acc * p18 + v % q) % q);
+  }
+  return acc;
+}
+
 /* ---------------- shared seeded generator ---------------- */
 
 static u64 sm_mix(u64 z) { /* splitmix64 finalizer, reference bench.cpp:40-45 */
@@ -862,4 +882,28 @@ void or_gen_digits(u64 seed, int mode, size_t n, char* out) {
 void or_gen_residues(u64 seed, size_t n, u64 p, u64* out) {
   u64 key = sm_mix(seed + GOLDEN);
   for (size_t i = 0; i < n; ++i) out[i] = sm_mix(key + (u64)(i + 1) * GOLDEN) % p;
+}
+
+/* build_plan_with_root (ntt.cpp:88-112) + dif_impl (ntt.cpp:29-50) for an explicit root:
+ * the reference's hand examples use p = 17, n = 4, root = 4 (test_ntt.cpp:23-37, :81-88). */
+int or_ntt_plan_root(u64 p, size_t n, u64 root, u64* fwd, u64* inv) {
+  mctx c;
+  nttplan pl;
+  int rc = make_ctx(p, &c);
+  if (rc || (rc = ntt_plan_root(&c, n, root, &pl))) return rc;
+  if (n > 1) {
+    memcpy(fwd, pl.fwd, (n - 1) * sizeof(u64));
+    memcpy(inv, pl.inv, (n - 1) * sizeof(u64));
+  }
+  ntt_free(&pl);
+  return 0;
+}
+int or_dif_forward_root(u64 p, size_t n, u64 root, u64* a) {
+  mctx c;
+  nttplan pl;
+  int rc = make_ctx(p, &c);
+  if (rc || (rc = ntt_plan_root(&c, n, root, &pl))) return rc;
+  dif(&pl, a);
+  ntt_free(&pl);
+  return 0;
 }

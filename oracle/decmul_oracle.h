@@ -5,7 +5,8 @@
  * and bench.py's cpu_baseline leg may load it, and only as the checker.
  * Parity pinning: tests/test_oracle.py checks every function here against the
  * reference's own known-answer tests (copied as numbers into
- * tests/golden/kat.json) and against the compiled reference (oracle/_ref).
+ * tests/golden/golden.json, "kat") and against the compiled reference
+ * (oracle/_ref, and its outputs frozen in golden.json "ref").
  *
  * Return codes: 0 ok, 1 invalid argument, 2 operand too large,
  * 3 runtime error (bound violation), 4 logic error, 6 buffer too small.
@@ -40,6 +41,8 @@ int or_ntt_plan(uint64_t p, size_t n, uint64_t* fwd, uint64_t* inv, uint64_t* ro
 int or_dif_forward(uint64_t p, size_t n, uint64_t* a);
 int or_dit_inverse(uint64_t p, size_t n, uint64_t* a);
 void or_bit_rev_permute(uint64_t* a, size_t n);
+int or_ntt_plan_root(uint64_t p, size_t n, uint64_t root, uint64_t* fwd, uint64_t* inv);
+int or_dif_forward_root(uint64_t p, size_t n, uint64_t root, uint64_t* a);
 
 /* Transposition (transpose.cpp). */
 void or_transpose_square_sub(uint64_t* a, size_t n, size_t stride);
@@ -73,6 +76,9 @@ int or_naive_dft(const uint64_t* x, size_t n, uint64_t root, uint64_t p, uint64_
 int or_naive_convolve(const uint64_t* x, const uint64_t* y, size_t n, uint64_t p, uint64_t* out);
 int or_schoolbook_multiply(const char* x, size_t nx, const char* y, size_t ny, char* out, size_t cap,
                            size_t* out_len);
+
+/* Decimal value of s[0..n) mod q (fingerprint for products beyond the quadratic oracle). */
+uint64_t or_residue_mod(const char* s, size_t n, uint64_t q);
 
 /* Shared seeded digit generator; mode 0 uniform, 1 all nines. */
 void or_gen_digits(uint64_t seed, int mode, size_t n, char* out);

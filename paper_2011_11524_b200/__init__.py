@@ -53,7 +53,8 @@ EXPORTED_SYMBOLS = [
     "decmul_gpu_multiply_batch_device", "decmul_gpu_convolve_mod_p", "decmul_gpu_forward_transform",
     "decmul_gpu_inverse_transform", "decmul_gpu_pointwise_product", "decmul_gpu_pack",
     "decmul_gpu_recover_decimal", "decmul_gpu_transpose_square_sub", "decmul_gpu_transpose_n_x_2n",
-    "decmul_gpu_transpose_2n_x_n", "decmul_gpu_get_stats",
+    "decmul_gpu_transpose_2n_x_n", "decmul_gpu_generate_digits", "decmul_gpu_measure_modmul_rate",
+    "decmul_gpu_get_stats",
 ]
 
 
@@ -269,6 +270,26 @@ class Context:
                    C.c_size_t(nx if x_stride is None else x_stride), C.c_size_t(nx), C.c_void_p(d_ys),
                    C.c_size_t(ny if y_stride is None else y_stride), C.c_size_t(ny), C.c_void_p(d_outs),
                    C.c_size_t(out_stride), C.c_void_p(d_lens), C.c_void_p(stream))
+
+    def multiply_batch_ptr(self, count: int, xs_ptr: int, nx: int, ys_ptr: int, ny: int, outs_ptr: int,
+                           out_stride: int, lens_ptr: int) -> None:
+        """Uniform-size batch from caller-owned HOST buffers given as raw pointers (pinned
+        memory from torch, say); lens_ptr receives size_t lengths."""
+        self._call("decmul_gpu_multiply_batch", C.c_size_t(count), C.c_void_p(xs_ptr), C.c_size_t(nx),
+                   C.c_size_t(nx), C.c_void_p(ys_ptr), C.c_size_t(ny), C.c_size_t(ny), C.c_void_p(outs_ptr),
+                   C.c_size_t(out_stride), C.c_void_p(lens_ptr))
+
+    def generate_digits(self, d_out: int, n: int, seed0: int, count: int = 1, seed_step: int = 1,
+                        stride: int | None = None, mode: int = 0, stream: int = 0) -> None:
+        """Seeded digits written in place on the device (same stream as inputs.gen_digits)."""
+        self._call("decmul_gpu_generate_digits", C.c_uint64(seed0), C.c_uint64(seed_step), C.c_size_t(count),
+                   C.c_size_t(n), C.c_size_t(n if stride is None else stride), C.c_int(mode), C.c_void_p(d_out),
+                   C.c_void_p(stream))
+
+    def measure_modmul_rate(self, variant: int = 0) -> float:
+        r = C.c_double()
+        self._call("decmul_gpu_measure_modmul_rate", C.c_int(variant), C.byref(r))
+        return r.value
 
     # ---- parity hooks ----
     def convolve_mod_p(self, p: int, n: int, x, y=None) -> np.ndarray:

@@ -208,6 +208,22 @@ int decmul_gpu_transpose_2n_x_n(decmul_gpu_ctx* ctx, uint64_t* a, size_t n) {
   LOCKED(ctx, ctx->eng->transpose(2, reinterpret_cast<dmg::u64*>(a), n, n));
 }
 
+int decmul_gpu_generate_digits(decmul_gpu_ctx* ctx, uint64_t seed0, uint64_t seed_step, size_t count, size_t n,
+                               size_t stride, int mode, char* d_out, void* stream) {
+  LOCKED(ctx, {
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->eng->stream();
+    dmg::launch_generate(seed0, seed_step, count, n, stride, mode, d_out, st);
+    dmg::cuda_check(cudaGetLastError(), "generate");
+  });
+}
+
+int decmul_gpu_measure_modmul_rate(decmul_gpu_ctx* ctx, int variant, double* rate) {
+  LOCKED(ctx, {
+    *rate = dmg::measure_modmul_rate(variant, ctx->eng->stream());
+    if (*rate <= 0) throw dmg::CudaError("modmul rate measurement failed");
+  });
+}
+
 int decmul_gpu_get_stats(decmul_gpu_ctx* ctx, decmul_gpu_stats* out) {
   LOCKED(ctx, {
     out->last_launches = ctx->eng->last_launches();

@@ -12,6 +12,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -161,7 +162,12 @@ struct PairChoice {
 
 // The reference pair wherever it can hold the product (bit-comparable spectra);
 // otherwise the larger-2-adic pair from the reference's own prime search.
+// DECMUL_FORCE_LARGE_PAIR=1 (test knob) selects the large pair at any size so its
+// code path is parity-tested on small operands.
 inline PairChoice choose_pair(std::size_t dx, std::size_t dy, unsigned forced, bool allow_large) {
+  const char* force = std::getenv("DECMUL_FORCE_LARGE_PAIR");
+  if (allow_large && force && force[0] == '1')
+    return {kQ1, kQ2, select_base_and_length(dx, dy, kQ1, kQ2, forced), true};
   try {
     return {kP1, kP2, select_base_and_length(dx, dy, kP1, kP2, forced), false};
   } catch (const OperandTooLarge&) {

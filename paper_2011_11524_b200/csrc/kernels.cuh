@@ -108,6 +108,12 @@ struct SmallArgs {
 bool launch_small(const SmallArgs& a, cudaStream_t st);
 int small_max_logc(int three);
 
+// Seeded digit generator (gen.cu): operand j = seed0 + j * seed_step, n digits at out + j * stride.
+void launch_generate(u64 seed0, u64 seed_step, unsigned long long count, unsigned long long n,
+                     unsigned long long stride, int mode, char* out, cudaStream_t st);
+// Integer-pipe roofline denominator (diag.cu): modmul/s, variant 0 Shoup, 1 Montgomery.
+double measure_modmul_rate(int variant, cudaStream_t st);
+
 // In-place transposes (reference transpose.cpp) on device memory.
 void launch_transpose_square_sub(u64* a, unsigned long long n, unsigned long long stride, cudaStream_t st);
 // rho per row of 2n words (n rows), through scratch (>= 2 n^2 words); inverse = unpermute_rho.

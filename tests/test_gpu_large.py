@@ -1,0 +1,102 @@
+"""GPU parity at BASELINE.json's full sizes through size-independent properties:
+the reference's own 1e6-digit bench product (golden SHA-256), the all-nines closed
+form (10^n - 1)^2 (reference oracle.cpp:171-180), residue fingerprints
+z == x y (mod q) for 61-bit primes q, the exact low window
+z mod 10^K == (x mod 10^K)(y mod 10^K) mod 10^K, and the digit count."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2011_11524_b200 as dm
+
+pytestmark = pytest.mark.gpu
+
+FINGERPRINT_PRIMES = (2305843009213693951, 2305843009213693921, 1152921504606846883, 4611686018427387847)
+
+
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+def test_config1_reference_bench_stream(gpu, ref, golden):
+    g = golden["ref"]["bench_mul_stream_seed42"]["1000000"]
+    x, y = ref.bench_inputs(10**6, 42)
+    assert sha(x) == g["x_sha"]
+    z = gpu.multiply_text(x, y)
+    assert len(z) == g["len"] and sha(z) == g["z_sha"]
+
+
+def _device_product(gpu, nx, ny, seed_x, seed_y, mode=0):
+    import torch
+
+    x = torch.empty(nx, dtype=torch.uint8, device="cuda")
+    gpu.generate_digits(x.data_ptr(), nx, seed_x, mode=mode)
+    if mode == 1 and nx == ny:
+        y = x
+    else:
+        y = torch.empty(ny, dtype=torch.uint8, device="cuda")
+        gpu.generate_digits(y.data_ptr(), ny, seed_y, mode=mode)
+    out = torch.empty(nx + ny, dtype=torch.uint8, device="cuda")
+    ln = gpu.multiply_device(x.data_ptr(), nx, y.data_ptr(), ny, out.data_ptr(), nx + ny, squaring=y is x)
+    return x, y, out, ln
+
+
+def _check_fingerprints(port, ref, hx, hy, hz, k=20000):
+    for q in FINGERPRINT_PRIMES:
+        assert port.residue_mod(hz, q) == port.residue_mod(hx, q) * port.residue_mod(hy, q) % q
+    lo = ref.multiply(hx[-k:].lstrip(b"0") or b"0", hy[-k:].lstrip(b"0") or b"0")
+    assert hz[-k:] == lo[-k:].rjust(k, b"0")
+
+
+def test_config3_all_nines_closed_form(gpu):
+    n = 10**8
+    x, y, out, ln = _device_product(gpu, n, n, 0, 0, mode=1)
+    assert ln == 2 * n
+    z = out[:ln].cpu().numpy()
+    assert (z[: n - 1] == ord("9")).all() and z[n - 1] == ord("8")
+    assert (z[n: 2 * n - 1] == ord("0")).all() and z[2 * n - 1] == ord("1")
+
+
+def test_config3_uniform_fingerprints(gpu, port, ref):
+    n = 10**8
+    x, y, out, ln = _device_product(gpu, n, n, 0, 1)
+    assert ln in (2 * n - 1, 2 * n)
+    hx, hy, hz = bytes(x.cpu().numpy()), bytes(y.cpu().numpy()), bytes(out[:ln].cpu().numpy())
+    assert hz[:1] != b"0"
+    _check_fingerprints(port, ref, hx, hy, hz)
+
+
+def test_config3_uniform_times_nines(gpu, port, ref):
+    """Non-squaring worst case: one operand all nines."""
+    import torch
+
+    n = 3 * 10**7
+    x = torch.empty(n, dtype=torch.uint8, device="cuda")
+    y = torch.empty(n, dtype=torch.uint8, device="cuda")
+    gpu.generate_digits(x.data_ptr(), n, 5)
+    gpu.generate_digits(y.data_ptr(), n, 0, mode=1)
+    out = torch.empty(2 * n, dtype=torch.uint8, device="cuda")
+    ln = gpu.multiply_device(x.data_ptr(), n, y.data_ptr(), n, out.data_ptr(), 2 * n)
+    hx, hy, hz = bytes(x.cpu().numpy()), bytes(y.cpu().numpy()), bytes(out[:ln].cpu().numpy())
+    _check_fingerprints(port, ref, hx, hy, hz)
+
+
+def test_lambda16_cap_all_nines(gpu):
+    """All nines at the largest lambda = 16 size (reference acceptance.cpp:275-321, 850705 limbs)."""
+    n = 850705 * 16
+    x, y, out, ln = _device_product(gpu, n, n, 0, 0, mode=1)
+    assert gpu.plan(n, n)["base_exp"] == 16
+    z = out[:ln].cpu().numpy()
+    assert ln == 2 * n and (z[: n - 1] == 57).all() and z[n - 1] == 56 and (z[n:-1] == 48).all() and z[-1] == 49
+
+
+def test_config4_unbalanced_fingerprints(gpu, port, ref):
+    """2e9 x 1e9 digits: beyond the reference's 3*2^24 cap (large prime pair, N = 3*2^26)."""
+    nx, ny = 2 * 10**9, 10**9
+    plan = gpu.plan(nx, ny)
+    assert plan["large_pair"] and plan["length"] == 3 << 26 and plan["base_exp"] == 15
+    x, y, out, ln = _device_product(gpu, nx, ny, 40, 41)
+    assert ln in (nx + ny - 1, nx + ny)
+    hx, hy, hz = bytes(x.cpu().numpy()), bytes(y.cpu().numpy()), bytes(out[:ln].cpu().numpy())
+    _check_fingerprints(port, ref, hx, hy, hz, k=10000)

@@ -1,0 +1,219 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden outputs. Bit-exact everywhere (integer arithmetic)."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import paper_2011_11524_b200 as dm
+from paper_2011_11524_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+P1, P2 = dm.P1, dm.P2
+
+
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+def nines_square(n):
+    return b"9" * (n - 1) + b"8" + b"0" * (n - 1) + b"1"
+
+
+def test_multiply_known_answers(gpu, golden):
+    for a, b, z in golden["kat"]["multiply"]:
+        assert dm.multiply(dm.DecimalNumber.parse(a), dm.DecimalNumber.parse(b), ctx=gpu).text() == z.encode()
+    for n in (1, 2, 17, 18, 100, 1000):
+        x = dm.DecimalNumber.parse(b"9" * n)
+        assert dm.multiply(x, x, ctx=gpu).text() == nines_square(n)
+
+
+def test_products_match_reference_hashes(gpu, golden):
+    for d, g in golden["ref"]["products_splitmix"].items():
+        z = gpu.multiply_text(inputs.gen_digits(g["seed_x"], g["nx"]), inputs.gen_digits(g["seed_y"], g["ny"]))
+        assert len(z) == g["len"] and sha(z) == g["sha"], d
+
+
+def test_random_products_vs_schoolbook(gpu, port):
+    rng = np.random.default_rng(127)
+    for _ in range(200):
+        nx, ny = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+        x = inputs.gen_digits(int(rng.integers(1 << 40)), nx)
+        y = inputs.gen_digits(int(rng.integers(1 << 40)), ny)
+        assert gpu.multiply_text(x, y) == port.schoolbook_multiply(x, y)
+    for d in (997, 2000, 5000):
+        x, y = inputs.gen_digits(d, d), inputs.gen_digits(d + 1, d - 1)
+        assert gpu.multiply_text(x, y) == port.schoolbook_multiply(x, y)
+
+
+@pytest.mark.parametrize("digits", [33, 34, 35, 50, 51, 67, 68, 101, 102])
+def test_padding_neutrality(gpu, port, digits):
+    x, y = inputs.gen_digits(digits, digits), inputs.gen_digits(digits + 99, digits)
+    assert gpu.multiply_text(x, y) == port.schoolbook_multiply(x, y)
+
+
+# digit counts whose transform lengths cross the one-CTA / multi-pass boundary and
+# every pass-count regime: N = 3072 (one CTA) ... 3 * 2^15, 2^17
+@pytest.mark.parametrize("nx,ny", [(20000, 20000), (26000, 20000), (40000, 30000), (50000, 50000),
+                                   (70000, 60000), (100000, 100000), (200000, 150000), (300000, 300000),
+                                   (1000000, 999999), (1, 1000000), (17, 2000000), (123457, 1)])
+def test_sizes_across_engines_vs_reference(gpu, ref, nx, ny):
+    x, y = inputs.gen_digits(nx + 5, nx), inputs.gen_digits(ny + 6, ny)
+    assert gpu.multiply_text(x, y) == ref.multiply(x, y)
+
+
+def test_squaring_paths(gpu, ref):
+    for d in (1, 40, 1234, 30000, 200000):
+        s = inputs.gen_digits(d * 3, d)
+        want = ref.multiply(s, None)
+        assert gpu.multiply_text(s, None) == want  # aliased (&x == &y)
+        assert gpu.multiply_text(s, bytes(s)) == want  # equal text, distinct buffers
+
+
+def test_every_forced_base(gpu, port):
+    x, y = inputs.gen_digits(1, 4211), inputs.gen_digits(2, 3999)
+    want = port.schoolbook_multiply(x, y)
+    for be in (0, 14, 15, 16, 17):
+        assert gpu.multiply_text(x, y, forced_base_exp=be) == want
+
+
+def test_large_prime_pair_path(gpu, ref):
+    """The pair used beyond the reference's 3*2^24 cap, exercised at small sizes."""
+    os.environ["DECMUL_FORCE_LARGE_PAIR"] = "1"
+    try:
+        for nx, ny in ((10000, 10000), (70000, 50000), (400000, 300000)):
+            assert gpu.plan(nx, ny)["p1"] == dm.Q1
+            x, y = inputs.gen_digits(nx, nx), inputs.gen_digits(ny, ny)
+            assert gpu.multiply_text(x, y) == ref.multiply(x, y)
+    finally:
+        del os.environ["DECMUL_FORCE_LARGE_PAIR"]
+    assert gpu.plan(10000, 10000)["p1"] == P1
+
+
+def test_errors_match_reference_types(gpu):
+    with pytest.raises(ValueError, match="non-digit"):
+        gpu.multiply_text(b"12a4" * 1000, b"5" * 100)
+    with pytest.raises(ValueError, match="leading zero"):
+        gpu.multiply_text(b"0123" * 1000, b"5" * 100)
+    with pytest.raises(ValueError, match="empty"):
+        gpu.multiply_text(b"", b"5")
+    with pytest.raises(dm.OperandTooLarge):
+        gpu.multiply_text(b"9" * 3000000, b"9" * 3000000, forced_base_exp=17)
+    assert gpu.multiply_text(b"0", b"123") == b"0"
+    # the context stays usable after errors
+    assert gpu.multiply_text(b"12", b"34") == b"408"
+
+
+def test_batch_api_matches_reference(gpu, golden):
+    xs = b"".join(inputs.gen_digits(2 * k, 10000) for k in range(64))
+    ys = b"".join(inputs.gen_digits(2 * k + 1, 10000) for k in range(64))
+    outs = gpu.multiply_batch(xs, ys, 64, 10000, 10000)
+    assert [sha(z) for z in outs] == golden["ref"]["config2_first64_sha"]
+
+
+def test_batch_uneven_sizes_and_pass_engine(gpu, ref):
+    for nx, ny, count in ((1, 1, 5), (35, 17, 33), (3000, 1000, 40), (60000, 40000, 3)):
+        xs = [inputs.gen_digits(7 * k + nx, nx) for k in range(count)]
+        ys = [inputs.gen_digits(7 * k + ny + 1, ny) for k in range(count)]
+        outs = gpu.multiply_batch(b"".join(xs), b"".join(ys), count, nx, ny)
+        assert outs == [ref.multiply(a, b) for a, b in zip(xs, ys)]
+
+
+def test_convolution_hook_vs_reference(gpu, ref, golden):
+    for key, want in golden["ref"]["conv"].items():
+        p, n = map(int, key.split(":"))
+        x = ref.random_residues(want["seed_x"], n, p)
+        y = ref.random_residues(want["seed_y"], n, p)
+        got = gpu.convolve_mod_p(p, n, x, y)
+        fwd = gpu.forward_transform(p, x)
+        if "conv" in want:
+            assert [int(v) for v in got] == want["conv"], key
+            assert [int(v) for v in fwd] == want["fwd"], key
+        else:
+            assert sha(got.tobytes()) == want["conv_sha"], key
+            assert sha(fwd.tobytes()) == want["fwd_sha"], key
+        assert np.array_equal(gpu.inverse_transform(p, fwd), x), key
+
+
+def test_convolution_hook_shorter_inputs_and_squaring(gpu, port):
+    for p in (P1, P2, dm.Q1, dm.Q2):
+        for n in (6, 64, 1536, 1 << 14, 3 << 13):
+            x = port.gen_residues(n, n // 3, p)
+            y = port.gen_residues(n + 1, n // 2, p)
+            xp = np.zeros(n, np.uint64)
+            yp = np.zeros(n, np.uint64)
+            xp[: x.size] = x
+            yp[: y.size] = y
+            want = port.convolve_mod_p(p, n, xp, yp)
+            assert np.array_equal(gpu.convolve_mod_p(p, n, x, y), want)
+            assert np.array_equal(gpu.convolve_mod_p(p, n, xp), port.convolve_mod_p(p, n, xp, None))
+    with pytest.raises(ValueError):
+        gpu.convolve_mod_p(P1, 8, np.ones(9, np.uint64), np.ones(8, np.uint64))
+    with pytest.raises(ValueError):
+        gpu.convolve_mod_p(P1, 5, np.ones(5, np.uint64), np.ones(5, np.uint64))
+
+
+def test_pointwise_and_pack_hooks(gpu, port):
+    for p in (P1, P2):
+        a, b = port.gen_residues(1, 1000, p), port.gen_residues(2, 1000, p)
+        assert np.array_equal(gpu.pointwise_product(p, a, b), port.pointwise_product(p, a, b))
+        assert np.array_equal(gpu.pointwise_product(p, a), port.pointwise_product(p, a, None))
+    for d in (1, 14, 15, 16, 17, 18, 1000, 123457):
+        s = inputs.gen_digits(d, d)
+        for be in (14, 15, 16, 17):
+            assert np.array_equal(gpu.pack(s, be), port.pack(s, be))
+    with pytest.raises(ValueError):
+        gpu.pack(b"1", 18)
+
+
+def test_recover_decimal_hook(gpu, port):
+    """CRT + carry + formatting on the device, from exact convolution residues."""
+    for nx, ny in ((100, 90), (5000, 5000), (40000, 35000)):
+        x, y = inputs.gen_digits(nx, nx), inputs.gen_digits(ny, ny)
+        be, n = port.select_base_and_length(nx, ny)
+        lx, ly = port.pack(x, be), port.pack(y, be)
+        r1 = port.convolve_mod_p(P1, n, lx, ly)
+        r2 = port.convolve_mod_p(P2, n, lx, ly)
+        z = gpu.recover_decimal(r1, r2, P1, P2, be, min(lx.size, ly.size), nx + ny)
+        assert z == port.multiply(x, y)
+    # corrupted residues exceed the analytic bound -> runtime_error (decimal.cpp:174-176)
+    bad = np.full(64, P1 - 1, dtype=np.uint64)
+    with pytest.raises(RuntimeError, match="analytic bound"):
+        gpu.recover_decimal(bad, np.full(64, P2 - 5, dtype=np.uint64), P1, P2, 17, 3, 100)
+
+
+def test_transpose_hooks(gpu, port, golden):
+    a, want = golden["kat"]["transpose_n_x_2n_2"]
+    assert list(gpu.transpose_n_x_2n(a, 2)) == want
+    a, want = golden["kat"]["transpose_2n_x_n_2"]
+    assert list(gpu.transpose_2n_x_n(a, 2)) == want
+    rng = np.random.default_rng(29)
+    for n in list(range(1, 66, 4)) + [256]:
+        m = rng.integers(0, 2**63, 2 * n * n, dtype=np.uint64)
+        assert np.array_equal(gpu.transpose_n_x_2n(m, n), port.transpose_n_x_2n(m, n))
+        assert np.array_equal(gpu.transpose_2n_x_n(m, n), port.transpose_2n_x_n(m, n))
+    for n, stride in ((3, 3), (31, 31), (33, 64), (100, 100), (128, 200)):
+        m = rng.integers(0, 2**63, n * stride, dtype=np.uint64)
+        assert np.array_equal(gpu.transpose_square_sub(m, n, stride), port.transpose_square_sub(m, n, stride))
+
+
+def test_device_api_and_generator(gpu, port):
+    import torch
+
+    n = 250000
+    x = torch.empty(n, dtype=torch.uint8, device="cuda")
+    y = torch.empty(n - 7, dtype=torch.uint8, device="cuda")
+    out = torch.empty(2 * n, dtype=torch.uint8, device="cuda")
+    gpu.generate_digits(x.data_ptr(), n, 1234)
+    gpu.generate_digits(y.data_ptr(), n - 7, 99)
+    torch.cuda.synchronize()
+    hx, hy = bytes(x.cpu().numpy()), bytes(y.cpu().numpy())
+    assert hx == inputs.gen_digits(1234, n) and hy == inputs.gen_digits(99, n - 7)
+    ln = gpu.multiply_device(x.data_ptr(), n, y.data_ptr(), n - 7, out.data_ptr(), 2 * n)
+    assert bytes(out[:ln].cpu().numpy()) == port.multiply(hx, hy)
+    # asynchronous form on torch's stream
+    s = torch.cuda.current_stream().cuda_stream
+    gpu.multiply_device(x.data_ptr(), n, y.data_ptr(), n - 7, out.data_ptr(), 2 * n, stream=s, sync=False)
+    torch.cuda.synchronize()
+    assert gpu.result_length() == ln
