@@ -216,8 +216,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         import torch.distributed as dist  # noqa: F811
         dist.init_process_group("nccl", device_id=dev)
     ctx = dm.Context(local_rank)
-    stream = torch.cuda.current_stream(dev)
+    # a real (non-NULL) stream: the library launches on the stream it is given, and the
+    # CUDA events below are recorded on that same stream
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
+    assert sptr != 0
     count, nx, ny, mode = cfg["count"], cfg["nx"], cfg["ny"], cfg["mode"]
     squaring = mode == 1
     plan = ctx.plan(nx, ny)

@@ -123,9 +123,14 @@ __global__ void __launch_bounds__(1024) k_carry_scan(CarryArgs a, unsigned nchun
 }
 
 // Phase 3: apply carries and print each limb at its place in the output string.
+// The chunk's digits are staged in shared memory and stored as 16-byte vectors.
 __global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
   __shared__ unsigned wsm[NT / 32 + 1];
-  const unsigned long long k0 = (unsigned long long)blockIdx.x * CH + threadIdx.x * PER;
+  __shared__ __align__(16) char buf[CH * 17 + 32];
+  const unsigned long long cbase = (unsigned long long)blockIdx.x * CH;
+  const unsigned long long top = a.meta[0];
+  if (cbase > top) return;  // nothing of this chunk is printed (uniform per block)
+  const unsigned long long k0 = cbase + threadIdx.x * PER;
   const unsigned long long K = a.n + 2;
   const u64 B = a.div.base;
   u64 s[PER];
@@ -138,9 +143,13 @@ __global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
   }
   const unsigned pre = block_scan_maps<NT>(agg, wsm, nullptr);
   unsigned c = map_apply(pre, a.maps[blockIdx.x]);
-  const unsigned long long top = a.meta[0];
   const unsigned top_len = unsigned(a.meta[1]);
   const unsigned be = a.base_exp;
+  const unsigned long long khi = cbase + CH - 1 < top ? cbase + CH - 1 : top;
+  const unsigned long long start = limb_pos(khi, top, top_len, be);
+  const unsigned long long end = limb_pos(cbase, top, top_len, be) + (cbase == top ? top_len : be);
+  char* g = a.out + start;
+  char* sb = buf + (reinterpret_cast<unsigned long long>(g) & 15);
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const unsigned long long k = k0 + j;
@@ -150,11 +159,10 @@ __global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
     if (v >= B) { v -= B; ++q; }
     c = q;
     if (k > top) continue;
-    if (k == top)
-      write_digits(a.out, v, top_len);
-    else
-      write_digits(a.out + top_len + (top - 1 - k) * be, v, be);
+    write_digits(sb + (limb_pos(k, top, top_len, be) - start), v, k == top ? top_len : be);
   }
+  __syncthreads();
+  cta_store_bytes(g, sb, unsigned(end - start), threadIdx.x, NT);
 }
 
 }  // namespace

@@ -78,6 +78,26 @@ __device__ __forceinline__ void write_digits(char* out, u64 v, unsigned len) {
   }
 }
 
+// Copy len bytes from shared s to global g with 16-byte stores in the aligned middle.
+// Requires (g mod 16) == (s mod 16): callers place the staged text at that offset.
+__device__ __forceinline__ void cta_store_bytes(char* g, const char* s, unsigned len, int tid, int nt) {
+  unsigned head = unsigned((16 - (reinterpret_cast<unsigned long long>(g) & 15)) & 15);
+  if (head > len) head = len;
+  for (unsigned i = tid; i < head; i += nt) g[i] = s[i];
+  const unsigned nvec = (len - head) / 16;
+  const uint4* sv = reinterpret_cast<const uint4*>(s + head);
+  uint4* gv = reinterpret_cast<uint4*>(g + head);
+  for (unsigned i = tid; i < nvec; i += nt) gv[i] = sv[i];
+  for (unsigned i = head + nvec * 16 + tid; i < len; i += nt) g[i] = s[i];
+}
+
+// Byte offset of limb k in the most-significant-first output (to_decimal layout,
+// reference decimal.cpp:120-134): the top limb unpadded first, then lambda digits each.
+__device__ __forceinline__ unsigned long long limb_pos(unsigned long long k, unsigned long long top, unsigned top_len,
+                                                       unsigned be) {
+  return k == top ? 0 : top_len + (top - 1 - k) * be;
+}
+
 // Exclusive ordered scan of maps across a block of NT threads (NT multiple of 32).
 // Returns the composition of all earlier threads' maps; *total gets the block composition.
 template <int NT>

@@ -9,6 +9,7 @@
 // 128 B row segments (16 adjacent columns) so the reference's explicit
 // transpositions (conv.cpp:30-38) become strided addressing.
 #include <cstdio>
+#include <type_traits>
 
 #include "kernels.cuh"
 #include "ntt_tile.cuh"
@@ -20,170 +21,274 @@ namespace {
 constexpr int W = kTileW;
 constexpr int NT = kPassThreads;
 
-struct TileGeom {
-  bool rows;  // S >= W: tile = one group, 16 adjacent columns; else S == 1: 16 adjacent groups
+// Tile geometry. Row passes (S >= 16): one group g, 16 adjacent columns s0..s0+15;
+// element (r, w) at g R S + r S + s0 + w. Column passes (S == 1): 16 adjacent
+// groups, each a contiguous run of R words; element (r, w) at (c0 + w) R + r.
+template <int LOGR, bool ROWS>
+struct Geom {
   unsigned long long base, s0;
+  unsigned long long S;
   int logS;
-  template <int LOGR>
-  __device__ __forceinline__ void at(int i, int& r, int& w, unsigned long long& addr) const {
-    if (rows) {
-      r = i >> kTileLogW;
-      w = i & (W - 1);
-      addr = base + ((unsigned long long)r << logS) + w;
+  __device__ __forceinline__ Geom(const PassArgs& a) {
+    const unsigned long long c0 = (unsigned long long)(blockIdx.x / a.np) * W;
+    S = a.S;
+    logS = a.logS;
+    if (ROWS) {
+      const unsigned long long g = c0 >> a.logS;
+      s0 = c0 & (a.S - 1);
+      base = (g << (LOGR + a.logS)) + s0;
     } else {
-      w = i >> LOGR;
-      r = i & ((1 << LOGR) - 1);
-      addr = base + i;
+      s0 = 0;
+      base = c0 << LOGR;
     }
+  }
+  __device__ __forceinline__ unsigned long long at(int r, int w) const {
+    return ROWS ? base + ((unsigned long long)r << logS) + w : base + ((unsigned long long)w << LOGR) + r;
+  }
+  // inter-pass twiddle omega_M^{f s} for the element at row r (frequency bitrev(r) after DIF)
+  __device__ __forceinline__ const TwPair& tw(const TwPair* T, int r, int w) const {
+    return T[((unsigned long long)bitrev(r, LOGR) << logS) + s0 + w];
   }
 };
 
-template <int LOGR>
-__device__ __forceinline__ TileGeom tile_geom(const PassArgs& a) {
-  TileGeom t;
-  const unsigned long long c0 = (unsigned long long)blockIdx.x * W;
-  t.rows = a.S > 1;
-  t.logS = a.logS;
-  if (t.rows) {
-    const unsigned long long g = c0 >> a.logS;
-    t.s0 = c0 & (a.S - 1);
-    t.base = (g << (LOGR + a.logS)) + t.s0;
-  } else {
-    t.s0 = 0;
-    t.base = c0 << LOGR;
-  }
-  return t;
-}
+template <int LOGR, bool ROWS>
+using TileLayout = typename std::conditional<ROWS, Rows<W>, ContigColumns<LOGR>>::type;
 
 template <int LOGR>
 __device__ __forceinline__ void load_table(TwPair* dst, const TwPair* src) {
   for (int i = threadIdx.x; i < (1 << LOGR) / 2; i += NT) dst[i] = src[i];
 }
 
-template <int LOGR>
+template <int LOGR, bool ROWS, int E>
+__device__ __forceinline__ void group_coords(int g, int& w, int& q) {
+  group_of<ROWS, ((1 << LOGR) >> E), W>(g, w, q);
+}
+
+// Forward pass: column DIFs, then the inter-pass twiddle omega_M^{f s} (row passes).
+// The first round reads HBM into registers and the last round writes HBM from
+// registers; shared memory carries only the rounds in between.
+template <int LOGR, bool ROWS>
 __global__ void __launch_bounds__(NT) k_pass_fwd(PassArgs a) {
   constexpr int R = 1 << LOGR;
-  extern __shared__ u64 sm[];
+  constexpr int E1 = Sched<LOGR>::e_dif(LOGR), EL = Sched<LOGR>::first_e;
+  extern __shared__ __align__(16) u64 sm[];
   TwPair* tw = reinterpret_cast<TwPair*>(sm + R * W);
-  const int pr = blockIdx.y, tid = threadIdx.x;
+  const int pr = int(blockIdx.x % a.np), tid = threadIdx.x;
   const u64 p = a.p[pr];
   const u64* src = a.src[pr];
   u64* dst = a.dst[pr];
-  load_table<LOGR>(tw, a.dft_fwd[pr]);
-  const TileGeom t = tile_geom<LOGR>(a);
-  const SwizzledRows<W> L;
-  for (int i = tid; i < R * W; i += NT) {
-    int r, w;
-    unsigned long long addr;
-    t.at<LOGR>(i, r, w, addr);
-    sm[L(r, w)] = src[addr];
-  }
-  __syncthreads();
-  tile_dif<LOGR, W>(sm, L, UniformField{p, tw}, tid, NT);
   const TwPair* __restrict__ T = a.pass_tw[pr];
-  for (int i = tid; i < R * W; i += NT) {
-    int r, w;
-    unsigned long long addr;
-    t.at<LOGR>(i, r, w, addr);
-    u64 v = sm[L(r, w)];
-    if (t.rows) v = shoup_mul(v, T[((unsigned long long)bitrev(r, LOGR) << t.logS) + t.s0 + w], p);
-    dst[addr] = v;
+  load_table<LOGR>(tw, a.dft_fwd[pr]);
+  __syncthreads();
+  const Geom<LOGR, ROWS> G(a);
+  const TileLayout<LOGR, ROWS> L;
+  if constexpr (LOGR == E1) {  // one round: HBM -> registers -> HBM
+    for (int g = tid; g < (R >> E1) * W; g += NT) {
+      int w, q, j0, base;
+      group_coords<LOGR, ROWS, E1>(g, w, q);
+      dif_group<LOGR, E1>(q, j0, base);
+      u64 v[1 << E1];
+#pragma unroll
+      for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i, w)];
+      dif_regs<LOGR, LOGR, E1>(v, j0, tw, p);
+#pragma unroll
+      for (int i = 0; i < (1 << E1); ++i) {
+        if (ROWS) v[i] = shoup_mul(v[i], G.tw(T, base + i, w), p);
+        dst[G.at(base + i, w)] = v[i];
+      }
+    }
+    return;
+  } else {
+    constexpr int ST1 = 1 << (LOGR - E1);
+    for (int g = tid; g < (R >> E1) * W; g += NT) {
+      int w, q, j0, base;
+      group_coords<LOGR, ROWS, E1>(g, w, q);
+      dif_group<LOGR, E1>(q, j0, base);
+      u64 v[1 << E1];
+#pragma unroll
+      for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i * ST1, w)];
+      dif_regs<LOGR, LOGR, E1>(v, j0, tw, p);
+#pragma unroll
+      for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
+    }
+    __syncthreads();
+    dif_rounds_smem<LOGR, LOGR - E1, EL, W>(sm, L, UniformField{p, tw}, tid, NT);
+    for (int g = tid; g < (R >> EL) * W; g += NT) {
+      int w, q, j0, base;
+      group_coords<LOGR, ROWS, EL>(g, w, q);
+      dif_group<EL, EL>(q, j0, base);
+      u64 v[1 << EL];
+#pragma unroll
+      for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i, w)];
+      dif_regs<LOGR, EL, EL>(v, 0, tw, p);
+#pragma unroll
+      for (int i = 0; i < (1 << EL); ++i) {
+        if (ROWS) v[i] = shoup_mul(v[i], G.tw(T, base + i, w), p);
+        dst[G.at(base + i, w)] = v[i];
+      }
+    }
   }
 }
 
-template <int LOGR>
+// Inverse pass: conjugate inter-pass twiddle (row passes; carries the convolution
+// scale on the first inverse pass), then column DITs.
+template <int LOGR, bool ROWS>
 __global__ void __launch_bounds__(NT) k_pass_inv(PassArgs a) {
   constexpr int R = 1 << LOGR;
-  extern __shared__ u64 sm[];
+  constexpr int E1 = Sched<LOGR>::first_e;
+  constexpr int EL = Sched<LOGR>::rem ? Sched<LOGR>::rem : E1;  // last DIT round
+  constexpr int AL = LOGR - EL;                                   // its starting stage
+  extern __shared__ __align__(16) u64 sm[];
   TwPair* tw = reinterpret_cast<TwPair*>(sm + R * W);
-  const int pr = blockIdx.y, tid = threadIdx.x;
+  const int pr = int(blockIdx.x % a.np), tid = threadIdx.x;
   const u64 p = a.p[pr];
   const u64* src = a.src[pr];
   u64* dst = a.dst[pr];
-  load_table<LOGR>(tw, a.dft_inv[pr]);
-  const TileGeom t = tile_geom<LOGR>(a);
-  const SwizzledRows<W> L;
   const TwPair* __restrict__ T = a.pass_tw[pr];
-  for (int i = tid; i < R * W; i += NT) {
-    int r, w;
-    unsigned long long addr;
-    t.at<LOGR>(i, r, w, addr);
-    u64 v = src[addr];
-    if (t.rows) v = shoup_mul(v, T[((unsigned long long)bitrev(r, LOGR) << t.logS) + t.s0 + w], p);
-    sm[L(r, w)] = v;
-  }
+  const TwPair sc = a.final_scale[pr];
+  load_table<LOGR>(tw, a.dft_inv[pr]);
   __syncthreads();
-  tile_dit<LOGR, W>(sm, L, UniformField{p, tw}, tid, NT);
-  for (int i = tid; i < R * W; i += NT) {
-    int r, w;
-    unsigned long long addr;
-    t.at<LOGR>(i, r, w, addr);
-    u64 v = sm[L(r, w)];
-    if (a.has_final_scale) v = shoup_mul(v, a.final_scale[pr], p);
-    dst[addr] = v;
+  const Geom<LOGR, ROWS> G(a);
+  const TileLayout<LOGR, ROWS> L;
+  for (int g = tid; g < (R >> E1) * W; g += NT) {
+    int w, q, j0, base;
+    group_coords<LOGR, ROWS, E1>(g, w, q);
+    dit_group<0, E1>(q, j0, base);
+    u64 v[1 << E1];
+#pragma unroll
+    for (int i = 0; i < (1 << E1); ++i) {
+      v[i] = src[G.at(base + i, w)];
+      if (ROWS) v[i] = shoup_mul(v[i], G.tw(T, base + i, w), p);
+    }
+    dit_regs<LOGR, 0, E1>(v, 0, tw, p);
+#pragma unroll
+    for (int i = 0; i < (1 << E1); ++i) {
+      if constexpr (LOGR == E1) {
+        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
+        dst[G.at(base + i, w)] = v[i];
+      } else {
+        sm[L(base + i, w)] = v[i];
+      }
+    }
+  }
+  if constexpr (LOGR > E1) {
+    __syncthreads();
+    dit_rounds_smem<LOGR, E1, AL, W>(sm, L, UniformField{p, tw}, tid, NT);
+    constexpr int STL = 1 << AL;
+    for (int g = tid; g < (R >> EL) * W; g += NT) {
+      int w, q, j0, base;
+      group_coords<LOGR, ROWS, EL>(g, w, q);
+      dit_group<AL, EL>(q, j0, base);
+      u64 v[1 << EL];
+#pragma unroll
+      for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i * STL, w)];
+      dit_regs<LOGR, AL, EL>(v, j0, tw, p);
+#pragma unroll
+      for (int i = 0; i < (1 << EL); ++i) {
+        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
+        dst[G.at(base + i * STL, w)] = v[i];
+      }
+    }
   }
 }
 
 // Last forward pass (S == 1) of one operand fused with the pointwise REDC
 // product against the other operand's finished spectrum (reference
-// conv.cpp:205-208, :299-305) and the first inverse pass (DIT of the same
-// contiguous groups).
+// conv.cpp:205-208, :299-305) and the first inverse pass. The last DIF round
+// and the first DIT round act on the same 8-element groups, so DIF -> pointwise
+// -> DIT happens in registers.
 template <int LOGR>
 __global__ void __launch_bounds__(NT) k_pass_fused(PassArgs a) {
   constexpr int R = 1 << LOGR;
-  extern __shared__ u64 sm[];
+  constexpr int E1 = Sched<LOGR>::e_dif(LOGR), EM = Sched<LOGR>::first_e;
+  constexpr int EL = Sched<LOGR>::rem ? Sched<LOGR>::rem : EM;
+  constexpr int AL = LOGR - EL;
+  extern __shared__ __align__(16) u64 sm[];
   TwPair* twf = reinterpret_cast<TwPair*>(sm + R * W);
   TwPair* twi = twf + R / 2;
-  const int pr = blockIdx.y, tid = threadIdx.x;
+  const int pr = int(blockIdx.x % a.np), tid = threadIdx.x;
   const u64 p = a.p[pr], pp = a.pp[pr];
   const u64* src = a.src[pr];
   const u64* oth = a.other[pr];
   u64* dst = a.dst[pr];
+  const TwPair sc = a.final_scale[pr];
   load_table<LOGR>(twf, a.dft_fwd[pr]);
   load_table<LOGR>(twi, a.dft_inv[pr]);
-  const TileGeom t = tile_geom<LOGR>(a);
-  const SwizzledRows<W> L;
-  for (int i = tid; i < R * W; i += NT) {
-    int r, w;
-    unsigned long long addr;
-    t.at<LOGR>(i, r, w, addr);
-    sm[L(r, w)] = src[addr];
-  }
   __syncthreads();
-  tile_dif<LOGR, W>(sm, L, UniformField{p, twf}, tid, NT);
-  for (int i = tid; i < R * W; i += NT) {
-    int r, w;
-    unsigned long long addr;
-    t.at<LOGR>(i, r, w, addr);
-    const int k = L(r, w);
-    const u64 v = sm[k];
-    sm[k] = mont_mul(v, oth ? oth[addr] : v, p, pp);
+  const Geom<LOGR, false> G(a);
+  const ContigColumns<LOGR> L;
+  if constexpr (LOGR > EM) {
+    constexpr int ST1 = 1 << (LOGR - E1);
+    for (int g = tid; g < (R >> E1) * W; g += NT) {
+      int w, q, j0, base;
+      group_coords<LOGR, false, E1>(g, w, q);
+      dif_group<LOGR, E1>(q, j0, base);
+      u64 v[1 << E1];
+#pragma unroll
+      for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i * ST1, w)];
+      dif_regs<LOGR, LOGR, E1>(v, j0, twf, p);
+#pragma unroll
+      for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
+    }
+    __syncthreads();
+    dif_rounds_smem<LOGR, LOGR - E1, EM, W>(sm, L, UniformField{p, twf}, tid, NT);
   }
-  __syncthreads();
-  tile_dit<LOGR, W>(sm, L, UniformField{p, twi}, tid, NT);
-  for (int i = tid; i < R * W; i += NT) {
-    int r, w;
-    unsigned long long addr;
-    t.at<LOGR>(i, r, w, addr);
-    u64 v = sm[L(r, w)];
-    if (a.has_final_scale) v = shoup_mul(v, a.final_scale[pr], p);
-    dst[addr] = v;
+  for (int g = tid; g < (R >> EM) * W; g += NT) {
+    int w, q, j0, base;
+    group_coords<LOGR, false, EM>(g, w, q);
+    dit_group<0, EM>(q, j0, base);
+    u64 v[1 << EM];
+#pragma unroll
+    for (int i = 0; i < (1 << EM); ++i) v[i] = LOGR > EM ? sm[L(base + i, w)] : src[G.at(base + i, w)];
+    dif_regs<LOGR, EM, EM>(v, 0, twf, p);
+#pragma unroll
+    for (int i = 0; i < (1 << EM); ++i) v[i] = mont_mul(v[i], oth ? oth[G.at(base + i, w)] : v[i], p, pp);
+    dit_regs<LOGR, 0, EM>(v, 0, twi, p);
+#pragma unroll
+    for (int i = 0; i < (1 << EM); ++i) {
+      if constexpr (LOGR == EM) {
+        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
+        dst[G.at(base + i, w)] = v[i];
+      } else {
+        sm[L(base + i, w)] = v[i];
+      }
+    }
+  }
+  if constexpr (LOGR > EM) {
+    __syncthreads();
+    dit_rounds_smem<LOGR, EM, AL, W>(sm, L, UniformField{p, twi}, tid, NT);
+    constexpr int STL = 1 << AL;
+    for (int g = tid; g < (R >> EL) * W; g += NT) {
+      int w, q, j0, base;
+      group_coords<LOGR, false, EL>(g, w, q);
+      dit_group<AL, EL>(q, j0, base);
+      u64 v[1 << EL];
+#pragma unroll
+      for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i * STL, w)];
+      dit_regs<LOGR, AL, EL>(v, j0, twi, p);
+#pragma unroll
+      for (int i = 0; i < (1 << EL); ++i) {
+        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
+        dst[G.at(base + i * STL, w)] = v[i];
+      }
+    }
   }
 }
 
 // Radix-3 pass (reference three_row_forward_columns conv.cpp:109-125, with the
 // length-3 DFT written with one multiplication: omega_3^2 = -1 - omega_3).
 __global__ void k_radix3_fwd(Radix3Args a) {
-  const int pr = blockIdx.y;
-  const u64 p = a.p[pr];
+  const int pr = blockIdx.y;  // select, not index: keeps the parameter block out of local memory
+  const u64 p = pr ? a.p[1] : a.p[0];
   const unsigned long long S = a.S;
-  const u64* src = a.src[pr];
-  u64* dst = a.dst[pr];
-  const TwPair* __restrict__ T = a.tw[pr];
+  const u64* src = pr ? a.src[1] : a.src[0];
+  u64* dst = pr ? a.dst[1] : a.dst[0];
+  const TwPair* __restrict__ T = pr ? a.tw[1] : a.tw[0];
+  const TwPair lam = pr ? a.lam[1] : a.lam[0];
   for (unsigned long long s = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x) {
     const u64 x0 = src[s], x1 = src[S + s], x2 = src[2 * S + s];
-    const u64 t = shoup_mul(mod_sub(x1, x2, p), a.lam[pr], p);
+    const u64 t = shoup_mul(mod_sub(x1, x2, p), lam, p);
     const u64 y0 = mod_add(mod_add(x0, x1, p), x2, p);
     const u64 y1 = mod_add(mod_sub(x0, x2, p), t, p);
     const u64 y2 = mod_sub(mod_sub(x0, x1, p), t, p);
@@ -196,18 +301,19 @@ __global__ void k_radix3_fwd(Radix3Args a) {
 // Inverse radix-3 pass (conv.cpp:129-147): twiddle (with the convolution scale
 // folded into the table when this is the first inverse pass) then length-3 IDFT*.
 __global__ void k_radix3_inv(Radix3Args a) {
-  const int pr = blockIdx.y;
-  const u64 p = a.p[pr];
+  const int pr = blockIdx.y;  // select, not index: keeps the parameter block out of local memory
+  const u64 p = pr ? a.p[1] : a.p[0];
   const unsigned long long S = a.S;
-  const u64* src = a.src[pr];
-  u64* dst = a.dst[pr];
-  const TwPair* __restrict__ T = a.tw[pr];
+  const u64* src = pr ? a.src[1] : a.src[0];
+  u64* dst = pr ? a.dst[1] : a.dst[0];
+  const TwPair* __restrict__ T = pr ? a.tw[1] : a.tw[0];
+  const TwPair lam = pr ? a.lam[1] : a.lam[0];
   for (unsigned long long s = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x) {
     const u64 y0 = shoup_mul(src[s], T[s], p);
     const u64 y1 = shoup_mul(src[S + s], T[S + s], p);
     const u64 y2 = shoup_mul(src[2 * S + s], T[2 * S + s], p);
-    const u64 t = shoup_mul(mod_sub(y1, y2, p), a.lam[pr], p);
+    const u64 t = shoup_mul(mod_sub(y1, y2, p), lam, p);
     dst[s] = mod_add(mod_add(y0, y1, p), y2, p);
     dst[S + s] = mod_add(mod_sub(y0, y2, p), t, p);
     dst[2 * S + s] = mod_sub(mod_sub(y0, y1, p), t, p);
@@ -300,40 +406,46 @@ int grid_for(unsigned long long n, int threads) {
   return int(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
-template <int LOGR>
-void set_smem(const void* fn, int bytes) {
-  static bool done = false;
+// One-time opt-in to the large dynamic shared-memory carve-out for kernel fn.
+template <auto FN>
+void set_smem(int bytes) {
+  static bool done = false;  // one flag per kernel instantiation
   if (!done) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((const void*)FN, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     done = true;
   }
+}
+
+// blockIdx.x = tile * np + prime: both primes of a tile run back to back, so a shared
+// source (the packed limbs of pass 0) is read from HBM once and from L2 the second time.
+template <auto FN>
+void launch_pass_kernel(const PassArgs& a, unsigned long long ncols, int np, int smem, cudaStream_t st) {
+  set_smem<FN>(smem);
+  PassArgs b = a;
+  b.np = np;
+  FN<<<unsigned((ncols + W - 1) / W * np), NT, smem, st>>>(b);
 }
 
 template <int LOGR>
 void pass_fwd_t(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   const int sm = (1 << LOGR) * W * 8 + (1 << LOGR) / 2 * 16;
-  set_smem<LOGR>((const void*)k_pass_fwd<LOGR>, sm);
-  k_pass_fwd<LOGR><<<dim3(unsigned((ncols + W - 1) / W), np), NT, sm, st>>>(a);
+  if (a.S > 1)
+    launch_pass_kernel<k_pass_fwd<LOGR, true>>(a, ncols, np, sm, st);
+  else
+    launch_pass_kernel<k_pass_fwd<LOGR, false>>(a, ncols, np, sm, st);
 }
 template <int LOGR>
 void pass_inv_t(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   const int sm = (1 << LOGR) * W * 8 + (1 << LOGR) / 2 * 16;
-  static bool done = false;
-  if (!done) {
-    cudaFuncSetAttribute((const void*)k_pass_inv<LOGR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    done = true;
-  }
-  k_pass_inv<LOGR><<<dim3(unsigned((ncols + W - 1) / W), np), NT, sm, st>>>(a);
+  if (a.S > 1)
+    launch_pass_kernel<k_pass_inv<LOGR, true>>(a, ncols, np, sm, st);
+  else
+    launch_pass_kernel<k_pass_inv<LOGR, false>>(a, ncols, np, sm, st);
 }
 template <int LOGR>
 void pass_fused_t(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   const int sm = (1 << LOGR) * W * 8 + (1 << LOGR) * 16;
-  static bool done = false;
-  if (!done) {
-    cudaFuncSetAttribute((const void*)k_pass_fused<LOGR>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    done = true;
-  }
-  k_pass_fused<LOGR><<<dim3(unsigned((ncols + W - 1) / W), np), NT, sm, st>>>(a);
+  launch_pass_kernel<k_pass_fused<LOGR>>(a, ncols, np, sm, st);
 }
 
 }  // namespace

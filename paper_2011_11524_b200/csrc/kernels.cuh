@@ -22,7 +22,7 @@ enum : unsigned {
   kErrCarryBound = 8u,
 };
 
-// One pass of a multi-pass transform over both primes (blockIdx.y = prime).
+// One pass of a multi-pass transform over both primes.
 struct PassArgs {
   const u64* src[2];       // input (may equal dst; pass 0 of an operand reads the shared packed limbs)
   u64* dst[2];             // output
@@ -35,6 +35,7 @@ struct PassArgs {
   unsigned long long S;    // column stride (elements)
   int logS;
   int has_final_scale;
+  int np;                  // primes in this launch; blockIdx.x = tile * np + prime (primes of one tile adjacent)
 };
 
 struct Radix3Args {

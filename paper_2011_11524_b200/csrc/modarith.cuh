@@ -21,20 +21,21 @@ struct TwPair {  // Shoup form of one root-of-unity factor
   u64 w, wp;
 };
 
-__device__ __forceinline__ u64 mod_add(u64 a, u64 b, u64 p) {
-  u64 s = a + b;
-  return s >= p ? s - p : s;
+// Because p < 2^63, a value in [-p, p) is unambiguous as a signed 64-bit word:
+// corrections test the sign bit (reference words.hpp:38-45, adjust_signed).
+__device__ __forceinline__ u64 adjust_signed(u64 t, u64 p) {
+  long long s = (long long)t;
+  if (s < 0) s += (long long)p;
+  return (u64)s;
 }
-__device__ __forceinline__ u64 mod_sub(u64 a, u64 b, u64 p) {
-  u64 d = a - b;
-  return a >= b ? d : d + p;
-}
+__device__ __forceinline__ u64 mod_add(u64 a, u64 b, u64 p) { return adjust_signed(a + b - p, p); }
+__device__ __forceinline__ u64 mod_sub(u64 a, u64 b, u64 p) { return adjust_signed(a - b, p); }
 
 // x in [0, 2^64), w < p: returns x w mod p in [0, p).
 __device__ __forceinline__ u64 shoup_mul(u64 x, u64 w, u64 wp, u64 p) {
   u64 q = __umul64hi(x, wp);
   u64 r = x * w - q * p;  // exact, r < 2p
-  return r >= p ? r - p : r;
+  return adjust_signed(r - p, p);
 }
 __device__ __forceinline__ u64 shoup_mul(u64 x, TwPair t, u64 p) { return shoup_mul(x, t.w, t.wp, p); }
 
@@ -43,8 +44,8 @@ __device__ __forceinline__ u64 mont_mul(u64 a, u64 b, u64 p, u64 pp) {
   u64 lo = a * b, hi = __umul64hi(a, b);
   u64 m = lo * pp;
   // lo + lo(m p) == 0 mod 2^64: the carry out of the low word is (lo != 0).
-  u64 r = hi + __umul64hi(m, p) + (lo != 0 ? 1ull : 0ull);
-  return r >= p ? r - p : r;
+  u64 r = hi + __umul64hi(m, p) + (lo != 0 ? 1ull : 0ull);  // r < 2p
+  return adjust_signed(r - p, p);
 }
 
 // Gentleman-Sande butterfly (reference ntt.cpp:42-47): (u + v, (u - v) w).

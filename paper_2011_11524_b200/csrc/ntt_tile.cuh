@@ -1,34 +1,121 @@
-// Shared-memory column transforms for sm_100a.
+// Column transforms for sm_100a, built from register-resident radix-8 rounds.
 //
-// A "tile" is W independent columns of length R = 2^LOGR held in shared memory.
-// tile_dif runs the reference's Gentleman-Sande DIF on every column (natural
-// order in, bit-reversed out; reference ntt.cpp:29-50) and tile_dit the
-// Cooley-Tukey DIT (bit-reversed in, natural out, unscaled; ntt.cpp:52-73).
-// The radix-2 stages are grouped into register-resident rounds of up to three
-// stages (radix-8 blocks): each thread loads 8 elements of one column, runs the
-// stages in registers, and writes back — one shared-memory round trip per three
-// stages instead of per stage.
+// A column of R = 2^LOGR words runs the reference's Gentleman-Sande DIF
+// (natural order in, bit-reversed out; reference ntt.cpp:29-50) or Cooley-Tukey
+// DIT (bit-reversed in, natural out, unscaled; ntt.cpp:52-73). The radix-2
+// stages are grouped into rounds of up to three stages: a thread holds the 8
+// (or 4, 2) elements of one group in registers and runs the round's stages
+// there, so memory (shared or global) is touched once per round, not per stage.
+//
+// Schedules: DIF takes the remainder round first and ends with full radix-8
+// rounds; DIT starts with radix-8 rounds and ends with the remainder. Hence the
+// last DIF round and the first DIT round act on the same groups (8 consecutive
+// positions), which lets a pass run DIF -> pointwise -> DIT in registers.
 //
 // Twiddles come from a shared table tw[k] = omega_R^k (k < R/2) in Shoup form;
-// the stage with span M uses omega_M^j = tw[j * R / M] exactly like the
-// reference's flat stage slices (ntt.hpp:10-19). The column -> (prime, table)
-// mapping is a functor so one tile can carry both primes.
+// the stage with span M uses omega_M^j = tw[j * R / M] like the reference's flat
+// stage slices (ntt.hpp:10-19). A radix-8 group needs 7 distinct factors, each
+// loaded once; in rounds with stride 1 the j = 0 factors are 1 and skipped
+// (the reference's peel, ntt.cpp:39-41).
+//
+// Bank conflicts: a half-warp's 16 u64 accesses must hit 16 distinct 8-byte
+// slots. Row-major tiles (16 columns) map threads column-fastest, so a
+// half-warp reads one 128 B row. Column-major tiles map threads along the
+// column and XOR-swizzle the in-column index (r ^ ((r >> 3) & 15)), which makes
+// every round of these schedules conflict-free (checked offline for R = 2^4..2^11).
 #pragma once
 #include "modarith.cuh"
 
 namespace dmg {
 
-// Row-major [r][w] with an XOR swizzle on the column so that both row-wise
-// (S >= W passes) and column-wise (S == 1 pass) global<->shared copies are
-// bank-conflict free.
-template <int W>
-struct SwizzledRows {
-  __device__ __forceinline__ int operator()(int r, int w) const { return r * W + (w ^ (r & (W - 1))); }
+// ---- round schedules ----
+template <int LOGR>
+struct Sched {
+  static constexpr int rem = LOGR % 3;
+  // DIF: the round starting at span 2^MLOG has e_dif(MLOG) stages
+  static constexpr int e_dif(int mlog) { return (mlog == LOGR && rem) ? rem : (mlog < 3 ? mlog : 3); }
+  // DIT: the round starting after ALOG stages has e_dit(ALOG) stages
+  static constexpr int e_dit(int alog) { return (LOGR - alog == rem && rem) ? rem : (LOGR - alog < 3 ? LOGR - alog : 3); }
+  static constexpr int first_e = LOGR < 3 ? LOGR : 3;  // last DIF round == first DIT round
 };
-// Column-major [w][r] (each column contiguous): used by the one-CTA-per-product kernel.
+
+// ---- register stages ----
+// DIF stages of one group: elements v[i] at positions base + i * STRIDE, STRIDE = 2^(MLOG-E),
+// j0 = base mod STRIDE. Spans 2^MLOG down to 2^(MLOG-E+1).
+template <int LOGR, int MLOG, int E>
+__device__ __forceinline__ void dif_regs(u64 (&v)[1 << E], int j0, const TwPair* tw, u64 p) {
+  constexpr int NE = 1 << E, STRIDE = 1 << (MLOG - E);
+#pragma unroll
+  for (int st = 0; st < E; ++st) {
+    const int half = NE >> (st + 1);
+    const int mlog = MLOG - st;  // span 2^mlog
+    TwPair t[NE / 2];
+#pragma unroll
+    for (int k = 0; k < half; ++k)
+      if (!(STRIDE == 1 && k == 0)) t[k] = tw[(j0 + k * STRIDE) << (LOGR - mlog)];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      if (i & half) continue;
+      if (STRIDE == 1 && (i & (half - 1)) == 0)
+        bfly_dif1(v[i], v[i + half], p);  // j = 0: factor 1 (reference ntt.cpp:39-41 peel)
+      else
+        bfly_dif(v[i], v[i + half], t[i & (half - 1)], p);
+    }
+  }
+}
+
+// DIT stages of one group: positions base + i * STRIDE, STRIDE = 2^ALOG; spans 2^(ALOG+1)..2^(ALOG+E).
+template <int LOGR, int ALOG, int E>
+__device__ __forceinline__ void dit_regs(u64 (&v)[1 << E], int j0, const TwPair* tw, u64 p) {
+  constexpr int NE = 1 << E, STRIDE = 1 << ALOG;
+#pragma unroll
+  for (int st = 0; st < E; ++st) {
+    const int d = 1 << st;
+    const int mlog = ALOG + st + 1;
+    TwPair t[NE / 2];
+#pragma unroll
+    for (int k = 0; k < d; ++k)
+      if (!(STRIDE == 1 && k == 0)) t[k] = tw[(j0 + k * STRIDE) << (LOGR - mlog)];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      if (i & d) continue;
+      if (STRIDE == 1 && (i & (d - 1)) == 0)
+        bfly_dit1(v[i], v[i + d], p);  // j = 0: factor 1 (reference ntt.cpp:62-64 peel)
+      else
+        bfly_dit(v[i], v[i + d], t[i & (d - 1)], p);
+    }
+  }
+}
+
+// Group geometry of a round: group q (0 <= q < R >> E) covers positions base + i * STRIDE.
+template <int MLOG, int E>
+__device__ __forceinline__ void dif_group(int q, int& j0, int& base) {
+  constexpr int STRIDE = 1 << (MLOG - E);
+  j0 = q & (STRIDE - 1);
+  base = ((q >> (MLOG - E)) << MLOG) + j0;
+}
+template <int ALOG, int E>
+__device__ __forceinline__ void dit_group(int q, int& j0, int& base) {
+  constexpr int STRIDE = 1 << ALOG;
+  j0 = q & (STRIDE - 1);
+  base = ((q >> ALOG) << (ALOG + E)) + j0;
+}
+
+// ---- shared-memory layouts ----
+// Row-major [r][W]: threads column-fastest, a half-warp reads one 128 B row.
+template <int W>
+struct Rows {
+  static constexpr bool kColumnFastest = true;
+  __device__ __forceinline__ int operator()(int r, int w) const { return r * W + w; }
+};
+
+__device__ __forceinline__ int col_swizzle(int r) { return r ^ ((r >> 3) & 15); }
+
+// Column-major [w][r] (each column contiguous, swizzled inside), threads along the column.
 template <int LOGR>
 struct ContigColumns {
-  __device__ __forceinline__ int operator()(int r, int w) const { return (w << LOGR) + r; }
+  static constexpr bool kColumnFastest = false;
+  __device__ __forceinline__ int operator()(int r, int w) const { return (w << LOGR) + col_swizzle(r); }
 };
 
 // Same prime and table for every column.
@@ -39,97 +126,80 @@ struct UniformField {
   __device__ __forceinline__ const TwPair* tw(int) const { return t; }
 };
 
-// One register round of DIF covering spans 2^MLOG down to 2^(MLOG-E+1).
+template <bool COLFAST, int NQ, int W>
+__device__ __forceinline__ void group_of(int g, int& w, int& q) {
+  if constexpr (COLFAST) {
+    w = g % W;
+    q = g / W;
+  } else {
+    q = g % NQ;
+    w = g / NQ;
+  }
+}
+
+// ---- shared-memory rounds ----
 template <int LOGR, int MLOG, int E, int W, class L, class F>
-__device__ __forceinline__ void dif_round(u64* s, const L& idx, const F& fld, int tid, int nt) {
-  constexpr int R = 1 << LOGR, NE = 1 << E, STRIDE = 1 << (MLOG - E);
-  constexpr int NG = (R >> E) * W;
-  for (int g = tid; g < NG; g += nt) {
-    const int w = g % W;
-    const int q = g / W;
-    const int j0 = q & (STRIDE - 1);
-    const int base = ((q >> (MLOG - E)) << MLOG) + j0;
-    const u64 p = fld.p(w);
-    const TwPair* tw = fld.tw(w);
+__device__ __forceinline__ void dif_round_smem(u64* s, const L& idx, const F& fld, int tid, int nt) {
+  constexpr int NE = 1 << E, STRIDE = 1 << (MLOG - E), NQ = (1 << LOGR) >> E;
+  for (int g = tid; g < NQ * W; g += nt) {
+    int w, q, j0, base;
+    group_of<L::kColumnFastest, NQ, W>(g, w, q);
+    dif_group<MLOG, E>(q, j0, base);
     u64 v[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) v[i] = s[idx(base + i * STRIDE, w)];
-#pragma unroll
-    for (int st = 0; st < E; ++st) {
-      const int half = NE >> (st + 1);
-      const int mlog = MLOG - st;  // span of this stage is 2^mlog
-#pragma unroll
-      for (int i = 0; i < NE; ++i) {
-        if (i & half) continue;
-        const int j = (j0 + i * STRIDE) & ((1 << (mlog - 1)) - 1);
-        bfly_dif(v[i], v[i + half], tw[j << (LOGR - mlog)], p);
-      }
-    }
+    dif_regs<LOGR, MLOG, E>(v, j0, fld.tw(w), fld.p(w));
 #pragma unroll
     for (int i = 0; i < NE; ++i) s[idx(base + i * STRIDE, w)] = v[i];
   }
 }
 
-// One register round of DIT covering spans 2^(ALOG+1) up to 2^(ALOG+E).
 template <int LOGR, int ALOG, int E, int W, class L, class F>
-__device__ __forceinline__ void dit_round(u64* s, const L& idx, const F& fld, int tid, int nt) {
-  constexpr int R = 1 << LOGR, NE = 1 << E, STRIDE = 1 << ALOG;
-  constexpr int NG = (R >> E) * W;
-  for (int g = tid; g < NG; g += nt) {
-    const int w = g % W;
-    const int q = g / W;
-    const int j0 = q & (STRIDE - 1);
-    const int base = ((q >> ALOG) << (ALOG + E)) + j0;
-    const u64 p = fld.p(w);
-    const TwPair* tw = fld.tw(w);
+__device__ __forceinline__ void dit_round_smem(u64* s, const L& idx, const F& fld, int tid, int nt) {
+  constexpr int NE = 1 << E, STRIDE = 1 << ALOG, NQ = (1 << LOGR) >> E;
+  for (int g = tid; g < NQ * W; g += nt) {
+    int w, q, j0, base;
+    group_of<L::kColumnFastest, NQ, W>(g, w, q);
+    dit_group<ALOG, E>(q, j0, base);
     u64 v[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) v[i] = s[idx(base + i * STRIDE, w)];
-#pragma unroll
-    for (int st = 0; st < E; ++st) {
-      const int d = 1 << st;
-      const int mlog = ALOG + st + 1;
-#pragma unroll
-      for (int i = 0; i < NE; ++i) {
-        if (i & d) continue;
-        const int j = (j0 + i * STRIDE) & ((1 << (mlog - 1)) - 1);
-        bfly_dit(v[i], v[i + d], tw[j << (LOGR - mlog)], p);
-      }
-    }
+    dit_regs<LOGR, ALOG, E>(v, j0, fld.tw(w), fld.p(w));
 #pragma unroll
     for (int i = 0; i < NE; ++i) s[idx(base + i * STRIDE, w)] = v[i];
   }
 }
 
-template <int LOGR, int MLOG, int W, class L, class F>
-__device__ __forceinline__ void dif_rounds(u64* s, const L& idx, const F& fld, int tid, int nt) {
-  if constexpr (MLOG > 0) {
-    constexpr int E = MLOG >= 3 ? 3 : MLOG;
-    dif_round<LOGR, MLOG, E, W>(s, idx, fld, tid, nt);
+// DIF rounds whose first span is 2^MLOG, down to (but excluding) span 2^STOP.
+template <int LOGR, int MLOG, int STOP, int W, class L, class F>
+__device__ __forceinline__ void dif_rounds_smem(u64* s, const L& idx, const F& fld, int tid, int nt) {
+  if constexpr (MLOG > STOP) {
+    constexpr int E = Sched<LOGR>::e_dif(MLOG);
+    dif_round_smem<LOGR, MLOG, E, W>(s, idx, fld, tid, nt);
     __syncthreads();
-    dif_rounds<LOGR, MLOG - E, W>(s, idx, fld, tid, nt);
+    dif_rounds_smem<LOGR, MLOG - E, STOP, W>(s, idx, fld, tid, nt);
+  }
+}
+// DIT rounds starting after ALOG stages, up to (but excluding) the round starting at STOP.
+template <int LOGR, int ALOG, int STOP, int W, class L, class F>
+__device__ __forceinline__ void dit_rounds_smem(u64* s, const L& idx, const F& fld, int tid, int nt) {
+  if constexpr (ALOG < STOP) {
+    constexpr int E = Sched<LOGR>::e_dit(ALOG);
+    dit_round_smem<LOGR, ALOG, E, W>(s, idx, fld, tid, nt);
+    __syncthreads();
+    dit_rounds_smem<LOGR, ALOG + E, STOP, W>(s, idx, fld, tid, nt);
   }
 }
 
-template <int LOGR, int ALOG, int W, class L, class F>
-__device__ __forceinline__ void dit_rounds(u64* s, const L& idx, const F& fld, int tid, int nt) {
-  if constexpr (ALOG < LOGR) {
-    constexpr int E = (LOGR - ALOG) >= 3 ? 3 : (LOGR - ALOG);
-    dit_round<LOGR, ALOG, E, W>(s, idx, fld, tid, nt);
-    __syncthreads();
-    dit_rounds<LOGR, ALOG + E, W>(s, idx, fld, tid, nt);
-  }
-}
-
-// Full column transforms. Caller must __syncthreads() before (data and table
-// resident); both end with a barrier (none when LOGR == 0: identity).
+// Full column transforms in shared memory. Caller must __syncthreads() before;
+// both end with a barrier (none when LOGR == 0: identity).
 template <int LOGR, int W, class L, class F>
 __device__ __forceinline__ void tile_dif(u64* s, const L& idx, const F& fld, int tid, int nt) {
-  dif_rounds<LOGR, LOGR, W>(s, idx, fld, tid, nt);
+  dif_rounds_smem<LOGR, LOGR, 0, W>(s, idx, fld, tid, nt);
 }
 template <int LOGR, int W, class L, class F>
 __device__ __forceinline__ void tile_dit(u64* s, const L& idx, const F& fld, int tid, int nt) {
-  dit_rounds<LOGR, 0, W>(s, idx, fld, tid, nt);
+  dit_rounds_smem<LOGR, 0, LOGR, W>(s, idx, fld, tid, nt);
 }
 
 __device__ __forceinline__ int bitrev(int x, int bits) { return bits ? int(__brev(unsigned(x)) >> (32 - bits)) : 0; }

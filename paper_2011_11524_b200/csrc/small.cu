@@ -6,6 +6,10 @@
 // whole reference multiply (decimal.cpp:191-216): pack :102-118, the
 // three-row / direct convolution conv.cpp:149-166, :292-309, crt2 :148-152,
 // recover_digits :154-189 and to_decimal :120-134.
+//
+// Shared layout: arrays (X mod p1, X mod p2, Y mod p1, Y mod p2) of N words, each
+// a set of NR rows of C = 2^LOGC words; element (array a, logical index i) lives
+// at a N + (i & ~(C-1)) + col_swizzle(i & (C-1)) (ContigColumns, conflict-free).
 #include "carry.cuh"
 #include "kernels.cuh"
 #include "ntt_tile.cuh"
@@ -37,16 +41,26 @@ struct SmallCfg {
   static constexpr int KL = N + 2;                  // limbs after carry
   static constexpr int KPT = (KL + NT - 1) / NT;    // limbs per thread
   static constexpr int TBL = C / 2 > 0 ? C / 2 : 1;
-  static constexpr size_t smem = size_t(NARR) * N * 8 + 4 * size_t(TBL) * 16;
+  // data arrays, or (after the carry) limbs + staged text (<= 17 digits per limb)
+  static constexpr size_t raw_bytes = size_t(NARR) * N * 8 > size_t(KL) * 8 + size_t(N) * 17 + 64
+                                          ? size_t(NARR) * N * 8
+                                          : size_t(KL) * 8 + size_t(N) * 17 + 64;
+  static constexpr size_t data_bytes = (raw_bytes + 15) / 16 * 16;  // twiddle tables follow, 16 B aligned
+  static constexpr size_t smem = data_bytes + 4 * size_t(TBL) * 16;
 };
+
+template <int LOGC>
+__device__ __forceinline__ int phys(int i) {  // logical index -> swizzled offset inside one array
+  return (i & ~((1 << LOGC) - 1)) + col_swizzle(i & ((1 << LOGC) - 1));
+}
 
 // arrays: 0 = X mod p1, 1 = X mod p2, 2 = Y mod p1, 3 = Y mod p2 (each N words).
 template <int LOGC, int THREE, int SQ>
 __global__ void __launch_bounds__(NT) k_small(SmallArgs a) {
   using Cfg = SmallCfg<LOGC, THREE, SQ>;
   constexpr int C = Cfg::C, N = Cfg::N, NR = Cfg::NR;
-  extern __shared__ u64 sm[];
-  TwPair* tf0 = reinterpret_cast<TwPair*>(sm + Cfg::NARR * N);
+  extern __shared__ __align__(16) u64 sm[];
+  TwPair* tf0 = reinterpret_cast<TwPair*>(reinterpret_cast<char*>(sm) + Cfg::data_bytes);
   TwPair* tf1 = tf0 + Cfg::TBL;
   TwPair* ti0 = tf1 + Cfg::TBL;
   TwPair* ti1 = ti0 + Cfg::TBL;
@@ -80,8 +94,9 @@ __global__ void __launch_bounds__(NT) k_small(SmallArgs a) {
           limb = limb * 10 + c;
         }
       }
-      sm[(2 * o) * N + t] = limb;
-      sm[(2 * o + 1) * N + t] = limb;
+      const int ph = phys<LOGC>(t);
+      sm[(2 * o) * N + ph] = limb;
+      sm[(2 * o + 1) * N + ph] = limb;
     }
     if (bad) atomicOr(a.err, kErrBadDigit);
     if (tid == 0 && nd > 1 && d[0] == '0') atomicOr(a.err, kErrLeadingZero);
@@ -92,18 +107,19 @@ __global__ void __launch_bounds__(NT) k_small(SmallArgs a) {
     for (int i = tid; i < 2 * Cfg::NOPER * C; i += NT) {
       const int arr = i / C, s = i % C, q = arr & 1;
       const u64 p = q ? p1 : p0;
-      u64* x = sm + arr * N;
+      u64* x = sm + arr * N + col_swizzle(s);
       const TwPair* T = a.r3_fwd[q];
-      const u64 x0 = x[s], x1 = x[C + s], x2 = x[2 * C + s];
+      const u64 x0 = x[0], x1 = x[C], x2 = x[2 * C];
       const u64 t = shoup_mul(mod_sub(x1, x2, p), a.lam[q], p);
-      x[s] = mod_add(mod_add(x0, x1, p), x2, p);
-      x[C + s] = shoup_mul(mod_add(mod_sub(x0, x2, p), t, p), T[C + s], p);
-      x[2 * C + s] = shoup_mul(mod_sub(mod_sub(x0, x1, p), t, p), T[2 * C + s], p);
+      x[0] = mod_add(mod_add(x0, x1, p), x2, p);
+      x[C] = shoup_mul(mod_add(mod_sub(x0, x2, p), t, p), T[C + s], p);
+      x[2 * C] = shoup_mul(mod_sub(mod_sub(x0, x1, p), t, p), T[2 * C + s], p);
     }
     __syncthreads();
   }
   tile_dif<LOGC, Cfg::W>(sm, ContigColumns<LOGC>(), SmallField{p0, p1, tf0, tf1, NR}, tid, NT);
-  // ---- pointwise REDC (conv.cpp:205-208); squaring reuses X ----
+  // ---- pointwise REDC (conv.cpp:205-208); squaring reuses X. X and Y share the
+  // same swizzle, so physical offsets pair the same spectrum index. ----
   for (int i = tid; i < 2 * N; i += NT) {
     const int q = i / N;
     const u64 v = sm[i];
@@ -115,15 +131,15 @@ __global__ void __launch_bounds__(NT) k_small(SmallArgs a) {
     for (int i = tid; i < 2 * C; i += NT) {
       const int q = i / C, s = i % C;
       const u64 p = q ? p1 : p0;
-      u64* x = sm + q * N;
+      u64* x = sm + q * N + col_swizzle(s);
       const TwPair* T = a.r3_inv[q];
-      const u64 y0 = shoup_mul(x[s], T[s], p);
-      const u64 y1 = shoup_mul(x[C + s], T[C + s], p);
-      const u64 y2 = shoup_mul(x[2 * C + s], T[2 * C + s], p);
+      const u64 y0 = shoup_mul(x[0], T[s], p);
+      const u64 y1 = shoup_mul(x[C], T[C + s], p);
+      const u64 y2 = shoup_mul(x[2 * C], T[2 * C + s], p);
       const u64 t = shoup_mul(mod_sub(y1, y2, p), a.lam_inv[q], p);
-      x[s] = mod_add(mod_add(y0, y1, p), y2, p);
-      x[C + s] = mod_add(mod_sub(y0, y2, p), t, p);
-      x[2 * C + s] = mod_sub(mod_sub(y0, y1, p), t, p);
+      x[0] = mod_add(mod_add(y0, y1, p), y2, p);
+      x[C] = mod_add(mod_sub(y0, y2, p), t, p);
+      x[2 * C] = mod_sub(mod_sub(y0, y1, p), t, p);
     }
   } else {
     for (int i = tid; i < 2 * N; i += NT) {
@@ -132,7 +148,7 @@ __global__ void __launch_bounds__(NT) k_small(SmallArgs a) {
     }
   }
   __syncthreads();
-  // ---- CRT + digit split (decimal.cpp:148-152, bounds :174-180) ----
+  // ---- CRT + digit split (decimal.cpp:148-152, bounds :174-180), per physical slot ----
   u64* D0 = sm;
   u64* D1 = sm + N;
   u64* D2 = sm + 2 * N;
@@ -146,7 +162,7 @@ __global__ void __launch_bounds__(NT) k_small(SmallArgs a) {
     D2[i] = d2;
   }
   __syncthreads();
-  // ---- carry scan over limbs k < N + 2 ----
+  // ---- carry scan over limbs k < N + 2 (logical order) ----
   const u64 B = a.div.base;
   u64 s[Cfg::KPT];
   unsigned agg = kIdentityMap;
@@ -156,9 +172,9 @@ __global__ void __launch_bounds__(NT) k_small(SmallArgs a) {
     const int k = k0 + j;
     u64 v = 0;
     if (k < Cfg::KL) {
-      if (k < N) v += D0[k];
-      if (k >= 1 && k - 1 < N) v += D1[k - 1];
-      if (k >= 2 && k - 2 < N) v += D2[k - 2];
+      if (k < N) v += D0[phys<LOGC>(k)];
+      if (k >= 1 && k - 1 < N) v += D1[phys<LOGC>(k - 1)];
+      if (k >= 2 && k - 2 < N) v += D2[phys<LOGC>(k - 2)];
     }
     s[j] = v;
     agg = map_compose(limb_map(v, B), agg);
@@ -196,16 +212,17 @@ __global__ void __launch_bounds__(NT) k_small(SmallArgs a) {
     a.out_lens[prod] = meta[2];
   }
   __syncthreads();
+  // ---- to_decimal: stage the text in shared memory, store 16-byte vectors ----
   const unsigned long long top = meta[0];
   const unsigned top_len = unsigned(meta[1]);
   char* out = a.outs + prod * a.out_stride;
-  for (int k = tid; k <= (int)top; k += NT) {
-    const u64 v = Z[k];
-    if ((unsigned long long)k == top)
-      write_digits(out, v, top_len);
-    else
-      write_digits(out + top_len + (top - 1 - k) * be, v, be);
-  }
+  char* text = reinterpret_cast<char*>(sm + Cfg::KL) + 16 + (reinterpret_cast<unsigned long long>(out) & 15);
+  text = reinterpret_cast<char*>(reinterpret_cast<unsigned long long>(text) & ~15ull) +
+         (reinterpret_cast<unsigned long long>(out) & 15);
+  for (int k = tid; k <= (int)top; k += NT)
+    write_digits(text + limb_pos(k, top, top_len, be), Z[k], (unsigned long long)k == top ? top_len : be);
+  __syncthreads();
+  cta_store_bytes(out, text, unsigned(meta[2]), tid, NT);
 }
 
 template <int LOGC, int THREE, int SQ>
