@@ -18,7 +18,7 @@ namespace dmg {
 
 namespace {
 
-constexpr int NT = 256;
+constexpr int NT = 384;  // 12 warps; 3 CTAs/SM at <= 56 registers (36 warps per SM)
 
 struct SmallField {
   u64 p0, p1;
@@ -56,7 +56,7 @@ __device__ __forceinline__ int phys(int i) {  // logical index -> swizzled offse
 
 // arrays: 0 = X mod p1, 1 = X mod p2, 2 = Y mod p1, 3 = Y mod p2 (each N words).
 template <int LOGC, int THREE, int SQ>
-__global__ void __launch_bounds__(NT) k_small(SmallArgs a) {
+__global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
   using Cfg = SmallCfg<LOGC, THREE, SQ>;
   constexpr int C = Cfg::C, N = Cfg::N, NR = Cfg::NR;
   extern __shared__ __align__(16) u64 sm[];
