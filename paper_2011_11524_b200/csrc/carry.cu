@@ -12,6 +12,7 @@ namespace {
 constexpr int CH = kCarryChunk;
 constexpr int NT = kCarryThreads;
 constexpr int PER = CH / NT;  // limbs per thread
+static_assert(PER == 8, "per-thread limb maps are moved as one 8-byte word");
 
 __device__ __forceinline__ void coeff_digits(const CarryArgs& a, long long i, u64& d0, u64& d1, u64& d2) {
   d0 = d1 = d2 = 0;
@@ -23,15 +24,20 @@ __device__ __forceinline__ void coeff_digits(const CarryArgs& a, long long i, u6
 }
 
 // Phase 1: s_k for the chunk's limbs and the chunk's composed transfer map.
+// Coefficients are read and limb sums written in coalesced order (loc = j NT + tid);
+// each limb's 6-bit transfer map goes to shared memory as a byte, and each thread
+// then composes the maps of PER consecutive limbs (one 8-byte shared load).
 __global__ void __launch_bounds__(NT) k_carry_split(CarryArgs a) {
   __shared__ u64 d1s[CH + 2], d2s[CH + 2];
+  __shared__ __align__(8) unsigned char mp[CH];
   __shared__ unsigned wsm[NT / 32 + 1];
   const unsigned long long k0 = (unsigned long long)blockIdx.x * CH;
   const unsigned long long K = a.n + 2;
+  const u64 B = a.div.base;
   u64 d0r[PER];
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
-    const int loc = threadIdx.x * PER + j;
+    const int loc = j * NT + threadIdx.x;
     u64 d0, d1, d2;
     coeff_digits(a, (long long)(k0 + loc), d0, d1, d2);
     d0r[j] = d0;
@@ -45,17 +51,19 @@ __global__ void __launch_bounds__(NT) k_carry_split(CarryArgs a) {
     d2s[threadIdx.x] = d2;
   }
   __syncthreads();
-  unsigned agg = kIdentityMap;
-  const u64 B = a.div.base;
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
-    const int loc = threadIdx.x * PER + j;
+    const int loc = j * NT + threadIdx.x;
     const unsigned long long k = k0 + loc;
-    if (k >= K) break;
     const u64 s = d0r[j] + d1s[loc + 1] + d2s[loc];
-    a.s[k] = s;
-    agg = map_compose(limb_map(s, B), agg);
+    if (k < K) a.s[k] = s;
+    mp[loc] = (unsigned char)(k < K ? limb_map(s, B) : kIdentityMap);
   }
+  __syncthreads();
+  const unsigned long long m8 = reinterpret_cast<const unsigned long long*>(mp)[threadIdx.x];
+  unsigned agg = kIdentityMap;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
   unsigned total;
   block_scan_maps<NT>(agg, wsm, &total);
   if (threadIdx.x == 0) a.maps[blockIdx.x] = total;
@@ -127,22 +135,36 @@ __global__ void __launch_bounds__(1024) k_carry_scan(CarryArgs a, unsigned nchun
 __global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
   __shared__ unsigned wsm[NT / 32 + 1];
   __shared__ __align__(16) char buf[CH * 17 + 32];
+  __shared__ __align__(8) unsigned char mp[CH];  // limb maps, then limb carry-ins
   const unsigned long long cbase = (unsigned long long)blockIdx.x * CH;
   const unsigned long long top = a.meta[0];
   if (cbase > top) return;  // nothing of this chunk is printed (uniform per block)
-  const unsigned long long k0 = cbase + threadIdx.x * PER;
   const unsigned long long K = a.n + 2;
   const u64 B = a.div.base;
+  // coalesced limb sums (loc = j NT + tid); their maps to shared memory
   u64 s[PER];
-  unsigned agg = kIdentityMap;
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
-    const unsigned long long k = k0 + j;
+    const unsigned long long k = cbase + j * NT + threadIdx.x;
     s[j] = k < K ? a.s[k] : 0;
-    agg = map_compose(limb_map(s[j], B), agg);
+    mp[j * NT + threadIdx.x] = (unsigned char)limb_map(s[j], B);
   }
-  const unsigned pre = block_scan_maps<NT>(agg, wsm, nullptr);
+  __syncthreads();
+  // each thread: PER consecutive limbs -> composed map -> block scan -> per-limb carry-ins
+  unsigned long long m8 = reinterpret_cast<const unsigned long long*>(mp)[threadIdx.x];
+  unsigned agg = kIdentityMap;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
+  const unsigned pre = block_scan_maps<NT>(agg, wsm, nullptr);  // ends with a barrier
   unsigned c = map_apply(pre, a.maps[blockIdx.x]);
+  unsigned long long cin8 = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    cin8 |= (unsigned long long)c << (8 * j);
+    c = map_apply(unsigned(m8 >> (8 * j)) & 63u, c);
+  }
+  reinterpret_cast<unsigned long long*>(mp)[threadIdx.x] = cin8;
+  __syncthreads();
   const unsigned top_len = unsigned(a.meta[1]);
   const unsigned be = a.base_exp;
   const unsigned long long khi = cbase + CH - 1 < top ? cbase + CH - 1 : top;
@@ -150,15 +172,16 @@ __global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
   const unsigned long long end = limb_pos(cbase, top, top_len, be) + (cbase == top ? top_len : be);
   char* g = a.out + start;
   char* sb = buf + (reinterpret_cast<unsigned long long>(g) & 15);
+  // digits: each thread prints PER consecutive limbs (a contiguous 8 lambda-byte run)
+  const unsigned long long* sg = reinterpret_cast<const unsigned long long*>(a.s);
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
-    const unsigned long long k = k0 + j;
-    u64 v = s[j] + c;
-    unsigned q = 0;
-    if (v >= B) { v -= B; ++q; }
-    if (v >= B) { v -= B; ++q; }
-    c = q;
-    if (k > top) continue;
+    const int loc = threadIdx.x * PER + j;
+    const unsigned long long k = cbase + loc;
+    if (k > top) break;
+    u64 v = sg[k] + mp[loc];  // re-read from L1/L2 (this block just streamed it)
+    if (v >= B) v -= B;
+    if (v >= B) v -= B;
     write_digits(sb + (limb_pos(k, top, top_len, be) - start), v, k == top ? top_len : be);
   }
   __syncthreads();

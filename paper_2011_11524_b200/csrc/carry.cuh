@@ -41,12 +41,39 @@ __device__ __forceinline__ void crt2(u64 a1, u64 a2, u64 p1, u64 p2, u64 p2p, u6
   hi += lo < l ? 1ull : 0ull;
 }
 
-// c = d0 + d1 B + d2 B^2 (each < B).
+// c = d0 + d1 B + d2 B^2 (each < B), for c < B^3.
+// d2 = floor(c / B^2) from a double-precision estimate (error <= 1 for c < 2^126,
+// corrected exactly in 128-bit arithmetic), then (d1, d0) from one 2-by-1 reciprocal
+// division of the remainder (< B^2, so the quotient fits one word; reference
+// udiv_2by1, decimal.hpp:106-121).
 __device__ __forceinline__ void split3(const DivB& d, u64 lo, u64 hi, u64& d0, u64& d1, u64& d2) {
-  u64 qlo, qhi, q2lo, q2hi;
-  d0 = divmod_base(d, lo, hi, qlo, qhi);
-  d1 = divmod_base(d, qlo, qhi, q2lo, q2hi);
-  d2 = q2lo;
+  const double cd = __ull2double_rn(hi) * 18446744073709551616.0 + __ull2double_rn(lo);
+  long long q = (long long)(cd * d.inv_b2);
+  if (q < 0) q = 0;
+  // r = c - q B^2 (two's-complement 128-bit)
+  u64 tlo = (u64)q * d.b2lo;
+  u64 thi = __umul64hi((u64)q, d.b2lo) + (u64)q * d.b2hi;
+  u64 rlo = lo - tlo;
+  u64 rhi = hi - thi - (lo < tlo ? 1ull : 0ull);
+  while ((long long)rhi < 0) {  // r < 0: q was one too large
+    --q;
+    const u64 s = rlo + d.b2lo;
+    rhi += d.b2hi + (s < rlo ? 1ull : 0ull);
+    rlo = s;
+  }
+  while (rhi > d.b2hi || (rhi == d.b2hi && rlo >= d.b2lo)) {  // r >= B^2: q one too small
+    ++q;
+    rhi -= d.b2hi + (rlo < d.b2lo ? 1ull : 0ull);
+    rlo -= d.b2lo;
+  }
+  d2 = (u64)q;
+  // r < B^2: r = d1 B + d0 with d1 < B < 2^64 — one normalized 2-by-1 step
+  const unsigned sh = d.shift;
+  const u64 n1 = sh ? (rhi << sh) | (rlo >> (64 - sh)) : rhi;
+  const u64 n0 = rlo << sh;
+  u64 r;
+  udiv_2by1(n1, n0, d.d_norm, d.recip, d1, r);
+  d0 = r >> sh;
 }
 
 __device__ __forceinline__ bool above_cap(u64 lo, u64 hi, u64 cap_lo, u64 cap_hi) {
@@ -62,7 +89,20 @@ __device__ __forceinline__ unsigned decimal_len(u64 v) {
   return n;
 }
 
+// x < 10^8 -> its 8 ASCII digits, most significant in the lowest byte (SWAR:
+// 4+4 digit lanes, then pairs, then single digits via reciprocal multiplies).
+__device__ __forceinline__ u64 ascii8(unsigned x) {
+  const unsigned hi4 = x / 10000u, lo4 = x - hi4 * 10000u;
+  const u64 y = (u64)hi4 | ((u64)lo4 << 32);
+  const u64 z = ((y * 5243) >> 19) & 0x0000007F0000007Full;  // lane / 100 (exact below 43699)
+  const u64 w = z | ((y - z * 100) << 16);
+  const u64 t = ((w * 103) >> 10) & 0x000F000F000F000Full;   // lane / 10 (exact below 179)
+  return (t | ((w - t * 10) << 8)) | 0x3030303030303030ull;
+}
+
 // Write the `len` least-significant decimal digits of v (zero padded) to out[0..len).
+// (Measured: a SWAR ascii8-based variant with predicated byte stores was slower here —
+// the byte stores, not the divisions, dominate.)
 __device__ __forceinline__ void write_digits(char* out, u64 v, unsigned len) {
   // split at 10^9 so the digit loop runs on 32-bit values
   unsigned lo = unsigned(v % 1000000000ull);

@@ -25,6 +25,10 @@ DivB div_for(u64 base) {
   d.shift = __builtin_clzll(base);
   d.d_norm = base << d.shift;
   d.recip = recip_of(d.d_norm);
+  const u128 b2 = (u128)base * base;
+  d.b2lo = u64(b2);
+  d.b2hi = u64(b2 >> 64);
+  d.inv_b2 = 1.0 / (double(base) * double(base));
   return d;
 }
 
@@ -156,7 +160,37 @@ void Engine::build_passes(PrimePlan& pl) {
     PassPlan& ps = *pl.passes[i];
     const std::size_t M = std::size_t(ps.R) * ps.S;
     const u64 wM = F.pow(pl.xi, pl.N / M);
-    if (ps.radix3 || ps.S > 1) {
+    if (ps.radix3) {
+      // factorised twiddles: omega^{f s} = omega^{f (s mod L)} * omega^{f L (s / L)}
+      const std::size_t L = std::min<std::size_t>(ps.S, 8192), H = ps.S / L;
+      ps.r3_lbits = __builtin_ctzll(L);
+      const u64 scale = int(i) == last_table ? pl.conv_scale : 1;
+      std::vector<TwPair> lf(3 * L), li(3 * L), hf(3 * H), hi(3 * H);
+      const u64 wMi = F.inv(wM), wL = F.pow(wM, L), wLi = F.inv(wL);
+      for (int f = 0; f < 3; ++f) {
+        const u64 sf = F.pow(wM, f), sfi = F.pow(wMi, f), hf_step = F.pow(wL, f), hi_step = F.pow(wLi, f);
+        u64 a = 1, b = 1;
+        for (std::size_t s = 0; s < L; ++s) {
+          lf[f * L + s] = shoup_pair(F, a);
+          li[f * L + s] = shoup_pair(F, b);
+          a = F.mul(a, sf);
+          b = F.mul(b, sfi);
+        }
+        a = 1;
+        b = scale;
+        for (std::size_t s = 0; s < H; ++s) {
+          hf[f * H + s] = shoup_pair(F, a);
+          hi[f * H + s] = shoup_pair(F, b);
+          a = F.mul(a, hf_step);
+          b = F.mul(b, hi_step);
+        }
+      }
+      upload(ps.r3_lo_fwd, lf, stream_);
+      upload(ps.r3_hi_fwd, hf, stream_);
+      upload(ps.r3_lo_inv, li, stream_);
+      upload(ps.r3_hi_inv, hi, stream_);
+      cuda_check(cudaStreamSynchronize(stream_), "radix-3 tables");
+    } else if (ps.S > 1) {
       const std::size_t cnt = std::size_t(ps.R) * ps.S;
       ps.tw_fwd.ensure(cnt);
       ps.tw_inv.ensure(cnt);
@@ -227,7 +261,9 @@ std::size_t Engine::table_bytes() const {
   std::size_t b = 0;
   for (const auto& kv : plans_)
     for (const auto& ps : kv.second->passes)
-      b += (ps->tw_fwd.n + ps->tw_inv.n + ps->dft_fwd.n + ps->dft_inv.n) * sizeof(TwPair);
+      b += (ps->tw_fwd.n + ps->tw_inv.n + ps->dft_fwd.n + ps->dft_inv.n + ps->r3_lo_fwd.n + ps->r3_hi_fwd.n +
+            ps->r3_lo_inv.n + ps->r3_hi_inv.n) *
+           sizeof(TwPair);
   return b;
 }
 
@@ -255,11 +291,13 @@ void Engine::transform_forward(const PrimePlan* pl[2], int np, const u64* const 
       for (int q = 0; q < np; ++q) {
         a.src[q] = first ? src[q] : dst[q];
         a.dst[q] = dst[q];
-        a.tw[q] = pl[q]->passes[i]->tw_fwd.ptr;
+        a.lo[q] = pl[q]->passes[i]->r3_lo_fwd.ptr;
+        a.hi[q] = pl[q]->passes[i]->r3_hi_fwd.ptr;
         a.p[q] = pl[q]->p;
         a.lam[q] = pl[q]->lam;
       }
       a.S = pl[0]->passes[i]->S;
+      a.lbits = pl[0]->passes[i]->r3_lbits;
       launch_radix3(false, a, np, st);
     } else {
       PassArgs a{};
@@ -276,6 +314,7 @@ void Engine::transform_forward(const PrimePlan* pl[2], int np, const u64* const 
       }
       a.S = P.S;
       a.logS = P.logS;
+      a.G = pl[0]->N / (std::size_t(P.R) * P.S);
       launch_pass_fwd(P.logR, a, pl[0]->N / std::size_t(P.R), np, st);
     }
     ++launches_;
@@ -303,6 +342,7 @@ void Engine::transform_fused_last(const PrimePlan* pl[2], int np, u64* const dat
   }
   a.S = 1;
   a.logS = 0;
+  a.G = pl[0]->N / std::size_t(P.R);
   a.has_final_scale = any_table ? 0 : 1;
   launch_pass_fused(P.logR, a, pl[0]->N / std::size_t(P.R), np, st);
   ++launches_;
@@ -320,11 +360,13 @@ void Engine::transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2
       for (int q = 0; q < np; ++q) {
         a.src[q] = data[q];
         a.dst[q] = data[q];
-        a.tw[q] = pl[q]->passes[ii]->tw_inv.ptr;
+        a.lo[q] = pl[q]->passes[ii]->r3_lo_inv.ptr;
+        a.hi[q] = pl[q]->passes[ii]->r3_hi_inv.ptr;
         a.p[q] = pl[q]->p;
         a.lam[q] = pl[q]->lam_inv;
       }
       a.S = pl[0]->passes[ii]->S;
+      a.lbits = pl[0]->passes[ii]->r3_lbits;
       launch_radix3(true, a, np, st);
     } else {
       PassArgs a{};
@@ -342,6 +384,7 @@ void Engine::transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2
       }
       a.S = P.S;
       a.logS = P.logS;
+      a.G = pl[0]->N / (std::size_t(P.R) * P.S);
       a.has_final_scale = (!any_table && ii == 0) ? 1 : 0;
       launch_pass_inv(P.logR, a, pl[0]->N / std::size_t(P.R), np, st);
     }

@@ -49,8 +49,11 @@ struct PassPlan {
   int logR = 0, R = 0;
   unsigned long long S = 0;
   int logS = 0;
-  DevBuf<TwPair> tw_fwd, tw_inv;    // R x S inter-pass twiddles (S > 1) / 3 x S for radix-3
+  DevBuf<TwPair> tw_fwd, tw_inv;    // R x S inter-pass twiddles (power-of-two passes, S > 1)
   DevBuf<TwPair> dft_fwd, dft_inv;  // omega_R^{+-k}, k < R/2
+  // radix-3 passes: omega_N^{+-f s} = lo[f][s mod 2^lbits] * hi[f][s >> lbits]
+  DevBuf<TwPair> r3_lo_fwd, r3_hi_fwd, r3_lo_inv, r3_hi_inv;
+  int r3_lbits = 0;
 };
 
 // Transform plan for one prime and one length N = 2^k or 3*2^k (root chosen

@@ -30,14 +30,17 @@ struct Geom {
   unsigned long long S;
   int logS;
   __device__ __forceinline__ Geom(const PassArgs& a) {
-    const unsigned long long c0 = (unsigned long long)(blockIdx.x / a.np) * W;
+    const unsigned long long tile = blockIdx.x / a.np;
     S = a.S;
     logS = a.logS;
     if (ROWS) {
-      const unsigned long long g = c0 >> a.logS;
-      s0 = c0 & (a.S - 1);
+      // group-fastest tile order: the G groups share the twiddle rows T[f][s0..s0+15],
+      // so consecutive CTAs reuse them from L2 instead of re-streaming them from HBM
+      const unsigned long long g = tile % a.G;
+      s0 = (tile / a.G) * W;
       base = (g << (LOGR + a.logS)) + s0;
     } else {
+      const unsigned long long c0 = tile * W;
       s0 = 0;
       base = c0 << LOGR;
     }
@@ -283,36 +286,42 @@ __global__ void k_radix3_fwd(Radix3Args a) {
   const unsigned long long S = a.S;
   const u64* src = pr ? a.src[1] : a.src[0];
   u64* dst = pr ? a.dst[1] : a.dst[0];
-  const TwPair* __restrict__ T = pr ? a.tw[1] : a.tw[0];
+  const TwPair* __restrict__ lo = pr ? a.lo[1] : a.lo[0];
+  const TwPair* __restrict__ hi = pr ? a.hi[1] : a.hi[0];
   const TwPair lam = pr ? a.lam[1] : a.lam[0];
+  const unsigned long long L = 1ull << a.lbits, H = S >> a.lbits;
   for (unsigned long long s = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long sl = s & (L - 1), sh = s >> a.lbits;
     const u64 x0 = src[s], x1 = src[S + s], x2 = src[2 * S + s];
     const u64 t = shoup_mul(mod_sub(x1, x2, p), lam, p);
     const u64 y0 = mod_add(mod_add(x0, x1, p), x2, p);
     const u64 y1 = mod_add(mod_sub(x0, x2, p), t, p);
     const u64 y2 = mod_sub(mod_sub(x0, x1, p), t, p);
     dst[s] = y0;
-    dst[S + s] = shoup_mul(y1, T[S + s], p);
-    dst[2 * S + s] = shoup_mul(y2, T[2 * S + s], p);
+    dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hi[H + sh], p);
+    dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
   }
 }
 
 // Inverse radix-3 pass (conv.cpp:129-147): twiddle (with the convolution scale
-// folded into the table when this is the first inverse pass) then length-3 IDFT*.
+// folded into the hi table when this is the first inverse pass) then length-3 IDFT*.
 __global__ void k_radix3_inv(Radix3Args a) {
   const int pr = blockIdx.y;  // select, not index: keeps the parameter block out of local memory
   const u64 p = pr ? a.p[1] : a.p[0];
   const unsigned long long S = a.S;
   const u64* src = pr ? a.src[1] : a.src[0];
   u64* dst = pr ? a.dst[1] : a.dst[0];
-  const TwPair* __restrict__ T = pr ? a.tw[1] : a.tw[0];
+  const TwPair* __restrict__ lo = pr ? a.lo[1] : a.lo[0];
+  const TwPair* __restrict__ hi = pr ? a.hi[1] : a.hi[0];
   const TwPair lam = pr ? a.lam[1] : a.lam[0];
+  const unsigned long long L = 1ull << a.lbits, H = S >> a.lbits;
   for (unsigned long long s = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x) {
-    const u64 y0 = shoup_mul(src[s], T[s], p);
-    const u64 y1 = shoup_mul(src[S + s], T[S + s], p);
-    const u64 y2 = shoup_mul(src[2 * S + s], T[2 * S + s], p);
+    const unsigned long long sl = s & (L - 1), sh = s >> a.lbits;
+    const u64 y0 = shoup_mul(src[s], hi[sh], p);  // lo[0][.] = 1
+    const u64 y1 = shoup_mul(shoup_mul(src[S + s], lo[L + sl], p), hi[H + sh], p);
+    const u64 y2 = shoup_mul(shoup_mul(src[2 * S + s], lo[2 * L + sl], p), hi[2 * H + sh], p);
     const u64 t = shoup_mul(mod_sub(y1, y2, p), lam, p);
     dst[s] = mod_add(mod_add(y0, y1, p), y2, p);
     dst[S + s] = mod_add(mod_sub(y0, y2, p), t, p);
@@ -360,26 +369,81 @@ __global__ void k_gen_table(GenArgs g) {
 
 // pack (reference decimal.cpp:102-118): limb t holds digits
 // [nd - (t+1) lambda, nd - t lambda) of the most-significant-first string.
-__global__ void k_pack(const char* __restrict__ d, unsigned long long nd, unsigned be, u64* __restrict__ limbs,
-                       unsigned long long total, unsigned* err) {
+// A CTA packs kPackLimbs consecutive limbs: their digit span (<= 17 kPackLimbs bytes,
+// contiguous in the string) is staged in shared memory with 16-byte loads, then
+// each thread parses its lambda digits 8 at a time (SWAR).
+constexpr int kPackLimbs = 256;
+
+// 8 bytes of shared memory at any byte offset (buf 8-aligned, readable 8 bytes past).
+__device__ __forceinline__ u64 smem_bytes8(const char* buf, int pos) {
+  const u64* w = reinterpret_cast<const u64*>(buf + (pos & ~7));
+  const int sh = (pos & 7) * 8;
+  return sh ? (w[0] >> sh) | (w[1] << (64 - sh)) : w[0];
+}
+
+// Value of 8 ASCII digits (first byte most significant) whose first `skip` bytes are
+// treated as '0'; flags any non-digit byte.
+__device__ __forceinline__ u64 swar8(u64 x, int skip, unsigned& bad) {
+  const u64 keep = skip >= 8 ? 0 : (~0ull << (8 * skip));
+  x = (x & keep) | (0x3030303030303030ull & ~keep);
+  bad |= ((x & 0xF0F0F0F0F0F0F0F0ull) != 0x3030303030303030ull) |
+         ((((x & 0x0F0F0F0F0F0F0F0Full) + 0x0606060606060606ull) & 0xF0F0F0F0F0F0F0F0ull) != 0);
+  x &= 0x0F0F0F0F0F0F0F0Full;
+  x = (x * 2561) >> 8;                                    // pairs: 10 d0 + d1
+  x = ((x & 0x00FF00FF00FF00FFull) * 6553601) >> 16;     // quads
+  x = ((x & 0x0000FFFF0000FFFFull) * 42949672960001ull) >> 32;  // 8 digits
+  return x;
+}
+
+// Digits buf[s, s + n), n <= 24, as an integer (three 8-digit chunks from the right).
+__device__ __forceinline__ u64 parse_digits(const char* buf, int s, int n, unsigned& bad) {
+  const int e = s + n;
+  u64 v = swar8(smem_bytes8(buf, e - 8), n >= 8 ? 0 : 8 - n, bad);
+  if (n > 8) v += swar8(smem_bytes8(buf, e - 16), n >= 16 ? 0 : 16 - n, bad) * 100000000ull;
+  if (n > 16) v += swar8(smem_bytes8(buf, e - 24), 24 - n, bad) * 10000000000000000ull;
+  return v;
+}
+
+__global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d, unsigned long long nd, unsigned be,
+                                                     u64* __restrict__ limbs, unsigned long long total, unsigned* err) {
+  __shared__ __align__(16) char smem[kPackLimbs * 17 + 96];
+  char* buf = smem + 32;  // parse_digits may read up to 24 bytes before a limb and 8 past it
   const unsigned long long nl = (nd + be - 1) / be;
-  for (unsigned long long t = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; t < total;
-       t += (unsigned long long)gridDim.x * blockDim.x) {
-    u64 limb = 0;
-    if (t < nl) {
-      const long long end = (long long)nd - (long long)(t * be);
-      const long long begin = end > (long long)be ? end - (long long)be : 0;
-      unsigned bad = 0;
-      for (long long i = begin; i < end; ++i) {
-        const unsigned c = (unsigned char)d[i] - '0';
-        bad |= c > 9;
-        limb = limb * 10 + c;
+  unsigned bad = 0;
+  for (unsigned long long t0 = (unsigned long long)blockIdx.x * kPackLimbs; t0 < total;
+       t0 += (unsigned long long)gridDim.x * kPackLimbs) {
+    const unsigned long long t = t0 + threadIdx.x;
+    // digit span of limbs [t0, min(t0 + kPackLimbs, nl)): [lo, hi)
+    const long long hi = (long long)nd - (long long)(t0 * be);
+    const long long lo = hi - (long long)kPackLimbs * be > 0 ? hi - (long long)kPackLimbs * be : 0;
+    if (hi > 0) {
+      // 16-byte vectors aligned in the ADDRESS space; string position x lands at buf[x - lo + o]
+      const int o = int((reinterpret_cast<unsigned long long>(d) + (unsigned long long)lo) & 15);
+      const long long g0 = lo - o;  // string position of buf[0] (may be < 0)
+      const int nvec = int((o + (hi - lo) + 15) / 16);
+      for (int v = threadIdx.x; v < nvec; v += kPackLimbs) {
+        const long long g = g0 + 16LL * v;
+        if (g >= 0 && g + 16 <= (long long)nd) {
+          reinterpret_cast<uint4*>(buf)[v] = *reinterpret_cast<const uint4*>(d + g);
+        } else {  // head or tail: byte loads inside the string only
+          for (int b = 0; b < 16; ++b) buf[v * 16 + b] = (g + b >= 0 && g + b < (long long)nd) ? d[g + b] : '0';
+        }
       }
-      if (bad) atomicOr(err, kErrBadDigit);
-      if (begin == 0 && nd > 1 && d[0] == '0') atomicOr(err, kErrLeadingZero);
+      __syncthreads();
+      u64 limb = 0;
+      if (t < nl) {
+        const long long end = (long long)nd - (long long)(t * be);
+        const long long begin = end > (long long)be ? end - (long long)be : 0;
+        limb = parse_digits(buf, int(begin - g0), int(end - begin), bad);
+        if (begin == 0 && nd > 1 && d[0] == '0') atomicOr(err, kErrLeadingZero);
+      }
+      __syncthreads();
+      if (t < total) limbs[t] = limb;
+    } else if (t < total) {
+      limbs[t] = 0;  // zero padding to the transform length
     }
-    limbs[t] = limb;
   }
+  if (bad) atomicOr(err, kErrBadDigit);
 }
 
 __global__ void k_pointwise(u64* a, const u64* b, unsigned long long n, u64 p, u64 pp) {

@@ -36,15 +36,21 @@ struct PassArgs {
   int logS;
   int has_final_scale;
   int np;                  // primes in this launch; blockIdx.x = tile * np + prime (primes of one tile adjacent)
+  unsigned long long G;    // groups of R x S (row passes: tiles run group-fastest)
 };
 
+// Radix-3 pass over N = 3 S. The twiddle omega_N^{+-f s} (times the convolution
+// scale on the inverse) is factorised as lo[f][s mod L] * hi[f][s / L], L = 2^lbits,
+// so the tables are 3 (L + S / L) pairs instead of 3 S (both stay L2-resident).
 struct Radix3Args {
   const u64* src[2];
   u64* dst[2];
-  const TwPair* tw[2];  // 3 x S table: omega_N^{+-f s} (* scale on inverse)
+  const TwPair* lo[2];  // 3 x L
+  const TwPair* hi[2];  // 3 x (S / L)
   u64 p[2];
   TwPair lam[2];        // omega_3 (forward) or omega_3^-1 (inverse)
   unsigned long long S;
+  int lbits;
 };
 
 // Launchers (kernels.cu).

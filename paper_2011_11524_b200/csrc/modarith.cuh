@@ -79,6 +79,8 @@ __device__ __forceinline__ void bfly_dit1(u64& u, u64& v, u64 p) {
 struct DivB {
   u64 base, d_norm, recip;
   unsigned shift;
+  u64 b2lo, b2hi;  // B^2 as a 128-bit value
+  double inv_b2;   // 1 / B^2
 };
 
 __device__ __forceinline__ void udiv_2by1(u64 u1, u64 u0, u64 d, u64 v, u64& q, u64& r) {
