@@ -113,6 +113,54 @@ int decmul_gpu_transpose_square_sub(decmul_gpu_ctx* ctx, uint64_t* a, size_t n, 
 int decmul_gpu_transpose_n_x_2n(decmul_gpu_ctx* ctx, uint64_t* a, size_t n);
 int decmul_gpu_transpose_2n_x_n(decmul_gpu_ctx* ctx, uint64_t* a, size_t n);
 
+/* ---- sharded large products (one product over `ranks` GPUs; not in the reference, which is
+ * single-threaded and caps N at 3 * 2^24). The caller owns the exchange (NCCL all-to-all or any
+ * transport) and runs, on every rank q, with device buffers of local_len words per prime:
+ *   pack(x) -> transform(COL_FWD) -> [reorder-free all-to-all] -> reorder(to_segments=1) ->
+ *   transform(ROW_FWD)  (same for y with ROW_FWD_CONV against x) -> reorder(to_segments=0) ->
+ *   all-to-all -> transform(COL_INV) -> all-to-all -> reorder(to_segments=1) ->
+ *   carry_begin (halo = p1, p1, p2, p2 residues of the two coefficients before this rank's block,
+ *   gathered from rank q-1) -> all-gather rank maps -> carry_probe -> all-gather -> carry_emit.
+ * All-to-all chunks are contiguous: local_len / ranks words per peer per prime.
+ * paper_2011_11524_b200/sharded.py is the reference driver. ---- */
+typedef struct {
+  size_t length;          /* N */
+  unsigned base_exp;      /* lambda */
+  uint64_t p1, p2;
+  int ranks;              /* G (power of two) */
+  int col_passes;         /* K: passes run column-sharded */
+  size_t rows;            /* Rtot: rows of the column phase (multiple of G) */
+  size_t seg_len;         /* Sc = N / Rtot */
+  size_t col_width;       /* Bc = Sc / G: this rank's columns */
+  size_t local_len;       /* N / G */
+  size_t s_words;         /* words of the carry scratch (d_s) */
+  size_t map_words;       /* words of the chunk-map scratch (d_maps) */
+  size_t digits_x, digits_y;
+  unsigned long long top_candidates[2];
+} decmul_gpu_shard_plan;
+
+enum { DECMUL_SHARD_COL_FWD = 0, DECMUL_SHARD_ROW_FWD = 1, DECMUL_SHARD_ROW_FWD_CONV = 2, DECMUL_SHARD_COL_INV = 3 };
+
+int decmul_gpu_shard_plan_create(decmul_gpu_ctx* ctx, size_t digits_x, size_t digits_y, int ranks,
+                                 decmul_gpu_shard_plan* plan);
+int decmul_gpu_shard_pack(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int rank, const char* d_digits,
+                          size_t nd, uint64_t* d_out, void* stream);
+int decmul_gpu_shard_transform(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int rank, int stage,
+                               const uint64_t* d_src1, const uint64_t* d_src2, uint64_t* d_dst1, uint64_t* d_dst2,
+                               const uint64_t* d_other1, const uint64_t* d_other2, void* stream);
+int decmul_gpu_shard_reorder(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int to_segments,
+                             const uint64_t* d_src, uint64_t* d_dst, void* stream);
+int decmul_gpu_shard_carry_begin(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int rank,
+                                 const uint64_t* d_z1, const uint64_t* d_z2, const uint64_t halo[4], uint64_t* d_s,
+                                 unsigned* d_maps, unsigned* rank_map, void* stream);
+int decmul_gpu_shard_carry_probe(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int rank,
+                                 unsigned rank_carry_in, const uint64_t* d_z1, const uint64_t* d_z2,
+                                 const uint64_t* d_s, unsigned* d_maps, uint64_t z_out[2], void* stream);
+int decmul_gpu_shard_carry_emit(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int rank,
+                                unsigned rank_carry_in, unsigned long long top, unsigned top_len,
+                                const uint64_t* d_z1, const uint64_t* d_z2, const uint64_t* d_s, unsigned* d_maps,
+                                char* d_out, void* stream);
+
 /* ---- workload generation (not in the reference: its bench_mul draws digits on the host,
  * bench.cpp:107-116). Seeded counter-based splitmix64 digits written in place in HBM:
  * operand j (seed seed0 + j * seed_step) gets n digits at d_out + j * stride; mode 0 uniform

@@ -208,6 +208,96 @@ int decmul_gpu_transpose_2n_x_n(decmul_gpu_ctx* ctx, uint64_t* a, size_t n) {
   LOCKED(ctx, ctx->eng->transpose(2, reinterpret_cast<dmg::u64*>(a), n, n));
 }
 
+}  // extern "C"
+
+namespace {
+dmg::ShardPlan shard_from(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* p) {
+  if (!p) throw std::invalid_argument("shard: null plan");
+  return ctx->eng->shard_plan(p->digits_x, p->digits_y, p->ranks);
+}
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+}  // namespace
+
+extern "C" {
+
+int decmul_gpu_shard_plan_create(decmul_gpu_ctx* ctx, size_t dx, size_t dy, int ranks, decmul_gpu_shard_plan* out) {
+  LOCKED(ctx, {
+    const dmg::ShardPlan sp = ctx->eng->shard_plan(dx, dy, ranks);
+    out->length = sp.pp.N;
+    out->base_exp = sp.pp.base_exp;
+    out->p1 = sp.pp.p1;
+    out->p2 = sp.pp.p2;
+    out->ranks = sp.geom.G;
+    out->col_passes = sp.geom.K;
+    out->rows = sp.geom.Rtot;
+    out->seg_len = sp.geom.Sc;
+    out->col_width = sp.geom.Bc;
+    out->local_len = sp.geom.local_len;
+    const size_t K = sp.geom.local_len + 2, ch = size_t(dmg::kCarryChunk);
+    out->s_words = (K + ch - 1) / ch * ch;
+    out->map_words = (K + ch - 1) / ch;
+    out->digits_x = dx;
+    out->digits_y = dy;
+    out->top_candidates[0] = sp.top_candidates[0];
+    out->top_candidates[1] = sp.top_candidates[1];
+  });
+}
+
+int decmul_gpu_shard_pack(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int rank, const char* d_digits,
+                          size_t nd, uint64_t* d_out, void* stream) {
+  LOCKED(ctx, ctx->eng->shard_pack(shard_from(ctx, plan), rank, d_digits, nd, reinterpret_cast<dmg::u64*>(d_out),
+                                   as_stream(stream)));
+}
+
+int decmul_gpu_shard_transform(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int rank, int stage,
+                               const uint64_t* s1, const uint64_t* s2, uint64_t* d1, uint64_t* d2,
+                               const uint64_t* o1, const uint64_t* o2, void* stream) {
+  LOCKED(ctx, {
+    const dmg::u64* src[2] = {reinterpret_cast<const dmg::u64*>(s1), reinterpret_cast<const dmg::u64*>(s2)};
+    dmg::u64* dst[2] = {reinterpret_cast<dmg::u64*>(d1), reinterpret_cast<dmg::u64*>(d2)};
+    const dmg::u64* oth[2] = {reinterpret_cast<const dmg::u64*>(o1), reinterpret_cast<const dmg::u64*>(o2)};
+    ctx->eng->shard_transform(shard_from(ctx, plan), rank, stage, src, dst, o1 ? oth : nullptr, as_stream(stream));
+  });
+}
+
+int decmul_gpu_shard_reorder(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int to_segments,
+                             const uint64_t* src, uint64_t* dst, void* stream) {
+  LOCKED(ctx, ctx->eng->shard_reorder(shard_from(ctx, plan), to_segments != 0, reinterpret_cast<const dmg::u64*>(src),
+                                      reinterpret_cast<dmg::u64*>(dst), as_stream(stream)));
+}
+
+int decmul_gpu_shard_carry_begin(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int rank,
+                                 const uint64_t* z1, const uint64_t* z2, const uint64_t halo[4], uint64_t* d_s,
+                                 unsigned* d_maps, unsigned* rank_map, void* stream) {
+  LOCKED(ctx, {
+    const dmg::u64 h1[2] = {halo[0], halo[1]}, h2[2] = {halo[2], halo[3]};
+    *rank_map = ctx->eng->shard_carry_begin(shard_from(ctx, plan), rank, reinterpret_cast<const dmg::u64*>(z1),
+                                            reinterpret_cast<const dmg::u64*>(z2), h1, h2,
+                                            reinterpret_cast<dmg::u64*>(d_s), d_maps, as_stream(stream));
+  });
+}
+
+int decmul_gpu_shard_carry_probe(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int rank, unsigned cin,
+                                 const uint64_t* z1, const uint64_t* z2, const uint64_t* d_s, unsigned* d_maps,
+                                 uint64_t z_out[2], void* stream) {
+  LOCKED(ctx, {
+    dmg::u64 z[2];
+    ctx->eng->shard_carry_probe(shard_from(ctx, plan), rank, cin, reinterpret_cast<const dmg::u64*>(z1),
+                                reinterpret_cast<const dmg::u64*>(z2), reinterpret_cast<const dmg::u64*>(d_s),
+                                d_maps, z, as_stream(stream));
+    z_out[0] = z[0];
+    z_out[1] = z[1];
+  });
+}
+
+int decmul_gpu_shard_carry_emit(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int rank, unsigned cin,
+                                unsigned long long top, unsigned top_len, const uint64_t* z1, const uint64_t* z2,
+                                const uint64_t* d_s, unsigned* d_maps, char* d_out, void* stream) {
+  LOCKED(ctx, ctx->eng->shard_carry_emit(shard_from(ctx, plan), rank, cin, top, top_len,
+                                         reinterpret_cast<const dmg::u64*>(z1), reinterpret_cast<const dmg::u64*>(z2),
+                                         reinterpret_cast<const dmg::u64*>(d_s), d_maps, d_out, as_stream(stream)));
+}
+
 int decmul_gpu_generate_digits(decmul_gpu_ctx* ctx, uint64_t seed0, uint64_t seed_step, size_t count, size_t n,
                                size_t stride, int mode, char* d_out, void* stream) {
   LOCKED(ctx, {

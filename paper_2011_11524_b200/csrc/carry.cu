@@ -14,11 +14,14 @@ constexpr int NT = kCarryThreads;
 constexpr int PER = CH / NT;  // limbs per thread
 static_assert(PER == 8, "per-thread limb maps are moved as one 8-byte word");
 
+// Local coefficient i (global k_off + i); i = -2, -1 are the previous rank's halo.
 __device__ __forceinline__ void coeff_digits(const CarryArgs& a, long long i, u64& d0, u64& d1, u64& d2) {
   d0 = d1 = d2 = 0;
-  if (i < 0 || (unsigned long long)i >= a.n) return;
+  if (i < -2 || (i >= 0 && (unsigned long long)i >= a.n)) return;
+  const u64 r1 = i < 0 ? a.halo1[i + 2] : a.z1[i];
+  const u64 r2 = i < 0 ? a.halo2[i + 2] : a.z2[i];
   u64 lo, hi;
-  crt2(a.z1[i], a.z2[i], a.p1, a.p2, a.p2_prime, a.r_tilde, lo, hi);
+  crt2(r1, r2, a.p1, a.p2, a.p2_prime, a.r_tilde, lo, hi);
   if (above_cap(lo, hi, a.coeff_cap_lo, a.coeff_cap_hi)) atomicOr(a.err, kErrCoeffBound);
   split3(a.div, lo, hi, d0, d1, d2);
 }
@@ -32,7 +35,7 @@ __global__ void __launch_bounds__(NT) k_carry_split(CarryArgs a) {
   __shared__ __align__(8) unsigned char mp[CH];
   __shared__ unsigned wsm[NT / 32 + 1];
   const unsigned long long k0 = (unsigned long long)blockIdx.x * CH;
-  const unsigned long long K = a.n + 2;
+  const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const u64 B = a.div.base;
   u64 d0r[PER];
 #pragma unroll
@@ -138,8 +141,8 @@ __global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
   __shared__ __align__(8) unsigned char mp[CH];  // limb maps, then limb carry-ins
   const unsigned long long cbase = (unsigned long long)blockIdx.x * CH;
   const unsigned long long top = a.meta[0];
-  if (cbase > top) return;  // nothing of this chunk is printed (uniform per block)
-  const unsigned long long K = a.n + 2;
+  if (a.k_off + cbase > top) return;  // nothing of this chunk is printed (uniform per block)
+  const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const u64 B = a.div.base;
   // coalesced limb sums (loc = j NT + tid); their maps to shared memory
   u64 s[PER];
@@ -167,9 +170,12 @@ __global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
   __syncthreads();
   const unsigned top_len = unsigned(a.meta[1]);
   const unsigned be = a.base_exp;
-  const unsigned long long khi = cbase + CH - 1 < top ? cbase + CH - 1 : top;
-  const unsigned long long start = limb_pos(khi, top, top_len, be);
-  const unsigned long long end = limb_pos(cbase, top, top_len, be) + (cbase == top ? top_len : be);
+  // global limb range printed by this chunk: [gbase, ghi]
+  const unsigned long long gbase = a.k_off + cbase;
+  const unsigned long long last_local = (cbase + CH < K ? cbase + CH : K) - 1;
+  const unsigned long long ghi = a.k_off + last_local < top ? a.k_off + last_local : top;
+  const unsigned long long start = limb_pos(ghi, top, top_len, be);
+  const unsigned long long end = limb_pos(gbase, top, top_len, be) + (gbase == top ? top_len : be);
   char* g = a.out + start;
   char* sb = buf + (reinterpret_cast<unsigned long long>(g) & 15);
   // digits: each thread prints PER consecutive limbs (a contiguous 8 lambda-byte run)
@@ -177,24 +183,95 @@ __global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int loc = threadIdx.x * PER + j;
-    const unsigned long long k = cbase + loc;
-    if (k > top) break;
+    const unsigned long long k = cbase + loc, kg = a.k_off + k;
+    if (kg > ghi) break;
     u64 v = sg[k] + mp[loc];  // re-read from L1/L2 (this block just streamed it)
     if (v >= B) v -= B;
     if (v >= B) v -= B;
-    write_digits(sb + (limb_pos(k, top, top_len, be) - start), v, k == top ? top_len : be);
+    write_digits(sb + (limb_pos(kg, top, top_len, be) - start), v, kg == top ? top_len : be);
   }
   __syncthreads();
   cta_store_bytes(g, sb, unsigned(end - start), threadIdx.x, NT);
 }
 
+// ---- sharded product: the rank's carry-in comes from the other ranks ----
+
+// Exclusive prefix maps of the chunks (in place in maps[]) and the rank's composed map.
+__global__ void __launch_bounds__(1024) k_carry_prefix(CarryArgs a, unsigned nchunks, unsigned* rank_map) {
+  __shared__ unsigned wsm[1024 / 32 + 1];
+  const unsigned per = (nchunks + 1023) / 1024;
+  const unsigned c0 = threadIdx.x * per;
+  unsigned agg = kIdentityMap;
+  for (unsigned c = c0; c < c0 + per && c < nchunks; ++c) agg = map_compose(a.maps[c], agg);
+  unsigned total;
+  unsigned pre = block_scan_maps<1024>(agg, wsm, &total);
+  for (unsigned c = c0; c < c0 + per && c < nchunks; ++c) {
+    const unsigned m = a.maps[c];
+    a.maps[c] = pre;  // maps of all earlier chunks of this rank
+    pre = map_compose(m, pre);
+  }
+  if (threadIdx.x == 0) *rank_map = total;
+}
+
+// z (the final limb value) at the candidate top limbs this rank owns.
+__global__ void __launch_bounds__(1024) k_carry_probe(CarryArgs a, unsigned rank_cin, u64* z) {
+  __shared__ unsigned wsm[1024 / 32 + 1];
+  const u64 B = a.div.base;
+  const unsigned long long K = a.n + (a.tail ? 2 : 0);
+  for (int t = 0; t < 2; ++t) {
+    const unsigned long long kg = a.top_candidates[t];
+    const bool mine = kg >= a.k_off && kg - a.k_off < K;  // uniform across the block
+    if (!mine) {
+      if (threadIdx.x == 0) z[t] = ~0ull;
+      continue;
+    }
+    const unsigned long long k = kg - a.k_off, cs = k / CH * CH;
+    const unsigned long long len = k - cs, seg = (len + 1023) / 1024;
+    const unsigned long long j0 = cs + threadIdx.x * seg;
+    unsigned m = kIdentityMap;
+    for (unsigned long long j = j0; j < j0 + seg && j < k; ++j) m = map_compose(limb_map(a.s[j], B), m);
+    block_scan_maps<1024>(m, wsm, &m);
+    if (threadIdx.x == 0) {
+      const unsigned c = map_apply(m, map_apply(a.maps[k / CH], rank_cin));
+      u64 v = a.s[k] + c;
+      v -= (v >= B ? B : 0);
+      v -= (v >= B ? B : 0);
+      z[t] = v;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_carry_cin(unsigned* maps, unsigned nchunks, unsigned rank_cin) {
+  const unsigned c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < nchunks) maps[c] = map_apply(maps[c], rank_cin);
+}
+
 }  // namespace
 
 void launch_carry(const CarryArgs& a, cudaStream_t st) {
-  const unsigned long long K = a.n + 2;
+  const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const unsigned nchunks = unsigned((K + CH - 1) / CH);
   k_carry_split<<<nchunks, NT, 0, st>>>(a);
   k_carry_scan<<<1, 1024, 0, st>>>(a, nchunks);
+  k_carry_emit<<<nchunks, NT, 0, st>>>(a);
+}
+
+void launch_carry_shard_begin(const CarryArgs& a, unsigned* rank_map_dev, cudaStream_t st) {
+  const unsigned long long K = a.n + (a.tail ? 2 : 0);
+  const unsigned nchunks = unsigned((K + CH - 1) / CH);
+  k_carry_split<<<nchunks, NT, 0, st>>>(a);
+  k_carry_prefix<<<1, 1024, 0, st>>>(a, nchunks, rank_map_dev);
+}
+
+void launch_carry_shard_probe(const CarryArgs& a, unsigned rank_cin, u64* z_dev, cudaStream_t st) {
+  k_carry_probe<<<1, 1024, 0, st>>>(a, rank_cin, z_dev);
+}
+
+void launch_carry_shard_emit(const CarryArgs& a, unsigned rank_cin, cudaStream_t st) {
+  const unsigned long long K = a.n + (a.tail ? 2 : 0);
+  const unsigned nchunks = unsigned((K + CH - 1) / CH);
+  k_carry_cin<<<(nchunks + 255) / 256, 256, 0, st>>>(a.maps, nchunks, rank_cin);
   k_carry_emit<<<nchunks, NT, 0, st>>>(a);
 }
 

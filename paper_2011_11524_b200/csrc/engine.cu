@@ -280,12 +280,43 @@ ProductPlan Engine::plan_product(std::size_t dx, std::size_t dy, unsigned forced
   return pp;
 }
 
-void Engine::transform_forward(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2],
-                               bool include_last, cudaStream_t st) {
-  const std::size_t m = pl[0]->passes.size();
-  for (std::size_t i = 0; i < m; ++i) {
-    if (i + 1 == m && !include_last) break;
-    const bool first = i == 0;
+// Local geometry of pass i. Unsharded: the whole array. Column phase (i < K): this
+// rank owns columns [q Bc, (q + 1) Bc) of every row of the first K passes' matrix,
+// so pass i keeps its groups, its stride shrinks to S_i / G, and its twiddle column
+// is the global one. Row phase (i >= K): this rank owns whole segments of length Sc,
+// so pass i keeps its stride and owns 1/G of the groups.
+PassLocal Engine::local_pass(const PrimePlan& pl, std::size_t i, const ShardGeom* sg) const {
+  const PassPlan& P = *pl.passes[i];
+  PassLocal L;
+  L.S = P.S;
+  L.logS = P.logS;
+  L.groups = pl.N / (std::size_t(P.R) * P.S);
+  L.ncols = pl.N / std::size_t(P.R);
+  L.tw_logS = P.logS;
+  L.tw_off = 0;
+  L.cb = L.sb = 0;
+  L.off = 0;
+  if (!sg) return L;
+  const std::size_t G = std::size_t(sg->G);
+  L.ncols = sg->local_len / std::size_t(P.R);
+  if (int(i) < sg->K) {
+    L.S = P.S / G;
+    L.logS = __builtin_ctzll(L.S);
+    L.tw_off = std::size_t(sg->q) * sg->Bc;  // valid for the last column pass (S_i = Sc)
+    L.cb = __builtin_ctzll(sg->Bc);
+    L.sb = __builtin_ctzll(sg->Sc);
+    L.off = std::size_t(sg->q) * sg->Bc;
+  } else {
+    L.groups /= G;
+  }
+  return L;
+}
+
+void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2], std::size_t begin,
+                        std::size_t end, const ShardGeom* sg, cudaStream_t st) {
+  for (std::size_t i = begin; i < end; ++i) {
+    const bool first = i == begin;
+    const PassLocal L = local_pass(*pl[0], i, sg);
     if (pl[0]->passes[i]->radix3) {
       Radix3Args a{};
       for (int q = 0; q < np; ++q) {
@@ -296,8 +327,12 @@ void Engine::transform_forward(const PrimePlan* pl[2], int np, const u64* const 
         a.p[q] = pl[q]->p;
         a.lam[q] = pl[q]->lam;
       }
-      a.S = pl[0]->passes[i]->S;
+      a.S = L.S;
       a.lbits = pl[0]->passes[i]->r3_lbits;
+      a.hrow = pl[0]->passes[i]->S >> a.lbits;
+      a.cb = L.cb;
+      a.sb = L.sb;
+      a.off = L.off;
       launch_radix3(false, a, np, st);
     } else {
       PassArgs a{};
@@ -312,19 +347,22 @@ void Engine::transform_forward(const PrimePlan* pl[2], int np, const u64* const 
         a.p[q] = pl[q]->p;
         a.pp[q] = pl[q]->pp;
       }
-      a.S = P.S;
-      a.logS = P.logS;
-      a.G = pl[0]->N / (std::size_t(P.R) * P.S);
-      launch_pass_fwd(P.logR, a, pl[0]->N / std::size_t(P.R), np, st);
+      a.S = L.S;
+      a.logS = L.logS;
+      a.G = L.groups;
+      a.tw_logS = L.tw_logS;
+      a.tw_off = L.tw_off;
+      launch_pass_fwd(P.logR, a, L.ncols, np, st);
     }
     ++launches_;
   }
 }
 
-void Engine::transform_fused_last(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
-                                  cudaStream_t st) {
+void Engine::pass_fused(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
+                        const ShardGeom* sg, cudaStream_t st) {
   const std::size_t m = pl[0]->passes.size();
   const PassPlan& P = *pl[0]->passes[m - 1];
+  const PassLocal L = local_pass(*pl[0], m - 1, sg);
   bool any_table = false;
   for (const auto& ps : pl[0]->passes) any_table |= ps->radix3 || ps->S > 1;
   PassArgs a{};
@@ -342,19 +380,19 @@ void Engine::transform_fused_last(const PrimePlan* pl[2], int np, u64* const dat
   }
   a.S = 1;
   a.logS = 0;
-  a.G = pl[0]->N / std::size_t(P.R);
+  a.G = L.groups;
+  a.tw_logS = 0;
   a.has_final_scale = any_table ? 0 : 1;
-  launch_pass_fused(P.logR, a, pl[0]->N / std::size_t(P.R), np, st);
+  launch_pass_fused(P.logR, a, L.ncols, np, st);
   ++launches_;
 }
 
-void Engine::transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2], bool skip_last,
-                               cudaStream_t st) {
-  const std::size_t m = pl[0]->passes.size();
+void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std::size_t begin, std::size_t end,
+                        const ShardGeom* sg, cudaStream_t st) {
   bool any_table = false;
   for (const auto& ps : pl[0]->passes) any_table |= ps->radix3 || ps->S > 1;
-  for (std::size_t ii = m; ii-- > 0;) {
-    if (ii + 1 == m && skip_last) continue;
+  for (std::size_t ii = end; ii-- > begin;) {
+    const PassLocal L = local_pass(*pl[0], ii, sg);
     if (pl[0]->passes[ii]->radix3) {
       Radix3Args a{};
       for (int q = 0; q < np; ++q) {
@@ -365,8 +403,12 @@ void Engine::transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2
         a.p[q] = pl[q]->p;
         a.lam[q] = pl[q]->lam_inv;
       }
-      a.S = pl[0]->passes[ii]->S;
+      a.S = L.S;
       a.lbits = pl[0]->passes[ii]->r3_lbits;
+      a.hrow = pl[0]->passes[ii]->S >> a.lbits;
+      a.cb = L.cb;
+      a.sb = L.sb;
+      a.off = L.off;
       launch_radix3(true, a, np, st);
     } else {
       PassArgs a{};
@@ -382,14 +424,33 @@ void Engine::transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2
         a.p[q] = pl[q]->p;
         a.pp[q] = pl[q]->pp;
       }
-      a.S = P.S;
-      a.logS = P.logS;
-      a.G = pl[0]->N / (std::size_t(P.R) * P.S);
+      a.S = L.S;
+      a.logS = L.logS;
+      a.G = L.groups;
+      a.tw_logS = L.tw_logS;
+      a.tw_off = L.tw_off;
       a.has_final_scale = (!any_table && ii == 0) ? 1 : 0;
-      launch_pass_inv(P.logR, a, pl[0]->N / std::size_t(P.R), np, st);
+      launch_pass_inv(P.logR, a, L.ncols, np, st);
     }
     ++launches_;
   }
+}
+
+void Engine::transform_forward(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2],
+                               bool include_last, cudaStream_t st) {
+  const std::size_t m = pl[0]->passes.size();
+  passes_fwd(pl, np, src, dst, 0, include_last ? m : (m ? m - 1 : 0), nullptr, st);
+}
+
+void Engine::transform_fused_last(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
+                                  cudaStream_t st) {
+  pass_fused(pl, np, data, other, nullptr, st);
+}
+
+void Engine::transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2], bool skip_last,
+                               cudaStream_t st) {
+  const std::size_t m = pl[0]->passes.size();
+  passes_inv(pl, np, data, 0, skip_last ? (m ? m - 1 : 0) : m, nullptr, st);
 }
 
 void Engine::check_err(cudaStream_t st) {
@@ -555,6 +616,7 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   c.top_candidates[1] = (dsum - 1) / be;
   c.meta = meta_.ptr;
   c.out = dout;
+  c.tail = 1;
   launch_carry(c, st);
   launches_ += 3;
   cuda_check(cudaGetLastError(), "product kernels");
@@ -857,6 +919,7 @@ std::size_t Engine::recover_decimal(const u64* r1, const u64* r2, std::size_t n,
   c.top_candidates[1] = (dsum - 1) / be;
   c.meta = meta_.ptr;
   c.out = dout_.ptr;
+  c.tail = 1;
   launch_carry(c, st);
   cuda_check(cudaGetLastError(), "carry");
   unsigned long long len = 0;
@@ -892,6 +955,175 @@ void Engine::transpose(int kind, u64* a, std::size_t n, std::size_t stride) {
   cuda_check(cudaGetLastError(), "transpose");
   cuda_check(cudaMemcpyAsync(a, X_[0].ptr, total * 8, cudaMemcpyDeviceToHost, st), "d2h");
   cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+}  // namespace dmg
+
+// ---------------- sharded large products ----------------
+
+namespace dmg {
+
+CarryArgs Engine::carry_args(const ProductPlan& pp, const u64* z1, const u64* z2, std::size_t n, char* out) const {
+  const unsigned be = pp.base_exp;
+  const std::size_t lx = (pp.dx + be - 1) / be, ly = (pp.dy + be - 1) / be;
+  const CrtConsts cc = crt_consts(pp.p1, pp.p2);
+  CarryArgs c{};
+  c.z1 = z1;
+  c.z2 = z2;
+  c.n = n;
+  c.p1 = pp.p1;
+  c.p2 = pp.p2;
+  c.p2_prime = cc.p2_prime;
+  c.r_tilde = cc.r_tilde;
+  c.div = div_for(pow10u(be));
+  coeff_cap(be, std::min(lx, ly), c.coeff_cap_lo, c.coeff_cap_hi);
+  c.base_exp = be;
+  c.err = err_.ptr;
+  const unsigned long long dsum = pp.dx + pp.dy;
+  c.top_candidates[0] = dsum >= 2 ? (dsum - 2) / be : 0;
+  c.top_candidates[1] = (dsum - 1) / be;
+  c.meta = meta_.ptr;
+  c.out = out;
+  c.tail = 1;
+  return c;
+}
+
+ShardPlan Engine::shard_plan(std::size_t dx, std::size_t dy, int G) {
+  if (G < 1 || (G & (G - 1))) throw std::invalid_argument("shard: the rank count must be a power of two");
+  ShardPlan sp;
+  sp.pp = plan_product(dx, dy, 0);
+  const PrimePlan& P1 = prime_plan(sp.pp.p1, sp.pp.N);
+  prime_plan(sp.pp.p2, sp.pp.N);
+  const std::size_t m = P1.passes.size();
+  if (!P1.last_pow2 || m < 2) throw std::invalid_argument("shard: product too small to shard");
+  std::size_t Rtot = 1;
+  int K = 0;
+  bool ok = false;
+  for (std::size_t i = 0; i + 1 < m; ++i) {
+    Rtot *= std::size_t(P1.passes[i]->R);
+    K = int(i) + 1;
+    const std::size_t Sc = sp.pp.N / Rtot;
+    if (Rtot % std::size_t(G) == 0 && Sc % std::size_t(G) == 0 && Sc / std::size_t(G) >= std::size_t(kTileW)) {
+      ok = true;
+      break;
+    }
+  }
+  if (!ok) throw std::invalid_argument("shard: product too small for this many ranks");
+  for (int i = 0; i + 1 < K; ++i)
+    if (!P1.passes[i]->radix3) throw std::logic_error("shard: unsupported column-phase pass layout");
+  ShardGeom& g = sp.geom;
+  g.G = G;
+  g.K = K;
+  g.Rtot = Rtot;
+  g.Sc = sp.pp.N / Rtot;
+  g.Bc = g.Sc / std::size_t(G);
+  g.local_len = sp.pp.N / std::size_t(G);
+  const unsigned be = sp.pp.base_exp;
+  sp.lx = (dx + be - 1) / be;
+  sp.ly = (dy + be - 1) / be;
+  sp.min_limbs = std::min(sp.lx, sp.ly);
+  const unsigned long long dsum = dx + dy;
+  sp.top_candidates[0] = dsum >= 2 ? (dsum - 2) / be : 0;
+  sp.top_candidates[1] = (dsum - 1) / be;
+  return sp;
+}
+
+void Engine::shard_pack(const ShardPlan& sp, int q, const char* d_digits, std::size_t nd, u64* d_out, cudaStream_t st) {
+  if (!st) st = stream_;
+  const ShardGeom& g = sp.geom;
+  launch_pack(d_digits, nd, sp.pp.base_exp, d_out, g.local_len, err_.ptr, st, __builtin_ctzll(g.Bc), g.Sc,
+              std::size_t(q) * g.Bc);
+  cuda_check(cudaGetLastError(), "shard pack");
+}
+
+void Engine::shard_transform(const ShardPlan& sp, int q, int stage, const u64* const src[2], u64* const dst[2],
+                             const u64* const other[2], cudaStream_t st) {
+  if (!st) st = stream_;
+  const PrimePlan* pl[2] = {&prime_plan(sp.pp.p1, sp.pp.N), &prime_plan(sp.pp.p2, sp.pp.N)};
+  ShardGeom g = sp.geom;
+  g.q = q;
+  const std::size_t m = pl[0]->passes.size(), K = std::size_t(g.K);
+  const u64* in_place[2] = {dst[0], dst[1]};
+  switch (stage) {
+    case kShardColFwd:
+      passes_fwd(pl, 2, src, dst, 0, K, &g, st);
+      break;
+    case kShardRowFwd:
+      passes_fwd(pl, 2, in_place, dst, K, m, &g, st);
+      break;
+    case kShardRowFwdConv:
+      passes_fwd(pl, 2, in_place, dst, K, m - 1, &g, st);
+      pass_fused(pl, 2, dst, other, &g, st);
+      passes_inv(pl, 2, dst, K, m - 1, &g, st);
+      break;
+    case kShardColInv:
+      passes_inv(pl, 2, dst, 0, K, &g, st);
+      break;
+    default:
+      throw std::invalid_argument("shard: unknown stage");
+  }
+  cuda_check(cudaGetLastError(), "shard transform");
+}
+
+void Engine::shard_reorder(const ShardPlan& sp, bool to_segments, const u64* src, u64* dst, cudaStream_t st) {
+  if (!st) st = stream_;
+  const ShardGeom& g = sp.geom;
+  launch_block_reorder(src, dst, std::size_t(g.G), g.Rtot / std::size_t(g.G), g.Bc, to_segments, st);
+  cuda_check(cudaGetLastError(), "shard reorder");
+}
+
+unsigned Engine::shard_carry_begin(const ShardPlan& sp, int q, const u64* z1, const u64* z2, const u64 h1[2],
+                                   const u64 h2[2], u64* s_buf, unsigned* maps_buf, cudaStream_t st) {
+  if (!st) st = stream_;
+  CarryArgs c = carry_args(sp.pp, z1, z2, sp.geom.local_len, nullptr);
+  c.k_off = std::size_t(q) * sp.geom.local_len;
+  c.halo1[0] = h1[0];
+  c.halo1[1] = h1[1];
+  c.halo2[0] = h2[0];
+  c.halo2[1] = h2[1];
+  c.tail = q == sp.geom.G - 1;
+  c.s = s_buf;
+  c.maps = maps_buf;
+  lens_.ensure(1);
+  unsigned* rmap = reinterpret_cast<unsigned*>(lens_.ptr);
+  launch_carry_shard_begin(c, rmap, st);
+  cuda_check(cudaGetLastError(), "shard carry");
+  unsigned m = 0;
+  cuda_check(cudaMemcpyAsync(&m, rmap, sizeof m, cudaMemcpyDeviceToHost, st), "rank map");
+  check_err(st);
+  return m;
+}
+
+void Engine::shard_carry_probe(const ShardPlan& sp, int q, unsigned rank_cin, const u64* z1, const u64* z2,
+                               const u64* s_buf, unsigned* maps_buf, u64 z_out[2], cudaStream_t st) {
+  if (!st) st = stream_;
+  CarryArgs c = carry_args(sp.pp, z1, z2, sp.geom.local_len, nullptr);
+  c.k_off = std::size_t(q) * sp.geom.local_len;
+  c.tail = q == sp.geom.G - 1;
+  c.s = const_cast<u64*>(s_buf);
+  c.maps = maps_buf;
+  lens_.ensure(2);
+  u64* zd = reinterpret_cast<u64*>(lens_.ptr);
+  launch_carry_shard_probe(c, rank_cin, zd, st);
+  cuda_check(cudaGetLastError(), "shard probe");
+  cuda_check(cudaMemcpyAsync(z_out, zd, 2 * sizeof(u64), cudaMemcpyDeviceToHost, st), "probe");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+void Engine::shard_carry_emit(const ShardPlan& sp, int q, unsigned rank_cin, unsigned long long top, unsigned top_len,
+                              const u64* z1, const u64* z2, const u64* s_buf, unsigned* maps_buf, char* d_out,
+                              cudaStream_t st) {
+  if (!st) st = stream_;
+  CarryArgs c = carry_args(sp.pp, z1, z2, sp.geom.local_len, d_out);
+  c.k_off = std::size_t(q) * sp.geom.local_len;
+  c.tail = q == sp.geom.G - 1;
+  c.s = const_cast<u64*>(s_buf);
+  c.maps = maps_buf;
+  const unsigned long long meta[3] = {top, top_len, top_len + top * sp.pp.base_exp};
+  cuda_check(cudaMemcpyAsync(meta_.ptr, meta, sizeof meta, cudaMemcpyHostToDevice, st), "meta");
+  launch_carry_shard_emit(c, rank_cin, st);
+  cuda_check(cudaGetLastError(), "shard emit");
+  check_err(st);
 }
 
 }  // namespace dmg

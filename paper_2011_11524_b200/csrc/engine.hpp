@@ -84,6 +84,39 @@ struct ProductPlan {
   bool large_pair = false;
 };
 
+// Distribution of one large product over G ranks. The first K passes
+// (their rows multiply to Rtot, a multiple of G) run column-sharded: rank q owns
+// columns [q Bc, (q + 1) Bc) of the Rtot x Sc matrix. An all-to-all then gives each
+// rank Rtot / G whole segments of length Sc for the remaining passes, the pointwise
+// product and the first inverse passes; the inverse undoes this, and a last exchange
+// leaves rank q with the natural-order coefficients [q N / G, (q + 1) N / G) for the
+// distributed carry.
+struct ShardGeom {
+  int G = 1, q = 0, K = 0;
+  std::size_t Rtot = 1, Sc = 0, Bc = 0, local_len = 0;
+};
+
+struct ShardPlan {
+  ProductPlan pp;
+  ShardGeom geom;  // q unset
+  std::size_t lx = 0, ly = 0, min_limbs = 0;
+  unsigned long long top_candidates[2] = {0, 0};
+};
+
+// Local geometry of one pass on a (possibly sharded) array.
+struct PassLocal {
+  unsigned long long S = 0, groups = 0, ncols = 0, tw_off = 0, off = 0;
+  int logS = 0, tw_logS = 0, cb = 0, sb = 0;
+};
+
+enum ShardStage {
+  kShardColFwd = 0,        // passes [0, K): src (packed limbs) -> dst, column layout
+  kShardRowFwd = 1,        // passes [K, m): segment layout, in place
+  kShardRowFwdConv = 2,    // passes [K, m-1), last pass fused with the pointwise product
+                           // against `other` (null = square) and its inverse, then inverse [K, m-1)
+  kShardColInv = 3,        // inverse passes [0, K): column layout, in place
+};
+
 class Engine {
  public:
   explicit Engine(int device);
@@ -122,6 +155,23 @@ class Engine {
   // In-place transposes (reference transpose.cpp) of a host matrix through the device.
   void transpose(int kind, u64* a, std::size_t n, std::size_t stride);
 
+  // ---- sharded large products: device steps on caller-owned buffers (both primes) ----
+  ShardPlan shard_plan(std::size_t dx, std::size_t dy, int G);
+  // digits of one operand (full string, device) -> this rank's column-layout limbs
+  void shard_pack(const ShardPlan& sp, int q, const char* d_digits, std::size_t nd, u64* d_out, cudaStream_t st);
+  void shard_transform(const ShardPlan& sp, int q, int stage, const u64* const src[2], u64* const dst[2],
+                       const u64* const other[2], cudaStream_t st);
+  void shard_reorder(const ShardPlan& sp, bool to_segments, const u64* src, u64* dst, cudaStream_t st);
+  // carry over this rank's natural block; halo = residues (p1: h1[0..1], p2: h2[0..1]) of the
+  // two coefficients before the block. Returns the rank's composed carry map (syncs).
+  unsigned shard_carry_begin(const ShardPlan& sp, int q, const u64* z1, const u64* z2, const u64 h1[2],
+                             const u64 h2[2], u64* s_buf, unsigned* maps_buf, cudaStream_t st);
+  void shard_carry_probe(const ShardPlan& sp, int q, unsigned rank_cin, const u64* z1, const u64* z2,
+                         const u64* s_buf, unsigned* maps_buf, u64 z_out[2], cudaStream_t st);
+  void shard_carry_emit(const ShardPlan& sp, int q, unsigned rank_cin, unsigned long long top, unsigned top_len,
+                        const u64* z1, const u64* z2, const u64* s_buf, unsigned* maps_buf, char* d_out,
+                        cudaStream_t st);
+
   const PrimePlan& prime_plan(u64 p, std::size_t N);
   // Length of the last product (after its stream was synchronised); raises its errors.
   std::size_t result_length();
@@ -142,6 +192,14 @@ class Engine {
   void transform_fused_last(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
                             cudaStream_t st);
   void transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2], bool skip_last, cudaStream_t st);
+  PassLocal local_pass(const PrimePlan& pl, std::size_t i, const ShardGeom* sg) const;
+  void passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2], std::size_t begin,
+                  std::size_t end, const ShardGeom* sg, cudaStream_t st);
+  void pass_fused(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
+                  const ShardGeom* sg, cudaStream_t st);
+  void passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std::size_t begin, std::size_t end,
+                  const ShardGeom* sg, cudaStream_t st);
+  CarryArgs carry_args(const ProductPlan& pp, const u64* z1, const u64* z2, std::size_t n, char* out) const;
   void check_err(cudaStream_t st);
 
   int device_ = 0;

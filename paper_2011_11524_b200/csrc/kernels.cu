@@ -27,12 +27,13 @@ constexpr int NT = kPassThreads;
 template <int LOGR, bool ROWS>
 struct Geom {
   unsigned long long base, s0;
-  unsigned long long S;
-  int logS;
+  unsigned long long S, tw_col;
+  int logS, tw_logS;
   __device__ __forceinline__ Geom(const PassArgs& a) {
     const unsigned long long tile = blockIdx.x / a.np;
     S = a.S;
     logS = a.logS;
+    tw_logS = a.tw_logS;
     if (ROWS) {
       // group-fastest tile order: the G groups share the twiddle rows T[f][s0..s0+15],
       // so consecutive CTAs reuse them from L2 instead of re-streaming them from HBM
@@ -44,13 +45,14 @@ struct Geom {
       s0 = 0;
       base = c0 << LOGR;
     }
+    tw_col = a.tw_off + s0;
   }
   __device__ __forceinline__ unsigned long long at(int r, int w) const {
     return ROWS ? base + ((unsigned long long)r << logS) + w : base + ((unsigned long long)w << LOGR) + r;
   }
   // inter-pass twiddle omega_M^{f s} for the element at row r (frequency bitrev(r) after DIF)
   __device__ __forceinline__ const TwPair& tw(const TwPair* T, int r, int w) const {
-    return T[((unsigned long long)bitrev(r, LOGR) << logS) + s0 + w];
+    return T[((unsigned long long)bitrev(r, LOGR) << tw_logS) + tw_col + w];
   }
 };
 
@@ -289,10 +291,11 @@ __global__ void k_radix3_fwd(Radix3Args a) {
   const TwPair* __restrict__ lo = pr ? a.lo[1] : a.lo[0];
   const TwPair* __restrict__ hi = pr ? a.hi[1] : a.hi[0];
   const TwPair lam = pr ? a.lam[1] : a.lam[0];
-  const unsigned long long L = 1ull << a.lbits, H = S >> a.lbits;
+  const unsigned long long L = 1ull << a.lbits, H = a.hrow;
   for (unsigned long long s = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long sl = s & (L - 1), sh = s >> a.lbits;
+    const unsigned long long sg = ((s >> a.cb) << a.sb) + a.off + (s & ((1ull << a.cb) - 1));  // global column
+    const unsigned long long sl = sg & (L - 1), sh = sg >> a.lbits;
     const u64 x0 = src[s], x1 = src[S + s], x2 = src[2 * S + s];
     const u64 t = shoup_mul(mod_sub(x1, x2, p), lam, p);
     const u64 y0 = mod_add(mod_add(x0, x1, p), x2, p);
@@ -315,10 +318,11 @@ __global__ void k_radix3_inv(Radix3Args a) {
   const TwPair* __restrict__ lo = pr ? a.lo[1] : a.lo[0];
   const TwPair* __restrict__ hi = pr ? a.hi[1] : a.hi[0];
   const TwPair lam = pr ? a.lam[1] : a.lam[0];
-  const unsigned long long L = 1ull << a.lbits, H = S >> a.lbits;
+  const unsigned long long L = 1ull << a.lbits, H = a.hrow;
   for (unsigned long long s = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; s < S;
        s += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long sl = s & (L - 1), sh = s >> a.lbits;
+    const unsigned long long sg = ((s >> a.cb) << a.sb) + a.off + (s & ((1ull << a.cb) - 1));  // global column
+    const unsigned long long sl = sg & (L - 1), sh = sg >> a.lbits;
     const u64 y0 = shoup_mul(src[s], hi[sh], p);  // lo[0][.] = 1
     const u64 y1 = shoup_mul(shoup_mul(src[S + s], lo[L + sl], p), hi[H + sh], p);
     const u64 y2 = shoup_mul(shoup_mul(src[2 * S + s], lo[2 * L + sl], p), hi[2 * H + sh], p);
@@ -405,14 +409,19 @@ __device__ __forceinline__ u64 parse_digits(const char* buf, int s, int n, unsig
 }
 
 __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d, unsigned long long nd, unsigned be,
-                                                     u64* __restrict__ limbs, unsigned long long total, unsigned* err) {
+                                                     u64* __restrict__ limbs, unsigned long long total, unsigned* err,
+                                                     int row_bits, unsigned long long row_stride,
+                                                     unsigned long long off) {
   __shared__ __align__(16) char smem[kPackLimbs * 17 + 96];
   char* buf = smem + 32;  // parse_digits may read up to 24 bytes before a limb and 8 past it
   const unsigned long long nl = (nd + be - 1) / be;
+  const unsigned long long rmask = row_bits >= 63 ? ~0ull : (1ull << row_bits) - 1;
   unsigned bad = 0;
-  for (unsigned long long t0 = (unsigned long long)blockIdx.x * kPackLimbs; t0 < total;
-       t0 += (unsigned long long)gridDim.x * kPackLimbs) {
-    const unsigned long long t = t0 + threadIdx.x;
+  for (unsigned long long i0 = (unsigned long long)blockIdx.x * kPackLimbs; i0 < total;
+       i0 += (unsigned long long)gridDim.x * kPackLimbs) {
+    // local limbs i0 .. i0 + 255 are global limbs t0 .. t0 + 255 (rows hold >= 256 limbs)
+    const unsigned long long t0 = (row_bits >= 63 ? 0 : (i0 >> row_bits) * row_stride) + off + (i0 & rmask);
+    const unsigned long long t = t0 + threadIdx.x, li = i0 + threadIdx.x;
     // digit span of limbs [t0, min(t0 + kPackLimbs, nl)): [lo, hi)
     const long long hi = (long long)nd - (long long)(t0 * be);
     const long long lo = hi - (long long)kPackLimbs * be > 0 ? hi - (long long)kPackLimbs * be : 0;
@@ -438,12 +447,56 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d,
         if (begin == 0 && nd > 1 && d[0] == '0') atomicOr(err, kErrLeadingZero);
       }
       __syncthreads();
-      if (t < total) limbs[t] = limb;
-    } else if (t < total) {
-      limbs[t] = 0;  // zero padding to the transform length
+      if (li < total) limbs[li] = limb;
+    } else if (li < total) {
+      limbs[li] = 0;  // zero padding to the transform length
     }
   }
   if (bad) atomicOr(err, kErrBadDigit);
+}
+
+// Column-sharded pack for rows narrower than one 256-limb block: one limb per thread.
+__global__ void k_pack_rows(const char* __restrict__ d, unsigned long long nd, unsigned be, u64* __restrict__ limbs,
+                            unsigned long long total, unsigned* err, int row_bits, unsigned long long row_stride,
+                            unsigned long long off) {
+  const unsigned long long nl = (nd + be - 1) / be;
+  const unsigned long long rmask = (1ull << row_bits) - 1;
+  unsigned bad = 0;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long t = (i >> row_bits) * row_stride + off + (i & rmask);
+    u64 limb = 0;
+    if (t < nl) {
+      const long long end = (long long)nd - (long long)(t * be);
+      const long long begin = end > (long long)be ? end - (long long)be : 0;
+      for (long long j = begin; j < end; ++j) {
+        const unsigned c = (unsigned char)d[j] - '0';
+        bad |= c > 9;
+        limb = limb * 10 + c;
+      }
+      if (begin == 0 && nd > 1 && d[0] == '0') atomicOr(err, kErrLeadingZero);
+    }
+    limbs[i] = limb;
+  }
+  if (bad) atomicOr(err, kErrBadDigit);
+}
+
+// [peer][row][c] <-> [row][peer][c]: the all-to-all block layout vs contiguous segments.
+__global__ void k_block_reorder(const u64* __restrict__ src, u64* __restrict__ dst, unsigned long long peers,
+                                unsigned long long rows, unsigned long long width, int to_segments) {
+  const unsigned long long total = peers * rows * width;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long c = i % width, t = i / width;
+    // i indexes the destination; decode its (row, peer) in the destination order
+    if (to_segments) {
+      const unsigned long long peer = t % peers, row = t / peers;
+      dst[i] = src[(peer * rows + row) * width + c];
+    } else {
+      const unsigned long long row = t % rows, peer = t / rows;
+      dst[i] = src[(row * peers + peer) * width + c];
+    }
+  }
 }
 
 __global__ void k_pointwise(u64* a, const u64* b, unsigned long long n, u64 p, u64 pp) {
@@ -567,8 +620,17 @@ void launch_gen_pass_table(TwPair* out, u64 root_mont, u64 scale_mont, int R, in
 }
 
 void launch_pack(const char* digits, unsigned long long nd, unsigned be, u64* limbs, unsigned long long total,
-                 unsigned* err, cudaStream_t st) {
-  k_pack<<<grid_for(total, 256), 256, 0, st>>>(digits, nd, be, limbs, total, err);
+                 unsigned* err, cudaStream_t st, int row_bits, unsigned long long row_stride,
+                 unsigned long long off) {
+  if (row_bits < 8)
+    k_pack_rows<<<grid_for(total, 256), 256, 0, st>>>(digits, nd, be, limbs, total, err, row_bits, row_stride, off);
+  else
+    k_pack<<<grid_for(total, 256), 256, 0, st>>>(digits, nd, be, limbs, total, err, row_bits, row_stride, off);
+}
+void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, unsigned long long rows,
+                          unsigned long long width, bool to_segments, cudaStream_t st) {
+  const unsigned long long total = peers * rows * width;
+  k_block_reorder<<<grid_for(total, 256), 256, 0, st>>>(src, dst, peers, rows, width, to_segments ? 1 : 0);
 }
 void launch_pointwise(u64* a, const u64* b, unsigned long long n, u64 p, u64 pp, cudaStream_t st) {
   k_pointwise<<<grid_for(n, 256), 256, 0, st>>>(a, b, n, p, pp);

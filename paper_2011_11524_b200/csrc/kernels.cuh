@@ -37,6 +37,10 @@ struct PassArgs {
   int has_final_scale;
   int np;                  // primes in this launch; blockIdx.x = tile * np + prime (primes of one tile adjacent)
   unsigned long long G;    // groups of R x S (row passes: tiles run group-fastest)
+  // twiddle addressing: T[f << tw_logS + tw_off + s]. Unsharded: tw_logS = logS, tw_off = 0.
+  // Column-sharded pass (this rank owns columns [tw_off, tw_off + S) of a global S' = 2^tw_logS).
+  int tw_logS;
+  unsigned long long tw_off;
 };
 
 // Radix-3 pass over N = 3 S. The twiddle omega_N^{+-f s} (times the convolution
@@ -49,8 +53,13 @@ struct Radix3Args {
   const TwPair* hi[2];  // 3 x (S / L)
   u64 p[2];
   TwPair lam[2];        // omega_3 (forward) or omega_3^-1 (inverse)
-  unsigned long long S;
+  unsigned long long S;    // local columns
   int lbits;
+  unsigned long long hrow;  // entries per f-row of hi (global S >> lbits)
+  // local column l -> global column s = ((l >> cb) << sb) + off + (l & (2^cb - 1)).
+  // Unsharded: cb = sb = 0, off = 0 (s = l).
+  int cb, sb;
+  unsigned long long off;
 };
 
 // Launchers (kernels.cu).
@@ -61,8 +70,15 @@ void launch_radix3(bool inverse, const Radix3Args& a, int nprimes, cudaStream_t 
 
 void launch_gen_pass_table(TwPair* out, u64 root_m, u64 scale, int R, int logR, unsigned long long S, u64 p,
                            u64 recip, cudaStream_t st);
+// Local limb i is global limb ((i >> row_bits) * row_stride) + off + (i & (2^row_bits - 1)):
+// unsharded packs use row_bits = 63, off = 0 (limb i = i). Sharded packs need 2^row_bits >= 256.
 void launch_pack(const char* digits, unsigned long long nd, unsigned base_exp, u64* limbs,
-                 unsigned long long nlimbs_total, unsigned* err, cudaStream_t st);
+                 unsigned long long nlimbs_total, unsigned* err, cudaStream_t st, int row_bits = 63,
+                 unsigned long long row_stride = 0, unsigned long long off = 0);
+// Block reorder between the all-to-all layout [peer][row][c] and segment rows [row][peer][c]
+// (c < width, row < rows, peer < peers); to_segments selects the direction.
+void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, unsigned long long rows,
+                          unsigned long long width, bool to_segments, cudaStream_t st);
 void launch_pointwise(u64* a, const u64* b, unsigned long long n, u64 p, u64 pp, cudaStream_t st);
 void launch_mont_scale(u64* a, unsigned long long n, u64 factor, u64 p, u64 pp, cudaStream_t st);
 void launch_gather(const u64* src, u64* dst, const unsigned long long* map, unsigned long long n, cudaStream_t st);
@@ -82,10 +98,20 @@ struct CarryArgs {
   unsigned long long top_candidates[2];
   unsigned long long* meta;  // [0] top limb index, [1] top digit count, [2] output length
   char* out;
+  // Sharded product (rank owns global coefficients [k_off, k_off + n)); unsharded: all zero / tail = 1.
+  unsigned long long k_off;
+  u64 halo1[2], halo2[2];  // residues of global coefficients k_off - 2, k_off - 1 (zeros on the first rank)
+  int tail;                // this rank also emits the two trailing limbs N, N + 1 (last rank)
 };
 constexpr int kCarryChunk = 2048;
 constexpr int kCarryThreads = 256;
 void launch_carry(const CarryArgs& a, cudaStream_t st);
+// Sharded carry: split + per-chunk exclusive prefix maps; *rank_map_dev gets the rank's composed map.
+void launch_carry_shard_begin(const CarryArgs& a, unsigned* rank_map_dev, cudaStream_t st);
+// z at the global limbs `cand` owned by this rank (others UINT64_MAX), given the carry into the rank.
+void launch_carry_shard_probe(const CarryArgs& a, unsigned rank_cin, u64* z_dev, cudaStream_t st);
+// Convert prefix maps to carry-ins, then print this rank's limbs at their global positions.
+void launch_carry_shard_emit(const CarryArgs& a, unsigned rank_cin, cudaStream_t st);
 
 // One-CTA-per-product batch kernel (small transforms).
 struct SmallArgs {
