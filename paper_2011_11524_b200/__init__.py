@@ -54,7 +54,9 @@ EXPORTED_SYMBOLS = [
     "decmul_gpu_inverse_transform", "decmul_gpu_pointwise_product", "decmul_gpu_pack",
     "decmul_gpu_recover_decimal", "decmul_gpu_transpose_square_sub", "decmul_gpu_transpose_n_x_2n",
     "decmul_gpu_transpose_2n_x_n", "decmul_gpu_generate_digits", "decmul_gpu_measure_modmul_rate",
-    "decmul_gpu_get_stats",
+    "decmul_gpu_get_stats", "decmul_gpu_shard_plan_create", "decmul_gpu_shard_pack", "decmul_gpu_shard_transform",
+    "decmul_gpu_shard_reorder", "decmul_gpu_shard_carry_begin", "decmul_gpu_shard_carry_probe",
+    "decmul_gpu_shard_carry_emit",
 ]
 
 

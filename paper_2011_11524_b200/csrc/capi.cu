@@ -220,9 +220,16 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 extern "C" {
 
+static void fill_shard_plan(const dmg::ShardPlan& sp, size_t dx, size_t dy, decmul_gpu_shard_plan* out);
+
+// ctx == NULL plans on the host only (no device tables), e.g. for CPU-side drivers.
 int decmul_gpu_shard_plan_create(decmul_gpu_ctx* ctx, size_t dx, size_t dy, int ranks, decmul_gpu_shard_plan* out) {
-  LOCKED(ctx, {
-    const dmg::ShardPlan sp = ctx->eng->shard_plan(dx, dy, ranks);
+  if (!ctx) return guarded(nullptr, [&] { fill_shard_plan(dmg::make_shard_plan(dx, dy, ranks), dx, dy, out); });
+  LOCKED(ctx, fill_shard_plan(ctx->eng->shard_plan(dx, dy, ranks), dx, dy, out));
+}
+
+static void fill_shard_plan(const dmg::ShardPlan& sp, size_t dx, size_t dy, decmul_gpu_shard_plan* out) {
+  {
     out->length = sp.pp.N;
     out->base_exp = sp.pp.base_exp;
     out->p1 = sp.pp.p1;
@@ -240,7 +247,7 @@ int decmul_gpu_shard_plan_create(decmul_gpu_ctx* ctx, size_t dx, size_t dy, int 
     out->digits_y = dy;
     out->top_candidates[0] = sp.top_candidates[0];
     out->top_candidates[1] = sp.top_candidates[1];
-  });
+  }
 }
 
 int decmul_gpu_shard_pack(decmul_gpu_ctx* ctx, const decmul_gpu_shard_plan* plan, int rank, const char* d_digits,

@@ -141,8 +141,7 @@ void Engine::build_passes(PrimePlan& pl) {
   HostField F(pl.p);
   const u64 recip = recip_of(pl.p << __builtin_clzll(pl.p));
   std::vector<std::pair<bool, int>> spec;  // (radix3, logR)
-  if (pl.three) spec.push_back({true, 0});
-  for (int lg : split_log(pl.k, kMaxPassLog)) spec.push_back({false, lg});
+  for (int r : pass_radices(pl.N, kMaxPassLog)) spec.push_back({r == 3, r == 3 ? 0 : __builtin_ctz(unsigned(r))});
   std::size_t done = 1;
   int last_table = -1;
   for (std::size_t i = 0; i < spec.size(); ++i) {
@@ -988,35 +987,24 @@ CarryArgs Engine::carry_args(const ProductPlan& pp, const u64* z1, const u64* z2
   return c;
 }
 
-ShardPlan Engine::shard_plan(std::size_t dx, std::size_t dy, int G) {
-  if (G < 1 || (G & (G - 1))) throw std::invalid_argument("shard: the rank count must be a power of two");
+// Host-only planning (no device): usable without a GPU context.
+ShardPlan make_shard_plan(std::size_t dx, std::size_t dy, int G) {
   ShardPlan sp;
-  sp.pp = plan_product(dx, dy, 0);
-  const PrimePlan& P1 = prime_plan(sp.pp.p1, sp.pp.N);
-  prime_plan(sp.pp.p2, sp.pp.N);
-  const std::size_t m = P1.passes.size();
-  if (!P1.last_pow2 || m < 2) throw std::invalid_argument("shard: product too small to shard");
-  std::size_t Rtot = 1;
-  int K = 0;
-  bool ok = false;
-  for (std::size_t i = 0; i + 1 < m; ++i) {
-    Rtot *= std::size_t(P1.passes[i]->R);
-    K = int(i) + 1;
-    const std::size_t Sc = sp.pp.N / Rtot;
-    if (Rtot % std::size_t(G) == 0 && Sc % std::size_t(G) == 0 && Sc / std::size_t(G) >= std::size_t(kTileW)) {
-      ok = true;
-      break;
-    }
-  }
-  if (!ok) throw std::invalid_argument("shard: product too small for this many ranks");
-  for (int i = 0; i + 1 < K; ++i)
-    if (!P1.passes[i]->radix3) throw std::logic_error("shard: unsupported column-phase pass layout");
+  const PairChoice pc = choose_pair(dx, dy, 0, /*allow_large=*/true);
+  sp.pp.dx = dx;
+  sp.pp.dy = dy;
+  sp.pp.base_exp = pc.bp.base_exp;
+  sp.pp.N = pc.bp.length;
+  sp.pp.p1 = pc.p1;
+  sp.pp.p2 = pc.p2;
+  sp.pp.large_pair = pc.large_pair;
+  const ShardShape sh = shard_shape(sp.pp.N, pass_radices(sp.pp.N, kMaxPassLog), G, std::size_t(kTileW));
   ShardGeom& g = sp.geom;
   g.G = G;
-  g.K = K;
-  g.Rtot = Rtot;
-  g.Sc = sp.pp.N / Rtot;
-  g.Bc = g.Sc / std::size_t(G);
+  g.K = sh.K;
+  g.Rtot = sh.Rtot;
+  g.Sc = sh.Sc;
+  g.Bc = sh.Bc;
   g.local_len = sp.pp.N / std::size_t(G);
   const unsigned be = sp.pp.base_exp;
   sp.lx = (dx + be - 1) / be;
@@ -1025,6 +1013,13 @@ ShardPlan Engine::shard_plan(std::size_t dx, std::size_t dy, int G) {
   const unsigned long long dsum = dx + dy;
   sp.top_candidates[0] = dsum >= 2 ? (dsum - 2) / be : 0;
   sp.top_candidates[1] = (dsum - 1) / be;
+  return sp;
+}
+
+ShardPlan Engine::shard_plan(std::size_t dx, std::size_t dy, int G) {
+  ShardPlan sp = make_shard_plan(dx, dy, G);
+  prime_plan(sp.pp.p1, sp.pp.N);  // device tables
+  prime_plan(sp.pp.p2, sp.pp.N);
   return sp;
 }
 

@@ -103,6 +103,9 @@ struct ShardPlan {
   unsigned long long top_candidates[2] = {0, 0};
 };
 
+// Host-only shard planning (no device): decmul_gpu_shard_plan_create with a NULL context.
+ShardPlan make_shard_plan(std::size_t dx, std::size_t dy, int G);
+
 // Local geometry of one pass on a (possibly sharded) array.
 struct PassLocal {
   unsigned long long S = 0, groups = 0, ncols = 0, tw_off = 0, off = 0;

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 namespace dmg {
 
@@ -152,6 +153,47 @@ inline BasePlan select_base_and_length(std::size_t dx, std::size_t dy, u64 p1, u
     return {be, len};
   }
   throw OperandTooLarge("operands violate the coefficient bound at every supported base");
+}
+
+// Pass radices of a length-N transform (N = 2^k or 3 * 2^k): a radix-3 pass first when
+// 3 | N, then the power of two split into ceil(k / maxlog) balanced radix-2^e passes,
+// larger ones first (each tile of 2^e x 16 columns must fit shared memory).
+inline std::vector<int> pass_radices(std::size_t N, int maxlog) {
+  std::vector<int> r;
+  std::size_t c = N;
+  if (N % 3 == 0) {
+    r.push_back(3);
+    c = N / 3;
+  }
+  const int k = c > 1 ? __builtin_ctzll(c) : 0;
+  if (k > 0) {
+    const int m = (k + maxlog - 1) / maxlog;
+    for (int i = 0; i < m; ++i) r.push_back(1 << (k / m + (i < k % m ? 1 : 0)));
+  }
+  return r;
+}
+
+// Column/row split of the passes for G ranks; see engine.hpp ShardGeom.
+struct ShardShape {
+  int K = 0;
+  std::size_t Rtot = 1, Sc = 0, Bc = 0;
+};
+inline ShardShape shard_shape(std::size_t N, const std::vector<int>& radices, int G, std::size_t min_width) {
+  if (G < 1 || (G & (G - 1))) throw std::invalid_argument("shard: the rank count must be a power of two");
+  if (radices.size() < 2 || radices.back() == 3) throw std::invalid_argument("shard: product too small to shard");
+  ShardShape s;
+  for (std::size_t i = 0; i + 1 < radices.size(); ++i) {
+    s.Rtot *= std::size_t(radices[i]);
+    s.K = int(i) + 1;
+    s.Sc = N / s.Rtot;
+    if (s.Rtot % std::size_t(G) == 0 && s.Sc % std::size_t(G) == 0 && s.Sc / std::size_t(G) >= min_width) {
+      s.Bc = s.Sc / std::size_t(G);
+      for (int j = 0; j + 1 < s.K; ++j)
+        if (radices[j] != 3) throw std::logic_error("shard: unsupported column-phase pass layout");
+      return s;
+    }
+  }
+  throw std::invalid_argument("shard: product too small for this many ranks");
 }
 
 struct PairChoice {
