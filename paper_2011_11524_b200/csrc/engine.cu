@@ -2,6 +2,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <stdexcept>
 
@@ -96,6 +97,12 @@ std::size_t PrimePlan::position_of(std::size_t spec) const {
 Engine::Engine(int device) : device_(device) {
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  for (auto& s : pipe_) cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaEventCreateWithFlags(&pipe_ev_, cudaEventDisableTiming), "cudaEventCreate");
+  for (int i = 0; i < kMaxChunks; ++i) {
+    cuda_check(cudaEventCreateWithFlags(&up_ev_[i], cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&done_ev_[i], cudaEventDisableTiming), "cudaEventCreate");
+  }
   err_.ensure(1);
   meta_.ensure(4);
   cuda_check(cudaMemsetAsync(err_.ptr, 0, sizeof(unsigned), stream_), "memset");
@@ -103,7 +110,15 @@ Engine::Engine(int device) : device_(device) {
 
 Engine::~Engine() {
   cudaStreamSynchronize(stream_);
+  for (auto s : pipe_) cudaStreamSynchronize(s);
   plans_.clear();
+  for (auto s : pipe_) cudaStreamDestroy(s);
+  cudaEventDestroy(pipe_ev_);
+  for (int i = 0; i < kMaxChunks; ++i) {
+    cudaEventDestroy(up_ev_[i]);
+    cudaEventDestroy(done_ev_[i]);
+  }
+  if (host_lens_) cudaFreeHost(host_lens_);
   cudaStreamDestroy(stream_);
 }
 
@@ -743,6 +758,12 @@ void Engine::multiply_batch_host(std::size_t count, const char* xs, std::size_t 
                                  const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
                                  std::size_t out_stride, std::size_t* lens) {
   if (count == 0) return;
+  if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
+  const ProductPlan pp = plan_product(nx, ny, 0);
+  if (prime_plan(pp.p1, pp.N).small_ok && prime_plan(pp.p2, pp.N).small_ok && count >= 2 * kPipe) {
+    batch_host_pipelined(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, lens);
+    return;
+  }
   const std::size_t xb = (count - 1) * x_stride + nx, yb = (count - 1) * y_stride + ny;
   const std::size_t ob = count * out_stride;
   din_x_.ensure(xb);
@@ -759,6 +780,98 @@ void Engine::multiply_batch_host(std::size_t count, const char* xs, std::size_t 
   cuda_check(cudaMemcpyAsync(outs, dout_.ptr, ob, cudaMemcpyDeviceToHost, stream_), "d2h");
   check_err(stream_);
   for (std::size_t i = 0; i < count; ++i) lens[i] = std::size_t(l[i]);
+}
+
+// Chunks of products flow through three streams — upload, compute, download — linked by
+// per-chunk events, so chunk c's H2D overlaps chunk c-1's kernel and chunk c-2's D2H (one
+// copy engine per direction; PCIe is full duplex). One-CTA products share no device
+// workspace, so the chunks are independent.
+void Engine::batch_host_pipelined(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
+                                  const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
+                                  std::size_t out_stride, std::size_t* lens) {
+  // whole waves of the one-CTA kernel per chunk (a partial wave costs a full one)
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_);
+  const ProductPlan pp = plan_product(nx, ny, 0);
+  const PrimePlan& P1 = prime_plan(pp.p1, pp.N);
+  const std::size_t wave = std::size_t(sms) * std::max(1, small_resident_ctas(P1.k, P1.three, 0));
+  // ~5 equal chunks of whole waves: fewer chunks lengthen pipeline fill and drain, more
+  // lose duplex copy throughput (measured on B200: both directions together sustain
+  // ~41-49 GB/s each for 9-20 MB copies, ~36 GB/s for 4 MB ones).
+  // DECMUL_PIPE_CHUNKS=k forces k equal chunks (tuning).
+  std::size_t k = 5;
+  if (const char* e = std::getenv("DECMUL_PIPE_CHUNKS")) k = std::max<std::size_t>(1, std::strtoull(e, 0, 10));
+  k = std::min<std::size_t>(std::min<std::size_t>(k, count), kMaxChunks);
+  std::size_t per = (count + k - 1) / k;
+  if (!std::getenv("DECMUL_PIPE_CHUNKS") && per > wave) per = (per + wave / 2) / wave * wave;
+  while ((count + per - 1) / per > std::size_t(kMaxChunks)) per += wave;
+  std::vector<std::size_t> bounds{0};
+  for (std::size_t c = per; c < count; c += per) bounds.push_back(c);
+  bounds.push_back(count);
+  din_x_.ensure((count - 1) * x_stride + nx);
+  din_y_.ensure((count - 1) * y_stride + ny);
+  lens_.ensure(count);
+  dout_.ensure(count * out_stride);
+  if (host_lens_n_ < count) {
+    if (host_lens_) cudaFreeHost(host_lens_);
+    host_lens_ = nullptr;
+    host_lens_n_ = 0;
+    cuda_check(cudaMallocHost(&host_lens_, count * sizeof(unsigned long long)), "cudaMallocHost");
+    host_lens_n_ = count;
+  }
+  cuda_check(cudaEventRecord(pipe_ev_, stream_), "event");  // after any earlier work of this context
+  for (auto s : pipe_) cuda_check(cudaStreamWaitEvent(s, pipe_ev_, 0), "wait");
+  // DECMUL_PIPE_TRACE=1: per-chunk stage timestamps on stderr (debugging the overlap)
+  const bool trace = std::getenv("DECMUL_PIPE_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t s) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    tev.push_back(e);
+  };
+  mark(stream_);
+  int launched = 0;
+  for (std::size_t c = 0; c + 1 < bounds.size(); ++c) {
+    const std::size_t c0 = bounds[c], n = bounds[c + 1] - c0;
+    if (n == 0) continue;
+    cudaStream_t up = pipe_[0], comp = pipe_[1], down = pipe_[2];
+    cuda_check(cudaMemcpyAsync(din_x_.ptr + c0 * x_stride, xs + c0 * x_stride, (n - 1) * x_stride + nx,
+                               cudaMemcpyHostToDevice, up), "h2d");
+    cuda_check(cudaMemcpyAsync(din_y_.ptr + c0 * y_stride, ys + c0 * y_stride, (n - 1) * y_stride + ny,
+                               cudaMemcpyHostToDevice, up), "h2d");
+    mark(up);
+    cuda_check(cudaEventRecord(up_ev_[c], up), "event");
+    cuda_check(cudaStreamWaitEvent(comp, up_ev_[c], 0), "wait");
+    multiply_batch_device(n, din_x_.ptr + c0 * x_stride, x_stride, nx, din_y_.ptr + c0 * y_stride, y_stride, ny,
+                          dout_.ptr + c0 * out_stride, out_stride, lens_.ptr + c0, comp);
+    launched += launches_;
+    mark(comp);
+    cuda_check(cudaEventRecord(done_ev_[c], comp), "event");
+    cuda_check(cudaStreamWaitEvent(down, done_ev_[c], 0), "wait");
+    cuda_check(cudaMemcpyAsync(outs + c0 * out_stride, dout_.ptr + c0 * out_stride, n * out_stride,
+                               cudaMemcpyDeviceToHost, down), "d2h");
+    cuda_check(cudaMemcpyAsync(host_lens_ + c0, lens_.ptr + c0, n * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, down), "d2h");
+    mark(down);
+  }
+  for (auto s : pipe_) {
+    cuda_check(cudaEventRecord(pipe_ev_, s), "event");
+    cuda_check(cudaStreamWaitEvent(stream_, pipe_ev_, 0), "wait");
+  }
+  check_err(stream_);
+  if (trace) {
+    for (std::size_t i = 1; i < tev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      std::fprintf(stderr, "%s%.3f", i % 3 == 1 ? "\n  up/comp/down " : " ", ms);
+    }
+    std::fprintf(stderr, "\n");
+    for (auto e : tev) cudaEventDestroy(e);
+  }
+  launches_ = launched;
+  for (std::size_t i = 0; i < count; ++i) lens[i] = std::size_t(host_lens_[i]);
 }
 
 // ---------------- parity hooks ----------------

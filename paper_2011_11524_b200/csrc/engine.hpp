@@ -205,8 +205,20 @@ class Engine {
   CarryArgs carry_args(const ProductPlan& pp, const u64* z1, const u64* z2, std::size_t n, char* out) const;
   void check_err(cudaStream_t st);
 
+  // H2D / compute / D2H pipeline of multiply_batch_host (one-CTA products)
+  void batch_host_pipelined(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx, const char* ys,
+                            std::size_t y_stride, std::size_t ny, char* outs, std::size_t out_stride,
+                            std::size_t* lens);
+
   int device_ = 0;
   cudaStream_t stream_ = nullptr;
+  static constexpr int kPipe = 3;        // upload, compute, download
+  static constexpr int kMaxChunks = 64;
+  cudaStream_t pipe_[kPipe] = {};
+  cudaEvent_t pipe_ev_ = nullptr;
+  cudaEvent_t up_ev_[kMaxChunks] = {}, done_ev_[kMaxChunks] = {};
+  unsigned long long* host_lens_ = nullptr;  // pinned
+  std::size_t host_lens_n_ = 0;
   std::mutex mu_;
   std::map<std::pair<u64, std::size_t>, std::unique_ptr<PrimePlan>> plans_;
   DevBuf<u64> X_[2], Y_[2], Px_, Py_, S_;

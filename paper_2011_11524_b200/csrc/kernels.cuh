@@ -140,6 +140,8 @@ struct SmallArgs {
 };
 bool launch_small(const SmallArgs& a, cudaStream_t st);
 int small_max_logc(int three);
+// CTAs of the one-CTA kernel resident per SM (occupancy API)
+int small_resident_ctas(int logc, int three, int squaring);
 
 // Seeded digit generator (gen.cu): operand j = seed0 + j * seed_step, n digits at out + j * stride.
 void launch_generate(u64 seed0, u64 seed_step, unsigned long long count, unsigned long long n,

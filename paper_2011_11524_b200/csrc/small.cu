@@ -228,12 +228,21 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
 template <int LOGC, int THREE, int SQ>
 bool run_small(const SmallArgs& a, cudaStream_t st) {
   using Cfg = SmallCfg<LOGC, THREE, SQ>;
-  static bool done = false;
-  if (!done) {
+  static unsigned long long done = 0;  // per device (the attribute is per device)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return false;
+  if (!(done >> dev & 1)) {
     if (cudaFuncSetAttribute((const void*)k_small<LOGC, THREE, SQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(Cfg::smem)) != cudaSuccess)
       return false;
-    done = true;
+    done |= 1ull << dev;
+  }
+  if (a.count == 0) {  // occupancy query (see small_resident_ctas)
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_small<LOGC, THREE, SQ>, NT, Cfg::smem) != cudaSuccess)
+      return false;
+    *a.out_lens = (unsigned long long)n;
+    return true;
   }
   k_small<LOGC, THREE, SQ><<<a.count, NT, Cfg::smem, st>>>(a);
   return true;
@@ -247,6 +256,17 @@ bool run_small_sq(const SmallArgs& a, cudaStream_t st) {
 }  // namespace
 
 int small_max_logc(int three) { return three ? 10 : 11; }
+
+int small_resident_ctas(int logc, int three, int squaring) {
+  unsigned long long n = 0;
+  SmallArgs a{};
+  a.logc = logc;
+  a.three = three;
+  a.squaring = squaring;
+  a.count = 0;
+  a.out_lens = &n;  // host pointer: the count == 0 branch writes the occupancy here
+  return launch_small(a, nullptr) ? int(n) : 0;
+}
 
 bool launch_small(const SmallArgs& a, cudaStream_t st) {
   if (a.three) {

@@ -112,6 +112,18 @@ def test_batch_api_matches_reference(gpu, golden):
     assert [sha(z) for z in outs] == golden["ref"]["config2_first64_sha"]
 
 
+def test_batch_host_pipeline_ragged_chunks(gpu, ref):
+    """3001 products: the host batch path uploads / computes / downloads in 7 chunks of
+    whole waves (444 one-CTA products on 148 SMs) with a ragged last chunk."""
+    count, n = 3001, 10000
+    xs = [inputs.gen_digits(9000 + 2 * k, n) for k in range(count)]
+    ys = [inputs.gen_digits(9001 + 2 * k, n) for k in range(count)]
+    outs = gpu.multiply_batch(b"".join(xs), b"".join(ys), count, n, n)
+    want = ref.multiply_batch(xs, ys, os.cpu_count() or 1)
+    bad = [k for k in range(count) if outs[k] != want[k]]
+    assert not bad, bad[:10]
+
+
 def test_batch_uneven_sizes_and_pass_engine(gpu, ref):
     for nx, ny, count in ((1, 1, 5), (35, 17, 33), (3000, 1000, 40), (60000, 40000, 3)):
         xs = [inputs.gen_digits(7 * k + nx, nx) for k in range(count)]
