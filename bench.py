@@ -18,8 +18,8 @@ are independent), as BASELINE config 2 specifies.
           unmodified reference sources compiled by oracle/Makefile) on all host
           threads over the same batch; rank 0 only.
 
-Other configs (--config 1|3|4): one product per step (1e6 x 1e6, 1e8 x 1e8,
-2e9 x 1e9 digits), same reporting.
+Other configs (--config 1|3|33|4|5): one product per step (1e6 x 1e6, 1e8 x 1e8
+uniform / all nines, 2e9 x 1e9, 1e10 x 1e10 digits), same reporting.
 """
 from __future__ import annotations
 
@@ -43,6 +43,8 @@ CONFIGS = {
     33: dict(workload="single product 1e8 x 1e8 digits, all nines (BASELINE config 3, squaring half)", count=1,
              nx=10**8, ny=10**8, mode=1),
     4: dict(workload="single product 2e9 x 1e9 digits (BASELINE config 4)", count=1, nx=2 * 10**9, ny=10**9,
+            mode=0),
+    5: dict(workload="single product 1e10 x 1e10 digits (BASELINE config 5)", count=1, nx=10**10, ny=10**10,
             mode=0),
 }
 PEAKS_FILE = os.path.join(HERE, "MEASURED_PEAKS.json")
@@ -312,6 +314,10 @@ def run_ours(args, cfg, rank, world, local_rank):
             hy = torch.empty(ny, dtype=torch.uint8, pin_memory=True)
             hy.copy_(ys)
         ho = torch.empty(out_stride, dtype=torch.uint8, pin_memory=True)
+        # the host API stages through its own device buffers: release the device-resident
+        # copies first (config 5 needs ~126 GB of HBM for the product itself)
+        del xs, ys, outs, flush
+        torch.cuda.empty_cache()
         import ctypes as C
         olen = C.c_size_t()
 

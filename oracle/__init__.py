@@ -266,6 +266,32 @@ class Port(_Lib):
     def residue_mod(self, s: bytes, q: int) -> int:
         return self.fn("residue_mod", C.c_uint64)(s, C.c_size_t(len(s)), C.c_uint64(q))
 
+    def residues(self, digits, qs, threads: int = 0) -> list[int]:
+        """Residues of a digit string (bytes or uint8 ndarray) modulo each q in qs; the
+        string is cut into per-thread slices (the C call releases the GIL) and the slice
+        residues are combined as r(ab) = r(a) 10^|b| + r(b)."""
+        from concurrent.futures import ThreadPoolExecutor
+
+        a = np.frombuffer(digits, dtype=np.uint8) if isinstance(digits, (bytes, bytearray)) else digits
+        n, nq = a.size, len(qs)
+        threads = threads or (os.cpu_count() or 1)
+        cuts = [n * t // threads for t in range(threads + 1)]
+        qarr = np.array(qs, dtype=np.uint64)
+        fn = self.fn("residues_multi", None)
+
+        def one(t):
+            out = np.zeros(nq, np.uint64)
+            lo, hi = cuts[t], cuts[t + 1]
+            fn(C.c_void_p(a.ctypes.data + lo), C.c_size_t(hi - lo), _ptr(qarr), C.c_int(nq), _ptr(out))
+            return [int(v) for v in out], hi - lo
+
+        with ThreadPoolExecutor(threads) as ex:
+            parts = list(ex.map(one, range(threads)))
+        res = [0] * nq
+        for r, ln in parts:
+            res = [(res[k] * pow(10, ln, qs[k]) + r[k]) % qs[k] for k in range(nq)]
+        return res
+
     def gen_residues(self, seed: int, n: int, p: int):
         out = np.zeros(n, np.uint64)
         self.fn("gen_residues", None)(C.c_uint64(seed), C.c_size_t(n), C.c_uint64(p), _ptr(out))

@@ -863,6 +863,29 @@ u64 or_residue_mod(const char* s, size_t n, u64 q) {
   return acc;
 }
 
+/* Residues of one digit string modulo nq primes q < 2^62 in a single pass (fingerprints
+ * of 1e10-digit products); callers combine chunk residues as
+ * r(ab) = r(a) 10^|b| + r(b). Reentrant (no shared state), so chunks run on threads. */
+void or_residues_multi(const char* s, size_t n, const u64* qs, int nq, u64* out) {
+  u64 p18[16];
+  if (nq > 16) nq = 16;
+  for (int k = 0; k < nq; ++k) {
+    p18[k] = 1000000000000000000ull % qs[k];
+    out[k] = 0;
+  }
+  size_t i = 0, head = n % 18;
+  if (head) {
+    u64 v = 0;
+    for (; i < head; ++i) v = v * 10 + (u64)(s[i] - '0');
+    for (int k = 0; k < nq; ++k) out[k] = v % qs[k];
+  }
+  for (; i < n; i += 18) {
+    u64 v = 0;
+    for (size_t j = 0; j < 18; ++j) v = v * 10 + (u64)(s[i + j] - '0');
+    for (int k = 0; k < nq; ++k) out[k] = (u64)(((u128)out[k] * p18[k] + v) % qs[k]);
+  }
+}
+
 /* ---------------- shared seeded generator ---------------- */
 
 static u64 sm_mix(u64 z) { /* splitmix64 finalizer, reference bench.cpp:40-45 */

@@ -456,6 +456,26 @@ void Engine::transform_forward(const PrimePlan* pl[2], int np, const u64* const 
   passes_fwd(pl, np, src, dst, 0, include_last ? m : (m ? m - 1 : 0), nullptr, st);
 }
 
+// Forward transform of limbs packed into data[1] (both primes' outputs in data[0..1]).
+void Engine::transform_forward_packed(const PrimePlan* pl[2], u64* const data[2], bool include_last,
+                                      cudaStream_t st) {
+  const std::size_t m = pl[0]->passes.size();
+  const std::size_t end = include_last ? m : (m ? m - 1 : 0);
+  if (end == 0) {  // no forward pass at all (N == 1, or one fused pass): just duplicate
+    cuda_check(cudaMemcpyAsync(data[0], data[1], padded_len(*pl[0]) * sizeof(u64), cudaMemcpyDeviceToDevice, st),
+               "copy");
+    return;
+  }
+  const u64* packed[2] = {data[1], data[1]};
+  const PrimePlan* p0[2] = {pl[0], pl[0]};
+  const PrimePlan* p1[2] = {pl[1], pl[1]};
+  u64* d0[2] = {data[0], data[0]};
+  u64* d1[2] = {data[1], data[1]};
+  passes_fwd(p0, 1, packed, d0, 0, 1, nullptr, st);  // prime 0 reads the packed limbs ...
+  passes_fwd(p1, 1, packed, d1, 0, 1, nullptr, st);  // ... before prime 1 overwrites them in place
+  passes_fwd(pl, 2, data, data, 1, end, nullptr, st);
+}
+
 void Engine::transform_fused_last(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
                                   cudaStream_t st) {
   pass_fused(pl, np, data, other, nullptr, st);
@@ -553,30 +573,53 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
     return;
   }
 
+  // HBM plan. Large transforms (>= 2 GB per residue array; config 5 is 12.9 GB) pack
+  // the limbs straight into the second prime's array, and the first pass reads them from
+  // there (prime 0 out of place, then prime 1 in place), so no packed-limb buffers; the
+  // carry's limb sums reuse the x spectrum, dead after the pointwise product. Smaller
+  // ones keep separate packed buffers so the first pass runs both primes in one launch.
   const std::size_t npad = padded_len(P1);
-  for (int q = 0; q < 2; ++q) {
-    X_[q].ensure(npad);
-    if (!squaring) Y_[q].ensure(npad);
-  }
-  Px_.ensure(npad);
-  if (!squaring) Py_.ensure(npad);
   const std::size_t K = pp.N + 2;
   const std::size_t nchunks = (K + kCarryChunk - 1) / kCarryChunk;
-  S_.ensure(nchunks * kCarryChunk);
+  const std::size_t s_words = nchunks * kCarryChunk;
+  const char* force_lean = std::getenv("DECMUL_FORCE_LEAN");  // test knob: lean plan at any size
+  const bool lean = npad * sizeof(u64) >= (std::size_t(2) << 30) || (force_lean && force_lean[0] == '1');
+  const bool s_in_x = lean && !squaring;
+  X_[0].ensure(s_in_x ? std::max(npad, s_words) : npad);
+  X_[1].ensure(npad);
+  if (!squaring) {
+    Y_[0].ensure(npad);
+    Y_[1].ensure(npad);
+  }
+  if (!s_in_x) S_.ensure(s_words);
+  if (!lean) {
+    Px_.ensure(npad);
+    if (!squaring) Py_.ensure(npad);
+  }
   maps_.ensure(nchunks);
+  u64* s_buf = s_in_x ? X_[0].ptr : S_.ptr;
+  u64* px = lean ? X_[1].ptr : Px_.ptr;
+  u64* py = lean ? Y_[1].ptr : Py_.ptr;
 
-  launch_pack(dx, pp.dx, be, Px_.ptr, npad, err_.ptr, st);
+  launch_pack(dx, pp.dx, be, px, npad, err_.ptr, st);
   ++launches_;
   if (!squaring) {
-    launch_pack(dy, pp.dy, be, Py_.ptr, npad, err_.ptr, st);
+    launch_pack(dy, pp.dy, be, py, npad, err_.ptr, st);
     ++launches_;
   }
   const PrimePlan* pl[2] = {&P1, &P2};
+  auto forward = [&](const u64* packed, u64* const dst[2], bool include_last) {
+    if (lean) {
+      transform_forward_packed(pl, dst, include_last, st);
+    } else {
+      const u64* src[2] = {packed, packed};
+      transform_forward(pl, 2, src, dst, include_last, st);
+    }
+  };
   u64* Z[2];
   if (squaring) {
-    const u64* src[2] = {Px_.ptr, Px_.ptr};
     u64* X[2] = {X_[0].ptr, X_[1].ptr};
-    transform_forward(pl, 2, src, X, !P1.last_pow2, st);
+    forward(px, X, !P1.last_pow2);
     if (P1.last_pow2) {
       transform_fused_last(pl, 2, X, nullptr, st);
     } else {
@@ -587,12 +630,10 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
     Z[0] = X[0];
     Z[1] = X[1];
   } else {
-    const u64* sx[2] = {Px_.ptr, Px_.ptr};
-    const u64* sy[2] = {Py_.ptr, Py_.ptr};
     u64* X[2] = {X_[0].ptr, X_[1].ptr};
     u64* Y[2] = {Y_[0].ptr, Y_[1].ptr};
-    transform_forward(pl, 2, sx, X, true, st);
-    transform_forward(pl, 2, sy, Y, !P1.last_pow2, st);
+    forward(px, X, true);
+    forward(py, Y, !P1.last_pow2);
     if (P1.last_pow2) {
       const u64* oth[2] = {X[0], X[1]};
       transform_fused_last(pl, 2, Y, oth, st);
@@ -622,7 +663,7 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   c.coeff_cap_lo = cap_lo;
   c.coeff_cap_hi = cap_hi;
   c.base_exp = be;
-  c.s = S_.ptr;
+  c.s = s_buf;
   c.maps = maps_.ptr;
   c.err = err_.ptr;
   const unsigned long long dsum = pp.dx + pp.dy;

@@ -192,6 +192,7 @@ class Engine {
                    cudaStream_t st);
   void transform_forward(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2],
                          bool include_last, cudaStream_t st);
+  void transform_forward_packed(const PrimePlan* pl[2], u64* const data[2], bool include_last, cudaStream_t st);
   void transform_fused_last(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
                             cudaStream_t st);
   void transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2], bool skip_last, cudaStream_t st);

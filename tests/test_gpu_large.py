@@ -91,6 +91,43 @@ def test_lambda16_cap_all_nines(gpu):
     assert ln == 2 * n and (z[: n - 1] == 57).all() and z[n - 1] == 56 and (z[n:-1] == 48).all() and z[-1] == 49
 
 
+def _device_residues(port, t, qs, chunk=1 << 31):
+    """Residues of a device digit tensor, streamed to the host in chunks (no full copy)."""
+    res = [0] * len(qs)
+    for off in range(0, t.numel(), chunk):
+        a = t[off:off + chunk].cpu().numpy()
+        r = port.residues(a, qs)
+        res = [(res[k] * pow(10, a.size, q) + r[k]) % q for k, q in enumerate(qs)]
+    return res
+
+
+def _low_window(t, k):
+    return bytes(t[-k:].cpu().numpy())
+
+
+def test_config5_ten_billion_digits(gpu, port, ref):
+    """1e10 x 1e10 digits (BASELINE config 5) on one B200: N = 3 * 2^29 under the large
+    pair, 4 residue arrays of 12.9 GB. Checked by streamed residue fingerprints, the
+    exact low window and the digit count."""
+    import torch
+
+    n = 10**10
+    plan = gpu.plan(n, n)
+    assert plan["large_pair"] and plan["length"] == 3 << 29 and plan["base_exp"] == 14
+    x, y, out, ln = _device_product(gpu, n, n, 50, 51)
+    assert ln in (2 * n - 1, 2 * n)
+    z = out[:ln]
+    assert int(z[0]) != ord("0")
+    rx, ry, rz = (_device_residues(port, t, FINGERPRINT_PRIMES) for t in (x, y, z))
+    for q, a, b, c in zip(FINGERPRINT_PRIMES, rx, ry, rz):
+        assert c == a * b % q
+    k = 10000
+    lo = ref.multiply(_low_window(x, k).lstrip(b"0") or b"0", _low_window(y, k).lstrip(b"0") or b"0")
+    assert _low_window(z, k) == lo[-k:].rjust(k, b"0")
+    del x, y, out, z
+    torch.cuda.empty_cache()
+
+
 def test_config4_unbalanced_fingerprints(gpu, port, ref):
     """2e9 x 1e9 digits: beyond the reference's 3*2^24 cap (large prime pair, N = 3*2^26)."""
     nx, ny = 2 * 10**9, 10**9

@@ -91,6 +91,24 @@ def test_large_prime_pair_path(gpu, ref):
     assert gpu.plan(10000, 10000)["p1"] == P1
 
 
+def test_lean_memory_plan(gpu, ref):
+    """The HBM-lean plan of config 5 (limbs packed into the second prime's array, first
+    pass split per prime, carry sums in the dead x spectrum) at small sizes, with both
+    prime pairs, squaring and not, radix-3 and power-of-two lengths."""
+    os.environ["DECMUL_FORCE_LEAN"] = "1"
+    try:
+        for large in (False, True):
+            if large:
+                os.environ["DECMUL_FORCE_LARGE_PAIR"] = "1"
+            for nx, ny in ((30000, 30000), (70000, 50000), (300001, 250000)):
+                x, y = inputs.gen_digits(nx + 1, nx), inputs.gen_digits(ny + 2, ny)
+                assert gpu.multiply_text(x, y) == ref.multiply(x, y), (large, nx, ny)
+                assert gpu.multiply_text(x, x) == ref.multiply(x, x), (large, nx)
+    finally:
+        os.environ.pop("DECMUL_FORCE_LEAN", None)
+        os.environ.pop("DECMUL_FORCE_LARGE_PAIR", None)
+
+
 def test_errors_match_reference_types(gpu):
     with pytest.raises(ValueError, match="non-digit"):
         gpu.multiply_text(b"12a4" * 1000, b"5" * 100)
