@@ -139,6 +139,12 @@ def run_reference(args, cfg, rank, world):
     ref = oracle.ref()
     from paper_2011_11524_b200 import inputs
 
+    try:  # configs 4 and 5: the reference's own planner refuses (decimal.cpp:96,99)
+        ref.select_base_and_length(cfg["nx"], cfg["ny"])
+    except oracle.OracleError as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference multiply refuses this size: {e}",
+                          "config": {"workload": cfg["workload"]}}), flush=True)
+        return
     threads = os.cpu_count() or 1
     count = cfg["count"]
     xs = [inputs.gen_digits(2 * k, cfg["nx"], cfg["mode"]) for k in range(count)]
@@ -203,6 +209,141 @@ def cpu_baseline(cfg) -> dict:
     return {"value": (nx + ny) / dt, "unit": "digits/s", "cores": 1, "kind": "reference",
             "sample": f"one {nx} x {ny}-digit product (1 thread; the reference has no intra-product parallelism)"
                       + ("" if nx == cfg["nx"] else "; smaller than the workload, throughput grows ~1/log N")}
+
+
+# ---------------------------------------------------------------------------------------------
+# our arm: one large product sharded over the ranks
+
+def run_sharded(args, cfg, rank, world, local_rank):
+    """Columns/rows of the transform distributed over the ranks, the layout changes done
+    as NCCL all-to-alls over NVLink (paper_2011_11524_b200/sharded.py): strong scaling."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2011_11524_b200 as dm
+    from paper_2011_11524_b200.sharded import DeviceBackend, TorchComm, rank_digit_range, sharded_multiply
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist.init_process_group("nccl", device_id=dev)
+    ctx = dm.Context(local_rank)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    sptr = stream.cuda_stream
+    backend = DeviceBackend(ctx, stream)
+    comm = TorchComm(dist)
+    nx, ny, mode = cfg["nx"], cfg["ny"], cfg["mode"]
+    squaring = mode == 1
+    plan = backend.plan(nx, ny, world)
+    xs = torch.empty(nx, dtype=torch.uint8, device=dev)
+    ctx.generate_digits(xs.data_ptr(), nx, 0, mode=mode, stream=sptr)
+    ys = xs
+    if not squaring:
+        ys = torch.empty(ny, dtype=torch.uint8, device=dev)
+        ctx.generate_digits(ys.data_ptr(), ny, 1, mode=mode, stream=sptr)
+    out = torch.zeros(nx + ny, dtype=torch.uint8, device=dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step():
+        return sharded_multiply(backend, comm, plan, [rank], [xs], [ys], [out], squaring)
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    for _ in range(args.warmup):
+        n = step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.stats()["last_launches"]
+    step_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n = step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches = ctx.stats()["last_launches"] - l0
+    clk = clocks.stop()
+    t = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ok = n in (nx + ny - 1, nx + ny)
+
+    # e2e: pinned host digits -> every rank's HBM, the sharded product, each rank's own
+    # contiguous digit range -> pinned host (the ranges tile the product text)
+    hx = torch.empty(nx, dtype=torch.uint8, pin_memory=True)
+    hx.copy_(xs)
+    hy = hx
+    if not squaring:
+        hy = torch.empty(ny, dtype=torch.uint8, pin_memory=True)
+        hy.copy_(ys)
+    ho = torch.empty(nx + ny, dtype=torch.uint8, pin_memory=True)
+    lo, hi = rank_digit_range(plan, rank, n)
+
+    def call():
+        with torch.cuda.stream(stream):
+            xs.copy_(hx, non_blocking=True)
+            if not squaring:
+                ys.copy_(hy, non_blocking=True)
+        m = step()
+        a, b = rank_digit_range(plan, rank, m)
+        with torch.cuda.stream(stream):
+            ho[a:b].copy_(out[a:b], non_blocking=True)
+        stream.synchronize()
+
+    call()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        call()
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    d2h = torch.tensor([hi - lo], dtype=torch.int64, device=dev)
+    dist.all_reduce(d2h)
+    digits = nx + ny
+    e2e = {"value": digits * args.steps / (e2e_ms * 1e-3), "unit": "digits/s",
+           "h2d_bytes_per_step": world * (nx + (0 if squaring else ny)), "d2h_bytes_per_step": int(d2h.item())}
+
+    rmm = ctx.measure_modmul_rate(0)
+    peaks = load_peaks()
+    N = int(plan.length)
+    step_s = total_ms / args.steps * 1e-3
+    mm = modmuls_per_product(N, squaring)
+    byt = hbm_bytes_per_product(N, nx, ny, False, squaring)
+    a2a = 8 * N * 2 * (3 if squaring else 4)  # words moved by the all-to-alls, all ranks
+    roofline = {
+        "bound": "int", "unit": "Gmodmul/s", "achieved": mm / step_s / world / 1e9, "peak": rmm / 1e9,
+        "frac": mm / step_s / world / rmm, "traffic": None,
+        "algorithmic": {"modmuls_per_step": mm, "hbm_bytes_per_step": byt, "all_to_all_bytes_per_step": a2a},
+        "peak_source": "live Shoup modmul micro-kernel on all SMs of one GPU (per-GPU achieved vs per-GPU peak)",
+        "hbm": {"achieved": byt / step_s / world / 1e9, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                "frac": byt / step_s / world / 1e9 / peaks.get("hbm_gbs", 6650.0)},
+        "kernel": "multi-pass NTT (k_pass_*), column/row sharded",
+    }
+    if rank == 0:
+        line = {
+            "metric": "decimal digits multiplied/sec", "value": digits * args.steps / (total_ms * 1e-3),
+            "unit": "digits/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded splitmix64 digits generated in HBM, SURVEY §8(d))",
+            "config": {"workload": cfg["workload"], "products": 1, "digits_x": nx, "digits_y": ny,
+                       "base_exp": int(plan.base_exp), "transform_length": N,
+                       "prime_pair": [int(plan.p1), int(plan.p2)],
+                       "parallelism": f"one product sharded over {world} GPU(s): {int(plan.col_passes)} column "
+                                      f"pass(es) on {int(plan.rows)} x {int(plan.seg_len)}, NCCL all-to-all",
+                       "l2": "flushed (512 MiB write) before every timed step; per-step CUDA events"},
+            "e2e": e2e, "roofline": roofline, "gpu_launches": launches, "clocks": clk, "outputs_ok": ok,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------------------------
@@ -395,6 +536,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--sharded", action="store_true",
+                    help="single-product configs: shard the product over the ranks even at N=1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))
@@ -403,6 +546,11 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
+    elif cfg["count"] == 1 and (world > 1 or args.sharded):
+        if "WORLD_SIZE" not in os.environ:  # --sharded without torchrun: a one-rank group
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=os.environ.get("MASTER_PORT", "29517"))
+        run_sharded(args, cfg, rank, world, local_rank)
     else:
         run_ours(args, cfg, rank, world, local_rank)
 

@@ -1182,6 +1182,7 @@ void Engine::shard_pack(const ShardPlan& sp, int q, const char* d_digits, std::s
   const ShardGeom& g = sp.geom;
   launch_pack(d_digits, nd, sp.pp.base_exp, d_out, g.local_len, err_.ptr, st, __builtin_ctzll(g.Bc), g.Sc,
               std::size_t(q) * g.Bc);
+  ++launches_;  // shard steps accumulate launches_ (callers read differences via get_stats)
   cuda_check(cudaGetLastError(), "shard pack");
 }
 
@@ -1218,6 +1219,7 @@ void Engine::shard_reorder(const ShardPlan& sp, bool to_segments, const u64* src
   if (!st) st = stream_;
   const ShardGeom& g = sp.geom;
   launch_block_reorder(src, dst, std::size_t(g.G), g.Rtot / std::size_t(g.G), g.Bc, to_segments, st);
+  ++launches_;
   cuda_check(cudaGetLastError(), "shard reorder");
 }
 
@@ -1236,6 +1238,7 @@ unsigned Engine::shard_carry_begin(const ShardPlan& sp, int q, const u64* z1, co
   lens_.ensure(1);
   unsigned* rmap = reinterpret_cast<unsigned*>(lens_.ptr);
   launch_carry_shard_begin(c, rmap, st);
+  launches_ += 2;
   cuda_check(cudaGetLastError(), "shard carry");
   unsigned m = 0;
   cuda_check(cudaMemcpyAsync(&m, rmap, sizeof m, cudaMemcpyDeviceToHost, st), "rank map");
@@ -1254,6 +1257,7 @@ void Engine::shard_carry_probe(const ShardPlan& sp, int q, unsigned rank_cin, co
   lens_.ensure(2);
   u64* zd = reinterpret_cast<u64*>(lens_.ptr);
   launch_carry_shard_probe(c, rank_cin, zd, st);
+  ++launches_;
   cuda_check(cudaGetLastError(), "shard probe");
   cuda_check(cudaMemcpyAsync(z_out, zd, 2 * sizeof(u64), cudaMemcpyDeviceToHost, st), "probe");
   cuda_check(cudaStreamSynchronize(st), "sync");
@@ -1271,6 +1275,7 @@ void Engine::shard_carry_emit(const ShardPlan& sp, int q, unsigned rank_cin, uns
   const unsigned long long meta[3] = {top, top_len, top_len + top * sp.pp.base_exp};
   cuda_check(cudaMemcpyAsync(meta_.ptr, meta, sizeof meta, cudaMemcpyHostToDevice, st), "meta");
   launch_carry_shard_emit(c, rank_cin, st);
+  launches_ += 2;
   cuda_check(cudaGetLastError(), "shard emit");
   check_err(st);
 }

@@ -60,6 +60,22 @@ def decimal_len(v: int) -> int:
     return len(str(v))
 
 
+def rank_digit_range(plan, q: int, n: int) -> tuple[int, int]:
+    """Bytes [lo, hi) of the n-digit product text written by shard q (its limbs
+    [q L, (q + 1) L) are one contiguous digit range; the top limb is unpadded)."""
+    be, L = int(plan.base_exp), int(plan.local_len)
+    top = (n - 1) // be
+    top_len = n - top * be
+    k_lo, k_hi = q * L, min((q + 1) * L - 1, top)
+    if k_lo > top:
+        return n, n
+
+    def pos(k):
+        return 0 if k == top else top_len + (top - 1 - k) * be
+
+    return pos(k_hi), pos(k_lo) + (top_len if k_lo == top else be)
+
+
 # ---- transports ----
 
 class LocalComm:

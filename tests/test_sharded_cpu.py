@@ -12,7 +12,8 @@ import torch
 
 import paper_2011_11524_b200 as dm
 from paper_2011_11524_b200 import inputs
-from paper_2011_11524_b200.sharded import LocalComm, TorchComm, ShardPlan, rank_carry_ins, sharded_multiply
+from paper_2011_11524_b200.sharded import (LocalComm, ShardPlan, TorchComm, rank_carry_ins, rank_digit_range,
+                                            sharded_multiply)
 
 from shard_emu import EmuBackend
 
@@ -71,6 +72,10 @@ def test_four_local_shards_nines_square(port):
     x = b"9" * 30000
     n, outs = _run(4, [0, 1, 2, 3], LocalComm(4), 30000, 30000, x, x, squaring=True)
     assert _merge(n, outs, [0, 1, 2, 3], 4) == port.multiply(x, x)
+    plan = EmuBackend().plan(30000, 30000, 4)
+    ranges = [rank_digit_range(plan, q, n) for q in range(4)]
+    assert ranges[-1][0] == 0 and ranges[0][1] == n
+    assert all(ranges[q + 1][1] == ranges[q][0] for q in range(3))  # contiguous, descending
 
 
 def _gloo_worker(rank, world, port_no, q, nx, ny, sx, sy):
@@ -108,6 +113,8 @@ def test_two_rank_gloo_sharded_product(port, nx, ny, sx, sy):
         assert p.exitcode == 0
     merged = bytes(a | b for a, b in zip(*parts))
     assert merged == port.multiply(inputs.gen_digits(sx, nx), inputs.gen_digits(sy, ny))
-    # each rank wrote a disjoint, non-empty part of the digits
-    assert all(any(p) for p in parts)
-    assert not any(a and b for a, b in zip(*parts))
+    # each rank wrote exactly its own contiguous digit range
+    plan = EmuBackend().plan(nx, ny, 2)
+    for q, part in enumerate(parts):
+        lo, hi = rank_digit_range(plan, q, n)
+        assert all(part[lo:hi]) and not any(part[:lo]) and not any(part[hi:])
