@@ -24,7 +24,7 @@ constexpr int NT = kPassThreads;
 // Tile geometry. Row passes (S >= 16): one group g, 16 adjacent columns s0..s0+15;
 // element (r, w) at g R S + r S + s0 + w. Column passes (S == 1): 16 adjacent
 // groups, each a contiguous run of R words; element (r, w) at (c0 + w) R + r.
-template <int LOGR, bool ROWS>
+template <int LOGR, bool ROWS, int TW>
 struct Geom {
   unsigned long long base, s0;
   unsigned long long S, tw_col;
@@ -38,10 +38,10 @@ struct Geom {
       // group-fastest tile order: the G groups share the twiddle rows T[f][s0..s0+15],
       // so consecutive CTAs reuse them from L2 instead of re-streaming them from HBM
       const unsigned long long g = tile % a.G;
-      s0 = (tile / a.G) * W;
+      s0 = (tile / a.G) * TW;
       base = (g << (LOGR + a.logS)) + s0;
     } else {
-      const unsigned long long c0 = tile * W;
+      const unsigned long long c0 = tile * TW;
       s0 = 0;
       base = c0 << LOGR;
     }
@@ -56,41 +56,46 @@ struct Geom {
   }
 };
 
-template <int LOGR, bool ROWS>
-using TileLayout = typename std::conditional<ROWS, Rows<W>, ContigColumns<LOGR>>::type;
+template <int LOGR, bool ROWS, int TW>
+using TileLayout = typename std::conditional<ROWS, Rows<TW>, ContigColumns<LOGR>>::type;
 
-template <int LOGR>
-__device__ __forceinline__ void load_table(TwPair* dst, const TwPair* src) {
-  for (int i = threadIdx.x; i < (1 << LOGR) / 2; i += NT) dst[i] = src[i];
+// Threads of a pass CTA: one 8-element register group per thread, 32..256.
+constexpr int pass_threads(int logr, int tw) {
+  return ((1 << logr) * tw / 8) < 32 ? 32 : (((1 << logr) * tw / 8) > NT ? NT : ((1 << logr) * tw / 8));
 }
 
-template <int LOGR, bool ROWS, int E>
+template <int LOGR, int NTK>
+__device__ __forceinline__ void load_table(TwPair* dst, const TwPair* src) {
+  for (int i = threadIdx.x; i < (1 << LOGR) / 2; i += NTK) dst[i] = src[i];
+}
+
+template <int LOGR, bool ROWS, int E, int TW>
 __device__ __forceinline__ void group_coords(int g, int& w, int& q) {
-  group_of<ROWS, ((1 << LOGR) >> E), W>(g, w, q);
+  group_of<ROWS, ((1 << LOGR) >> E), TW>(g, w, q);
 }
 
 // Forward pass: column DIFs, then the inter-pass twiddle omega_M^{f s} (row passes).
 // The first round reads HBM into registers and the last round writes HBM from
 // registers; shared memory carries only the rounds in between.
-template <int LOGR, bool ROWS>
-__global__ void __launch_bounds__(NT) k_pass_fwd(PassArgs a) {
-  constexpr int R = 1 << LOGR;
+template <int LOGR, bool ROWS, int TW>
+__global__ void __launch_bounds__(pass_threads(LOGR, TW)) k_pass_fwd(PassArgs a) {
+  constexpr int R = 1 << LOGR, NTK = pass_threads(LOGR, TW);
   constexpr int E1 = Sched<LOGR>::e_dif(LOGR), EL = Sched<LOGR>::first_e;
   extern __shared__ __align__(16) u64 sm[];
-  TwPair* tw = reinterpret_cast<TwPair*>(sm + R * W);
+  TwPair* tw = reinterpret_cast<TwPair*>(sm + R * TW);
   const int pr = int(blockIdx.x % a.np), tid = threadIdx.x;
   const u64 p = a.p[pr];
   const u64* src = a.src[pr];
   u64* dst = a.dst[pr];
   const TwPair* __restrict__ T = a.pass_tw[pr];
-  load_table<LOGR>(tw, a.dft_fwd[pr]);
+  load_table<LOGR, NTK>(tw, a.dft_fwd[pr]);
   __syncthreads();
-  const Geom<LOGR, ROWS> G(a);
-  const TileLayout<LOGR, ROWS> L;
+  const Geom<LOGR, ROWS, TW> G(a);
+  const TileLayout<LOGR, ROWS, TW> L;
   if constexpr (LOGR == E1) {  // one round: HBM -> registers -> HBM
-    for (int g = tid; g < (R >> E1) * W; g += NT) {
+    for (int g = tid; g < (R >> E1) * TW; g += NTK) {
       int w, q, j0, base;
-      group_coords<LOGR, ROWS, E1>(g, w, q);
+      group_coords<LOGR, ROWS, E1, TW>(g, w, q);
       dif_group<LOGR, E1>(q, j0, base);
       u64 v[1 << E1];
 #pragma unroll
@@ -105,9 +110,9 @@ __global__ void __launch_bounds__(NT) k_pass_fwd(PassArgs a) {
     return;
   } else {
     constexpr int ST1 = 1 << (LOGR - E1);
-    for (int g = tid; g < (R >> E1) * W; g += NT) {
+    for (int g = tid; g < (R >> E1) * TW; g += NTK) {
       int w, q, j0, base;
-      group_coords<LOGR, ROWS, E1>(g, w, q);
+      group_coords<LOGR, ROWS, E1, TW>(g, w, q);
       dif_group<LOGR, E1>(q, j0, base);
       u64 v[1 << E1];
 #pragma unroll
@@ -117,10 +122,10 @@ __global__ void __launch_bounds__(NT) k_pass_fwd(PassArgs a) {
       for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
     }
     __syncthreads();
-    dif_rounds_smem<LOGR, LOGR - E1, EL, W>(sm, L, UniformField{p, tw}, tid, NT);
-    for (int g = tid; g < (R >> EL) * W; g += NT) {
+    dif_rounds_smem<LOGR, LOGR - E1, EL, TW>(sm, L, UniformField{p, tw}, tid, NTK);
+    for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
-      group_coords<LOGR, ROWS, EL>(g, w, q);
+      group_coords<LOGR, ROWS, EL, TW>(g, w, q);
       dif_group<EL, EL>(q, j0, base);
       u64 v[1 << EL];
 #pragma unroll
@@ -137,27 +142,27 @@ __global__ void __launch_bounds__(NT) k_pass_fwd(PassArgs a) {
 
 // Inverse pass: conjugate inter-pass twiddle (row passes; carries the convolution
 // scale on the first inverse pass), then column DITs.
-template <int LOGR, bool ROWS>
-__global__ void __launch_bounds__(NT) k_pass_inv(PassArgs a) {
-  constexpr int R = 1 << LOGR;
+template <int LOGR, bool ROWS, int TW>
+__global__ void __launch_bounds__(pass_threads(LOGR, TW)) k_pass_inv(PassArgs a) {
+  constexpr int R = 1 << LOGR, NTK = pass_threads(LOGR, TW);
   constexpr int E1 = Sched<LOGR>::first_e;
   constexpr int EL = Sched<LOGR>::rem ? Sched<LOGR>::rem : E1;  // last DIT round
   constexpr int AL = LOGR - EL;                                   // its starting stage
   extern __shared__ __align__(16) u64 sm[];
-  TwPair* tw = reinterpret_cast<TwPair*>(sm + R * W);
+  TwPair* tw = reinterpret_cast<TwPair*>(sm + R * TW);
   const int pr = int(blockIdx.x % a.np), tid = threadIdx.x;
   const u64 p = a.p[pr];
   const u64* src = a.src[pr];
   u64* dst = a.dst[pr];
   const TwPair* __restrict__ T = a.pass_tw[pr];
   const TwPair sc = a.final_scale[pr];
-  load_table<LOGR>(tw, a.dft_inv[pr]);
+  load_table<LOGR, NTK>(tw, a.dft_inv[pr]);
   __syncthreads();
-  const Geom<LOGR, ROWS> G(a);
-  const TileLayout<LOGR, ROWS> L;
-  for (int g = tid; g < (R >> E1) * W; g += NT) {
+  const Geom<LOGR, ROWS, TW> G(a);
+  const TileLayout<LOGR, ROWS, TW> L;
+  for (int g = tid; g < (R >> E1) * TW; g += NTK) {
     int w, q, j0, base;
-    group_coords<LOGR, ROWS, E1>(g, w, q);
+    group_coords<LOGR, ROWS, E1, TW>(g, w, q);
     dit_group<0, E1>(q, j0, base);
     u64 v[1 << E1];
 #pragma unroll
@@ -178,11 +183,11 @@ __global__ void __launch_bounds__(NT) k_pass_inv(PassArgs a) {
   }
   if constexpr (LOGR > E1) {
     __syncthreads();
-    dit_rounds_smem<LOGR, E1, AL, W>(sm, L, UniformField{p, tw}, tid, NT);
+    dit_rounds_smem<LOGR, E1, AL, TW>(sm, L, UniformField{p, tw}, tid, NTK);
     constexpr int STL = 1 << AL;
-    for (int g = tid; g < (R >> EL) * W; g += NT) {
+    for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
-      group_coords<LOGR, ROWS, EL>(g, w, q);
+      group_coords<LOGR, ROWS, EL, TW>(g, w, q);
       dit_group<AL, EL>(q, j0, base);
       u64 v[1 << EL];
 #pragma unroll
@@ -202,14 +207,14 @@ __global__ void __launch_bounds__(NT) k_pass_inv(PassArgs a) {
 // conv.cpp:205-208, :299-305) and the first inverse pass. The last DIF round
 // and the first DIT round act on the same 8-element groups, so DIF -> pointwise
 // -> DIT happens in registers.
-template <int LOGR>
-__global__ void __launch_bounds__(NT) k_pass_fused(PassArgs a) {
-  constexpr int R = 1 << LOGR;
+template <int LOGR, int TW>
+__global__ void __launch_bounds__(pass_threads(LOGR, TW)) k_pass_fused(PassArgs a) {
+  constexpr int R = 1 << LOGR, NTK = pass_threads(LOGR, TW);
   constexpr int E1 = Sched<LOGR>::e_dif(LOGR), EM = Sched<LOGR>::first_e;
   constexpr int EL = Sched<LOGR>::rem ? Sched<LOGR>::rem : EM;
   constexpr int AL = LOGR - EL;
   extern __shared__ __align__(16) u64 sm[];
-  TwPair* twf = reinterpret_cast<TwPair*>(sm + R * W);
+  TwPair* twf = reinterpret_cast<TwPair*>(sm + R * TW);
   TwPair* twi = twf + R / 2;
   const int pr = int(blockIdx.x % a.np), tid = threadIdx.x;
   const u64 p = a.p[pr], pp = a.pp[pr];
@@ -217,16 +222,16 @@ __global__ void __launch_bounds__(NT) k_pass_fused(PassArgs a) {
   const u64* oth = a.other[pr];
   u64* dst = a.dst[pr];
   const TwPair sc = a.final_scale[pr];
-  load_table<LOGR>(twf, a.dft_fwd[pr]);
-  load_table<LOGR>(twi, a.dft_inv[pr]);
+  load_table<LOGR, NTK>(twf, a.dft_fwd[pr]);
+  load_table<LOGR, NTK>(twi, a.dft_inv[pr]);
   __syncthreads();
-  const Geom<LOGR, false> G(a);
+  const Geom<LOGR, false, TW> G(a);
   const ContigColumns<LOGR> L;
   if constexpr (LOGR > EM) {
     constexpr int ST1 = 1 << (LOGR - E1);
-    for (int g = tid; g < (R >> E1) * W; g += NT) {
+    for (int g = tid; g < (R >> E1) * TW; g += NTK) {
       int w, q, j0, base;
-      group_coords<LOGR, false, E1>(g, w, q);
+      group_coords<LOGR, false, E1, TW>(g, w, q);
       dif_group<LOGR, E1>(q, j0, base);
       u64 v[1 << E1];
 #pragma unroll
@@ -236,11 +241,11 @@ __global__ void __launch_bounds__(NT) k_pass_fused(PassArgs a) {
       for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
     }
     __syncthreads();
-    dif_rounds_smem<LOGR, LOGR - E1, EM, W>(sm, L, UniformField{p, twf}, tid, NT);
+    dif_rounds_smem<LOGR, LOGR - E1, EM, TW>(sm, L, UniformField{p, twf}, tid, NTK);
   }
-  for (int g = tid; g < (R >> EM) * W; g += NT) {
+  for (int g = tid; g < (R >> EM) * TW; g += NTK) {
     int w, q, j0, base;
-    group_coords<LOGR, false, EM>(g, w, q);
+    group_coords<LOGR, false, EM, TW>(g, w, q);
     dit_group<0, EM>(q, j0, base);
     u64 v[1 << EM];
 #pragma unroll
@@ -261,11 +266,11 @@ __global__ void __launch_bounds__(NT) k_pass_fused(PassArgs a) {
   }
   if constexpr (LOGR > EM) {
     __syncthreads();
-    dit_rounds_smem<LOGR, EM, AL, W>(sm, L, UniformField{p, twi}, tid, NT);
+    dit_rounds_smem<LOGR, EM, AL, TW>(sm, L, UniformField{p, twi}, tid, NTK);
     constexpr int STL = 1 << AL;
-    for (int g = tid; g < (R >> EL) * W; g += NT) {
+    for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
-      group_coords<LOGR, false, EL>(g, w, q);
+      group_coords<LOGR, false, EL, TW>(g, w, q);
       dit_group<AL, EL>(q, j0, base);
       u64 v[1 << EL];
 #pragma unroll
@@ -523,46 +528,81 @@ int grid_for(unsigned long long n, int threads) {
   return int(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
-// One-time opt-in to the large dynamic shared-memory carve-out for kernel fn.
+// One-time (per device) opt-in to the large dynamic shared-memory carve-out for kernel fn.
 template <auto FN>
 void set_smem(int bytes) {
-  static bool done = false;  // one flag per kernel instantiation
-  if (!done) {
+  static unsigned long long done = 0;  // one bit per device, one flag set per kernel instantiation
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !(done >> dev & 1)) {
     cudaFuncSetAttribute((const void*)FN, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    done = true;
+    done |= 1ull << dev;
   }
 }
 
 // blockIdx.x = tile * np + prime: both primes of a tile run back to back, so a shared
 // source (the packed limbs of pass 0) is read from HBM once and from L2 the second time.
-template <auto FN>
+template <auto FN, int TW, int NTK>
 void launch_pass_kernel(const PassArgs& a, unsigned long long ncols, int np, int smem, cudaStream_t st) {
   set_smem<FN>(smem);
   PassArgs b = a;
   b.np = np;
-  FN<<<unsigned((ncols + W - 1) / W * np), NT, smem, st>>>(b);
+  FN<<<unsigned((ncols + TW - 1) / TW * np), NTK, smem, st>>>(b);
+}
+
+// Tile width: 16 columns (128 B row segments) normally; 4 when a pass would otherwise
+// launch fewer than two CTAs per SM (small transforms, e.g. config 1's N = 2^17 has
+// 16 tiles of 512 x 16 per prime), trading segment length for parallelism.
+constexpr int kNarrowW = 4;
+inline bool narrow_tiles(int logR, unsigned long long ncols, int np) {
+  return logR >= 5 && (ncols / W) * (unsigned long long)np < 2ull * 148;
+}
+
+template <int LOGR, int TW>
+void pass_fwd_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
+  constexpr int NTK = pass_threads(LOGR, TW);
+  const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) / 2 * 16;
+  if (a.S > 1)
+    launch_pass_kernel<k_pass_fwd<LOGR, true, TW>, TW, NTK>(a, ncols, np, sm, st);
+  else
+    launch_pass_kernel<k_pass_fwd<LOGR, false, TW>, TW, NTK>(a, ncols, np, sm, st);
+}
+template <int LOGR, int TW>
+void pass_inv_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
+  constexpr int NTK = pass_threads(LOGR, TW);
+  const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) / 2 * 16;
+  if (a.S > 1)
+    launch_pass_kernel<k_pass_inv<LOGR, true, TW>, TW, NTK>(a, ncols, np, sm, st);
+  else
+    launch_pass_kernel<k_pass_inv<LOGR, false, TW>, TW, NTK>(a, ncols, np, sm, st);
+}
+template <int LOGR, int TW>
+void pass_fused_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
+  constexpr int NTK = pass_threads(LOGR, TW);
+  const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) * 16;
+  launch_pass_kernel<k_pass_fused<LOGR, TW>, TW, NTK>(a, ncols, np, sm, st);
 }
 
 template <int LOGR>
 void pass_fwd_t(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
-  const int sm = (1 << LOGR) * W * 8 + (1 << LOGR) / 2 * 16;
-  if (a.S > 1)
-    launch_pass_kernel<k_pass_fwd<LOGR, true>>(a, ncols, np, sm, st);
-  else
-    launch_pass_kernel<k_pass_fwd<LOGR, false>>(a, ncols, np, sm, st);
+  if constexpr (LOGR >= 5) {
+    if (narrow_tiles(LOGR, ncols, np)) return pass_fwd_w<LOGR, kNarrowW>(a, ncols, np, st);
+  }
+  pass_fwd_w<LOGR, W>(a, ncols, np, st);
 }
 template <int LOGR>
 void pass_inv_t(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
-  const int sm = (1 << LOGR) * W * 8 + (1 << LOGR) / 2 * 16;
-  if (a.S > 1)
-    launch_pass_kernel<k_pass_inv<LOGR, true>>(a, ncols, np, sm, st);
-  else
-    launch_pass_kernel<k_pass_inv<LOGR, false>>(a, ncols, np, sm, st);
+  if constexpr (LOGR >= 5) {
+    if (narrow_tiles(LOGR, ncols, np)) return pass_inv_w<LOGR, kNarrowW>(a, ncols, np, st);
+  }
+  pass_inv_w<LOGR, W>(a, ncols, np, st);
 }
 template <int LOGR>
 void pass_fused_t(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
-  const int sm = (1 << LOGR) * W * 8 + (1 << LOGR) * 16;
-  launch_pass_kernel<k_pass_fused<LOGR>>(a, ncols, np, sm, st);
+  if constexpr (LOGR >= 5) {
+    if (narrow_tiles(LOGR, ncols, np)) return pass_fused_w<LOGR, kNarrowW>(a, ncols, np, st);
+  }
+  pass_fused_w<LOGR, W>(a, ncols, np, st);
 }
 
 }  // namespace
