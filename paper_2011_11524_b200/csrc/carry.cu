@@ -9,10 +9,14 @@ namespace dmg {
 
 namespace {
 
-constexpr int CH = kCarryChunk;
+// Chunk of CH = 8 NTC limbs per CTA of NTC threads (each thread composes the maps of
+// PER = 8 consecutive limbs, moved as one 8-byte word): NTC = 256 normally, 64 for small
+// products (more CTAs), where the chunk scan also folds into the emit kernel.
+constexpr int PER = 8;
+constexpr int CH = kCarryChunk;  // chunk of the large-product and sharded paths
 constexpr int NT = kCarryThreads;
-constexpr int PER = CH / NT;  // limbs per thread
-static_assert(PER == 8, "per-thread limb maps are moved as one 8-byte word");
+static_assert(CH == NT * PER, "chunk = threads x 8 limbs");
+constexpr int NT_SMALL = kCarryChunkSmall / PER;
 
 // Local coefficient i (global k_off + i); i = -2, -1 are the previous rank's halo.
 __device__ __forceinline__ void coeff_digits(const CarryArgs& a, long long i, u64& d0, u64& d1, u64& d2) {
@@ -30,17 +34,19 @@ __device__ __forceinline__ void coeff_digits(const CarryArgs& a, long long i, u6
 // Coefficients are read and limb sums written in coalesced order (loc = j NT + tid);
 // each limb's 6-bit transfer map goes to shared memory as a byte, and each thread
 // then composes the maps of PER consecutive limbs (one 8-byte shared load).
-__global__ void __launch_bounds__(NT) k_carry_split(CarryArgs a) {
-  __shared__ u64 d1s[CH + 2], d2s[CH + 2];
-  __shared__ __align__(8) unsigned char mp[CH];
-  __shared__ unsigned wsm[NT / 32 + 1];
-  const unsigned long long k0 = (unsigned long long)blockIdx.x * CH;
+template <int NTC>
+__global__ void __launch_bounds__(NTC) k_carry_split(CarryArgs a) {
+  constexpr int CHC = NTC * PER;
+  __shared__ u64 d1s[CHC + 2], d2s[CHC + 2];
+  __shared__ __align__(8) unsigned char mp[CHC];
+  __shared__ unsigned wsm[NTC / 32 + 1];
+  const unsigned long long k0 = (unsigned long long)blockIdx.x * CHC;
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const u64 B = a.div.base;
   u64 d0r[PER];
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
-    const int loc = j * NT + threadIdx.x;
+    const int loc = j * NTC + threadIdx.x;
     u64 d0, d1, d2;
     coeff_digits(a, (long long)(k0 + loc), d0, d1, d2);
     d0r[j] = d0;
@@ -56,7 +62,7 @@ __global__ void __launch_bounds__(NT) k_carry_split(CarryArgs a) {
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
-    const int loc = j * NT + threadIdx.x;
+    const int loc = j * NTC + threadIdx.x;
     const unsigned long long k = k0 + loc;
     const u64 s = d0r[j] + d1s[loc + 1] + d2s[loc];
     if (k < K) a.s[k] = s;
@@ -68,7 +74,7 @@ __global__ void __launch_bounds__(NT) k_carry_split(CarryArgs a) {
 #pragma unroll
   for (int j = 0; j < PER; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
   unsigned total;
-  block_scan_maps<NT>(agg, wsm, &total);
+  block_scan_maps<NTC>(agg, wsm, &total);
   if (threadIdx.x == 0) a.maps[blockIdx.x] = total;
 }
 
@@ -133,24 +139,75 @@ __global__ void __launch_bounds__(1024) k_carry_scan(CarryArgs a, unsigned nchun
   }
 }
 
+// z (final value) of limb k given its chunk's carry-in: compose the maps of the limbs
+// before k inside its chunk (block-wide, ordered segments).
+template <int NTB, int CHC>
+__device__ __forceinline__ u64 limb_value(const CarryArgs& a, unsigned long long k, unsigned chunk_cin,
+                                          unsigned* wsm) {
+  const u64 B = a.div.base;
+  const unsigned long long cs = k / CHC * CHC, len = k - cs, seg = (len + NTB - 1) / NTB;
+  const unsigned long long j0 = cs + threadIdx.x * seg;
+  unsigned m = kIdentityMap;
+  for (unsigned long long j = j0; j < j0 + seg && j < k; ++j) m = map_compose(limb_map(a.s[j], B), m);
+  block_scan_maps<NTB>(m, wsm, &m);
+  u64 v = a.s[k] + map_apply(m, chunk_cin);
+  v -= (v >= B ? B : 0);
+  v -= (v >= B ? B : 0);
+  return v;
+}
+
+// Composition of chunk maps [0, c) applied to 0: the carry into chunk c (block-wide).
+template <int NTB>
+__device__ __forceinline__ unsigned chunk_carry_in(const unsigned* maps, unsigned c, unsigned* wsm) {
+  const unsigned per = (c + NTB - 1) / NTB, c0 = threadIdx.x * per;
+  unsigned agg = kIdentityMap;
+  for (unsigned i = c0; i < c0 + per && i < c; ++i) agg = map_compose(maps[i], agg);
+  unsigned total;
+  block_scan_maps<NTB>(agg, wsm, &total);
+  return map_apply(total, 0);
+}
+
 // Phase 3: apply carries and print each limb at its place in the output string.
 // The chunk's digits are staged in shared memory and stored as 16-byte vectors.
-__global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
-  __shared__ unsigned wsm[NT / 32 + 1];
-  __shared__ __align__(16) char buf[CH * 17 + 32];
-  __shared__ __align__(8) unsigned char mp[CH];  // limb maps, then limb carry-ins
-  const unsigned long long cbase = (unsigned long long)blockIdx.x * CH;
-  const unsigned long long top = a.meta[0];
-  if (a.k_off + cbase > top) return;  // nothing of this chunk is printed (uniform per block)
+// SELF (small products): no phase 2 — every CTA derives its chunk carry-in and the
+// top limb from the chunk maps itself (a few thousand maps at most).
+template <int NTC, bool SELF>
+__global__ void __launch_bounds__(NTC) k_carry_emit(CarryArgs a) {
+  constexpr int CHC = NTC * PER;
+  __shared__ unsigned wsm[NTC / 32 + 1];
+  __shared__ __align__(16) char buf[CHC * 17 + 32];
+  __shared__ __align__(8) unsigned char mp[CHC];  // limb maps, then limb carry-ins
+  const unsigned long long cbase = (unsigned long long)blockIdx.x * CHC;
+  unsigned long long top;
+  unsigned top_len, chunk_cin;
+  if constexpr (SELF) {
+    const unsigned long long k0 = a.top_candidates[0], k1 = a.top_candidates[1];
+    const u64 z0 = limb_value<NTC, CHC>(a, k0, chunk_carry_in<NTC>(a.maps, unsigned(k0 / CHC), wsm), wsm);
+    const u64 z1 = limb_value<NTC, CHC>(a, k1, chunk_carry_in<NTC>(a.maps, unsigned(k1 / CHC), wsm), wsm);
+    top = z1 != 0 ? k1 : (z0 != 0 ? k0 : 0);
+    top_len = decimal_len(z1 != 0 ? z1 : z0);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.meta[0] = top;
+      a.meta[1] = top_len;
+      a.meta[2] = top_len + top * a.base_exp;
+    }
+    if (cbase > top) return;  // uniform per block
+    chunk_cin = chunk_carry_in<NTC>(a.maps, blockIdx.x, wsm);
+  } else {
+    top = a.meta[0];
+    top_len = unsigned(a.meta[1]);
+    if (a.k_off + cbase > top) return;  // nothing of this chunk is printed (uniform per block)
+    chunk_cin = a.maps[blockIdx.x];
+  }
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const u64 B = a.div.base;
-  // coalesced limb sums (loc = j NT + tid); their maps to shared memory
+  // coalesced limb sums (loc = j NTC + tid); their maps to shared memory
   u64 s[PER];
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
-    const unsigned long long k = cbase + j * NT + threadIdx.x;
+    const unsigned long long k = cbase + j * NTC + threadIdx.x;
     s[j] = k < K ? a.s[k] : 0;
-    mp[j * NT + threadIdx.x] = (unsigned char)limb_map(s[j], B);
+    mp[j * NTC + threadIdx.x] = (unsigned char)limb_map(s[j], B);
   }
   __syncthreads();
   // each thread: PER consecutive limbs -> composed map -> block scan -> per-limb carry-ins
@@ -158,8 +215,8 @@ __global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
   unsigned agg = kIdentityMap;
 #pragma unroll
   for (int j = 0; j < PER; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
-  const unsigned pre = block_scan_maps<NT>(agg, wsm, nullptr);  // ends with a barrier
-  unsigned c = map_apply(pre, a.maps[blockIdx.x]);
+  const unsigned pre = block_scan_maps<NTC>(agg, wsm, nullptr);  // ends with a barrier
+  unsigned c = map_apply(pre, chunk_cin);
   unsigned long long cin8 = 0;
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
@@ -168,11 +225,10 @@ __global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
   }
   reinterpret_cast<unsigned long long*>(mp)[threadIdx.x] = cin8;
   __syncthreads();
-  const unsigned top_len = unsigned(a.meta[1]);
   const unsigned be = a.base_exp;
   // global limb range printed by this chunk: [gbase, ghi]
   const unsigned long long gbase = a.k_off + cbase;
-  const unsigned long long last_local = (cbase + CH < K ? cbase + CH : K) - 1;
+  const unsigned long long last_local = (cbase + CHC < K ? cbase + CHC : K) - 1;
   const unsigned long long ghi = a.k_off + last_local < top ? a.k_off + last_local : top;
   const unsigned long long start = limb_pos(ghi, top, top_len, be);
   const unsigned long long end = limb_pos(gbase, top, top_len, be) + (gbase == top ? top_len : be);
@@ -191,7 +247,7 @@ __global__ void __launch_bounds__(NT) k_carry_emit(CarryArgs a) {
     write_digits(sb + (limb_pos(kg, top, top_len, be) - start), v, kg == top ? top_len : be);
   }
   __syncthreads();
-  cta_store_bytes(g, sb, unsigned(end - start), threadIdx.x, NT);
+  cta_store_bytes(g, sb, unsigned(end - start), threadIdx.x, NTC);
 }
 
 // ---- sharded product: the rank's carry-in comes from the other ranks ----
@@ -249,18 +305,25 @@ __global__ void k_carry_cin(unsigned* maps, unsigned nchunks, unsigned rank_cin)
 
 }  // namespace
 
-void launch_carry(const CarryArgs& a, cudaStream_t st) {
+int launch_carry(const CarryArgs& a, cudaStream_t st) {
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const unsigned nchunks = unsigned((K + CH - 1) / CH);
-  k_carry_split<<<nchunks, NT, 0, st>>>(a);
+  if (nchunks < 2 * 148) {  // small product: 512-limb chunks, no separate scan
+    const unsigned ns = unsigned((K + kCarryChunkSmall - 1) / kCarryChunkSmall);
+    k_carry_split<NT_SMALL><<<ns, NT_SMALL, 0, st>>>(a);
+    k_carry_emit<NT_SMALL, true><<<ns, NT_SMALL, 0, st>>>(a);
+    return 2;
+  }
+  k_carry_split<NT><<<nchunks, NT, 0, st>>>(a);
   k_carry_scan<<<1, 1024, 0, st>>>(a, nchunks);
-  k_carry_emit<<<nchunks, NT, 0, st>>>(a);
+  k_carry_emit<NT, false><<<nchunks, NT, 0, st>>>(a);
+  return 3;
 }
 
 void launch_carry_shard_begin(const CarryArgs& a, unsigned* rank_map_dev, cudaStream_t st) {
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const unsigned nchunks = unsigned((K + CH - 1) / CH);
-  k_carry_split<<<nchunks, NT, 0, st>>>(a);
+  k_carry_split<NT><<<nchunks, NT, 0, st>>>(a);
   k_carry_prefix<<<1, 1024, 0, st>>>(a, nchunks, rank_map_dev);
 }
 
@@ -272,7 +335,7 @@ void launch_carry_shard_emit(const CarryArgs& a, unsigned rank_cin, cudaStream_t
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const unsigned nchunks = unsigned((K + CH - 1) / CH);
   k_carry_cin<<<(nchunks + 255) / 256, 256, 0, st>>>(a.maps, nchunks, rank_cin);
-  k_carry_emit<<<nchunks, NT, 0, st>>>(a);
+  k_carry_emit<NT, false><<<nchunks, NT, 0, st>>>(a);
 }
 
 }  // namespace dmg

@@ -596,7 +596,7 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
     Px_.ensure(npad);
     if (!squaring) Py_.ensure(npad);
   }
-  maps_.ensure(nchunks);
+  maps_.ensure(carry_map_words(K));
   u64* s_buf = s_in_x ? X_[0].ptr : S_.ptr;
   u64* px = lean ? X_[1].ptr : Px_.ptr;
   u64* py = lean ? Y_[1].ptr : Py_.ptr;
@@ -672,8 +672,7 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   c.meta = meta_.ptr;
   c.out = dout;
   c.tail = 1;
-  launch_carry(c, st);
-  launches_ += 3;
+  launches_ += launch_carry(c, st);
   cuda_check(cudaGetLastError(), "product kernels");
 }
 
@@ -1049,7 +1048,7 @@ std::size_t Engine::recover_decimal(const u64* r1, const u64* r2, std::size_t n,
   X_[1].ensure(n);
   const std::size_t K = n + 2, nchunks = (K + kCarryChunk - 1) / kCarryChunk;
   S_.ensure(nchunks * kCarryChunk);
-  maps_.ensure(nchunks);
+  maps_.ensure(carry_map_words(K));
   dout_.ensure(std::max<std::size_t>(dsum, 1) + 64);
   cudaStream_t st = stream_;
   cuda_check(cudaMemcpyAsync(X_[0].ptr, r1, n * 8, cudaMemcpyHostToDevice, st), "h2d");

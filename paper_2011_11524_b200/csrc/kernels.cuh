@@ -103,9 +103,13 @@ struct CarryArgs {
   u64 halo1[2], halo2[2];  // residues of global coefficients k_off - 2, k_off - 1 (zeros on the first rank)
   int tail;                // this rank also emits the two trailing limbs N, N + 1 (last rank)
 };
-constexpr int kCarryChunk = 2048;
+constexpr int kCarryChunk = 2048;       // limbs per carry chunk (large products, shards)
 constexpr int kCarryThreads = 256;
-void launch_carry(const CarryArgs& a, cudaStream_t st);
+constexpr int kCarryChunkSmall = 512;   // small products: 4x the CTAs
+// maps[] entries the carry of K limbs may use (sized for the small chunk)
+inline std::size_t carry_map_words(std::size_t K) { return (K + kCarryChunkSmall - 1) / kCarryChunkSmall; }
+// Returns the number of kernels launched.
+int launch_carry(const CarryArgs& a, cudaStream_t st);
 // Sharded carry: split + per-chunk exclusive prefix maps; *rank_map_dev gets the rank's composed map.
 void launch_carry_shard_begin(const CarryArgs& a, unsigned* rank_map_dev, cudaStream_t st);
 // z at the global limbs `cand` owned by this rank (others UINT64_MAX), given the carry into the rank.
