@@ -177,6 +177,16 @@ typedef struct {
 } decmul_gpu_stats;
 int decmul_gpu_get_stats(decmul_gpu_ctx* ctx, decmul_gpu_stats* out);
 
+/* GPU self-test, replaces run_selftest (selftest.cpp:79-219; CLI `selftest [--inject-fault]`,
+ * main.cpp:162): field identities, transform round trips, convolution vs a direct O(n^2)
+ * sum, CRT, base division, carry recovery and small products, all on the device path and
+ * checked on the host. inject_fault corrupts one root-table entry of a plan (restored
+ * afterwards) and adds a suite that must fail. The report ("suite=<name> checks=<n>
+ * failures=<n>" lines, then "selftest_failures=<n>", the reference's format) is written
+ * NUL-terminated to report (truncated to cap); *failures gets the total. Returns 0 when
+ * the test ran, whatever its outcome. */
+int decmul_gpu_selftest(decmul_gpu_ctx* ctx, int inject_fault, char* report, size_t cap, int* failures);
+
 #ifdef __cplusplus
 }
 #endif

@@ -56,7 +56,7 @@ EXPORTED_SYMBOLS = [
     "decmul_gpu_transpose_2n_x_n", "decmul_gpu_generate_digits", "decmul_gpu_measure_modmul_rate",
     "decmul_gpu_get_stats", "decmul_gpu_shard_plan_create", "decmul_gpu_shard_pack", "decmul_gpu_shard_transform",
     "decmul_gpu_shard_reorder", "decmul_gpu_shard_carry_begin", "decmul_gpu_shard_carry_probe",
-    "decmul_gpu_shard_carry_emit",
+    "decmul_gpu_shard_carry_emit", "decmul_gpu_selftest",
 ]
 
 
@@ -224,6 +224,13 @@ class Context:
         self._call("decmul_gpu_plan", C.c_size_t(dx), C.c_size_t(dy), C.c_uint(forced_base_exp), C.byref(info))
         return dict(base_exp=info.base_exp, length=info.length, p1=info.p1, p2=info.p2,
                     large_pair=bool(info.large_pair), one_cta=bool(info.one_cta))
+
+    def selftest(self, inject_fault: bool = False) -> tuple[int, str]:
+        """GPU self-test (reference run_selftest, selftest.cpp:79-219): (failures, report)."""
+        buf = C.create_string_buffer(1 << 14)
+        f = C.c_int()
+        self._call("decmul_gpu_selftest", C.c_int(int(inject_fault)), buf, C.c_size_t(len(buf)), C.byref(f))
+        return f.value, buf.value.decode()
 
     def stats(self) -> dict:
         s = _Stats()

@@ -321,6 +321,19 @@ int decmul_gpu_measure_modmul_rate(decmul_gpu_ctx* ctx, int variant, double* rat
   });
 }
 
+int decmul_gpu_selftest(decmul_gpu_ctx* ctx, int inject_fault, char* report, size_t cap, int* failures) {
+  LOCKED(ctx, {
+    std::string r;
+    const int f = ctx->eng->selftest(inject_fault != 0, r);
+    if (failures) *failures = f;
+    if (report && cap) {
+      const size_t n = r.size() < cap - 1 ? r.size() : cap - 1;
+      std::memcpy(report, r.data(), n);
+      report[n] = '\0';
+    }
+  });
+}
+
 int decmul_gpu_get_stats(decmul_gpu_ctx* ctx, decmul_gpu_stats* out) {
   LOCKED(ctx, {
     out->last_launches = ctx->eng->last_launches();

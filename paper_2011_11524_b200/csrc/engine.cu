@@ -20,7 +20,7 @@ u64 recip_of(u64 d) {  // reference make_div_by_const (decimal.hpp:93-104), for 
   return u64(~(u128)0 / d - ((u128)1 << 64));
 }
 
-DivB div_for(u64 base) {
+DivB div_for_impl(u64 base) {
   DivB d;
   d.base = base;
   d.shift = __builtin_clzll(base);
@@ -501,10 +501,7 @@ void Engine::check_err(cudaStream_t st) {
 
 namespace {
 
-struct CrtConsts {
-  u64 p2_prime, r_tilde;
-};
-CrtConsts crt_consts(u64 p1, u64 p2) {  // make_crt_ctx, decimal.cpp:136-146
+CrtConsts crt_consts_impl(u64 p1, u64 p2) {  // make_crt_ctx, decimal.cpp:136-146
   if (p1 >= p2) throw std::invalid_argument("make_crt_ctx: requires p1 < p2");
   HostField F2(p2);
   return {F2.pp, F2.to_mont(F2.inv(p1 % p2))};
@@ -1278,5 +1275,8 @@ void Engine::shard_carry_emit(const ShardPlan& sp, int q, unsigned rank_cin, uns
   cuda_check(cudaGetLastError(), "shard emit");
   check_err(st);
 }
+
+DivB div_for(u64 base) { return div_for_impl(base); }
+CrtConsts crt_consts(u64 p1, u64 p2) { return crt_consts_impl(p1, p2); }
 
 }  // namespace dmg

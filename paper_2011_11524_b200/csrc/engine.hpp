@@ -103,6 +103,14 @@ struct ShardPlan {
   unsigned long long top_candidates[2] = {0, 0};
 };
 
+// Reciprocal-division constants for B = 10^lambda (reference make_div_by_const, decimal.hpp:93-104).
+DivB div_for(u64 base);
+// CRT constants of a pair (reference make_crt_ctx, decimal.cpp:136-146).
+struct CrtConsts {
+  u64 p2_prime, r_tilde;
+};
+CrtConsts crt_consts(u64 p1, u64 p2);
+
 // Host-only shard planning (no device): decmul_gpu_shard_plan_create with a NULL context.
 ShardPlan make_shard_plan(std::size_t dx, std::size_t dy, int G);
 
@@ -178,6 +186,13 @@ class Engine {
   const PrimePlan& prime_plan(u64 p, std::size_t N);
   // Length of the last product (after its stream was synchronised); raises its errors.
   std::size_t result_length();
+
+  // GPU self-test mirroring the reference's run_selftest (selftest.cpp:79-219): suites of
+  // field identities, transform round trips, convolution vs direct, CRT, base division,
+  // carry recovery and small products on the device path; inject_fault corrupts one
+  // root-table entry of a plan (restored afterwards) to prove the checks detect it.
+  // Appends "suite=... checks=... failures=..." lines to report; returns the failures.
+  int selftest(bool inject_fault, std::string& report);
 
   // bytes of device tables currently held by plans
   std::size_t table_bytes() const;

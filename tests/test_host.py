@@ -45,6 +45,24 @@ def test_no_gpu_fails_loudly():
         dm.Context(0)
 
 
+def test_cli_usage_errors_and_no_gpu_failure():
+    """tools/decmul: malformed invocations exit 1 with "error: ..." (reference
+    main.cpp:150-153); without a GPU a product fails loudly instead of falling back."""
+    import subprocess
+
+    import torch
+
+    cli = os.path.join(ROOT, "tools", "decmul")
+    if not os.path.exists(cli):
+        pytest.skip("CLI not built")
+    for args in (["foo"], ["mul", "1"], ["bench", "mul"], ["bench", "modmul", "--variant", "x"], []):
+        r = subprocess.run([cli, *args], capture_output=True, text=True, timeout=60)
+        assert r.returncode == 1 and r.stderr.startswith("error: "), args
+    if not torch.cuda.is_available():
+        r = subprocess.run([cli, "mul", "12", "34"], capture_output=True, text=True, timeout=60)
+        assert r.returncode == 1 and r.stderr.startswith("error: ") and r.stdout == ""
+
+
 def test_planner_through_c_abi_matches_reference_kats(golden):
     for need, want in golden["kat"]["smallest_supported_length"]:
         assert dm.smallest_supported_length(need) == want
