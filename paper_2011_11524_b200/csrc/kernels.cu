@@ -12,6 +12,7 @@
 #include <type_traits>
 
 #include "kernels.cuh"
+#include "digits.cuh"
 #include "ntt_tile.cuh"
 
 namespace dmg {
@@ -88,9 +89,19 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW)) k_pass_fwd(PassArgs a)
   const u64* src = a.src[pr];
   u64* dst = a.dst[pr];
   const TwPair* __restrict__ T = a.pass_tw[pr];
+  const Geom<LOGR, ROWS, TW> G(a);
+  if constexpr (ROWS) {
+    // The twiddles are applied in the epilogue, after the DIF; start pulling the tile's
+    // rows T[f][s0 .. s0 + TW) (TW pairs = TW * 16 bytes each) into L2 now so those
+    // loads hit L2 instead of DRAM (large-S passes stream a table of N / 3 .. N pairs).
+    constexpr int LINES = TW * 16 / 128 > 0 ? TW * 16 / 128 : 1;
+    for (int i = tid; i < R * LINES; i += NTK) {
+      const TwPair* row = &G.tw(T, i / LINES, 0) + (i % LINES) * 8;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+    }
+  }
   load_table<LOGR, NTK>(tw, a.dft_fwd[pr]);
   __syncthreads();
-  const Geom<LOGR, ROWS, TW> G(a);
   const TileLayout<LOGR, ROWS, TW> L;
   if constexpr (LOGR == E1) {  // one round: HBM -> registers -> HBM
     for (int g = tid; g < (R >> E1) * TW; g += NTK) {
@@ -382,36 +393,6 @@ __global__ void k_gen_table(GenArgs g) {
 // contiguous in the string) is staged in shared memory with 16-byte loads, then
 // each thread parses its lambda digits 8 at a time (SWAR).
 constexpr int kPackLimbs = 256;
-
-// 8 bytes of shared memory at any byte offset (buf 8-aligned, readable 8 bytes past).
-__device__ __forceinline__ u64 smem_bytes8(const char* buf, int pos) {
-  const u64* w = reinterpret_cast<const u64*>(buf + (pos & ~7));
-  const int sh = (pos & 7) * 8;
-  return sh ? (w[0] >> sh) | (w[1] << (64 - sh)) : w[0];
-}
-
-// Value of 8 ASCII digits (first byte most significant) whose first `skip` bytes are
-// treated as '0'; flags any non-digit byte.
-__device__ __forceinline__ u64 swar8(u64 x, int skip, unsigned& bad) {
-  const u64 keep = skip >= 8 ? 0 : (~0ull << (8 * skip));
-  x = (x & keep) | (0x3030303030303030ull & ~keep);
-  bad |= ((x & 0xF0F0F0F0F0F0F0F0ull) != 0x3030303030303030ull) |
-         ((((x & 0x0F0F0F0F0F0F0F0Full) + 0x0606060606060606ull) & 0xF0F0F0F0F0F0F0F0ull) != 0);
-  x &= 0x0F0F0F0F0F0F0F0Full;
-  x = (x * 2561) >> 8;                                    // pairs: 10 d0 + d1
-  x = ((x & 0x00FF00FF00FF00FFull) * 6553601) >> 16;     // quads
-  x = ((x & 0x0000FFFF0000FFFFull) * 42949672960001ull) >> 32;  // 8 digits
-  return x;
-}
-
-// Digits buf[s, s + n), n <= 24, as an integer (three 8-digit chunks from the right).
-__device__ __forceinline__ u64 parse_digits(const char* buf, int s, int n, unsigned& bad) {
-  const int e = s + n;
-  u64 v = swar8(smem_bytes8(buf, e - 8), n >= 8 ? 0 : 8 - n, bad);
-  if (n > 8) v += swar8(smem_bytes8(buf, e - 16), n >= 16 ? 0 : 16 - n, bad) * 100000000ull;
-  if (n > 16) v += swar8(smem_bytes8(buf, e - 24), 24 - n, bad) * 10000000000000000ull;
-  return v;
-}
 
 __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d, unsigned long long nd, unsigned be,
                                                      u64* __restrict__ limbs, unsigned long long total, unsigned* err,

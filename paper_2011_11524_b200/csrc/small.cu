@@ -88,10 +88,14 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
       if (t < nl) {
         const long long end = (long long)nd - (long long)t * be;
         const long long begin = end > (long long)be ? end - (long long)be : 0;
-        for (long long i = begin; i < end; ++i) {
-          const unsigned c = (unsigned char)d[i] - '0';
-          bad |= c > 9;
-          limb = limb * 10 + c;
+        // fixed trip count, predicated: the <= 17 byte loads issue back to back
+#pragma unroll
+        for (int j = 0; j < 17; ++j) {
+          if (begin + j < end) {
+            const unsigned c = (unsigned char)d[begin + j] - '0';
+            bad |= c > 9;
+            limb = limb * 10 + c;
+          }
         }
       }
       const int ph = phys<LOGC>(t);
