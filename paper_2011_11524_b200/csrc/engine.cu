@@ -119,6 +119,11 @@ Engine::~Engine() {
     cudaEventDestroy(done_ev_[i]);
   }
   if (host_lens_) cudaFreeHost(host_lens_);
+  copy_pool_.reset();
+  for (int k = 0; k < kStageSlots; ++k) {
+    if (stage_[k]) cudaFreeHost(stage_[k]);
+    if (stage_ev_[k]) cudaEventDestroy(stage_ev_[k]);
+  }
   cudaStreamDestroy(stream_);
 }
 
@@ -517,7 +522,7 @@ void coeff_cap(unsigned be, std::size_t min_limbs, u64& lo, u64& hi) {
 }  // namespace
 
 void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, bool squaring, char* dout,
-                         cudaStream_t st) {
+                         cudaStream_t st, const std::function<void()>& before_y) {
   const PrimePlan& P1 = prime_plan(pp.p1, pp.N);
   const PrimePlan& P2 = prime_plan(pp.p2, pp.N);
   const unsigned be = pp.base_exp;
@@ -529,6 +534,7 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   launches_ = 0;
 
   if (P1.small_ok && P2.small_ok) {
+    if (before_y) before_y();
     SmallArgs a{};
     a.xs = dx;
     a.ys = squaring ? dx : dy;
@@ -600,10 +606,6 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
 
   launch_pack(dx, pp.dx, be, px, npad, err_.ptr, st);
   ++launches_;
-  if (!squaring) {
-    launch_pack(dy, pp.dy, be, py, npad, err_.ptr, st);
-    ++launches_;
-  }
   const PrimePlan* pl[2] = {&P1, &P2};
   auto forward = [&](const u64* packed, u64* const dst[2], bool include_last) {
     if (lean) {
@@ -630,6 +632,9 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
     u64* X[2] = {X_[0].ptr, X_[1].ptr};
     u64* Y[2] = {Y_[0].ptr, Y_[1].ptr};
     forward(px, X, true);
+    if (before_y) before_y();
+    launch_pack(dy, pp.dy, be, py, npad, err_.ptr, st);
+    ++launches_;
     forward(py, Y, !P1.last_pow2);
     if (P1.last_pow2) {
       const u64* oth[2] = {X[0], X[1]};
@@ -708,20 +713,37 @@ std::size_t Engine::result_length() {
 std::size_t Engine::multiply_host(const char* x, std::size_t nx, const char* y, std::size_t ny, char* out,
                                   std::size_t cap, unsigned forced, bool alias) {
   if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
-  const bool squaring = alias || (nx == ny && (x == y || std::memcmp(x, y, nx) == 0));
-  din_x_.ensure(nx);
-  cuda_check(cudaMemcpyAsync(din_x_.ptr, x, nx, cudaMemcpyHostToDevice, stream_), "h2d");
-  if (!squaring) {
-    din_y_.ensure(ny);
-    cuda_check(cudaMemcpyAsync(din_y_.ptr, y, ny, cudaMemcpyHostToDevice, stream_), "h2d");
+  if ((nx == 1 && x[0] == '0') || (ny == 1 && y[0] == '0')) {  // zero short-circuit (decimal.cpp:193)
+    if (cap < 1) throw std::length_error("multiply: output buffer too small");
+    out[0] = '0';
+    return 1;
   }
+  const bool squaring = alias || (nx == ny && (x == y || std::memcmp(x, y, nx) == 0));
+  const ProductPlan pp = plan_product(nx, ny, forced);
+  if (cap < nx + ny) throw std::length_error("multiply: output buffer too small");
+  din_x_.ensure(nx);
+  if (!squaring) din_y_.ensure(ny);
   dout_.ensure(nx + ny);
-  const std::size_t len = multiply_device(din_x_.ptr, nx, squaring ? din_x_.ptr : din_y_.ptr, squaring ? nx : ny,
-                                          dout_.ptr, nx + ny, forced, squaring, stream_, true);
+  // x uploads on the copy stream; the product runs on the context stream once x is in
+  // HBM, and y uploads while x is packed and transformed (run_product's before_y)
+  cudaStream_t cs = pipe_[0], st = stream_;
+  cuda_check(cudaEventRecord(pipe_ev_, st), "event");
+  cuda_check(cudaStreamWaitEvent(cs, pipe_ev_, 0), "wait");
+  stage_h2d(din_x_.ptr, x, nx, cs);
+  cuda_check(cudaEventRecord(up_ev_[0], cs), "event");
+  cuda_check(cudaStreamWaitEvent(st, up_ev_[0], 0), "wait");
+  run_product(pp, din_x_.ptr, squaring ? din_x_.ptr : din_y_.ptr, squaring, dout_.ptr, st, [&] {
+    if (squaring) return;
+    stage_h2d(din_y_.ptr, y, ny, cs);
+    cuda_check(cudaEventRecord(up_ev_[1], cs), "event");
+    cuda_check(cudaStreamWaitEvent(st, up_ev_[1], 0), "wait");
+  });
+  unsigned long long len = 0;
+  cuda_check(cudaMemcpyAsync(&len, meta_.ptr + 2, sizeof len, cudaMemcpyDeviceToHost, st), "len");
+  check_err(st);
   if (len > cap) throw std::length_error("multiply: output buffer too small");
-  cuda_check(cudaMemcpyAsync(out, dout_.ptr, len, cudaMemcpyDeviceToHost, stream_), "d2h");
-  cuda_check(cudaStreamSynchronize(stream_), "sync");
-  return len;
+  stage_d2h(out, dout_.ptr, std::size_t(len), st);
+  return std::size_t(len);
 }
 
 void Engine::multiply_batch_device(std::size_t count, const char* dxs, std::size_t x_stride, std::size_t nx,
