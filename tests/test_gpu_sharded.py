@@ -53,3 +53,34 @@ def test_sharded_large_pair_radix3_columns(gpu, ref, G):
     finally:
         del os.environ["DECMUL_FORCE_LARGE_PAIR"]
     assert z == ref.multiply(hx, hy)
+
+
+def test_nccl_transport_single_rank(gpu, ref):
+    """The TorchComm path over a real NCCL process group (all_to_all_single,
+    all_gather_object) — world size 1, the only NCCL group one GPU can host."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2011_11524_b200.sharded import TorchComm, rank_digit_range
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        be = DeviceBackend(gpu)
+        hx, hy = inputs.gen_digits(41, 900000), inputs.gen_digits(42, 800000)
+        plan = be.plan(len(hx), len(hy), 1)
+        x = torch.frombuffer(bytearray(hx), dtype=torch.uint8).cuda()
+        y = torch.frombuffer(bytearray(hy), dtype=torch.uint8).cuda()
+        out = torch.zeros(len(hx) + len(hy), dtype=torch.uint8, device="cuda")
+        n = sharded_multiply(be, TorchComm(dist), plan, [0], [x], [y], [out])
+        torch.cuda.synchronize()
+        assert rank_digit_range(plan, 0, n) == (0, n)
+        assert bytes(out[:n].cpu().numpy()) == ref.multiply(hx, hy)
+    finally:
+        dist.destroy_process_group()
