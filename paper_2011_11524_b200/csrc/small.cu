@@ -18,7 +18,7 @@ namespace dmg {
 
 namespace {
 
-constexpr int NT = 384;  // 12 warps; 3 CTAs/SM at <= 56 registers (36 warps per SM)
+constexpr int NT = 256;  // 8 warps, 3 CTAs/SM at <= 85 registers; measured fastest of 192/256/320/384(x3) and 512(x2)
 
 struct SmallField {
   u64 p0, p1;
