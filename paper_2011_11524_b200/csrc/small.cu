@@ -11,6 +11,7 @@
 // a set of NR rows of C = 2^LOGC words; element (array a, logical index i) lives
 // at a N + (i & ~(C-1)) + col_swizzle(i & (C-1)) (ContigColumns, conflict-free).
 #include "carry.cuh"
+#include "digits.cuh"
 #include "kernels.cuh"
 #include "ntt_tile.cuh"
 
@@ -78,32 +79,98 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
     ti1[i] = a.dft_inv[1][i];
   }
   // ---- pack (decimal.cpp:102-118) ----
-  for (int o = 0; o < Cfg::NOPER; ++o) {
-    const char* d = o ? a.ys + prod * a.y_stride : a.xs + prod * a.x_stride;
-    const unsigned long long nd = o ? a.ny : a.nx;
-    const long long nl = (long long)((nd + be - 1) / be);
+  const char* dxs = a.xs + prod * a.x_stride;
+  const char* dys = a.ys + prod * a.y_stride;
+  // Fast path: both digit strings land in shared memory in one burst of 16-byte
+  // cp.async copies (all in flight at once) into the y arrays, which are not written
+  // yet; x parses from there into its arrays, y's limbs wait in registers across one
+  // barrier. Strings whose aligned spans do not fit take the direct per-limb loads.
+  const unsigned long long ax0 = reinterpret_cast<unsigned long long>(dxs) & ~15ull;
+  const unsigned long long ay0 = reinterpret_cast<unsigned long long>(dys) & ~15ull;
+  const int nxv = int((reinterpret_cast<unsigned long long>(dxs) + a.nx + 15 - ax0) / 16);
+  const int nyv = Cfg::NOPER > 1 ? int((reinterpret_cast<unsigned long long>(dys) + a.ny + 15 - ay0) / 16) : 0;
+  constexpr int kRegion = (Cfg::NOPER > 1 ? 2 : 1) * N * 8;  // bytes of the y arrays (array 2 when squaring)
+  if (32 + 16 * (nxv + nyv) + 48 + 16 <= kRegion) {
+    char* xb = reinterpret_cast<char*>(sm + 2 * N) + 32;  // xb[k] = byte at address ax0 + k
+    char* yb = xb + 16 * nxv + 48;
+    for (int v = tid; v < nxv + nyv; v += NT) {
+      const bool isx = v < nxv;
+      char* dst = isx ? xb + 16 * v : yb + 16 * (v - nxv);
+      const char* src = reinterpret_cast<const char*>(isx ? ax0 + 16ull * v : ay0 + 16ull * (v - nxv));
+      const unsigned saddr = unsigned(__cvta_generic_to_shared(dst));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
     unsigned bad = 0;
-    for (int t = tid; t < N; t += NT) {
-      u64 limb = 0;
-      if (t < nl) {
-        const long long end = (long long)nd - (long long)t * be;
-        const long long begin = end > (long long)be ? end - (long long)be : 0;
-        // fixed trip count, predicated: the <= 17 byte loads issue back to back
+    constexpr int LPT = (N + NT - 1) / NT;  // limbs per thread
+    u64 ylimb[LPT];
+    for (int o = 0; o < Cfg::NOPER; ++o) {
+      const long long nd = (long long)(o ? a.ny : a.nx);
+      const long long nl = (nd + be - 1) / be;
+      const char* b = o ? yb : xb;
+      const int sh = int(reinterpret_cast<unsigned long long>(o ? dys : dxs) - (o ? ay0 : ax0));
 #pragma unroll
-        for (int j = 0; j < 17; ++j) {
-          if (begin + j < end) {
-            const unsigned c = (unsigned char)d[begin + j] - '0';
-            bad |= c > 9;
-            limb = limb * 10 + c;
+      for (int j = 0; j < LPT; ++j) {
+        const int t = tid + j * NT;
+        u64 limb = 0;
+        if (t < nl) {
+          const long long end = nd - (long long)t * be, begin = end > (long long)be ? end - (long long)be : 0;
+          limb = parse_digits(b, sh + int(begin), int(end - begin), bad);
+        }
+        if (o == 0) {
+          if (t < N) {
+            const int ph = phys<LOGC>(t);
+            sm[ph] = limb;
+            sm[N + ph] = limb;
           }
+        } else {
+          ylimb[j] = limb;
         }
       }
-      const int ph = phys<LOGC>(t);
-      sm[(2 * o) * N + ph] = limb;
-      sm[(2 * o + 1) * N + ph] = limb;
+      if (tid == 0 && nd > 1 && b[sh] == '0') atomicOr(a.err, kErrLeadingZero);
     }
     if (bad) atomicOr(a.err, kErrBadDigit);
-    if (tid == 0 && nd > 1 && d[0] == '0') atomicOr(a.err, kErrLeadingZero);
+    if constexpr (Cfg::NOPER > 1) {
+      __syncthreads();  // the staged text is dead: y's arrays may be written
+#pragma unroll
+      for (int j = 0; j < LPT; ++j) {
+        const int t = tid + j * NT;
+        if (t < N) {
+          const int ph = phys<LOGC>(t);
+          sm[2 * N + ph] = ylimb[j];
+          sm[3 * N + ph] = ylimb[j];
+        }
+      }
+    }
+  } else {
+    for (int o = 0; o < Cfg::NOPER; ++o) {
+      const char* d = o ? dys : dxs;
+      const unsigned long long nd = o ? a.ny : a.nx;
+      const long long nl = (long long)((nd + be - 1) / be);
+      unsigned bad = 0;
+      for (int t = tid; t < N; t += NT) {
+        u64 limb = 0;
+        if (t < nl) {
+          const long long end = (long long)nd - (long long)t * be;
+          const long long begin = end > (long long)be ? end - (long long)be : 0;
+          // fixed trip count, predicated: the <= 17 byte loads issue back to back
+#pragma unroll
+          for (int j = 0; j < 17; ++j) {
+            if (begin + j < end) {
+              const unsigned c = (unsigned char)d[begin + j] - '0';
+              bad |= c > 9;
+              limb = limb * 10 + c;
+            }
+          }
+        }
+        const int ph = phys<LOGC>(t);
+        sm[(2 * o) * N + ph] = limb;
+        sm[(2 * o + 1) * N + ph] = limb;
+      }
+      if (bad) atomicOr(a.err, kErrBadDigit);
+      if (tid == 0 && nd > 1 && d[0] == '0') atomicOr(a.err, kErrLeadingZero);
+    }
   }
   __syncthreads();
   // ---- forward: radix-3 columns (conv.cpp:109-125), then rows ----
