@@ -535,7 +535,17 @@ def run_ours(args, cfg, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def claim_stdout() -> None:
+    """Keep stdout for the one JSON line: libraries that print there (NCCL writes its
+    "NCCL version" banner to fd 1 when a communicator comes up) go to stderr instead."""
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(json_fd, "w", buffering=1)
+
+
 def main():
+    claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

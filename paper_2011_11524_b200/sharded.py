@@ -96,11 +96,18 @@ class LocalComm:
 
 
 class TorchComm:
-    """One shard per process over torch.distributed (NCCL for CUDA tensors, gloo for CPU)."""
+    """One shard per process over torch.distributed (NCCL for CUDA tensors, gloo for CPU).
+    The carry protocol's small all-gathers (halo residues, carry maps, top-limb probes)
+    go as int64 tensors — on the GPU under NCCL — rather than pickled objects."""
 
     def __init__(self, dist):
+        import torch
+
         self.dist = dist
+        self.torch = torch
         self.G = dist.get_world_size()
+        nccl = dist.get_backend() == "nccl"
+        self.device = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
 
     def all_to_all(self, sends, recvs):
         (send,), (recv,) = sends, recvs
@@ -108,9 +115,10 @@ class TorchComm:
 
     def all_gather(self, values):
         (v,) = values
-        out = [None] * self.G
-        self.dist.all_gather_object(out, np.asarray(v).tolist())
-        return [np.asarray(o, dtype=np.uint64) for o in out]
+        t = self.torch.from_numpy(np.ascontiguousarray(np.asarray(v, dtype=np.uint64)).view(np.int64)).to(self.device)
+        out = [self.torch.empty_like(t) for _ in range(self.G)]
+        self.dist.all_gather(out, t)
+        return [o.cpu().numpy().view(np.uint64) for o in out]
 
 
 # ---- device backend (libdecmul_gpu.so on torch CUDA tensors) ----

@@ -193,3 +193,19 @@ def test_two_rank_gloo_sharding(port):
     for (a, b), h in zip(seeds, [h for g in gathered for h in g[1]]):
         z = port.multiply(inputs.gen_digits(a, 300), inputs.gen_digits(b, 300))
         assert hashlib.sha256(z).hexdigest() == h
+
+
+def test_bench_reference_arm_prints_one_json_line():
+    """bench.py keeps stdout for exactly one JSON line (libraries' banners go to stderr);
+    the reference arm reports the reference's own refusal beyond its 3*2^24 cap."""
+    import json
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "4"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.strip().splitlines()
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and "unavailable" in d
