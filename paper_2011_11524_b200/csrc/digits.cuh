@@ -1,38 +1,45 @@
 // ASCII digits -> integers with SWAR arithmetic, from text staged in shared memory
 // (the pack step, reference decimal.cpp:102-118). Used by k_pack and k_small.
+//
+// 32-bit lanes throughout: a limb's <= 20 digits are five 4-digit groups taken from the
+// right with funnel shifts, each converted by two multiply-add steps (one IMAD each on
+// 32-bit words, where 64-bit SWAR needs 3-4 per multiply and multi-instruction variable
+// shifts).
 #pragma once
 #include "modarith.cuh"
 
 namespace dmg {
 
-// 8 bytes of shared memory at any byte offset (buf 8-aligned, readable 8 bytes past).
-__device__ __forceinline__ u64 smem_bytes8(const char* buf, int pos) {
-  const u64* w = reinterpret_cast<const u64*>(buf + (pos & ~7));
-  const int sh = (pos & 7) * 8;
-  return sh ? (w[0] >> sh) | (w[1] << (64 - sh)) : w[0];
+// 4 bytes of shared memory at any byte offset (buf 4-aligned, readable 4 bytes past).
+__device__ __forceinline__ unsigned smem_bytes4(const char* buf, int pos) {
+  const unsigned* w = reinterpret_cast<const unsigned*>(buf + (pos & ~3));
+  return __funnelshift_r(w[0], w[1], (pos & 3) * 8);
 }
 
-// Value of 8 ASCII digits (first byte most significant) whose first `skip` bytes are
-// treated as '0'; flags any non-digit byte.
-__device__ __forceinline__ u64 swar8(u64 x, int skip, unsigned& bad) {
-  const u64 keep = skip >= 8 ? 0 : (~0ull << (8 * skip));
-  x = (x & keep) | (0x3030303030303030ull & ~keep);
-  bad |= ((x & 0xF0F0F0F0F0F0F0F0ull) != 0x3030303030303030ull) |
-         ((((x & 0x0F0F0F0F0F0F0F0Full) + 0x0606060606060606ull) & 0xF0F0F0F0F0F0F0F0ull) != 0);
-  x &= 0x0F0F0F0F0F0F0F0Full;
-  x = (x * 2561) >> 8;                                    // pairs: 10 d0 + d1
-  x = ((x & 0x00FF00FF00FF00FFull) * 6553601) >> 16;     // quads
-  x = ((x & 0x0000FFFF0000FFFFull) * 42949672960001ull) >> 32;  // 8 digits
-  return x;
+// Value of 4 ASCII digits (first byte most significant) whose first `skip` bytes are
+// treated as '0'; flags any byte outside '0'..'9'.
+__device__ __forceinline__ unsigned swar4(unsigned x, int skip, unsigned& bad) {
+  const unsigned keep = skip >= 4 ? 0u : (0xFFFFFFFFu << (8 * skip));
+  x = (x & keep) | (0x30303030u & ~keep);
+  // per byte b: high bit of b (non-ASCII), of b + 0x46 (b > '9'), or clear in
+  // (b | 0x80) - 0x30 (b < '0'); no carry or borrow crosses a byte for ASCII bytes
+  bad |= (x | (x + 0x46464646u) | ~((x | 0x80808080u) - 0x30303030u)) & 0x80808080u;
+  x &= 0x0F0F0F0Fu;
+  x = (x * 10u + (x >> 8)) & 0x00FF00FFu;  // bytes 0, 2: 10 d0 + d1, 10 d2 + d3
+  return (x * 100u + (x >> 16)) & 0xFFFFu;
 }
 
-// Digits buf[s, s + n), n <= 24, as an integer (three 8-digit chunks from the right).
+// Digits buf[s, s + n), n <= 20, as an integer (five 4-digit groups from the right).
 __device__ __forceinline__ u64 parse_digits(const char* buf, int s, int n, unsigned& bad) {
   const int e = s + n;
-  u64 v = swar8(smem_bytes8(buf, e - 8), n >= 8 ? 0 : 8 - n, bad);
-  if (n > 8) v += swar8(smem_bytes8(buf, e - 16), n >= 16 ? 0 : 16 - n, bad) * 100000000ull;
-  if (n > 16) v += swar8(smem_bytes8(buf, e - 24), 24 - n, bad) * 10000000000000000ull;
-  return v;
+  unsigned g[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const int skip = 4 * (k + 1) - n;  // bytes of the group before s
+    g[k] = skip < 4 ? swar4(smem_bytes4(buf, e - 4 * (k + 1)), skip < 0 ? 0 : skip, bad) : 0u;
+  }
+  const unsigned lo8 = g[1] * 10000u + g[0], hi8 = g[3] * 10000u + g[2];
+  return (u64)g[4] * 10000000000000000ull + (u64)hi8 * 100000000ull + lo8;
 }
 
 }  // namespace dmg

@@ -19,6 +19,24 @@ namespace dmg {
 
 namespace {
 
+#ifdef DMG_PHASE_TIMING
+// Diagnostic build only (make PHASE_TIMING=1): cycles per k_small phase summed over CTAs.
+__device__ unsigned long long g_phase_cycles[12];
+#define DMG_PHASE(i)                                         \
+  do {                                                       \
+    __syncthreads();                                         \
+    if (threadIdx.x == 0) {                                  \
+      const long long t_ = clock64();                        \
+      atomicAdd(&g_phase_cycles[i], (unsigned long long)(t_ - t_phase)); \
+      t_phase = t_;                                          \
+    }                                                        \
+  } while (0)
+#else
+#define DMG_PHASE(i) \
+  do {               \
+  } while (0)
+#endif
+
 constexpr int NT = 256;  // 8 warps, 3 CTAs/SM at <= 85 registers; measured fastest of 192/256/320/384(x3) and 512(x2)
 
 struct SmallField {
@@ -70,6 +88,9 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
   const int tid = threadIdx.x;
   const unsigned prod = blockIdx.x;
   const unsigned be = a.base_exp;
+#ifdef DMG_PHASE_TIMING
+  long long t_phase = clock64();
+#endif
   const u64 p0 = a.p[0], p1 = a.p[1];
 
   for (int i = tid; i < C / 2; i += NT) {
@@ -102,6 +123,7 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    DMG_PHASE(8);  // tables + digit loads
     unsigned bad = 0;
     constexpr int LPT = (N + NT - 1) / NT;  // limbs per thread
     u64 ylimb[LPT];
@@ -129,6 +151,7 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
         }
       }
       if (tid == 0 && nd > 1 && b[sh] == '0') atomicOr(a.err, kErrLeadingZero);
+      if (o == 0) DMG_PHASE(9);  // parse x
     }
     if (bad) atomicOr(a.err, kErrBadDigit);
     if constexpr (Cfg::NOPER > 1) {
@@ -173,6 +196,7 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
     }
   }
   __syncthreads();
+  DMG_PHASE(0);  // pack
   // ---- forward: radix-3 columns (conv.cpp:109-125), then rows ----
   if constexpr (THREE) {
     for (int i = tid; i < 2 * Cfg::NOPER * C; i += NT) {
@@ -188,7 +212,9 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
     }
     __syncthreads();
   }
+  DMG_PHASE(1);  // radix-3 forward
   tile_dif<LOGC, Cfg::W>(sm, ContigColumns<LOGC>(), SmallField{p0, p1, tf0, tf1, NR}, tid, NT);
+  DMG_PHASE(2);  // forward rows
   // ---- pointwise REDC (conv.cpp:205-208); squaring reuses X. X and Y share the
   // same swizzle, so physical offsets pair the same spectrum index. ----
   for (int i = tid; i < 2 * N; i += NT) {
@@ -197,6 +223,7 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
     sm[i] = mont_mul(v, SQ ? v : sm[2 * N + i], q ? p1 : p0, a.pp[q]);
   }
   __syncthreads();
+  DMG_PHASE(3);  // pointwise
   tile_dit<LOGC, 2 * NR>(sm, ContigColumns<LOGC>(), SmallField{p0, p1, ti0, ti1, NR}, tid, NT);
   if constexpr (THREE) {
     for (int i = tid; i < 2 * C; i += NT) {
@@ -219,6 +246,7 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
     }
   }
   __syncthreads();
+  DMG_PHASE(4);  // inverse (rows + radix-3)
   // ---- CRT + digit split (decimal.cpp:148-152, bounds :174-180), per physical slot ----
   u64* D0 = sm;
   u64* D1 = sm + N;
@@ -233,6 +261,7 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
     D2[i] = d2;
   }
   __syncthreads();
+  DMG_PHASE(5);  // CRT + split
   // ---- carry scan over limbs k < N + 2 (logical order) ----
   const u64 B = a.div.base;
   u64 s[Cfg::KPT];
@@ -283,6 +312,7 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
     a.out_lens[prod] = meta[2];
   }
   __syncthreads();
+  DMG_PHASE(6);  // carry scan
   // ---- to_decimal: stage the text in shared memory, store 16-byte vectors ----
   const unsigned long long top = meta[0];
   const unsigned top_len = unsigned(meta[1]);
@@ -294,6 +324,7 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
     write_digits(text + limb_pos(k, top, top_len, be), Z[k], (unsigned long long)k == top ? top_len : be);
   __syncthreads();
   cta_store_bytes(out, text, unsigned(meta[2]), tid, NT);
+  DMG_PHASE(7);  // digits out
 }
 
 template <int LOGC, int THREE, int SQ>
@@ -373,3 +404,12 @@ bool launch_small(const SmallArgs& a, cudaStream_t st) {
 }
 
 }  // namespace dmg
+
+#ifdef DMG_PHASE_TIMING
+extern "C" int decmul_gpu_debug_phase_cycles(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, dmg::g_phase_cycles, sizeof dmg::g_phase_cycles) != cudaSuccess) return 1;
+  unsigned long long z[12] = {0};
+  return cudaMemcpyToSymbol(dmg::g_phase_cycles, z, sizeof z) == cudaSuccess ? 0 : 1;
+}
+#endif
