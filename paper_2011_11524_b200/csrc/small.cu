@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
   const int nxv = int((reinterpret_cast<unsigned long long>(dxs) + a.nx + 15 - ax0) / 16);
   const int nyv = Cfg::NOPER > 1 ? int((reinterpret_cast<unsigned long long>(dys) + a.ny + 15 - ay0) / 16) : 0;
   constexpr int kRegion = (Cfg::NOPER > 1 ? 2 : 1) * N * 8;  // bytes of the y arrays (array 2 when squaring)
+  bool fused3 = false;  // the radix-3 column pass already ran on the packed limbs
   if (32 + 16 * (nxv + nyv) + 48 + 16 <= kRegion) {
     char* xb = reinterpret_cast<char*>(sm + 2 * N) + 32;  // xb[k] = byte at address ax0 + k
     char* yb = xb + 16 * nxv + 48;
@@ -126,7 +127,28 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
     DMG_PHASE(8);  // tables + digit loads
     unsigned bad = 0;
     constexpr int LPT = (N + NT - 1) / NT;  // limbs per thread
-    u64 ylimb[LPT];
+    // C = 2 NT (config 2: 3 x 512 at 256 threads): a thread's limbs t = tid + j NT are the
+    // three limbs s, s + C, s + 2C of its columns s = tid and tid + NT, so the radix-3
+    // column pass runs on them in registers (no limb store and reload).
+    constexpr bool kFuse3 = THREE && C == 2 * NT && LPT == 6;
+    auto r3_columns = [&](const u64* lim, int first_arr) {
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int sc = tid + cc * NT;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const u64 p = q ? p1 : p0;
+          const TwPair* T = a.r3_fwd[q];
+          u64* x = sm + (first_arr + q) * N + col_swizzle(sc);
+          const u64 x0 = lim[cc], x1 = lim[cc + 2], x2 = lim[cc + 4];
+          const u64 t = shoup_mul(mod_sub(x1, x2, p), a.lam[q], p);
+          x[0] = mod_add(mod_add(x0, x1, p), x2, p);
+          x[C] = shoup_mul(mod_add(mod_sub(x0, x2, p), t, p), T[C + sc], p);
+          x[2 * C] = shoup_mul(mod_sub(mod_sub(x0, x1, p), t, p), T[2 * C + sc], p);
+        }
+      }
+    };
+    u64 xlimb[LPT], ylimb[LPT];
     for (int o = 0; o < Cfg::NOPER; ++o) {
       const long long nd = (long long)(o ? a.ny : a.nx);
       const long long nl = (nd + be - 1) / be;
@@ -141,7 +163,8 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
           limb = parse_digits(b, sh + int(begin), int(end - begin), bad);
         }
         if (o == 0) {
-          if (t < N) {
+          xlimb[j] = limb;
+          if (!kFuse3 && t < N) {
             const int ph = phys<LOGC>(t);
             sm[ph] = limb;
             sm[N + ph] = limb;
@@ -151,21 +174,29 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
         }
       }
       if (tid == 0 && nd > 1 && b[sh] == '0') atomicOr(a.err, kErrLeadingZero);
-      if (o == 0) DMG_PHASE(9);  // parse x
+      if (o == 0) {
+        if constexpr (kFuse3) r3_columns(xlimb, 0);
+        DMG_PHASE(9);  // parse x
+      }
     }
     if (bad) atomicOr(a.err, kErrBadDigit);
     if constexpr (Cfg::NOPER > 1) {
       __syncthreads();  // the staged text is dead: y's arrays may be written
+      if constexpr (kFuse3) {
+        r3_columns(ylimb, 2);
+      } else {
 #pragma unroll
-      for (int j = 0; j < LPT; ++j) {
-        const int t = tid + j * NT;
-        if (t < N) {
-          const int ph = phys<LOGC>(t);
-          sm[2 * N + ph] = ylimb[j];
-          sm[3 * N + ph] = ylimb[j];
+        for (int j = 0; j < LPT; ++j) {
+          const int t = tid + j * NT;
+          if (t < N) {
+            const int ph = phys<LOGC>(t);
+            sm[2 * N + ph] = ylimb[j];
+            sm[3 * N + ph] = ylimb[j];
+          }
         }
       }
     }
+    fused3 = kFuse3;
   } else {
     for (int o = 0; o < Cfg::NOPER; ++o) {
       const char* d = o ? dys : dxs;
@@ -198,7 +229,7 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
   __syncthreads();
   DMG_PHASE(0);  // pack
   // ---- forward: radix-3 columns (conv.cpp:109-125), then rows ----
-  if constexpr (THREE) {
+  if (THREE && !fused3) {
     for (int i = tid; i < 2 * Cfg::NOPER * C; i += NT) {
       const int arr = i / C, s = i % C, q = arr & 1;
       const u64 p = q ? p1 : p0;
