@@ -292,6 +292,13 @@ class Port(_Lib):
             res = [(res[k] * pow(10, ln, qs[k]) + r[k]) % qs[k] for k in range(nq)]
         return res
 
+    def add_shifted(self, acc: np.ndarray, p: bytes, shift: int) -> None:
+        """acc (little-endian uint8 decimal digits) += int(p) * 10^shift, exactly."""
+        rc = self.fn("add_shifted")(C.c_void_p(acc.ctypes.data), C.c_size_t(acc.size), p, C.c_size_t(len(p)),
+                                    C.c_size_t(shift))
+        if rc:
+            raise OracleError(rc, "add_shifted: sum does not fit the accumulator")
+
     def gen_residues(self, seed: int, n: int, p: int):
         out = np.zeros(n, np.uint64)
         self.fn("gen_residues", None)(C.c_uint64(seed), C.c_size_t(n), C.c_uint64(p), _ptr(out))

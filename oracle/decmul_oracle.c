@@ -863,6 +863,29 @@ u64 or_residue_mod(const char* s, size_t n, u64 q) {
   return acc;
 }
 
+/* Composed-reference oracle for products beyond the reference's cap:
+ * acc (little-endian decimal digits 0..9, acc_len of them) += p * 10^shift, where p is
+ * plen ASCII digits, most significant first. Exact, with carry propagation; returns 0, or
+ * 1 if the sum does not fit acc. */
+int or_add_shifted(unsigned char* acc, size_t acc_len, const char* p, size_t plen, size_t shift) {
+  unsigned carry = 0;
+  size_t i = 0;
+  for (; i < plen; ++i) {
+    const size_t k = shift + i;
+    if (k >= acc_len) return 1;
+    const unsigned v = acc[k] + (unsigned)(p[plen - 1 - i] - '0') + carry;
+    acc[k] = (unsigned char)(v >= 10 ? v - 10 : v);
+    carry = v >= 10;
+  }
+  for (size_t k = shift + i; carry; ++k) {
+    if (k >= acc_len) return 1;
+    const unsigned v = acc[k] + carry;
+    acc[k] = (unsigned char)(v >= 10 ? v - 10 : v);
+    carry = v >= 10;
+  }
+  return 0;
+}
+
 /* Residues of one digit string modulo nq primes q < 2^62 in a single pass (fingerprints
  * of 1e10-digit products); callers combine chunk residues as
  * r(ab) = r(a) 10^|b| + r(b). Reentrant (no shared state), so chunks run on threads. */

@@ -1,9 +1,12 @@
-"""GPU parity at BASELINE.json's full sizes through size-independent properties:
-the reference's own 1e6-digit bench product (golden SHA-256), the all-nines closed
-form (10^n - 1)^2 (reference oracle.cpp:171-180), residue fingerprints
-z == x y (mod q) for 61-bit primes q, the exact low window
-z mod 10^K == (x mod 10^K)(y mod 10^K) mod 10^K, and the digit count."""
+"""GPU parity at BASELINE.json's full sizes: the reference's own 1e6-digit bench product
+(golden SHA-256), exact SHA-256 goldens of configs 3 and 4 from the compiled reference
+(config 4 by the composed-reference oracle beyond the reference's cap;
+tests/golden/make_golden_large.py), the all-nines closed form (10^n - 1)^2 (reference
+oracle.cpp:171-180), residue fingerprints z == x y (mod q) for 61-bit primes q, the exact
+low window z mod 10^K == (x mod 10^K)(y mod 10^K) mod 10^K, and the digit count."""
 import hashlib
+import json
+import os
 
 import numpy as np
 import pytest
@@ -13,6 +16,12 @@ import paper_2011_11524_b200 as dm
 pytestmark = pytest.mark.gpu
 
 FINGERPRINT_PRIMES = (2305843009213693951, 2305843009213693921, 1152921504606846883, 4611686018427387847)
+GOLDEN_LARGE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_large.json")
+
+
+def large_golden(key):
+    with open(GOLDEN_LARGE) as f:
+        return json.load(f)[key]
 
 
 def sha(b):
@@ -64,6 +73,8 @@ def test_config3_uniform_fingerprints(gpu, port, ref):
     assert ln in (2 * n - 1, 2 * n)
     hx, hy, hz = bytes(x.cpu().numpy()), bytes(y.cpu().numpy()), bytes(out[:ln].cpu().numpy())
     assert hz[:1] != b"0"
+    g = large_golden("config3")  # the reference's own product of the same operands
+    assert g["seeds"] == [0, 1] and (len(hz), sha(hz)) == (g["length"], g["sha256"])
     _check_fingerprints(port, ref, hx, hy, hz)
 
 
@@ -136,4 +147,6 @@ def test_config4_unbalanced_fingerprints(gpu, port, ref):
     x, y, out, ln = _device_product(gpu, nx, ny, 40, 41)
     assert ln in (nx + ny - 1, nx + ny)
     hx, hy, hz = bytes(x.cpu().numpy()), bytes(y.cpu().numpy()), bytes(out[:ln].cpu().numpy())
+    g = large_golden("config4")  # composed from 18 reference chunk products
+    assert g["seeds"] == [40, 41] and (len(hz), sha(hz)) == (g["length"], g["sha256"])
     _check_fingerprints(port, ref, hx, hy, hz, k=10000)

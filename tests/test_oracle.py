@@ -3,6 +3,7 @@ against the reference's own known-answer tests and against the compiled
 reference (golden fixtures from tests/golden/make_golden.py and, where present,
 oracle/_ref live). CPU only."""
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -203,3 +204,19 @@ def test_residue_fingerprint(port):
     for q in (2**61 - 1, 1000000007, 998244353):
         assert port.residue_mod(z, q) == port.residue_mod(x, q) * port.residue_mod(y, q) % q
         assert port.residue_mod(x[:4000], q) == int(x[:4000]) % q
+
+
+def test_composed_reference_oracle_small(port, ref):
+    """the composed-reference oracle (chunk products by the reference's
+    multiply, exact shifted decimal sum) equals the reference's direct product; it is how
+    the config-4 golden (tests/golden/golden_large.json) is made beyond the reference's cap."""
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+    from make_golden_large import composed_product
+
+    for (sx, nx), (sy, ny), k in (((7, 200_003), (8, 100_001), 30_001), ((9, 5_000), (10, 4_999), 997)):
+        x, y = port.gen_digits(sx, nx), port.gen_digits(sy, ny)
+        assert composed_product(port, ref, x, y, k, 4) == ref.multiply(x, y)
+    nines = b"9" * 20_000
+    assert composed_product(port, ref, nines, nines, 3_000, 4) == b"9" * 19_999 + b"8" + b"0" * 19_999 + b"1"
