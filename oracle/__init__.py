@@ -299,6 +299,15 @@ class Port(_Lib):
         if rc:
             raise OracleError(rc, "add_shifted: sum does not fit the accumulator")
 
+    def carry_u16(self, acc: np.ndarray) -> bytes:
+        """Decimal string (most significant first, leading zeros stripped) of a carry-free
+        little-endian uint16 digit-column accumulator."""
+        out = C.create_string_buffer(acc.size + 1)
+        rc = self.fn("carry_u16")(C.c_void_p(acc.ctypes.data), C.c_size_t(acc.size), out)
+        if rc:
+            raise OracleError(rc, "carry_u16: carry overflow")
+        return out.raw[: acc.size + 1].lstrip(b"0") or b"0"
+
     def gen_residues(self, seed: int, n: int, p: int):
         out = np.zeros(n, np.uint64)
         self.fn("gen_residues", None)(C.c_uint64(seed), C.c_size_t(n), C.c_uint64(p), _ptr(out))

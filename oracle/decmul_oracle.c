@@ -886,6 +886,22 @@ int or_add_shifted(unsigned char* acc, size_t acc_len, const char* p, size_t ple
   return 0;
 }
 
+/* Carry pass of a carry-free digit accumulator: acc[k] (little-endian positions, sums of
+ * digit columns, each < 2^16) -> the decimal string, most significant digit first,
+ * written to out[0, n] (n + 1 bytes; the top byte absorbs the final carry; leading
+ * zeros are left for the caller to strip). Returns 0, or 1 if the carry overflows. */
+int or_carry_u16(const unsigned short* acc, size_t n, char* out) {
+  unsigned long long carry = 0;
+  for (size_t k = 0; k < n; ++k) {
+    const unsigned long long v = acc[k] + carry;
+    out[n - k] = (char)('0' + v % 10);
+    carry = v / 10;
+  }
+  if (carry > 9) return 1;
+  out[0] = (char)('0' + carry);
+  return 0;
+}
+
 /* Residues of one digit string modulo nq primes q < 2^62 in a single pass (fingerprints
  * of 1e10-digit products); callers combine chunk residues as
  * r(ab) = r(a) 10^|b| + r(b). Reentrant (no shared state), so chunks run on threads. */

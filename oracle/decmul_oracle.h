@@ -79,6 +79,7 @@ int or_schoolbook_multiply(const char* x, size_t nx, const char* y, size_t ny, c
 
 /* Decimal value of s[0..n) mod q (fingerprint for products beyond the quadratic oracle). */
 uint64_t or_residue_mod(const char* s, size_t n, uint64_t q);
+int or_carry_u16(const unsigned short* acc, size_t n, char* out);
 int or_add_shifted(unsigned char* acc, size_t acc_len, const char* p, size_t plen, size_t shift);
 void or_residues_multi(const char* s, size_t n, const uint64_t* qs, int nq, uint64_t* out);
 
