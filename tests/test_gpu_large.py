@@ -118,8 +118,9 @@ def _low_window(t, k):
 
 def test_config5_ten_billion_digits(gpu, port, ref):
     """1e10 x 1e10 digits (BASELINE config 5) on one B200: N = 3 * 2^29 under the large
-    pair, 4 residue arrays of 12.9 GB. Checked by streamed residue fingerprints, the
-    exact low window and the digit count (SURVEY §8(c) 2)."""
+    pair, 4 residue arrays of 12.9 GB. Checked against the composed-reference SHA-256
+    (when tests/golden/golden_large.json holds it), streamed residue fingerprints, the
+    exact low window and the digit count (SURVEY §8(c))."""
     import torch
 
     n = 10**10
@@ -129,6 +130,13 @@ def test_config5_ten_billion_digits(gpu, port, ref):
     assert ln in (2 * n - 1, 2 * n)
     z = out[:ln]
     assert int(z[0]) != ord("0")
+    with open(GOLDEN_LARGE) as f:
+        g = json.load(f).get("config5")  # composed from 841 reference chunk products
+    if g is not None:
+        h = hashlib.sha256()
+        for off in range(0, ln, 1 << 31):
+            h.update(z[off:off + (1 << 31)].cpu().numpy().tobytes())
+        assert g["seeds"] == [50, 51] and (ln, h.hexdigest()) == (g["length"], g["sha256"])
     rx, ry, rz = (_device_residues(port, t, FINGERPRINT_PRIMES) for t in (x, y, z))
     for q, a, b, c in zip(FINGERPRINT_PRIMES, rx, ry, rz):
         assert c == a * b % q
