@@ -552,6 +552,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=None,
+                    help="batch configs: products per step instead of BASELINE's 4096 (experiments, e.g. the "
+                         "per-GPU share of an N-GPU split)")
     ap.add_argument("--sharded", action="store_true",
                     help="single-product configs: shard the product over the ranks even at N=1")
     args = ap.parse_args()
@@ -559,7 +562,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.impl == "reference" else 1)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.batch and cfg["count"] > 1:
+        cfg["count"] = args.batch
+        cfg["workload"] += f" [--batch {args.batch}]"
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
     elif cfg["count"] == 1 and (world > 1 or args.sharded):
