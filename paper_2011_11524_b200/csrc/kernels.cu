@@ -75,11 +75,14 @@ __device__ __forceinline__ void group_coords(int g, int& w, int& q) {
   group_of<ROWS, ((1 << LOGR) >> E), TW>(g, w, q);
 }
 
+// Launch bounds: tiles of R <= 256 use <= 34 KB of shared memory, so the register file
+// is the occupancy limit; capping them at 64 registers gives 4 CTAs per SM (measured
+// 1-2% faster on configs 3 and 4 despite a few spilled bytes in two instantiations).
 // Forward pass: column DIFs, then the inter-pass twiddle omega_M^{f s} (row passes).
 // The first round reads HBM into registers and the last round writes HBM from
 // registers; shared memory carries only the rounds in between.
 template <int LOGR, bool ROWS, int TW>
-__global__ void __launch_bounds__(pass_threads(LOGR, TW)) k_pass_fwd(PassArgs a) {
+__global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k_pass_fwd(PassArgs a) {
   constexpr int R = 1 << LOGR, NTK = pass_threads(LOGR, TW);
   constexpr int E1 = Sched<LOGR>::e_dif(LOGR), EL = Sched<LOGR>::first_e;
   extern __shared__ __align__(16) u64 sm[];
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW)) k_pass_fwd(PassArgs a)
 // Inverse pass: conjugate inter-pass twiddle (row passes; carries the convolution
 // scale on the first inverse pass), then column DITs.
 template <int LOGR, bool ROWS, int TW>
-__global__ void __launch_bounds__(pass_threads(LOGR, TW)) k_pass_inv(PassArgs a) {
+__global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k_pass_inv(PassArgs a) {
   constexpr int R = 1 << LOGR, NTK = pass_threads(LOGR, TW);
   constexpr int E1 = Sched<LOGR>::first_e;
   constexpr int EL = Sched<LOGR>::rem ? Sched<LOGR>::rem : E1;  // last DIT round
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW)) k_pass_inv(PassArgs a)
 // and the first DIT round act on the same 8-element groups, so DIF -> pointwise
 // -> DIT happens in registers.
 template <int LOGR, int TW>
-__global__ void __launch_bounds__(pass_threads(LOGR, TW)) k_pass_fused(PassArgs a) {
+__global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k_pass_fused(PassArgs a) {
   constexpr int R = 1 << LOGR, NTK = pass_threads(LOGR, TW);
   constexpr int E1 = Sched<LOGR>::e_dif(LOGR), EM = Sched<LOGR>::first_e;
   constexpr int EL = Sched<LOGR>::rem ? Sched<LOGR>::rem : EM;
