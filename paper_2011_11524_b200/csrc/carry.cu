@@ -36,6 +36,7 @@ __device__ __forceinline__ void coeff_digits(const CarryArgs& a, long long i, u6
 // then composes the maps of PER consecutive limbs (one 8-byte shared load).
 template <int NTC>
 __global__ void __launch_bounds__(NTC) k_carry_split(CarryArgs a) {
+  pdl_wait();
   constexpr int CHC = NTC * PER;
   __shared__ u64 d1s[CHC + 2], d2s[CHC + 2];
   __shared__ __align__(8) unsigned char mp[CHC];
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(NTC) k_carry_split(CarryArgs a) {
 // Phase 2 (one block): exclusive scan of chunk maps -> chunk carry-ins (stored in
 // place), then the top limb, its digit count and the output length.
 __global__ void __launch_bounds__(1024) k_carry_scan(CarryArgs a, unsigned nchunks) {
+  pdl_wait();
   __shared__ unsigned wsm[1024 / 32 + 1];
   __shared__ u64 zc[2];
   const unsigned per = (nchunks + 1023) / 1024;
@@ -173,6 +175,7 @@ __device__ __forceinline__ unsigned chunk_carry_in(const unsigned* maps, unsigne
 // top limb from the chunk maps itself (a few thousand maps at most).
 template <int NTC, bool SELF>
 __global__ void __launch_bounds__(NTC) k_carry_emit(CarryArgs a) {
+  pdl_wait();
   constexpr int CHC = NTC * PER;
   __shared__ unsigned wsm[NTC / 32 + 1];
   __shared__ __align__(16) char buf[CHC * 17 + 32];
@@ -310,13 +313,13 @@ int launch_carry(const CarryArgs& a, cudaStream_t st) {
   const unsigned nchunks = unsigned((K + CH - 1) / CH);
   if (nchunks < 2 * 148) {  // small product: 512-limb chunks, no separate scan
     const unsigned ns = unsigned((K + kCarryChunkSmall - 1) / kCarryChunkSmall);
-    k_carry_split<NT_SMALL><<<ns, NT_SMALL, 0, st>>>(a);
-    k_carry_emit<NT_SMALL, true><<<ns, NT_SMALL, 0, st>>>(a);
+    launch_pdl(k_carry_split<NT_SMALL>, dim3(ns), dim3(NT_SMALL), 0, st, a);
+    launch_pdl(k_carry_emit<NT_SMALL, true>, dim3(ns), dim3(NT_SMALL), 0, st, a);
     return 2;
   }
-  k_carry_split<NT><<<nchunks, NT, 0, st>>>(a);
-  k_carry_scan<<<1, 1024, 0, st>>>(a, nchunks);
-  k_carry_emit<NT, false><<<nchunks, NT, 0, st>>>(a);
+  launch_pdl(k_carry_split<NT>, dim3(nchunks), dim3(NT), 0, st, a);
+  launch_pdl(k_carry_scan, dim3(1), dim3(1024), 0, st, a, nchunks);
+  launch_pdl(k_carry_emit<NT, false>, dim3(nchunks), dim3(NT), 0, st, a);
   return 3;
 }
 

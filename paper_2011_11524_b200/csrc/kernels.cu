@@ -9,6 +9,7 @@
 // 128 B row segments (16 adjacent columns) so the reference's explicit
 // transpositions (conv.cpp:30-38) become strided addressing.
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k
   }
   load_table<LOGR, NTK>(tw, a.dft_fwd[pr]);
   __syncthreads();
+  pdl_wait();  // tables above are constant; the data below may come from the previous kernel
   const TileLayout<LOGR, ROWS, TW> L;
   if constexpr (LOGR == E1) {  // one round: HBM -> registers -> HBM
     for (int g = tid; g < (R >> E1) * TW; g += NTK) {
@@ -172,6 +174,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k
   const TwPair sc = a.final_scale[pr];
   load_table<LOGR, NTK>(tw, a.dft_inv[pr]);
   __syncthreads();
+  pdl_wait();  // tables above are constant; the data below may come from the previous kernel
   const Geom<LOGR, ROWS, TW> G(a);
   const TileLayout<LOGR, ROWS, TW> L;
   for (int g = tid; g < (R >> E1) * TW; g += NTK) {
@@ -239,6 +242,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k
   load_table<LOGR, NTK>(twf, a.dft_fwd[pr]);
   load_table<LOGR, NTK>(twi, a.dft_inv[pr]);
   __syncthreads();
+  pdl_wait();  // tables above are constant; the data below may come from the previous kernel
   const Geom<LOGR, false, TW> G(a);
   const ContigColumns<LOGR> L;
   if constexpr (LOGR > EM) {
@@ -302,6 +306,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k
 // Radix-3 pass (reference three_row_forward_columns conv.cpp:109-125, with the
 // length-3 DFT written with one multiplication: omega_3^2 = -1 - omega_3).
 __global__ void k_radix3_fwd(Radix3Args a) {
+  pdl_wait();
   const int pr = blockIdx.y;  // select, not index: keeps the parameter block out of local memory
   const u64 p = pr ? a.p[1] : a.p[0];
   const unsigned long long S = a.S;
@@ -329,6 +334,7 @@ __global__ void k_radix3_fwd(Radix3Args a) {
 // Inverse radix-3 pass (conv.cpp:129-147): twiddle (with the convolution scale
 // folded into the hi table when this is the first inverse pass) then length-3 IDFT*.
 __global__ void k_radix3_inv(Radix3Args a) {
+  pdl_wait();
   const int pr = blockIdx.y;  // select, not index: keeps the parameter block out of local memory
   const u64 p = pr ? a.p[1] : a.p[0];
   const unsigned long long S = a.S;
@@ -401,6 +407,7 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d,
                                                      u64* __restrict__ limbs, unsigned long long total, unsigned* err,
                                                      int row_bits, unsigned long long row_stride,
                                                      unsigned long long off) {
+  pdl_wait();
   __shared__ __align__(16) char smem[kPackLimbs * 17 + 96];
   char* buf = smem + 32;  // parse_digits may read up to 24 bytes before a limb and 8 past it
   const unsigned long long nl = (nd + be - 1) / be;
@@ -531,7 +538,7 @@ void launch_pass_kernel(const PassArgs& a, unsigned long long ncols, int np, int
   set_smem<FN>(smem);
   PassArgs b = a;
   b.np = np;
-  FN<<<unsigned((ncols + TW - 1) / TW * np), NTK, smem, st>>>(b);
+  launch_pdl(FN, dim3(unsigned((ncols + TW - 1) / TW * np)), dim3(NTK), size_t(smem), st, b);
 }
 
 // Tile width: 16 columns (128 B row segments) normally; 4 when a pass would otherwise
@@ -618,9 +625,9 @@ void launch_pass_fused(int logR, const PassArgs& a, unsigned long long ncols, in
 void launch_radix3(bool inverse, const Radix3Args& a, int np, cudaStream_t st) {
   const int g = grid_for(a.S, 256);
   if (inverse)
-    k_radix3_inv<<<dim3(g, np), 256, 0, st>>>(a);
+    launch_pdl(k_radix3_inv, dim3(g, np), dim3(256), 0, st, a);
   else
-    k_radix3_fwd<<<dim3(g, np), 256, 0, st>>>(a);
+    launch_pdl(k_radix3_fwd, dim3(g, np), dim3(256), 0, st, a);
 }
 
 void launch_gen_pass_table(TwPair* out, u64 root_mont, u64 scale_mont, int R, int /*logR*/, unsigned long long S,
@@ -649,7 +656,8 @@ void launch_pack(const char* digits, unsigned long long nd, unsigned be, u64* li
   if (row_bits < 8)
     k_pack_rows<<<grid_for(total, 256), 256, 0, st>>>(digits, nd, be, limbs, total, err, row_bits, row_stride, off);
   else
-    k_pack<<<grid_for(total, 256), 256, 0, st>>>(digits, nd, be, limbs, total, err, row_bits, row_stride, off);
+    launch_pdl(k_pack, dim3(grid_for(total, 256)), dim3(256), 0, st, digits, nd, be, limbs, total, err, row_bits,
+               row_stride, off);
 }
 void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, unsigned long long rows,
                           unsigned long long width, bool to_segments, cudaStream_t st) {
@@ -664,6 +672,14 @@ void launch_mont_scale(u64* a, unsigned long long n, u64 f, u64 p, u64 pp, cudaS
 }
 void launch_gather(const u64* src, u64* dst, const unsigned long long* map, unsigned long long n, cudaStream_t st) {
   k_gather<<<grid_for(n, 256), 256, 0, st>>>(src, dst, map, n);
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DECMUL_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 }  // namespace dmg
