@@ -76,14 +76,27 @@ __device__ __forceinline__ void group_coords(int g, int& w, int& q) {
   group_of<ROWS, ((1 << LOGR) >> E), TW>(g, w, q);
 }
 
-// Launch bounds: tiles of R <= 256 use <= 34 KB of shared memory, so the register file
-// is the occupancy limit; capping them at 64 registers gives 4 CTAs per SM (measured
-// 1-2% faster on configs 3 and 4 despite a few spilled bytes in two instantiations).
+// Minimum resident CTAs per SM requested from ptxas (launch bounds), measured per shape:
+//  * R = 256: tiles use 34 KB of shared memory, so registers limit occupancy; capping them
+//    at 64 (4 CTAs/SM) is 1-2% faster on configs 3-5 than ptxas's own choice (80: 3 CTAs);
+//  * R = 512, 16-column tiles (68 KB, at most 3 CTAs/SM): no cap at all (1) lets ptxas use
+//    up to 124 registers at 2 CTAs/SM — faster on config 4 than 3 CTAs at <= 85;
+//  * R = 512, 4-column tiles (small transforms, config 1): 3;
+//  * smaller radices: ptxas's default (0 = unspecified). NB an explicit 1 is not the
+//    default: it let ptxas double the registers of the R = 128 passes (6 -> 4 CTAs/SM,
+//    config 5 +2.6%).
+constexpr int pass_min_blocks(int logr, int tw) {
+  return logr == 9 ? (tw == kTileW ? 1 : 3) : (logr == 8 ? 4 : 0);
+}
+
 // Forward pass: column DIFs, then the inter-pass twiddle omega_M^{f s} (row passes).
 // The first round reads HBM into registers and the last round writes HBM from
 // registers; shared memory carries only the rounds in between.
 template <int LOGR, bool ROWS, int TW>
-__global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k_pass_fwd(PassArgs a) {
+__global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_fwd(PassArgs a) {
+  // at entry: a wait placed after the table loads kept the compiler from hoisting the
+  // first round's HBM loads above that barrier (config 5 +5%)
+  pdl_wait();
   constexpr int R = 1 << LOGR, NTK = pass_threads(LOGR, TW);
   constexpr int E1 = Sched<LOGR>::e_dif(LOGR), EL = Sched<LOGR>::first_e;
   extern __shared__ __align__(16) u64 sm[];
@@ -106,7 +119,6 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k
   }
   load_table<LOGR, NTK>(tw, a.dft_fwd[pr]);
   __syncthreads();
-  pdl_wait();  // tables above are constant; the data below may come from the previous kernel
   const TileLayout<LOGR, ROWS, TW> L;
   if constexpr (LOGR == E1) {  // one round: HBM -> registers -> HBM
     for (int g = tid; g < (R >> E1) * TW; g += NTK) {
@@ -159,7 +171,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k
 // Inverse pass: conjugate inter-pass twiddle (row passes; carries the convolution
 // scale on the first inverse pass), then column DITs.
 template <int LOGR, bool ROWS, int TW>
-__global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k_pass_inv(PassArgs a) {
+__global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_inv(PassArgs a) {
+  // at entry: a wait placed after the table loads kept the compiler from hoisting the
+  // first round's HBM loads above that barrier (config 5 +5%)
+  pdl_wait();
   constexpr int R = 1 << LOGR, NTK = pass_threads(LOGR, TW);
   constexpr int E1 = Sched<LOGR>::first_e;
   constexpr int EL = Sched<LOGR>::rem ? Sched<LOGR>::rem : E1;  // last DIT round
@@ -174,7 +189,6 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k
   const TwPair sc = a.final_scale[pr];
   load_table<LOGR, NTK>(tw, a.dft_inv[pr]);
   __syncthreads();
-  pdl_wait();  // tables above are constant; the data below may come from the previous kernel
   const Geom<LOGR, ROWS, TW> G(a);
   const TileLayout<LOGR, ROWS, TW> L;
   for (int g = tid; g < (R >> E1) * TW; g += NTK) {
@@ -225,7 +239,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k
 // and the first DIT round act on the same 8-element groups, so DIF -> pointwise
 // -> DIT happens in registers.
 template <int LOGR, int TW>
-__global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k_pass_fused(PassArgs a) {
+__global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_fused(PassArgs a) {
+  // at entry: a wait placed after the table loads kept the compiler from hoisting the
+  // first round's HBM loads above that barrier (config 5 +5%)
+  pdl_wait();
   constexpr int R = 1 << LOGR, NTK = pass_threads(LOGR, TW);
   constexpr int E1 = Sched<LOGR>::e_dif(LOGR), EM = Sched<LOGR>::first_e;
   constexpr int EL = Sched<LOGR>::rem ? Sched<LOGR>::rem : EM;
@@ -242,7 +259,6 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), (LOGR <= 8 ? 4 : 1)) k
   load_table<LOGR, NTK>(twf, a.dft_fwd[pr]);
   load_table<LOGR, NTK>(twi, a.dft_inv[pr]);
   __syncthreads();
-  pdl_wait();  // tables above are constant; the data below may come from the previous kernel
   const Geom<LOGR, false, TW> G(a);
   const ContigColumns<LOGR> L;
   if constexpr (LOGR > EM) {
