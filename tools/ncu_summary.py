@@ -1,7 +1,10 @@
 """Summarise ncu --set full captures into profiles/r01_ncu_summary.txt and the dominant
 kernel's dram bytes per launch into profiles/ncu_summary.json (bench roofline.traffic).
 
-    python tools/ncu_summary.py TAG=report.ncu-rep [TAG=report.ncu-rep ...] [--traffic CONFIG=TAG]
+    python tools/ncu_summary.py TAG=report.ncu-rep [...] [CONFIG=TAG[:kernel-substring] ...]
+
+CONFIG=TAG entries set profiles/ncu_summary.json[CONFIG] from the first kernel of report
+TAG whose name contains the substring (default: the report's first kernel).
 """
 import csv
 import io
@@ -56,13 +59,15 @@ def main():
                 if k in r:
                     lines.append(f"   {k:85s} {r[k][0]} {r[k][1]}")
             rd, wr = r["dram__bytes_read.sum"], r["dram__bytes_write.sum"]
-            per_tag.setdefault(tag, (r["Kernel Name"][0], float(rd[0]) * UNITS[rd[1]] + float(wr[0]) * UNITS[wr[1]]))
+            per_tag.setdefault(tag, []).append(
+                (r["Kernel Name"][0], float(rd[0]) * UNITS[rd[1]] + float(wr[0]) * UNITS[wr[1]]))
     with open(os.path.join(HERE, "profiles", "r01_ncu_summary.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
     path = os.path.join(HERE, "profiles", "ncu_summary.json")
     summ = json.load(open(path)) if os.path.exists(path) else {}
-    for cfg, tag in traffic.items():
-        name, b = per_tag[tag]
+    for cfg, spec in traffic.items():
+        tag, _, sub = spec.partition(":")
+        name, b = next((k, v) for k, v in per_tag[tag] if sub in k)
         summ[cfg] = {"kernel": name, "dram_bytes_per_launch": b,
                      "source": f"profiles/r01_ncu_summary.txt ({tag}: ncu --set full --clock-control none)"}
     with open(path, "w") as f:
