@@ -9,14 +9,23 @@ namespace dmg {
 
 namespace {
 
-// Chunk of CH = 8 NTC limbs per CTA of NTC threads (each thread composes the maps of
-// PER = 8 consecutive limbs, moved as one 8-byte word): NTC = 256 normally, 64 for small
-// products (more CTAs), where the chunk scan also folds into the emit kernel.
+// Chunk of CH = PERC NTC limbs per CTA of NTC threads; each thread composes the maps of
+// PERC consecutive limbs, moved as one PERC-byte word. Large products: 256 threads x 8
+// limbs. Small products: 512-limb chunks as 256 threads x 2 limbs (more CTAs and short
+// per-thread chains: the kernels are latency-bound there), and the chunk scan folds into
+// the emit kernel.
 constexpr int PER = 8;
 constexpr int CH = kCarryChunk;  // chunk of the large-product and sharded paths
 constexpr int NT = kCarryThreads;
 static_assert(CH == NT * PER, "chunk = threads x 8 limbs");
-constexpr int NT_SMALL = kCarryChunkSmall / PER;
+constexpr int PER_SMALL = 2;
+constexpr int NT_SMALL = kCarryChunkSmall / PER_SMALL;
+
+template <int PERC> struct MapWord;  // PERC one-byte limb maps as one integer
+template <> struct MapWord<8> { typedef unsigned long long type; };
+template <> struct MapWord<4> { typedef unsigned type; };
+template <> struct MapWord<2> { typedef unsigned short type; };
+template <> struct MapWord<1> { typedef unsigned char type; };
 
 // Local coefficient i (global k_off + i); i = -2, -1 are the previous rank's halo.
 __device__ __forceinline__ void coeff_digits(const CarryArgs& a, long long i, u64& d0, u64& d1, u64& d2) {
@@ -33,20 +42,21 @@ __device__ __forceinline__ void coeff_digits(const CarryArgs& a, long long i, u6
 // Phase 1: s_k for the chunk's limbs and the chunk's composed transfer map.
 // Coefficients are read and limb sums written in coalesced order (loc = j NT + tid);
 // each limb's 6-bit transfer map goes to shared memory as a byte, and each thread
-// then composes the maps of PER consecutive limbs (one 8-byte shared load).
-template <int NTC>
+// then composes the maps of PERC consecutive limbs (one PERC-byte shared load).
+template <int NTC, int PERC>
 __global__ void __launch_bounds__(NTC) k_carry_split(CarryArgs a) {
   pdl_wait();
-  constexpr int CHC = NTC * PER;
+  constexpr int CHC = NTC * PERC;
+  typedef typename MapWord<PERC>::type Word;
   __shared__ u64 d1s[CHC + 2], d2s[CHC + 2];
   __shared__ __align__(8) unsigned char mp[CHC];
   __shared__ unsigned wsm[NTC / 32 + 1];
   const unsigned long long k0 = (unsigned long long)blockIdx.x * CHC;
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const u64 B = a.div.base;
-  u64 d0r[PER];
+  u64 d0r[PERC];
 #pragma unroll
-  for (int j = 0; j < PER; ++j) {
+  for (int j = 0; j < PERC; ++j) {
     const int loc = j * NTC + threadIdx.x;
     u64 d0, d1, d2;
     coeff_digits(a, (long long)(k0 + loc), d0, d1, d2);
@@ -62,7 +72,7 @@ __global__ void __launch_bounds__(NTC) k_carry_split(CarryArgs a) {
   }
   __syncthreads();
 #pragma unroll
-  for (int j = 0; j < PER; ++j) {
+  for (int j = 0; j < PERC; ++j) {
     const int loc = j * NTC + threadIdx.x;
     const unsigned long long k = k0 + loc;
     const u64 s = d0r[j] + d1s[loc + 1] + d2s[loc];
@@ -70,10 +80,10 @@ __global__ void __launch_bounds__(NTC) k_carry_split(CarryArgs a) {
     mp[loc] = (unsigned char)(k < K ? limb_map(s, B) : kIdentityMap);
   }
   __syncthreads();
-  const unsigned long long m8 = reinterpret_cast<const unsigned long long*>(mp)[threadIdx.x];
+  const unsigned long long m8 = reinterpret_cast<const Word*>(mp)[threadIdx.x];
   unsigned agg = kIdentityMap;
 #pragma unroll
-  for (int j = 0; j < PER; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
+  for (int j = 0; j < PERC; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
   unsigned total;
   block_scan_maps<NTC>(agg, wsm, &total);
   if (threadIdx.x == 0) a.maps[blockIdx.x] = total;
@@ -173,10 +183,11 @@ __device__ __forceinline__ unsigned chunk_carry_in(const unsigned* maps, unsigne
 // The chunk's digits are staged in shared memory and stored as 16-byte vectors.
 // SELF (small products): no phase 2 — every CTA derives its chunk carry-in and the
 // top limb from the chunk maps itself (a few thousand maps at most).
-template <int NTC, bool SELF>
+template <int NTC, int PERC, bool SELF>
 __global__ void __launch_bounds__(NTC) k_carry_emit(CarryArgs a) {
   pdl_wait();
-  constexpr int CHC = NTC * PER;
+  constexpr int CHC = NTC * PERC;
+  typedef typename MapWord<PERC>::type Word;
   __shared__ unsigned wsm[NTC / 32 + 1];
   __shared__ __align__(16) char buf[CHC * 17 + 32];
   __shared__ __align__(8) unsigned char mp[CHC];  // limb maps, then limb carry-ins
@@ -205,28 +216,28 @@ __global__ void __launch_bounds__(NTC) k_carry_emit(CarryArgs a) {
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const u64 B = a.div.base;
   // coalesced limb sums (loc = j NTC + tid); their maps to shared memory
-  u64 s[PER];
+  u64 s[PERC];
 #pragma unroll
-  for (int j = 0; j < PER; ++j) {
+  for (int j = 0; j < PERC; ++j) {
     const unsigned long long k = cbase + j * NTC + threadIdx.x;
     s[j] = k < K ? a.s[k] : 0;
     mp[j * NTC + threadIdx.x] = (unsigned char)limb_map(s[j], B);
   }
   __syncthreads();
-  // each thread: PER consecutive limbs -> composed map -> block scan -> per-limb carry-ins
-  unsigned long long m8 = reinterpret_cast<const unsigned long long*>(mp)[threadIdx.x];
+  // each thread: PERC consecutive limbs -> composed map -> block scan -> per-limb carry-ins
+  unsigned long long m8 = reinterpret_cast<const Word*>(mp)[threadIdx.x];
   unsigned agg = kIdentityMap;
 #pragma unroll
-  for (int j = 0; j < PER; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
+  for (int j = 0; j < PERC; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
   const unsigned pre = block_scan_maps<NTC>(agg, wsm, nullptr);  // ends with a barrier
   unsigned c = map_apply(pre, chunk_cin);
   unsigned long long cin8 = 0;
 #pragma unroll
-  for (int j = 0; j < PER; ++j) {
+  for (int j = 0; j < PERC; ++j) {
     cin8 |= (unsigned long long)c << (8 * j);
     c = map_apply(unsigned(m8 >> (8 * j)) & 63u, c);
   }
-  reinterpret_cast<unsigned long long*>(mp)[threadIdx.x] = cin8;
+  reinterpret_cast<Word*>(mp)[threadIdx.x] = Word(cin8);
   __syncthreads();
   const unsigned be = a.base_exp;
   // global limb range printed by this chunk: [gbase, ghi]
@@ -237,11 +248,11 @@ __global__ void __launch_bounds__(NTC) k_carry_emit(CarryArgs a) {
   const unsigned long long end = limb_pos(gbase, top, top_len, be) + (gbase == top ? top_len : be);
   char* g = a.out + start;
   char* sb = buf + (reinterpret_cast<unsigned long long>(g) & 15);
-  // digits: each thread prints PER consecutive limbs (a contiguous 8 lambda-byte run)
+  // digits: each thread prints PERC consecutive limbs (a contiguous PERC lambda-byte run)
   const unsigned long long* sg = reinterpret_cast<const unsigned long long*>(a.s);
 #pragma unroll
-  for (int j = 0; j < PER; ++j) {
-    const int loc = threadIdx.x * PER + j;
+  for (int j = 0; j < PERC; ++j) {
+    const int loc = threadIdx.x * PERC + j;
     const unsigned long long k = cbase + loc, kg = a.k_off + k;
     if (kg > ghi) break;
     u64 v = sg[k] + mp[loc];  // re-read from L1/L2 (this block just streamed it)
@@ -313,20 +324,20 @@ int launch_carry(const CarryArgs& a, cudaStream_t st) {
   const unsigned nchunks = unsigned((K + CH - 1) / CH);
   if (nchunks < 2 * 148) {  // small product: 512-limb chunks, no separate scan
     const unsigned ns = unsigned((K + kCarryChunkSmall - 1) / kCarryChunkSmall);
-    launch_pdl(k_carry_split<NT_SMALL>, dim3(ns), dim3(NT_SMALL), 0, st, a);
-    launch_pdl(k_carry_emit<NT_SMALL, true>, dim3(ns), dim3(NT_SMALL), 0, st, a);
+    launch_pdl(k_carry_split<NT_SMALL, PER_SMALL>, dim3(ns), dim3(NT_SMALL), 0, st, a);
+    launch_pdl(k_carry_emit<NT_SMALL, PER_SMALL, true>, dim3(ns), dim3(NT_SMALL), 0, st, a);
     return 2;
   }
-  launch_pdl(k_carry_split<NT>, dim3(nchunks), dim3(NT), 0, st, a);
+  launch_pdl(k_carry_split<NT, PER>, dim3(nchunks), dim3(NT), 0, st, a);
   launch_pdl(k_carry_scan, dim3(1), dim3(1024), 0, st, a, nchunks);
-  launch_pdl(k_carry_emit<NT, false>, dim3(nchunks), dim3(NT), 0, st, a);
+  launch_pdl(k_carry_emit<NT, PER, false>, dim3(nchunks), dim3(NT), 0, st, a);
   return 3;
 }
 
 void launch_carry_shard_begin(const CarryArgs& a, unsigned* rank_map_dev, cudaStream_t st) {
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const unsigned nchunks = unsigned((K + CH - 1) / CH);
-  k_carry_split<NT><<<nchunks, NT, 0, st>>>(a);
+  k_carry_split<NT, PER><<<nchunks, NT, 0, st>>>(a);
   k_carry_prefix<<<1, 1024, 0, st>>>(a, nchunks, rank_map_dev);
 }
 
@@ -338,7 +349,7 @@ void launch_carry_shard_emit(const CarryArgs& a, unsigned rank_cin, cudaStream_t
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const unsigned nchunks = unsigned((K + CH - 1) / CH);
   k_carry_cin<<<(nchunks + 255) / 256, 256, 0, st>>>(a.maps, nchunks, rank_cin);
-  k_carry_emit<NT, false><<<nchunks, NT, 0, st>>>(a);
+  k_carry_emit<NT, PER, false><<<nchunks, NT, 0, st>>>(a);
 }
 
 }  // namespace dmg
