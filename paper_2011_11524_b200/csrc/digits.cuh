@@ -29,17 +29,21 @@ __device__ __forceinline__ unsigned swar4(unsigned x, int skip, unsigned& bad) {
   return (x * 100u + (x >> 16)) & 0xFFFFu;
 }
 
-// Digits buf[s, s + n), n <= 20, as an integer (five 4-digit groups from the right).
+// Digits buf[s, s + n), n <= 4 NG, as an integer (NG 4-digit groups from the right; NG = 4
+// covers lambda <= 16, NG = 5 lambda = 17).
+template <int NG = 5>
 __device__ __forceinline__ u64 parse_digits(const char* buf, int s, int n, unsigned& bad) {
+  static_assert(NG == 4 || NG == 5, "4 or 5 groups");
   const int e = s + n;
-  unsigned g[5];
+  unsigned g[5] = {0, 0, 0, 0, 0};
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
+  for (int k = 0; k < NG; ++k) {
     const int skip = 4 * (k + 1) - n;  // bytes of the group before s
     g[k] = skip < 4 ? swar4(smem_bytes4(buf, e - 4 * (k + 1)), skip < 0 ? 0 : skip, bad) : 0u;
   }
   const unsigned lo8 = g[1] * 10000u + g[0], hi8 = g[3] * 10000u + g[2];
-  return (u64)g[4] * 10000000000000000ull + (u64)hi8 * 100000000ull + lo8;
+  const u64 v = (u64)hi8 * 100000000ull + lo8;
+  return NG == 5 ? v + (u64)g[4] * 10000000000000000ull : v;
 }
 
 }  // namespace dmg

@@ -419,6 +419,7 @@ __global__ void k_gen_table(GenArgs g) {
 // each thread parses its lambda digits 8 at a time (SWAR).
 constexpr int kPackLimbs = 256;
 
+template <bool ROWMAP, int NG>
 __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d, unsigned long long nd, unsigned be,
                                                      u64* __restrict__ limbs, unsigned long long total, unsigned* err,
                                                      int row_bits, unsigned long long row_stride,
@@ -431,8 +432,9 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d,
   unsigned bad = 0;
   for (unsigned long long i0 = (unsigned long long)blockIdx.x * kPackLimbs; i0 < total;
        i0 += (unsigned long long)gridDim.x * kPackLimbs) {
-    // local limbs i0 .. i0 + 255 are global limbs t0 .. t0 + 255 (rows hold >= 256 limbs)
-    const unsigned long long t0 = (row_bits >= 63 ? 0 : (i0 >> row_bits) * row_stride) + off + (i0 & rmask);
+    // local limbs i0 .. i0 + 255 are global limbs t0 .. t0 + 255 (rows hold >= 256 limbs);
+    // unsharded (ROWMAP false): the identity
+    const unsigned long long t0 = ROWMAP ? (i0 >> row_bits) * row_stride + off + (i0 & rmask) : i0;
     const unsigned long long t = t0 + threadIdx.x, li = i0 + threadIdx.x;
     // digit span of limbs [t0, min(t0 + kPackLimbs, nl)): [lo, hi)
     const long long hi = (long long)nd - (long long)(t0 * be);
@@ -455,7 +457,7 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d,
       if (t < nl) {
         const long long end = (long long)nd - (long long)(t * be);
         const long long begin = end > (long long)be ? end - (long long)be : 0;
-        limb = parse_digits(buf, int(begin - g0), int(end - begin), bad);
+        limb = parse_digits<NG>(buf, int(begin - g0), int(end - begin), bad);
         if (begin == 0 && nd > 1 && d[0] == '0') atomicOr(err, kErrLeadingZero);
       }
       __syncthreads();
@@ -672,8 +674,10 @@ void launch_pack(const char* digits, unsigned long long nd, unsigned be, u64* li
   if (row_bits < 8)
     k_pack_rows<<<grid_for(total, 256), 256, 0, st>>>(digits, nd, be, limbs, total, err, row_bits, row_stride, off);
   else
-    launch_pdl(k_pack, dim3(grid_for(total, 256)), dim3(256), 0, st, digits, nd, be, limbs, total, err, row_bits,
-               row_stride, off);
+    launch_pdl(row_bits >= 63 ? (be > 16 ? k_pack<false, 5> : k_pack<false, 4>)
+                              : (be > 16 ? k_pack<true, 5> : k_pack<true, 4>),
+               dim3(grid_for(total, 256)), dim3(256), 0, st, digits, nd, be, limbs, total, err, row_bits, row_stride,
+               off);
 }
 void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, unsigned long long rows,
                           unsigned long long width, bool to_segments, cudaStream_t st) {
