@@ -55,13 +55,14 @@ __device__ __forceinline__ void split3(const DivB& d, u64 lo, u64 hi, u64& d0, u
   u64 thi = __umul64hi((u64)q, d.b2lo) + (u64)q * d.b2hi;
   u64 rlo = lo - tlo;
   u64 rhi = hi - thi - (lo < tlo ? 1ull : 0ull);
-  while ((long long)rhi < 0) {  // r < 0: q was one too large
+  // the estimate is off by at most one either way: one predicated correction each
+  if ((long long)rhi < 0) {  // r < 0: q was one too large
     --q;
     const u64 s = rlo + d.b2lo;
     rhi += d.b2hi + (s < rlo ? 1ull : 0ull);
     rlo = s;
   }
-  while (rhi > d.b2hi || (rhi == d.b2hi && rlo >= d.b2lo)) {  // r >= B^2: q one too small
+  if (rhi > d.b2hi || (rhi == d.b2hi && rlo >= d.b2lo)) {  // r >= B^2: q one too small
     ++q;
     rhi -= d.b2hi + (rlo < d.b2lo ? 1ull : 0ull);
     rlo -= d.b2lo;
