@@ -169,7 +169,9 @@ int decmul_gpu_generate_digits(decmul_gpu_ctx* ctx, uint64_t seed0, uint64_t see
                                size_t stride, int mode, char* d_out, void* stream);
 
 /* ---- introspection ---- */
-/* Integer-pipe roofline denominator: measured modmul/s on this GPU (variant 0 Shoup, 1 Montgomery). */
+/* Integer-pipe roofline denominator: measured modmul/s on this GPU, chained independent lanes on
+ * all SMs (reference bench_modmul, bench.cpp:49-94): variant 0 Shoup (the transforms' form),
+ * 1 Montgomery REDC, 2 the Solinas reduction for the Goldilocks prime 2^64 - 2^32 + 1. */
 int decmul_gpu_measure_modmul_rate(decmul_gpu_ctx* ctx, int variant, double* modmul_per_s);
 typedef struct {
   int last_launches;       /* kernels launched by the last product */

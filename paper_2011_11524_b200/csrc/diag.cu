@@ -2,7 +2,8 @@
 // independent-lane 63-bit modular multiplications on all SMs, measured live so
 // bench.py can report the transform kernels as a fraction of it. Variant 0 is
 // the Shoup form the transforms use for every root-of-unity factor; variant 1 is
-// the reference's Montgomery REDC (montgomery.hpp:26-39).
+// the reference's Montgomery REDC (montgomery.hpp:26-39); variant 2 the reference's
+// Solinas reduction for the Goldilocks prime (montgomery.hpp:60-77, bench.cpp:82-88).
 #include "kernels.cuh"
 
 namespace dmg {
@@ -22,7 +23,8 @@ __global__ void k_modmul_rate(u64* out, u64 p, u64 pp, int iters, const TwPair* 
   }
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
-    for (int c = 0; c < C; ++c) acc[c] = V == 0 ? shoup_mul(acc[c], k[c], p) : mont_mul(acc[c], k[c].w, p, pp);
+    for (int c = 0; c < C; ++c)
+      acc[c] = V == 0 ? shoup_mul(acc[c], k[c], p) : V == 1 ? mont_mul(acc[c], k[c].w, p, pp) : solinas_mul(acc[c], k[c].w);
   }
   u64 s = 0;
 #pragma unroll
@@ -59,8 +61,10 @@ double measure_modmul_rate(int variant, cudaStream_t st) {
     cudaEventRecord(e0, st);
     if (variant == 0)
       k_modmul_rate<0><<<blocks, threads, 0, st>>>(dout, p, pp, iters, dk);
-    else
+    else if (variant == 1)
       k_modmul_rate<1><<<blocks, threads, 0, st>>>(dout, p, pp, iters, dk);
+    else
+      k_modmul_rate<2><<<blocks, threads, 0, st>>>(dout, p, pp, iters, dk);
     cudaEventRecord(e1, st);
     cudaEventSynchronize(e1);
     float ms = 0;

@@ -52,6 +52,22 @@ __device__ __forceinline__ u64 mont_mul(u64 a, u64 b, u64 p, u64 pp) {
   return adjust_signed(r - p, p);
 }
 
+// Goldilocks prime 2^64 - 2^32 + 1 with its Solinas reduction (2^64 = 2^32 - 1,
+// 2^96 = -1): the reference's third modmul benchmark variant (montgomery.hpp:60-77).
+// Not on the product path (the production primes are < 2^63); bench / self-test only.
+constexpr u64 kSolinasPrime = 0xffffffff00000001ull;
+__device__ __forceinline__ u64 solinas_mul(u64 a, u64 b) {
+  const u64 lo = a * b, hi = __umul64hi(a, b);
+  const u64 hh = hi >> 32, hl = hi & 0xffffffffull;
+  u64 t = lo - hh;  // lo - hh mod p: on a borrow, add p = subtract 2^32 - 1 mod 2^64
+  if (lo < hh) t -= 0xffffffffull;
+  const u64 m = hl * 0xffffffffull;  // hl (2^32 - 1)
+  u64 r = t + m;
+  if (r < m) r += 0xffffffffull;  // carry out of 2^64 = 2^32 - 1
+  if (r >= kSolinasPrime) r -= kSolinasPrime;
+  return r;
+}
+
 // Gentleman-Sande butterfly (reference ntt.cpp:42-47): (u + v, (u - v) w).
 __device__ __forceinline__ void bfly_dif(u64& u, u64& v, TwPair t, u64 p) {
   u64 a = mod_add(u, v, p);

@@ -16,14 +16,16 @@ namespace dmg {
 
 namespace {
 
-// out[4 i + 0..3] = Shoup(x w), REDC(x y), x + y, x - y (mod p)
+// out[5 i + 0..4] = Shoup(x w), REDC(x y), x + y, x - y (mod p), and the Goldilocks
+// Solinas product x y mod (2^64 - 2^32 + 1) of the benchmark variant
 __global__ void k_st_field(const u64* x, const u64* y, const TwPair* w, u64* out, unsigned n, u64 p, u64 pp) {
   const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  out[4 * i + 0] = shoup_mul(x[i], w[i], p);
-  out[4 * i + 1] = mont_mul(x[i], y[i], p, pp);
-  out[4 * i + 2] = mod_add(x[i], y[i], p);
-  out[4 * i + 3] = mod_sub(x[i], y[i], p);
+  out[5 * i + 0] = shoup_mul(x[i], w[i], p);
+  out[5 * i + 1] = mont_mul(x[i], y[i], p, pp);
+  out[5 * i + 2] = mod_add(x[i], y[i], p);
+  out[5 * i + 3] = mod_sub(x[i], y[i], p);
+  out[5 * i + 4] = solinas_mul(x[i] | (y[i] << 62), ~y[i]);  // full 64-bit operands
 }
 
 // (a1, a2) -> the 128-bit CRT value (reference crt2, decimal.cpp:147-152)
@@ -151,16 +153,18 @@ int Engine::selftest(bool inject_fault, std::string& out) {
       y[1] = p - 1;
       u64 *dx = to_device(x), *dy = to_device(y), *dout = nullptr;
       TwPair* dw = to_device(w);
-      cuda_check(cudaMalloc(&dout, 4 * n * sizeof(u64)), "selftest alloc");
+      cuda_check(cudaMalloc(&dout, 5 * n * sizeof(u64)), "selftest alloc");
       k_st_field<<<(n + 127) / 128, 128>>>(dx, dy, dw, dout, n, p, F.pp);
       cuda_check(cudaGetLastError(), "selftest field");
-      const std::vector<u64> r = to_host(dout, 4 * std::size_t(n));
+      const std::vector<u64> r = to_host(dout, 5 * std::size_t(n));
       const u64 rinv = F.inv(F.r);
       for (unsigned i = 0; i < n; ++i) {
-        s.expect(r[4 * i + 0] == F.mul(x[i], w[i].w));
-        s.expect(r[4 * i + 1] == F.mul(F.mul(x[i], y[i]), rinv));
-        s.expect(r[4 * i + 2] == F.add(x[i], y[i]));
-        s.expect(r[4 * i + 3] == F.sub(x[i], y[i]));
+        s.expect(r[5 * i + 0] == F.mul(x[i], w[i].w));
+        s.expect(r[5 * i + 1] == F.mul(F.mul(x[i], y[i]), rinv));
+        s.expect(r[5 * i + 2] == F.add(x[i], y[i]));
+        s.expect(r[5 * i + 3] == F.sub(x[i], y[i]));
+        const u64 sa = x[i] | (y[i] << 62), sb = ~y[i];
+        s.expect(r[5 * i + 4] == u64(u128(sa) * sb % kSolinasPrime));
       }
       s.expect(F.pow(5, p - 1) == 1);  // Fermat (the host planner's field)
       cudaFree(dx);

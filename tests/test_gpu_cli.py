@@ -50,8 +50,9 @@ def test_cli_bench_mul_key_values():
     assert kv[1]["base_exp"] == "16" and kv[1]["length"] == str(1 << 17) and kv[1]["iters"] == "3"
     assert all(int(k["product_digits"]) in (2 * int(k["digits"]), 2 * int(k["digits"]) - 1) for k in kv)
     assert all(float(k["seconds_per_mul"]) > 0 for k in kv)
-    r = run("bench", "modmul", "--variant", "montgomery")
-    assert r.returncode == 0 and float(re.search(r"modmuls_per_second=(\S+)", r.stdout).group(1)) > 1e10
+    for variant in ("shoup", "montgomery", "solinas"):
+        r = run("bench", "modmul", "--variant", variant)
+        assert r.returncode == 0 and float(re.search(r"modmuls_per_second=(\S+)", r.stdout).group(1)) > 1e10
 
 
 def test_selftest_passes_and_detects_injected_fault(gpu):
@@ -61,6 +62,7 @@ def test_selftest_passes_and_detects_injected_fault(gpu):
     assert [s[0] for s in suites] == ["field_identities", "transform_roundtrip", "convolution_vs_direct",
                                       "crt_recompose", "base_division", "carry_recovery", "small_products"]
     assert all(int(c) > 0 and f == "0" for _, c, f in suites)
+    assert int(dict((n, c) for n, c, _ in suites)["field_identities"]) == 4 * (200 * 5 + 1)
     assert r.stdout.strip().endswith("selftest_failures=0")
     r = run("selftest", "--inject-fault")
     assert r.returncode == 1

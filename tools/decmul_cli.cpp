@@ -4,7 +4,7 @@
 //   decmul [--device N] [--adjust-strategy bitwise|cselect] mul A B
 //   decmul mul --file PATH_A PATH_B
 //   decmul bench mul --digits D [--digits D ...] [--iters K]
-//   decmul bench modmul [--variant shoup|montgomery]
+//   decmul bench modmul [--variant shoup|montgomery|solinas]
 //   decmul selftest [--inject-fault]
 //
 // Errors print "error: <message>" and exit 1 (reference main.cpp:150-153).
@@ -29,7 +29,7 @@ namespace {
   throw std::invalid_argument(std::string(why) +
                               "\nusage: decmul [--device N] [--adjust-strategy bitwise|cselect] "
                               "{mul [--file] A B | bench mul --digits D... [--iters K] | "
-                              "bench modmul [--variant shoup|montgomery] | selftest [--inject-fault]}");
+                              "bench modmul [--variant shoup|montgomery|solinas] | selftest [--inject-fault]}");
 }
 
 // reference main.cpp:19-29
@@ -97,6 +97,8 @@ int cmd_bench_modmul(const std::string& variant) {
     v = 0;
   else if (variant == "montgomery")
     v = 1;
+  else if (variant == "solinas")
+    v = 2;
   else
     throw std::invalid_argument("unknown variant: " + variant);
   double rate = 0;
