@@ -496,20 +496,26 @@ __global__ void k_pack_rows(const char* __restrict__ d, unsigned long long nd, u
 }
 
 // [peer][row][c] <-> [row][peer][c]: the all-to-all block layout vs contiguous segments.
+// Segment <-> block reorder around the all-to-alls of the sharded product: the data is
+// peers x rows blocks of `width` contiguous words (width = the column-block width Bc, a
+// power of two >= 16), permuted as whole blocks. Work is split into tiles of up to 1024
+// 16-byte vectors inside a block: one division per tile, 16-byte loads and stores (an
+// element-wise version spent three 64-bit divisions per word).
 __global__ void k_block_reorder(const u64* __restrict__ src, u64* __restrict__ dst, unsigned long long peers,
                                 unsigned long long rows, unsigned long long width, int to_segments) {
-  const unsigned long long total = peers * rows * width;
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long c = i % width, t = i / width;
-    // i indexes the destination; decode its (row, peer) in the destination order
-    if (to_segments) {
-      const unsigned long long peer = t % peers, row = t / peers;
-      dst[i] = src[(peer * rows + row) * width + c];
-    } else {
-      const unsigned long long row = t % rows, peer = t / rows;
-      dst[i] = src[(row * peers + peer) * width + c];
+  const unsigned long long nvec = width / 2, tile = nvec < 1024 ? nvec : 1024, tpb = nvec / tile;
+  const unsigned long long ntiles = peers * rows * tpb;
+  for (unsigned long long u = blockIdx.x; u < ntiles; u += gridDim.x) {
+    const unsigned long long b = u / tpb, off = (u - b * tpb) * tile;
+    unsigned long long sb;
+    if (to_segments) {  // destination [row][peer], source [peer][row]
+      sb = (b % peers) * rows + b / peers;
+    } else {  // destination [peer][row], source [row][peer]
+      sb = (b % rows) * peers + b / rows;
     }
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + sb * width) + off;
+    uint4* d4 = reinterpret_cast<uint4*>(dst + b * width) + off;
+    for (unsigned long long i = threadIdx.x; i < tile; i += blockDim.x) d4[i] = s4[i];
   }
 }
 
@@ -681,8 +687,10 @@ void launch_pack(const char* digits, unsigned long long nd, unsigned be, u64* li
 }
 void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, unsigned long long rows,
                           unsigned long long width, bool to_segments, cudaStream_t st) {
-  const unsigned long long total = peers * rows * width;
-  k_block_reorder<<<grid_for(total, 256), 256, 0, st>>>(src, dst, peers, rows, width, to_segments ? 1 : 0);
+  const unsigned long long nvec = width / 2, tile = nvec < 1024 ? nvec : 1024;
+  const unsigned long long ntiles = peers * rows * (nvec / tile);
+  k_block_reorder<<<unsigned(ntiles < 148ull * 16 ? ntiles : 148ull * 16), 256, 0, st>>>(src, dst, peers, rows, width,
+                                                                                          to_segments ? 1 : 0);
 }
 void launch_pointwise(u64* a, const u64* b, unsigned long long n, u64 p, u64 pp, cudaStream_t st) {
   k_pointwise<<<grid_for(n, 256), 256, 0, st>>>(a, b, n, p, pp);
