@@ -84,6 +84,14 @@ int decmul_gpu_result_length(decmul_gpu_ctx* ctx, size_t* out_len);
 int decmul_gpu_multiply_batch(decmul_gpu_ctx* ctx, size_t count, const char* xs, size_t x_stride, size_t nx,
                               const char* ys, size_t y_stride, size_t ny, char* outs, size_t out_stride,
                               size_t* out_lens);
+/* Mixed-size batch from host memory (the pointer-array form of SURVEY §8(b)): product i is
+ * xs[i] (nxs[i] digits) times ys[i] (nys[i] digits) into outs[i] (caps[i] >= nxs[i] + nys[i]),
+ * length to out_lens[i]. Products of equal size pairs run as one batch each (the uniform path
+ * above, one CTA per product where N <= 3 * 2^10); the rest one by one. Errors (bad digits,
+ * too large) fail the call like the reference's multiply would for the first bad pair. */
+int decmul_gpu_multiply_batch_ptrs(decmul_gpu_ctx* ctx, size_t count, const char* const* xs, const size_t* nxs,
+                                   const char* const* ys, const size_t* nys, char* const* outs, const size_t* caps,
+                                   size_t* out_lens);
 int decmul_gpu_multiply_batch_device(decmul_gpu_ctx* ctx, size_t count, const char* d_xs, size_t x_stride,
                                      size_t nx, const char* d_ys, size_t y_stride, size_t ny, char* d_outs,
                                      size_t out_stride, unsigned long long* d_lens, void* stream);

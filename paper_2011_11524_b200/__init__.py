@@ -56,7 +56,7 @@ EXPORTED_SYMBOLS = [
     "decmul_gpu_transpose_2n_x_n", "decmul_gpu_generate_digits", "decmul_gpu_measure_modmul_rate",
     "decmul_gpu_get_stats", "decmul_gpu_shard_plan_create", "decmul_gpu_shard_pack", "decmul_gpu_shard_transform",
     "decmul_gpu_shard_reorder", "decmul_gpu_shard_carry_begin", "decmul_gpu_shard_carry_probe",
-    "decmul_gpu_shard_carry_emit", "decmul_gpu_selftest",
+    "decmul_gpu_shard_carry_emit", "decmul_gpu_selftest", "decmul_gpu_multiply_batch_ptrs",
 ]
 
 
@@ -279,6 +279,21 @@ class Context:
                    C.c_size_t(nx if x_stride is None else x_stride), C.c_size_t(nx), C.c_void_p(d_ys),
                    C.c_size_t(ny if y_stride is None else y_stride), C.c_size_t(ny), C.c_void_p(d_outs),
                    C.c_size_t(out_stride), C.c_void_p(d_lens), C.c_void_p(stream))
+
+    def multiply_batch_mixed(self, xs: list, ys: list) -> list:
+        """Products of mixed sizes (decmul_gpu_multiply_batch_ptrs): equal size pairs batched."""
+        n = len(xs)
+        if len(ys) != n:
+            raise ValueError("multiply_batch_mixed: xs and ys differ in length")
+        xb = [bytes(x) for x in xs]
+        yb = [bytes(y) for y in ys]
+        outs = [C.create_string_buffer(len(a) + len(b) + 1) for a, b in zip(xb, yb)]
+        arr = lambda T, v: (T * n)(*v)  # noqa: E731
+        lens = (C.c_size_t * n)()
+        self._call("decmul_gpu_multiply_batch_ptrs", C.c_size_t(n), arr(C.c_char_p, xb),
+                   arr(C.c_size_t, [len(a) for a in xb]), arr(C.c_char_p, yb), arr(C.c_size_t, [len(b) for b in yb]),
+                   arr(C.c_void_p, [C.addressof(o) for o in outs]), arr(C.c_size_t, [len(o) for o in outs]), lens)
+        return [o.raw[: lens[i]] for i, o in enumerate(outs)]
 
     def multiply_batch_ptr(self, count: int, xs_ptr: int, nx: int, ys_ptr: int, ny: int, outs_ptr: int,
                            out_stride: int, lens_ptr: int) -> None:

@@ -160,6 +160,12 @@ int decmul_gpu_multiply_batch(decmul_gpu_ctx* ctx, size_t count, const char* xs,
   LOCKED(ctx, ctx->eng->multiply_batch_host(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, out_lens));
 }
 
+int decmul_gpu_multiply_batch_ptrs(decmul_gpu_ctx* ctx, size_t count, const char* const* xs, const size_t* nxs,
+                                   const char* const* ys, const size_t* nys, char* const* outs, const size_t* caps,
+                                   size_t* out_lens) {
+  LOCKED(ctx, ctx->eng->multiply_batch_ptrs(count, xs, nxs, ys, nys, outs, caps, out_lens));
+}
+
 int decmul_gpu_multiply_batch_device(decmul_gpu_ctx* ctx, size_t count, const char* d_xs, size_t x_stride,
                                      size_t nx, const char* d_ys, size_t y_stride, size_t ny, char* d_outs,
                                      size_t out_stride, unsigned long long* d_lens, void* stream) {

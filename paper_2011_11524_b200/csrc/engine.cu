@@ -933,6 +933,38 @@ void Engine::batch_host_pipelined(std::size_t count, const char* xs, std::size_t
   for (std::size_t i = 0; i < count; ++i) lens[i] = std::size_t(host_lens_[i]);
 }
 
+void Engine::multiply_batch_ptrs(std::size_t count, const char* const* xs, const std::size_t* nxs,
+                                 const char* const* ys, const std::size_t* nys, char* const* outs,
+                                 const std::size_t* caps, std::size_t* lens) {
+  for (std::size_t i = 0; i < count; ++i)
+    if (caps[i] < nxs[i] + nys[i]) throw std::length_error("multiply: output buffer too small");
+  std::map<std::pair<std::size_t, std::size_t>, std::vector<std::size_t>> groups;
+  for (std::size_t i = 0; i < count; ++i) groups[{nxs[i], nys[i]}].push_back(i);
+  std::vector<char> bx, by, bo;
+  std::vector<std::size_t> bl;
+  for (const auto& [shape, idx] : groups) {
+    const auto [nx, ny] = shape;
+    if (idx.size() < 2 || nx == 0 || ny == 0) {  // singletons (and empty operands: the error path)
+      for (std::size_t i : idx) lens[i] = multiply_host(xs[i], nx, ys[i], ny, outs[i], caps[i], 0, false);
+      continue;
+    }
+    const std::size_t m = idx.size(), ostride = nx + ny;
+    bx.resize(m * nx);
+    by.resize(m * ny);
+    bo.resize(m * ostride);
+    bl.resize(m);
+    for (std::size_t j = 0; j < m; ++j) {
+      std::memcpy(&bx[j * nx], xs[idx[j]], nx);
+      std::memcpy(&by[j * ny], ys[idx[j]], ny);
+    }
+    multiply_batch_host(m, bx.data(), nx, nx, by.data(), ny, ny, bo.data(), ostride, bl.data());
+    for (std::size_t j = 0; j < m; ++j) {
+      std::memcpy(outs[idx[j]], &bo[j * ostride], bl[j]);
+      lens[idx[j]] = bl[j];
+    }
+  }
+}
+
 // ---------------- parity hooks ----------------
 
 void Engine::convolve_mod_p(u64 p, std::size_t n, const u64* x, std::size_t nx, const u64* y, std::size_t ny,

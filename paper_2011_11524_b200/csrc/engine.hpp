@@ -174,6 +174,9 @@ class Engine {
   void multiply_batch_device(std::size_t count, const char* dxs, std::size_t x_stride, std::size_t nx,
                              const char* dys, std::size_t y_stride, std::size_t ny, char* douts,
                              std::size_t out_stride, unsigned long long* dlens, cudaStream_t st);
+  // Mixed sizes from host pointers: equal (nx, ny) groups through multiply_batch_host.
+  void multiply_batch_ptrs(std::size_t count, const char* const* xs, const std::size_t* nxs, const char* const* ys,
+                           const std::size_t* nys, char* const* outs, const std::size_t* caps, std::size_t* lens);
   void multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
                            const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
                            std::size_t out_stride, std::size_t* lens);

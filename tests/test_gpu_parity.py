@@ -260,3 +260,20 @@ def test_host_api_pageable_staging(gpu, ref):
     assert len(z) == len(want) and sha(z) == sha(want)
     z2 = gpu.multiply_text(x, None)  # aliased squaring: only x is staged
     assert sha(z2) == sha(ref.multiply(x, None))
+
+
+def test_batch_mixed_sizes_pointer_arrays(gpu, ref):
+    """decmul_gpu_multiply_batch_ptrs (the pointer-array batch of SURVEY §8(b)): repeated
+    size pairs run as uniform batches, singletons one by one; results in input order."""
+    shapes = [(10000, 10000)] * 7 + [(3000, 1000)] * 3 + [(60000, 40000)] * 2 + [(5, 7), (250000, 1), (1, 1)]
+    xs, ys = [], []
+    for k, (nx, ny) in enumerate(shapes):
+        xs.append(inputs.gen_digits(500 + 2 * k, nx))
+        ys.append(inputs.gen_digits(501 + 2 * k, ny))
+    xs.append(b"0")
+    ys.append(inputs.gen_digits(9, 12345))
+    order = list(np.random.default_rng(5).permutation(len(xs)))  # interleave the groups
+    xs, ys = [xs[i] for i in order], [ys[i] for i in order]
+    assert gpu.multiply_batch_mixed(xs, ys) == [ref.multiply(a, b) for a, b in zip(xs, ys)]
+    with pytest.raises(ValueError, match="non-digit"):
+        gpu.multiply_batch_mixed([b"12", b"3x4"], [b"5", b"6"])
