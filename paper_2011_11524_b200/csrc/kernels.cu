@@ -66,9 +66,18 @@ constexpr int pass_threads(int logr, int tw) {
   return ((1 << logr) * tw / 8) < 32 ? 32 : (((1 << logr) * tw / 8) > NT ? NT : ((1 << logr) * tw / 8));
 }
 
-template <int LOGR, int NTK>
+// Twiddle tables of column-major tiles are swizzled (ntt_tile.cuh); row-major ones are not.
+#ifndef DMG_PASS_NOSWZ
+template <bool ROWS>
+constexpr bool kSwzTables = !ROWS;
+#else
+template <bool ROWS>
+constexpr bool kSwzTables = false;
+#endif
+
+template <int LOGR, int NTK, bool SWZ>
 __device__ __forceinline__ void load_table(TwPair* dst, const TwPair* src) {
-  for (int i = threadIdx.x; i < (1 << LOGR) / 2; i += NTK) dst[i] = src[i];
+  for (int i = threadIdx.x; i < (1 << LOGR) / 2; i += NTK) dst[tw_index<SWZ>(i)] = src[i];
 }
 
 template <int LOGR, bool ROWS, int E, int TW>
@@ -117,7 +126,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
     }
   }
-  load_table<LOGR, NTK>(tw, a.dft_fwd[pr]);
+  load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_fwd[pr]);
   __syncthreads();
   const TileLayout<LOGR, ROWS, TW> L;
   if constexpr (LOGR == E1) {  // one round: HBM -> registers -> HBM
@@ -128,7 +137,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << E1];
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i, w)];
-      dif_regs<LOGR, LOGR, E1>(v, j0, tw, p);
+      dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>>(v, j0, tw, p);
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) {
         if (ROWS) v[i] = shoup_mul(v[i], G.tw(T, base + i, w), p);
@@ -145,12 +154,12 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << E1];
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i * ST1, w)];
-      dif_regs<LOGR, LOGR, E1>(v, j0, tw, p);
+      dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>>(v, j0, tw, p);
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
     }
     __syncthreads();
-    dif_rounds_smem<LOGR, LOGR - E1, EL, TW>(sm, L, UniformField{p, tw}, tid, NTK);
+    dif_rounds_smem<LOGR, LOGR - E1, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
     for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
       group_coords<LOGR, ROWS, EL, TW>(g, w, q);
@@ -158,7 +167,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i, w)];
-      dif_regs<LOGR, EL, EL>(v, 0, tw, p);
+      dif_regs<LOGR, EL, EL, kSwzTables<ROWS>>(v, 0, tw, p);
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
         if (ROWS) v[i] = shoup_mul(v[i], G.tw(T, base + i, w), p);
@@ -187,7 +196,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   u64* dst = a.dst[pr];
   const TwPair* __restrict__ T = a.pass_tw[pr];
   const TwPair sc = a.final_scale[pr];
-  load_table<LOGR, NTK>(tw, a.dft_inv[pr]);
+  load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_inv[pr]);
   __syncthreads();
   const Geom<LOGR, ROWS, TW> G(a);
   const TileLayout<LOGR, ROWS, TW> L;
@@ -201,7 +210,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       v[i] = src[G.at(base + i, w)];
       if (ROWS) v[i] = shoup_mul(v[i], G.tw(T, base + i, w), p);
     }
-    dit_regs<LOGR, 0, E1>(v, 0, tw, p);
+    dit_regs<LOGR, 0, E1, kSwzTables<ROWS>>(v, 0, tw, p);
 #pragma unroll
     for (int i = 0; i < (1 << E1); ++i) {
       if constexpr (LOGR == E1) {
@@ -214,7 +223,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   }
   if constexpr (LOGR > E1) {
     __syncthreads();
-    dit_rounds_smem<LOGR, E1, AL, TW>(sm, L, UniformField{p, tw}, tid, NTK);
+    dit_rounds_smem<LOGR, E1, AL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
     constexpr int STL = 1 << AL;
     for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i * STL, w)];
-      dit_regs<LOGR, AL, EL>(v, j0, tw, p);
+      dit_regs<LOGR, AL, EL, kSwzTables<ROWS>>(v, j0, tw, p);
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
         if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
@@ -256,8 +265,8 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   const u64* oth = a.other[pr];
   u64* dst = a.dst[pr];
   const TwPair sc = a.final_scale[pr];
-  load_table<LOGR, NTK>(twf, a.dft_fwd[pr]);
-  load_table<LOGR, NTK>(twi, a.dft_inv[pr]);
+  load_table<LOGR, NTK, kSwzTables<false>>(twf, a.dft_fwd[pr]);
+  load_table<LOGR, NTK, kSwzTables<false>>(twi, a.dft_inv[pr]);
   __syncthreads();
   const Geom<LOGR, false, TW> G(a);
   const ContigColumns<LOGR> L;
@@ -270,12 +279,12 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << E1];
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i * ST1, w)];
-      dif_regs<LOGR, LOGR, E1>(v, j0, twf, p);
+      dif_regs<LOGR, LOGR, E1, kSwzTables<false>>(v, j0, twf, p);
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
     }
     __syncthreads();
-    dif_rounds_smem<LOGR, LOGR - E1, EM, TW>(sm, L, UniformField{p, twf}, tid, NTK);
+    dif_rounds_smem<LOGR, LOGR - E1, EM, TW>(sm, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
   }
   for (int g = tid; g < (R >> EM) * TW; g += NTK) {
     int w, q, j0, base;
@@ -284,10 +293,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
     u64 v[1 << EM];
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) v[i] = LOGR > EM ? sm[L(base + i, w)] : src[G.at(base + i, w)];
-    dif_regs<LOGR, EM, EM>(v, 0, twf, p);
+    dif_regs<LOGR, EM, EM, kSwzTables<false>>(v, 0, twf, p);
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) v[i] = mont_mul(v[i], oth ? oth[G.at(base + i, w)] : v[i], p, pp);
-    dit_regs<LOGR, 0, EM>(v, 0, twi, p);
+    dit_regs<LOGR, 0, EM, kSwzTables<false>>(v, 0, twi, p);
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) {
       if constexpr (LOGR == EM) {
@@ -300,7 +309,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   }
   if constexpr (LOGR > EM) {
     __syncthreads();
-    dit_rounds_smem<LOGR, EM, AL, TW>(sm, L, UniformField{p, twi}, tid, NTK);
+    dit_rounds_smem<LOGR, EM, AL, TW>(sm, L, UniformField<kSwzTables<false>>{p, twi}, tid, NTK);
     constexpr int STL = 1 << AL;
     for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
@@ -309,7 +318,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i * STL, w)];
-      dit_regs<LOGR, AL, EL>(v, j0, twi, p);
+      dit_regs<LOGR, AL, EL, kSwzTables<false>>(v, j0, twi, p);
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
         if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);

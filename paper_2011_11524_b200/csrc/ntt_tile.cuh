@@ -12,7 +12,7 @@
 // last DIF round and the first DIT round act on the same groups (8 consecutive
 // positions), which lets a pass run DIF -> pointwise -> DIT in registers.
 //
-// Twiddles come from a shared table tw[k] = omega_R^k (k < R/2) in Shoup form;
+// Twiddles come from a shared table tw[tw_index(k)] = omega_R^k (k < R/2) in Shoup form;
 // the stage with span M uses omega_M^j = tw[j * R / M] like the reference's flat
 // stage slices (ntt.hpp:10-19). A radix-8 group needs 7 distinct factors, each
 // loaded once; in rounds with stride 1 the j = 0 factors are 1 and skipped
@@ -23,10 +23,21 @@
 // half-warp reads one 128 B row. Column-major tiles map threads along the
 // column and XOR-swizzle the in-column index (r ^ ((r >> 3) & 15)), which makes
 // every round of these schedules conflict-free (checked offline for R = 2^4..2^11).
+// The 16-byte twiddle loads conflict too unless the table is swizzled: a column-major
+// warp spans 32 groups, so a middle round reads tw[(j0 + k STRIDE) << s] for 8 values
+// of j0, and the strides 4, 8, 16 put all 8 entries in 1-2 of the 8 sixteen-byte bank
+// slots (up to 8-way). Column-major kernels therefore store tables at tw_slot(k), which
+// XORs the low 3 bits with bits 3-5 ^ 6-8: conflict-free for every round of R = 2^7..2^9
+// (simulated offline; ncu counters in DESIGN.md §2). Row-major warps span only 2 groups,
+// so their few conflicts are cheaper than the swizzle's index arithmetic: SWZ = false.
 #pragma once
 #include "modarith.cuh"
 
 namespace dmg {
+
+__device__ __forceinline__ int tw_slot(int k) { return k ^ (((k >> 3) ^ (k >> 6)) & 7); }
+template <bool SWZ>
+__device__ __forceinline__ int tw_index(int k) { return SWZ ? tw_slot(k) : k; }
 
 // ---- round schedules ----
 template <int LOGR>
@@ -42,7 +53,7 @@ struct Sched {
 // ---- register stages ----
 // DIF stages of one group: elements v[i] at positions base + i * STRIDE, STRIDE = 2^(MLOG-E),
 // j0 = base mod STRIDE. Spans 2^MLOG down to 2^(MLOG-E+1).
-template <int LOGR, int MLOG, int E>
+template <int LOGR, int MLOG, int E, bool SWZ>
 __device__ __forceinline__ void dif_regs(u64 (&v)[1 << E], int j0, const TwPair* tw, u64 p) {
   constexpr int NE = 1 << E, STRIDE = 1 << (MLOG - E);
 #pragma unroll
@@ -52,7 +63,7 @@ __device__ __forceinline__ void dif_regs(u64 (&v)[1 << E], int j0, const TwPair*
     TwPair t[NE / 2];
 #pragma unroll
     for (int k = 0; k < half; ++k)
-      if (!(STRIDE == 1 && k == 0)) t[k] = tw[(j0 + k * STRIDE) << (LOGR - mlog)];
+      if (!(STRIDE == 1 && k == 0)) t[k] = tw[tw_index<SWZ>((j0 + k * STRIDE) << (LOGR - mlog))];
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
       if (i & half) continue;
@@ -65,7 +76,7 @@ __device__ __forceinline__ void dif_regs(u64 (&v)[1 << E], int j0, const TwPair*
 }
 
 // DIT stages of one group: positions base + i * STRIDE, STRIDE = 2^ALOG; spans 2^(ALOG+1)..2^(ALOG+E).
-template <int LOGR, int ALOG, int E>
+template <int LOGR, int ALOG, int E, bool SWZ>
 __device__ __forceinline__ void dit_regs(u64 (&v)[1 << E], int j0, const TwPair* tw, u64 p) {
   constexpr int NE = 1 << E, STRIDE = 1 << ALOG;
 #pragma unroll
@@ -75,7 +86,7 @@ __device__ __forceinline__ void dit_regs(u64 (&v)[1 << E], int j0, const TwPair*
     TwPair t[NE / 2];
 #pragma unroll
     for (int k = 0; k < d; ++k)
-      if (!(STRIDE == 1 && k == 0)) t[k] = tw[(j0 + k * STRIDE) << (LOGR - mlog)];
+      if (!(STRIDE == 1 && k == 0)) t[k] = tw[tw_index<SWZ>((j0 + k * STRIDE) << (LOGR - mlog))];
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
       if (i & d) continue;
@@ -118,8 +129,10 @@ struct ContigColumns {
   __device__ __forceinline__ int operator()(int r, int w) const { return (w << LOGR) + col_swizzle(r); }
 };
 
-// Same prime and table for every column.
+// Same prime and table for every column; SWZ: the table is stored at tw_slot(k).
+template <bool SWZ>
 struct UniformField {
+  static constexpr bool kSwz = SWZ;
   u64 pv;
   const TwPair* t;
   __device__ __forceinline__ u64 p(int) const { return pv; }
@@ -148,7 +161,7 @@ __device__ __forceinline__ void dif_round_smem(u64* s, const L& idx, const F& fl
     u64 v[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) v[i] = s[idx(base + i * STRIDE, w)];
-    dif_regs<LOGR, MLOG, E>(v, j0, fld.tw(w), fld.p(w));
+    dif_regs<LOGR, MLOG, E, F::kSwz>(v, j0, fld.tw(w), fld.p(w));
 #pragma unroll
     for (int i = 0; i < NE; ++i) s[idx(base + i * STRIDE, w)] = v[i];
   }
@@ -164,7 +177,7 @@ __device__ __forceinline__ void dit_round_smem(u64* s, const L& idx, const F& fl
     u64 v[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) v[i] = s[idx(base + i * STRIDE, w)];
-    dit_regs<LOGR, ALOG, E>(v, j0, fld.tw(w), fld.p(w));
+    dit_regs<LOGR, ALOG, E, F::kSwz>(v, j0, fld.tw(w), fld.p(w));
 #pragma unroll
     for (int i = 0; i < NE; ++i) s[idx(base + i * STRIDE, w)] = v[i];
   }

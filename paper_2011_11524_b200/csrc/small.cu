@@ -40,6 +40,7 @@ __device__ unsigned long long g_phase_cycles[12];
 constexpr int NT = 256;  // 8 warps, 3 CTAs/SM at <= 85 registers; measured fastest of 192/256/320/384(x3) and 512(x2)
 
 struct SmallField {
+  static constexpr bool kSwz = true;  // tables stored at tw_slot(k) (ntt_tile.cuh)
   u64 p0, p1;
   const TwPair* t0;
   const TwPair* t1;
@@ -94,10 +95,11 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
   const u64 p0 = a.p[0], p1 = a.p[1];
 
   for (int i = tid; i < C / 2; i += NT) {
-    tf0[i] = a.dft_fwd[0][i];
-    tf1[i] = a.dft_fwd[1][i];
-    ti0[i] = a.dft_inv[0][i];
-    ti1[i] = a.dft_inv[1][i];
+    const int k = tw_slot(i);  // swizzled table (ntt_tile.cuh)
+    tf0[k] = a.dft_fwd[0][i];
+    tf1[k] = a.dft_fwd[1][i];
+    ti0[k] = a.dft_inv[0][i];
+    ti1[k] = a.dft_inv[1][i];
   }
   // ---- pack (decimal.cpp:102-118) ----
   const char* dxs = a.xs + prod * a.x_stride;
