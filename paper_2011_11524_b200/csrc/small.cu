@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
         u64 limb = 0;
         if (t < nl) {
           const long long end = nd - (long long)t * be, begin = end > (long long)be ? end - (long long)be : 0;
-          limb = parse_digits(b, sh + int(begin), int(end - begin), bad);
+          limb = parse_digits<5, false>(b, sh + int(begin), int(end - begin), bad);
         }
         if (o == 0) {
           xlimb[j] = limb;
