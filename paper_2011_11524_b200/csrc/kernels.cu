@@ -75,6 +75,43 @@ template <bool ROWS>
 constexpr bool kSwzTables = false;
 #endif
 
+// Tiles are staged HBM -> SMEM by one burst of cp.async before the first round (every load
+// in flight at once) instead of the first round reading HBM into registers. Measured (A/B,
+// DMG_STAGE_MASK bits): 1 forward row tiles (config 3 -2.1%, 4 -1.3%, 5 -1.3%); 2 inverse
+// row tiles (config 4 a further -0.8%); 4 column tiles of the forward and fused passes —
+// only the narrow 4-column tiles gain (config 1 -2.4%); full 16-column ones lose 1%
+// (configs 3-5), so they keep the direct first round.
+#ifndef DMG_STAGE_MASK
+#define DMG_STAGE_MASK 7
+#endif
+template <bool ROWS, int TW>
+constexpr bool kStageFwd = ROWS ? (DMG_STAGE_MASK & 1) != 0 : ((DMG_STAGE_MASK & 4) != 0 && TW < kTileW);
+template <bool ROWS>
+constexpr bool kStageInv = ROWS && (DMG_STAGE_MASK & 2) != 0;
+
+// Issue the async copy of a tile into its shared layout: 16-byte chunks of the row segments
+// for row-major tiles; 8-byte words for swizzled columns (the swizzle may swap a 16-byte
+// pair), consecutive threads on consecutive rows of a column (coalesced). The caller waits
+// (cp.async.wait_all) and synchronises.
+template <int LOGR, bool ROWS, int TW, int NTK, class Gm, class Lay>
+__device__ __forceinline__ void stage_tile(u64* sm, const u64* src, const Gm& G, const Lay& L, int tid) {
+  constexpr int R = 1 << LOGR;
+  if constexpr (ROWS) {
+    constexpr int CH = TW / 2;  // 16-byte chunks per row segment
+    for (int i = tid; i < R * CH; i += NTK) {
+      const int r = i / CH, c = (i % CH) * 2;
+      const unsigned sa = unsigned(__cvta_generic_to_shared(&sm[L(r, c)]));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + G.at(r, c)) : "memory");
+    }
+  } else {
+    for (int i = tid; i < R * TW; i += NTK) {
+      const int w = i >> LOGR, r = i & (R - 1);
+      const unsigned sa = unsigned(__cvta_generic_to_shared(&sm[L(r, w)]));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src + G.at(r, w)) : "memory");
+    }
+  }
+}
+
 template <int LOGR, int NTK, bool SWZ>
 __device__ __forceinline__ void load_table(TwPair* dst, const TwPair* src) {
   for (int i = threadIdx.x; i < (1 << LOGR) / 2; i += NTK) dst[tw_index<SWZ>(i)] = src[i];
@@ -126,9 +163,11 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
     }
   }
-  load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_fwd[pr]);
-  __syncthreads();
   const TileLayout<LOGR, ROWS, TW> L;
+  if constexpr (kStageFwd<ROWS, TW> && LOGR > E1) stage_tile<LOGR, ROWS, TW, NTK>(sm, src, G, L, tid);
+  load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_fwd[pr]);
+  if constexpr (kStageFwd<ROWS, TW> && LOGR > E1) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
   if constexpr (LOGR == E1) {  // one round: HBM -> registers -> HBM
     for (int g = tid; g < (R >> E1) * TW; g += NTK) {
       int w, q, j0, base;
@@ -146,20 +185,24 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
     }
     return;
   } else {
-    constexpr int ST1 = 1 << (LOGR - E1);
-    for (int g = tid; g < (R >> E1) * TW; g += NTK) {
-      int w, q, j0, base;
-      group_coords<LOGR, ROWS, E1, TW>(g, w, q);
-      dif_group<LOGR, E1>(q, j0, base);
-      u64 v[1 << E1];
+    if constexpr (kStageFwd<ROWS, TW>) {
+      dif_rounds_smem<LOGR, LOGR, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
+    } else {
+      constexpr int ST1 = 1 << (LOGR - E1);
+      for (int g = tid; g < (R >> E1) * TW; g += NTK) {
+        int w, q, j0, base;
+        group_coords<LOGR, ROWS, E1, TW>(g, w, q);
+        dif_group<LOGR, E1>(q, j0, base);
+        u64 v[1 << E1];
 #pragma unroll
-      for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i * ST1, w)];
-      dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>>(v, j0, tw, p);
+        for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i * ST1, w)];
+        dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>>(v, j0, tw, p);
 #pragma unroll
-      for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
+        for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
+      }
+      __syncthreads();
+      dif_rounds_smem<LOGR, LOGR - E1, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
     }
-    __syncthreads();
-    dif_rounds_smem<LOGR, LOGR - E1, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
     for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
       group_coords<LOGR, ROWS, EL, TW>(g, w, q);
@@ -196,10 +239,13 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   u64* dst = a.dst[pr];
   const TwPair* __restrict__ T = a.pass_tw[pr];
   const TwPair sc = a.final_scale[pr];
-  load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_inv[pr]);
-  __syncthreads();
   const Geom<LOGR, ROWS, TW> G(a);
   const TileLayout<LOGR, ROWS, TW> L;
+  constexpr bool STAGE = kStageInv<ROWS> && LOGR > E1;
+  if constexpr (STAGE) stage_tile<LOGR, ROWS, TW, NTK>(sm, src, G, L, tid);
+  load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_inv[pr]);
+  if constexpr (STAGE) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
   for (int g = tid; g < (R >> E1) * TW; g += NTK) {
     int w, q, j0, base;
     group_coords<LOGR, ROWS, E1, TW>(g, w, q);
@@ -207,7 +253,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
     u64 v[1 << E1];
 #pragma unroll
     for (int i = 0; i < (1 << E1); ++i) {
-      v[i] = src[G.at(base + i, w)];
+      v[i] = STAGE ? sm[L(base + i, w)] : src[G.at(base + i, w)];
       if (ROWS) v[i] = shoup_mul(v[i], G.tw(T, base + i, w), p);
     }
     dit_regs<LOGR, 0, E1, kSwzTables<ROWS>>(v, 0, tw, p);
@@ -265,12 +311,17 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   const u64* oth = a.other[pr];
   u64* dst = a.dst[pr];
   const TwPair sc = a.final_scale[pr];
-  load_table<LOGR, NTK, kSwzTables<false>>(twf, a.dft_fwd[pr]);
-  load_table<LOGR, NTK, kSwzTables<false>>(twi, a.dft_inv[pr]);
-  __syncthreads();
   const Geom<LOGR, false, TW> G(a);
   const ContigColumns<LOGR> L;
-  if constexpr (LOGR > EM) {
+  constexpr bool STAGE = kStageFwd<false, TW> && LOGR > EM;
+  if constexpr (STAGE) stage_tile<LOGR, false, TW, NTK>(sm, src, G, L, tid);
+  load_table<LOGR, NTK, kSwzTables<false>>(twf, a.dft_fwd[pr]);
+  load_table<LOGR, NTK, kSwzTables<false>>(twi, a.dft_inv[pr]);
+  if constexpr (STAGE) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  if constexpr (STAGE) {
+    dif_rounds_smem<LOGR, LOGR, EM, TW>(sm, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
+  } else if constexpr (LOGR > EM) {
     constexpr int ST1 = 1 << (LOGR - E1);
     for (int g = tid; g < (R >> E1) * TW; g += NTK) {
       int w, q, j0, base;
