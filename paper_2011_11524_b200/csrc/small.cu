@@ -350,9 +350,11 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
   const unsigned long long top = meta[0];
   const unsigned top_len = unsigned(meta[1]);
   char* out = a.outs + prod * a.out_stride;
-  char* text = reinterpret_cast<char*>(sm + Cfg::KL) + 16 + (reinterpret_cast<unsigned long long>(out) & 15);
-  text = reinterpret_cast<char*>(reinterpret_cast<unsigned long long>(text) & ~15ull) +
-         (reinterpret_cast<unsigned long long>(out) & 15);
+  // text = out (mod 16) for cta_store_bytes, from the 16-byte aligned sm + KL + (KL & 1) (at
+  // most the old round-down's offset); plain pointer arithmetic keeps the shared address
+  // space visible to the compiler (STS/LDS, not generic stores)
+  char* text = reinterpret_cast<char*>(sm + Cfg::KL + (Cfg::KL & 1)) + 16 +
+               int(reinterpret_cast<unsigned long long>(out) & 15);
   for (int k = tid; k <= (int)top; k += NT)
     write_digits(text + limb_pos(k, top, top_len, be), Z[k], (unsigned long long)k == top ? top_len : be);
   __syncthreads();
