@@ -17,7 +17,8 @@ namespace dmg {
 
 typedef unsigned long long u64;
 
-struct TwPair {  // Shoup form of one root-of-unity factor
+// 16-byte aligned so a pair is one 128-bit load (LDG.E.128 / LDS.128), not two 64-bit ones.
+struct __align__(16) TwPair {  // Shoup form of one root-of-unity factor
   u64 w, wp;
 };
 
