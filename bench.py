@@ -13,7 +13,8 @@ are independent), as BASELINE config 2 specifies.
           flushed between steps; max over ranks.
   e2e   : the same metric through the public host API (decmul_gpu_multiply_batch)
           from pinned host buffers: H2D of the step's digits and D2H of the
-          products inside the timed region.
+          products inside the timed region (batches: median of three K-step
+          trials after W warm-up calls).
   --impl reference : the reference's own CPU implementation (oracle/_ref, the
           unmodified reference sources compiled by oracle/Makefile) on all host
           threads over the same batch; rank 0 only.
@@ -472,14 +473,20 @@ def run_ours(args, cfg, rank, world, local_rank):
         h2d = nx + (0 if squaring else ny)
         d2h = nx + ny
     call()
-    for _ in range(max(1, args.warmup // 2)):
+    for _ in range(max(1, args.warmup if count > 1 else args.warmup // 2)):
         call()
-    if dist:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        call()
-    e2e_ms = (time.perf_counter() - t0) * 1e3
+    # batches: the K-step loop is short (~25 ms for config 2), so one scheduling hiccup on a
+    # fresh box moved it by ~18%; report the median of three K-step trials (single products
+    # run for seconds and keep one trial)
+    trials = []
+    for _ in range(3 if count > 1 else 1):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            call()
+        trials.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = sorted(trials)[len(trials) // 2]
     if dist:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
