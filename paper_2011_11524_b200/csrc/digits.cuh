@@ -31,10 +31,10 @@ __device__ __forceinline__ unsigned swar4(unsigned x, int skip, unsigned& bad) {
 
 // Digits buf[s, s + n), n <= 4 NG, as an integer (NG 4-digit groups from the right; NG = 4
 // covers lambda <= 16, NG = 5 lambda = 17). buf must be 8-byte aligned and readable from
-// 4 NG + 7 bytes before s to 12 bytes past s + n.
+// 23 bytes before s to 8 bytes past s + n.
 //
-// WINDOW (k_pack): the 4 NG bytes ending at the limb's end are read as one 8-byte-aligned
-// window of 8-byte loads (3-4 LDS.64) and shifted into place with selects and funnel
+// WINDOW (k_pack): the 16 bytes ending at the limb's end are read as one 8-byte-aligned
+// window of three 8-byte loads and shifted into place with selects and funnel
 // shifts, so each group sits in a fixed register: half the shared-memory wavefronts of
 // one 4-byte funnel-shifted read per group, and k_pack's bank conflicts 34.7M -> 0.7M
 // (config 4). !WINDOW (k_small): the per-group reads; in k_small the window measured
@@ -43,16 +43,24 @@ template <int NG = 5, bool WINDOW = true>
 __device__ __forceinline__ u64 parse_digits(const char* buf, int s, int n, unsigned& bad) {
   static_assert(NG == 4 || NG == 5, "4 or 5 groups");
   unsigned g[5] = {0, 0, 0, 0, 0};
+  constexpr int NS = NG < 4 ? NG : 4;  // SWAR groups; with NG = 5 the fifth holds <= 1 digit
+  if constexpr (NG == 5) {
+    // n <= 17 leaves the fifth group's first 20 - n >= 3 bytes before s: it is the single
+    // digit buf[s] when n == 17, else 0
+    const unsigned c = n >= 17 ? unsigned((unsigned char)buf[s]) - '0' : 0u;
+    bad |= c > 9 ? 0x80u : 0u;
+    g[4] = c;
+  }
   if constexpr (!WINDOW) {
     const int e = s + n;
 #pragma unroll
-    for (int k = 0; k < NG; ++k) {
+    for (int k = 0; k < NS; ++k) {
       const int skip = 4 * (k + 1) - n;  // bytes of the group before s
       g[k] = skip < 4 ? swar4(smem_bytes4(buf, e - 4 * (k + 1)), skip < 0 ? 0 : skip, bad) : 0u;
     }
   } else {
-    constexpr int BYTES = 4 * NG, NQ = (BYTES + 14) / 8;  // window: BYTES + up to 7 bytes of offset
-    const int st = s + n - BYTES;                          // first byte of the NG groups
+    constexpr int BYTES = 4 * NS, NQ = (BYTES + 14) / 8;  // window: BYTES + up to 7 bytes of offset
+    const int st = s + n - BYTES;                          // first byte of the NS groups
     const int a0 = st & ~7;
     const int o = st - a0;  // 0..7
     const uint2* wp = reinterpret_cast<const uint2*>(buf + a0);
@@ -66,8 +74,8 @@ __device__ __forceinline__ u64 parse_digits(const char* buf, int s, int n, unsig
     const bool up = o >= 4;
     const int sh = (o & 3) * 8;
 #pragma unroll
-    for (int k = 0; k < NG; ++k) {  // group k from the right = word NG - 1 - k of the window
-      const int j = NG - 1 - k;
+    for (int k = 0; k < NS; ++k) {  // group k from the right = word NS - 1 - k of the window
+      const int j = NS - 1 - k;
       const unsigned lo = up ? w[j + 1] : w[j], hi = up ? w[j + 2] : w[j + 1];
       const int skip = 4 * (k + 1) - n;  // bytes of the group before s
       g[k] = skip < 4 ? swar4(__funnelshift_r(lo, hi, sh), skip < 0 ? 0 : skip, bad) : 0u;
