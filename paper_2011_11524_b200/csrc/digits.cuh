@@ -38,7 +38,7 @@ __device__ __forceinline__ unsigned swar4(unsigned x, int skip, unsigned& bad) {
 // shifts, so each group sits in a fixed register: half the shared-memory wavefronts of
 // one 4-byte funnel-shifted read per group, and k_pack's bank conflicts 34.7M -> 0.7M
 // (config 4). !WINDOW (k_small): the per-group reads; in k_small the window measured
-// 0.4% slower on config 2 (its parse overlaps other CTAs' transforms).
+// 0.4% slower on config 2 (re-checked with the 3-load window: +0.45%).
 template <int NG = 5, bool WINDOW = true>
 __device__ __forceinline__ u64 parse_digits(const char* buf, int s, int n, unsigned& bad) {
   static_assert(NG == 4 || NG == 5, "4 or 5 groups");
