@@ -1,30 +1,37 @@
 #!/usr/bin/env python3
 """Benchmark: decimal digits multiplied per second on B200 (BASELINE.json metric).
 
-Default workload (config 2 of BASELINE.json, the contract's configs[1]): a batch
-of 4096 independent products of two 10,000-digit integers, uniform digits with a
-nonzero leading digit, pair k seeded (2k, 2k+1). One "step" = the whole batch.
-Under torchrun the batch is split evenly over the ranks (rank r multiplies pairs
-[r 4096/N, (r+1) 4096/N)): strong scaling, no data-path collective (the products
-are independent), as BASELINE config 2 specifies.
+Default workload: BASELINE config 4, the largest single-GPU configuration and the product
+the north_star target names — one 2,000,000,000 x 1,000,000,000-digit product (uniform
+digits, seeds 40 and 41; lambda = 15, N = 3 * 2^26 under the large prime pair). One "step"
+is that whole product: ASCII digits in HBM -> pack -> two-prime NTT convolution -> CRT +
+carry -> ASCII product in HBM.
 
-  value : device-resident throughput — digits already in HBM, products written
-          to HBM; CUDA events on the launching stream around each step, L2
-          flushed between steps; max over ranks.
-  e2e   : the same metric through the public host API (decmul_gpu_multiply_batch)
-          from pinned host buffers: H2D of the step's digits and D2H of the
-          products inside the timed region (batches: median of three K-step
-          trials after W warm-up calls).
-  --impl reference : the reference's own CPU implementation (oracle/_ref, the
-          unmodified reference sources compiled by oracle/Makefile) on all host
-          threads over the same batch; rank 0 only.
+  value : device-resident throughput (digits_x + digits_y per step / step time): inputs
+          already in HBM, the product written to HBM; CUDA events on the launching stream
+          around each step; max over ranks.
+  e2e   : the same metric through the public host API (decmul_gpu_multiply; batches:
+          decmul_gpu_multiply_batch) from pinned host buffers, H2D of the operands and D2H
+          of the product inside the timed region.
+  roofline : the dominant kernel (CUDA events around every launch of a profiled step, on
+          the library's stream): algorithmic modmuls (bytes) per launch / its mean launch
+          time, against the live Shoup micro-kernel rate (MEASURED_PEAKS.json hbm_gbs);
+          plus the whole product against SURVEY §8(d)'s M_alg ("product").
+  outputs_ok : the timed product's SHA-256 equals the reference-derived golden
+          (tests/golden/golden_large.json; config 2: the first 64 products' hashes).
+  --impl reference : the reference's own CPU implementation (oracle/_ref: the unmodified
+          reference sources compiled by oracle/Makefile) on the box's host threads over the
+          same workload or, beyond the reference's 3 * 2^24 cap (configs 4, 5), over chunk
+          pairs of the same operands (see reference_sample); rank 0 only.
 
-Other configs (--config 1|3|33|4|5): one product per step (1e6 x 1e6, 1e8 x 1e8
-uniform / all nines, 2e9 x 1e9, 1e10 x 1e10 digits), same reporting.
+Other configs (--config 1|2|3|33|34|5): 1e6 x 1e6; the batch of 4096 products of 1e4 x 1e4
+digits (split evenly over the ranks under torchrun); 1e8 x 1e8 uniform / all nines /
+uniform x all nines; 1e10 x 1e10. Single products under torchrun (N > 1) run sharded.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -35,20 +42,28 @@ import time
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
+# modes: 0 uniform digits (nonzero leading digit), 1 all nines; golden: key of
+# tests/golden/golden_large.json (reference-derived SHA-256 of the product)
 CONFIGS = {
-    1: dict(workload="single product 1e6 x 1e6 digits (BASELINE config 1)", count=1, nx=10**6, ny=10**6, mode=0),
+    1: dict(workload="single product 1e6 x 1e6 digits (BASELINE config 1)", count=1, nx=10**6, ny=10**6,
+            modes=(0, 0), seeds=(0, 1), golden="config1"),
     2: dict(workload="batch of 4096 products of 1e4 x 1e4 digits (BASELINE config 2)", count=4096, nx=10**4,
-            ny=10**4, mode=0),
+            ny=10**4, modes=(0, 0), seeds=(0, 1), golden=None),
     3: dict(workload="single product 1e8 x 1e8 digits, uniform (BASELINE config 3)", count=1, nx=10**8, ny=10**8,
-            mode=0),
+            modes=(0, 0), seeds=(0, 1), golden="config3"),
     33: dict(workload="single product 1e8 x 1e8 digits, all nines (BASELINE config 3, squaring half)", count=1,
-             nx=10**8, ny=10**8, mode=1),
+             nx=10**8, ny=10**8, modes=(1, 1), seeds=(0, 0), golden="nines"),
+    34: dict(workload="single product 1e8 uniform x 1e8 all-nines digits (BASELINE config 3, non-squaring "
+                      "worst case)", count=1, nx=10**8, ny=10**8, modes=(0, 1), seeds=(2, 0), golden="config3x"),
     4: dict(workload="single product 2e9 x 1e9 digits (BASELINE config 4)", count=1, nx=2 * 10**9, ny=10**9,
-            mode=0),
+            modes=(0, 0), seeds=(40, 41), golden="config4", ref_chunked=True),
     5: dict(workload="single product 1e10 x 1e10 digits (BASELINE config 5)", count=1, nx=10**10, ny=10**10,
-            mode=0),
+            modes=(0, 0), seeds=(50, 51), golden="config5", ref_chunked=True),
 }
+DEFAULT_CONFIG = 4
 PEAKS_FILE = os.path.join(HERE, "MEASURED_PEAKS.json")
+GOLDEN_LARGE = os.path.join(HERE, "tests", "golden", "golden_large.json")
+GOLDEN = os.path.join(HERE, "tests", "golden", "golden.json")
 
 
 def modmuls_per_product(n: int, squaring: bool) -> int:
@@ -118,19 +133,118 @@ def load_peaks() -> dict:
         return {"hbm_gbs": 6650.0, "fallback": True}
 
 
-def ncu_traffic(config: int):
-    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+def ncu_traffic(config: int, kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture (profiles/), or None."""
     path = os.path.join(HERE, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get(str(config), {}).get("dram_bytes_per_launch")
+            d = json.load(f).get(str(config), {})
     except (OSError, ValueError):
         return None
+    k = d.get("kernels", {}).get(kernel)
+    return k.get("dram_bytes_per_launch") if k else None
+
+
+def golden_sha(cfg: dict):
+    key = cfg.get("golden")
+    if not key or key == "nines":
+        return None
+    try:
+        with open(GOLDEN_LARGE) as f:
+            g = json.load(f).get(key)
+    except OSError:
+        return None
+    if not g or list(g["digits"]) != [cfg["nx"], cfg["ny"]]:
+        return None
+    return g
+
+
+def nines_square_sha(n: int) -> tuple[int, str]:
+    """(10^n - 1)^2 = 9...980...01 (n-1 nines, 8, n-1 zeros, 1): the closed form of the
+    reference's all-nines squaring check (oracle.cpp:171-180)."""
+    h = hashlib.sha256()
+    step = 1 << 26
+    for body in (b"9", b"0"):
+        left = n - 1
+        while left:
+            k = min(step, left)
+            h.update(body * k)
+            left -= k
+        h.update(b"8" if body == b"9" else b"1")
+    return 2 * n, h.hexdigest()
+
+
+def device_sha(t, n: int, pinned) -> str:
+    """SHA-256 of the first n bytes of a device uint8 tensor, streamed through a pinned buffer."""
+    h = hashlib.sha256()
+    step = pinned.numel()
+    for off in range(0, n, step):
+        k = min(step, n - off)
+        pinned[:k].copy_(t[off:off + k])
+        h.update(memoryview(pinned[:k].numpy()))
+    return h.hexdigest()
 
 
 # ---------------------------------------------------------------------------------------------
-# reference arm
+# the reference's CPU path
+
+def reference_sample(cfg: dict, chunk_digits: int, threads: int):
+    """Inputs for one step of the reference on the host.
+
+    Configs the reference accepts: the workload itself (config 2: every product, one
+    multiply() per product over `threads` threads; single products: one multiply(), since
+    the reference has no intra-product parallelism). Configs 4 and 5 exceed its 3 * 2^24
+    transform cap (OperandTooLarge, decimal.cpp:94-96), so a step is `threads` chunk
+    products X_i * Y_j of the same operands cut into chunk_digits-digit decimal chunks from
+    the least significant end (the composed-reference decomposition of SURVEY §8(c) 1),
+    run concurrently. Digits multiplied per second over those chunk products is GENEROUS to
+    the reference: composing the whole product would need all (nx/K)(ny/K) chunk products
+    plus the shifted sums."""
+    from paper_2011_11524_b200 import inputs
+
+    nx, ny = cfg["nx"], cfg["ny"]
+    (sx, sy), (mx, my) = cfg["seeds"], cfg["modes"]
+    if cfg["count"] > 1:
+        n = cfg["count"]
+        xs = [inputs.gen_digits(2 * k, nx) for k in range(n)]
+        ys = [inputs.gen_digits(2 * k + 1, ny) for k in range(n)]
+        return xs, ys, threads, f"all {n} products per step, {threads} threads, one multiply() per product"
+    if not cfg.get("ref_chunked"):  # inside the reference's cap
+        x = inputs.gen_digits(sx, nx, mx)
+        y = None if cfg["modes"] == (1, 1) else inputs.gen_digits(sy, ny, my)
+        return [x], [y], 1, "the whole product per step, one multiply() on 1 thread (the reference has no " \
+                            "intra-product parallelism)"
+    k = chunk_digits
+    nxc, nyc = -(-nx // k), -(-ny // k)
+    pairs = [(i, j) for i in range(nxc) for j in range(nyc)][:threads]
+    xc = {i: inputs.gen_digits_range(sx, nx, max(0, nx - (i + 1) * k), nx - i * k, mx).lstrip(b"0") or b"0"
+          for i in {p[0] for p in pairs}}
+    yc = {j: inputs.gen_digits_range(sy, ny, max(0, ny - (j + 1) * k), ny - j * k, my).lstrip(b"0") or b"0"
+          for j in {p[1] for p in pairs}}
+    return [xc[i] for i, _ in pairs], [yc[j] for _, j in pairs], threads, \
+        (f"{len(pairs)} chunk products X_i*Y_j of {k}-digit decimal chunks of the config's operands per step, run "
+         f"concurrently on {threads} threads (the reference refuses the whole product: OperandTooLarge, "
+         f"N > 3*2^24); the composed product would need {nxc * nyc} chunk products plus shifted sums, so this "
+         "digits/s overstates the reference")
+
+
+def time_reference(ref, xs, ys, threads: int, steps: int, warmup: int) -> tuple[float, float]:
+    """Mean seconds per step and digits per step of the reference's multiply over the sample."""
+    digits = sum(len(x) + len(y if y is not None else x) for x, y in zip(xs, ys))
+
+    def step():
+        if len(xs) == 1:
+            ref.multiply(xs[0], ys[0])
+        else:
+            ref.multiply_batch(xs, [x if y is None else y for x, y in zip(xs, ys)], threads)
+
+    for _ in range(warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    return (time.perf_counter() - t0) / steps, digits
+
 
 def run_reference(args, cfg, rank, world):
     if rank != 0:
@@ -138,78 +252,86 @@ def run_reference(args, cfg, rank, world):
     import oracle
 
     ref = oracle.ref()
-    from paper_2011_11524_b200 import inputs
-
-    try:  # configs 4 and 5: the reference's own planner refuses (decimal.cpp:96,99)
-        ref.select_base_and_length(cfg["nx"], cfg["ny"])
-    except oracle.OracleError as e:
-        print(json.dumps({"impl": "reference", "unavailable": f"reference multiply refuses this size: {e}",
-                          "config": {"workload": cfg["workload"]}}), flush=True)
-        return
     threads = os.cpu_count() or 1
-    count = cfg["count"]
-    xs = [inputs.gen_digits(2 * k, cfg["nx"], cfg["mode"]) for k in range(count)]
-    ys = [inputs.gen_digits(2 * k + 1, cfg["ny"], cfg["mode"]) for k in range(count)]
-    if cfg["mode"] == 1:
-        ys = [None] * count
-
-    def step():
-        if count == 1:
-            ref.multiply(xs[0], ys[0])
-        else:
-            ref.multiply_batch(xs, ys, threads)
-
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = (time.perf_counter() - t0) / args.steps
-    digits = (cfg["nx"] + cfg["ny"]) * count
+    xs, ys, cores, sample = reference_sample(cfg, args.ref_chunk, threads)
+    dt, digits = time_reference(ref, xs, ys, cores, args.steps, args.warmup)
     value = digits / dt
-    cores = threads if count > 1 else 1
     line = {
         "impl": "reference", "metric": "decimal digits multiplied/sec", "value": value, "unit": "digits/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-        "higher_is_better": True, "scaling": "strong" if count > 1 else "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic (seeded splitmix64 digits, SURVEY §8(d))",
-        "config": {"workload": cfg["workload"], "products": count, "digits_x": cfg["nx"], "digits_y": cfg["ny"]},
+        "higher_is_better": True, "scaling": "strong" if cfg["count"] > 1 else "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic (seeded splitmix64 digits, SURVEY §8(d))",
+        "config": config_block(cfg, cfg["count"]),
         "cpu_baseline": {"value": value, "unit": "digits/s", "cores": cores, "kind": "reference",
-                         "sample": f"full workload per step ({count} product(s)) on {cores} host thread(s); "
-                                   "reference proj/src compiled unmodified (-O3 -DNDEBUG)"},
+                         "sample": sample + "; reference proj/src compiled unmodified (-O3 -DNDEBUG)"},
         "e2e": {"value": value, "unit": "digits/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg) -> dict:
-    """Reference CPU path on a bounded sample of the workload (rank 0, N=1)."""
+def cpu_baseline(cfg, chunk_digits) -> dict:
+    """The reference's CPU path on a bounded sample of the workload (rank 0, N = 1)."""
     import oracle
-    from paper_2011_11524_b200 import inputs
 
     ref = oracle.ref()
     threads = os.cpu_count() or 1
-    if cfg["count"] > 1:
-        n = min(cfg["count"], 2048)
-        xs = [inputs.gen_digits(2 * k, cfg["nx"]) for k in range(n)]
-        ys = [inputs.gen_digits(2 * k + 1, cfg["ny"]) for k in range(n)]
-        ref.multiply_batch(xs[:threads], ys[:threads], threads)  # warm
-        t0 = time.perf_counter()
-        ref.multiply_batch(xs, ys, threads)
-        dt = time.perf_counter() - t0
-        return {"value": n * (cfg["nx"] + cfg["ny"]) / dt, "unit": "digits/s", "cores": threads, "kind": "reference",
-                "sample": f"{n} of the {cfg['count']} products, {threads} threads, one multiply() per product"}
-    nx = min(cfg["nx"], 10**7)
-    ny = min(cfg["ny"], 10**7)
-    x = inputs.gen_digits(0, nx, cfg["mode"])
-    y = None if cfg["mode"] == 1 else inputs.gen_digits(1, ny)
-    ref.multiply(x[: 10**4], None if y is None else y[: 10**4])
-    t0 = time.perf_counter()
-    ref.multiply(x, y)
-    dt = time.perf_counter() - t0
-    return {"value": (nx + ny) / dt, "unit": "digits/s", "cores": 1, "kind": "reference",
-            "sample": f"one {nx} x {ny}-digit product (1 thread; the reference has no intra-product parallelism)"
-                      + ("" if nx == cfg["nx"] else "; smaller than the workload, throughput grows ~1/log N")}
+    if cfg["count"] > 1:  # a bounded share of the batch
+        c = dict(cfg, count=min(cfg["count"], 2048))
+        xs, ys, cores, sample = reference_sample(c, chunk_digits, threads)
+        sample = f"{c['count']} of the {cfg['count']} products, {threads} threads, one multiply() per product"
+    elif cfg["nx"] > 10**7 and cfg["nx"] <= 10**8:  # 1e8-digit configs: a 1e7-digit product (~1 s)
+        c = dict(cfg, nx=10**7, ny=10**7)
+        xs, ys, cores, sample = reference_sample(c, chunk_digits, threads)
+        sample = "one 1e7 x 1e7-digit product of the same kind on 1 thread (smaller than the workload; the " \
+                 "reference's digits/s falls ~1/log N as N grows)"
+    else:
+        xs, ys, cores, sample = reference_sample(cfg, chunk_digits, threads)
+    dt, digits = time_reference(ref, xs, ys, cores, 1, 1)
+    return {"value": digits / dt, "unit": "digits/s", "cores": cores, "kind": "reference", "sample": sample,
+            "seconds": dt}
+
+
+def config_block(cfg, per_gpu, extra=None) -> dict:
+    d = {"workload": cfg["workload"], "products": cfg["count"], "products_per_gpu": per_gpu,
+         "digits_x": cfg["nx"], "digits_y": cfg["ny"], "seeds": list(cfg["seeds"]),
+         "digit_modes": ["uniform" if m == 0 else "all nines" for m in cfg["modes"]]}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ---------------------------------------------------------------------------------------------
+# per-launch profile -> dominant kernel roofline
+
+def kernel_roofline(rep: list, steps: int, rmm: float, hbm_peak: float, config: int) -> dict:
+    agg: dict = {}
+    for name, ms, mm, by in rep:
+        a = agg.setdefault(name, [0, 0.0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += ms
+        a[2] += mm
+        a[3] += by
+    total = sum(a[1] for a in agg.values())
+    name, (n, ms, mm, by) = max(agg.items(), key=lambda kv: kv[1][1])
+    t = ms / n * 1e-3  # mean launch seconds
+    a_mm, a_bw = mm / n / t, by / n / t / 1e9
+    f_int, f_hbm = a_mm / rmm, a_bw / hbm_peak
+    kernels = {k: {"launches_per_step": v[0] / steps, "ms_per_step": v[1] / steps,
+                   "share": v[1] / total if total else None,
+                   "gmodmul_s": (v[2] / (v[1] * 1e-3) / 1e9) if v[1] else None,
+                   "gb_s": (v[3] / (v[1] * 1e-3) / 1e9) if v[1] else None} for k, v in agg.items()}
+    out = {"kernel": name, "launches_per_step": n / steps, "mean_launch_ms": ms / n,
+           "share_of_step": ms / total if total else None}
+    if f_int >= f_hbm:
+        out.update({"bound": "int", "unit": "Gmodmul/s", "achieved": a_mm / 1e9, "peak": rmm / 1e9, "frac": f_int,
+                    "hbm": {"achieved": a_bw, "peak": hbm_peak, "unit": "GB/s", "frac": f_hbm}})
+    else:
+        out.update({"bound": "hbm", "unit": "GB/s", "achieved": a_bw, "peak": hbm_peak, "frac": f_hbm,
+                    "int": {"achieved": a_mm / 1e9, "peak": rmm / 1e9, "unit": "Gmodmul/s", "frac": f_int}})
+    out["traffic"] = ncu_traffic(config, name)
+    out["algorithmic_per_launch"] = {"modmuls": mm / n, "hbm_bytes": by / n}
+    out["all_kernels"] = kernels
+    return out
 
 
 # ---------------------------------------------------------------------------------------------
@@ -233,15 +355,16 @@ def run_sharded(args, cfg, rank, world, local_rank):
     sptr = stream.cuda_stream
     backend = DeviceBackend(ctx, stream)
     comm = TorchComm(dist)
-    nx, ny, mode = cfg["nx"], cfg["ny"], cfg["mode"]
-    squaring = mode == 1
+    nx, ny = cfg["nx"], cfg["ny"]
+    (sx, sy), (mx, my) = cfg["seeds"], cfg["modes"]
+    squaring = cfg["modes"] == (1, 1)
     plan = backend.plan(nx, ny, world)
     xs = torch.empty(nx, dtype=torch.uint8, device=dev)
-    ctx.generate_digits(xs.data_ptr(), nx, 0, mode=mode, stream=sptr)
+    ctx.generate_digits(xs.data_ptr(), nx, sx, mode=mx, stream=sptr)
     ys = xs
     if not squaring:
         ys = torch.empty(ny, dtype=torch.uint8, device=dev)
-        ctx.generate_digits(ys.data_ptr(), ny, 1, mode=mode, stream=sptr)
+        ctx.generate_digits(ys.data_ptr(), ny, sy, mode=my, stream=sptr)
     out = torch.zeros(nx + ny, dtype=torch.uint8, device=dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
@@ -313,7 +436,6 @@ def run_sharded(args, cfg, rank, world, local_rank):
            "h2d_bytes_per_step": world * (nx + (0 if squaring else ny)), "d2h_bytes_per_step": int(d2h.item())}
 
     rmm = ctx.measure_modmul_rate(0)
-    rmm_mont = ctx.measure_modmul_rate(1)
     peaks = load_peaks()
     N = int(plan.length)
     step_s = total_ms / args.steps * 1e-3
@@ -325,8 +447,6 @@ def run_sharded(args, cfg, rank, world, local_rank):
         "frac": mm / step_s / world / rmm, "traffic": None,
         "algorithmic": {"modmuls_per_step": mm, "hbm_bytes_per_step": byt, "all_to_all_bytes_per_step": a2a},
         "peak_source": "live Shoup modmul micro-kernel on all SMs of one GPU (per-GPU achieved vs per-GPU peak)",
-        "survey_canonical": {"kernel": "independent-lane Montgomery REDC micro-kernel (SURVEY §8(d) R_mm)",
-                             "peak": rmm_mont / 1e9, "frac": mm / step_s / world / rmm_mont},
         "hbm": {"achieved": byt / step_s / world / 1e9, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": byt / step_s / world / 1e9 / peaks.get("hbm_gbs", 6650.0)},
         "kernel": "multi-pass NTT (k_pass_*), column/row sharded",
@@ -338,13 +458,13 @@ def run_sharded(args, cfg, rank, world, local_rank):
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded splitmix64 digits generated in HBM, SURVEY §8(d))",
-            "config": {"workload": cfg["workload"], "products": 1, "digits_x": nx, "digits_y": ny,
-                       "base_exp": int(plan.base_exp), "transform_length": N,
-                       "prime_pair": [int(plan.p1), int(plan.p2)],
-                       "parallelism": f"one product sharded over {world} GPU(s): {int(plan.col_passes)} column "
-                                      f"pass(es) on {int(plan.rows)} x {int(plan.seg_len)}, NCCL all-to-all",
-                       "l2": "flushed (512 MiB write) before every timed step; per-step CUDA events"},
+            "config": config_block(cfg, 1, {
+                "base_exp": int(plan.base_exp), "transform_length": N, "prime_pair": [int(plan.p1), int(plan.p2)],
+                "parallelism": f"one product sharded over {world} GPU(s): {int(plan.col_passes)} column "
+                               f"pass(es) on {int(plan.rows)} x {int(plan.seg_len)}, NCCL all-to-all",
+                "l2": "flushed (512 MiB write) before every timed step; per-step CUDA events"}),
             "e2e": e2e, "roofline": roofline, "gpu_launches": launches, "clocks": clk, "outputs_ok": ok,
+            "outputs_check": "product length only (sharded path)",
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -356,6 +476,7 @@ def run_sharded(args, cfg, rank, world, local_rank):
 def run_ours(args, cfg, rank, world, local_rank):
     import torch
     import paper_2011_11524_b200 as dm
+    from paper_2011_11524_b200 import shard
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -370,23 +491,29 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
     assert sptr != 0
-    count, nx, ny, mode = cfg["count"], cfg["nx"], cfg["ny"], cfg["mode"]
-    squaring = mode == 1
+    count, nx, ny = cfg["count"], cfg["nx"], cfg["ny"]
+    (sx, sy), (mx, my) = cfg["seeds"], cfg["modes"]
+    squaring = cfg["modes"] == (1, 1)
     plan = ctx.plan(nx, ny)
     total = count
     if count > 1:  # strong scaling: the batch is split evenly over the ranks
         if count % world:
             raise SystemExit(f"batch of {count} does not split over {world} ranks")
         count //= world
-    base = rank * count
+    base = shard.batch_range(rank, world, count).start
 
     xs = torch.empty(count * nx, dtype=torch.uint8, device=dev)
-    ys = torch.empty(count * ny, dtype=torch.uint8, device=dev)
+    ys = xs if squaring else torch.empty(count * ny, dtype=torch.uint8, device=dev)
     out_stride = nx + ny
     outs = torch.empty(count * out_stride, dtype=torch.uint8, device=dev)
     lens = torch.zeros(count, dtype=torch.int64, device=dev)
-    ctx.generate_digits(xs.data_ptr(), nx, 2 * base, count=count, seed_step=2, mode=mode, stream=sptr)
-    ctx.generate_digits(ys.data_ptr(), ny, 2 * base + 1, count=count, seed_step=2, mode=mode, stream=sptr)
+    if count > 1:  # pair k seeded (2k, 2k + 1)
+        ctx.generate_digits(xs.data_ptr(), nx, 2 * base, count=count, seed_step=2, mode=mx, stream=sptr)
+        ctx.generate_digits(ys.data_ptr(), ny, 2 * base + 1, count=count, seed_step=2, mode=my, stream=sptr)
+    else:
+        ctx.generate_digits(xs.data_ptr(), nx, sx, mode=mx, stream=sptr)
+        if not squaring:
+            ctx.generate_digits(ys.data_ptr(), ny, sy, mode=my, stream=sptr)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step():
@@ -394,8 +521,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             ctx.multiply_batch_device(count, xs.data_ptr(), nx, ys.data_ptr(), ny, outs.data_ptr(), out_stride,
                                       lens.data_ptr(), stream=sptr)
         else:
-            ctx.multiply_device(xs.data_ptr(), nx, xs.data_ptr() if squaring else ys.data_ptr(), ny,
-                                outs.data_ptr(), out_stride, stream=sptr, squaring=squaring, sync=False)
+            ctx.multiply_device(xs.data_ptr(), nx, ys.data_ptr(), ny, outs.data_ptr(), out_stride, stream=sptr,
+                                squaring=squaring, sync=False)
 
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -431,15 +558,47 @@ def run_ours(args, cfg, rank, world, local_rank):
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
+    ctx.check_errors(sptr)  # the asynchronous entry points' error word (bad digits, bound violations)
 
-    # correctness spot check of the last step's outputs (product lengths)
-    ok_len = True
+    # ---- the timed outputs against reference-derived goldens ----
+    check = "product lengths only"
     if count > 1:
         ln = lens.cpu()
-        ok_len = bool(((ln == nx + ny) | (ln == nx + ny - 1)).all())
+        ok = bool(((ln == nx + ny) | (ln == nx + ny - 1)).all())
+        if rank == 0 and (nx, ny) == (10**4, 10**4) and os.path.exists(GOLDEN):
+            with open(GOLDEN) as f:
+                want = json.load(f)["ref"]["config2_first64_sha"]
+            o = outs[:64 * out_stride].cpu().numpy()
+            got = [hashlib.sha256(o[k * out_stride: k * out_stride + int(ln[k])].tobytes()).hexdigest()
+                   for k in range(min(64, count))]
+            ok = ok and got == want[:len(got)]
+            check = f"all {count} lengths; SHA-256 of products 0..{len(got) - 1} == the reference's " \
+                    "(tests/golden/golden.json config2_first64_sha)"
+    else:
+        n_out = ctx.result_length()
+        pin = torch.empty(min(n_out, 1 << 28), dtype=torch.uint8, pin_memory=True)
+        got = device_sha(outs, n_out, pin)
+        del pin
+        g = golden_sha(cfg)
+        ok = n_out in (nx + ny - 1, nx + ny)
+        if cfg.get("golden") == "nines":
+            ln_w, sha_w = nines_square_sha(nx)
+            ok = ok and (n_out, got) == (ln_w, sha_w)
+            check = "SHA-256 of the product == the closed form (10^n - 1)^2"
+        elif g is not None and g["seeds"][0] == sx:
+            ok = ok and (n_out, got) == (g["length"], g["sha256"])
+            check = f"SHA-256 of the product == tests/golden/golden_large.json {cfg['golden']} ({g['method']})"
+
+    # ---- per-launch profile: dominant kernel ----
+    prof_steps = 3
+    ctx.profile(True)
+    for _ in range(prof_steps):
+        step()
+        torch.cuda.synchronize()
+    rep = ctx.profile_report()
+    ctx.profile(False)
 
     # ---- e2e through the public host API (pinned host buffers) ----
-    e2e = None
     if count > 1:
         hx = torch.empty(count * nx, dtype=torch.uint8, pin_memory=True)
         hy = torch.empty(count * ny, dtype=torch.uint8, pin_memory=True)
@@ -493,29 +652,31 @@ def run_ours(args, cfg, rank, world, local_rank):
         e2e_ms = float(t.item())
     digits_step = count * (nx + ny)
     e2e = {"value": world * digits_step * args.steps / (e2e_ms * 1e-3), "unit": "digits/s",
-           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
+           "api": "decmul_gpu_multiply_batch" if count > 1 else "decmul_gpu_multiply", "host_buffers": "pinned"}
 
-    # ---- roofline: integer pipe (modmuls) and HBM, for the dominant kernel ----
+    # ---- roofline: dominant kernel (per-launch events) and the whole product (SURVEY M_alg) ----
     rmm = ctx.measure_modmul_rate(0)
     rmm_mont = ctx.measure_modmul_rate(1)
     peaks = load_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
     n = plan["length"]
     mm = modmuls_per_product(n, squaring) * count
     byt = hbm_bytes_per_product(n, nx, ny, plan["one_cta"], squaring) * count
     step_s = total_ms / args.steps * 1e-3
-    ach_mm = mm / step_s
-    ach_bw = byt / step_s / 1e9
-    roofline = {
-        "bound": "int", "unit": "Gmodmul/s", "achieved": ach_mm / 1e9, "peak": rmm / 1e9, "frac": ach_mm / rmm,
-        "traffic": ncu_traffic(args.config),
-        "algorithmic": {"modmuls_per_step": mm, "hbm_bytes_per_step": byt},
-        "peak_source": "live Shoup modmul micro-kernel on all SMs (decmul_gpu_measure_modmul_rate)",
+    roofline = kernel_roofline(rep, prof_steps, rmm, hbm_peak, args.config)
+    roofline["peak_source"] = ("int: live Shoup modmul micro-kernel on all SMs (decmul_gpu_measure_modmul_rate, the "
+                               "transforms' multiply); hbm: MEASURED_PEAKS.json hbm_gbs"
+                               + (" (fallback)" if peaks.get("fallback") else ""))
+    roofline["timing"] = ("CUDA events after every launch of a profiled step on the library's stream "
+                          f"({prof_steps} steps after the timed loop)")
+    roofline["product"] = {
+        "bound": "int", "unit": "Gmodmul/s", "achieved": mm / step_s / 1e9, "peak": rmm / 1e9,
+        "frac": mm / step_s / rmm, "algorithmic": {"modmuls_per_step": mm, "hbm_bytes_per_step": byt},
         "survey_canonical": {"kernel": "independent-lane Montgomery REDC micro-kernel (SURVEY §8(d) R_mm)",
-                             "peak": rmm_mont / 1e9, "frac": ach_mm / rmm_mont},
-        "hbm": {"achieved": ach_bw, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                "frac": ach_bw / peaks.get("hbm_gbs", 6650.0),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not peaks.get("fallback") else "fallback"},
-        "kernel": "k_small (one CTA per product)" if plan["one_cta"] else "multi-pass NTT (k_pass_*)",
+                             "peak": rmm_mont / 1e9, "frac": mm / step_s / rmm_mont},
+        "hbm": {"achieved": byt / step_s / 1e9, "peak": hbm_peak, "unit": "GB/s", "frac": byt / step_s / 1e9 / hbm_peak},
+        "note": "whole product: SURVEY §8(d) M_alg per step / the timed step (the north_star's NTT-roofline fraction)",
     }
     if rank != 0:
         if dist:
@@ -527,16 +688,15 @@ def run_ours(args, cfg, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong" if total > 1 else "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seeded splitmix64 digits generated in HBM, SURVEY §8(d))",
-        "config": {"workload": cfg["workload"], "products": total, "products_per_gpu": count, "digits_x": nx,
-                   "digits_y": ny,
-                   "base_exp": plan["base_exp"], "transform_length": n, "prime_pair": [plan["p1"], plan["p2"]],
-                   "parallelism": f"batch split, {world} GPU(s)" if count > 1 else "replicas",
-                   "l2": "flushed (512 MiB write) before every timed step; per-step CUDA events"},
+        "config": config_block(cfg, count, {
+            "base_exp": plan["base_exp"], "transform_length": n, "prime_pair": [plan["p1"], plan["p2"]],
+            "parallelism": f"batch split, {world} GPU(s)" if count > 1 else "replicas",
+            "l2": "flushed (512 MiB write) before every timed step; per-step CUDA events"}),
         "e2e": e2e, "roofline": roofline, "gpu_launches": launches_per_step * args.steps, "clocks": clk,
-        "outputs_ok": ok_len,
+        "outputs_ok": ok, "outputs_check": check,
     }
     if world == 1:
-        line["cpu_baseline"] = cpu_baseline(cfg)
+        line["cpu_baseline"] = cpu_baseline(cfg, args.ref_chunk)
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -558,12 +718,14 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--batch", type=int, default=None,
                     help="batch configs: products per step instead of BASELINE's 4096 (experiments, e.g. the "
                          "per-GPU share of an N-GPU split)")
     ap.add_argument("--sharded", action="store_true",
                     help="single-product configs: shard the product over the ranks even at N=1")
+    ap.add_argument("--ref-chunk", type=int, default=2 * 10**7,
+                    help="configs 4/5, reference CPU path: decimal chunk size of its chunk products")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))

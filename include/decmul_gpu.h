@@ -92,9 +92,16 @@ int decmul_gpu_multiply_batch(decmul_gpu_ctx* ctx, size_t count, const char* xs,
 int decmul_gpu_multiply_batch_ptrs(decmul_gpu_ctx* ctx, size_t count, const char* const* xs, const size_t* nxs,
                                    const char* const* ys, const size_t* nys, char* const* outs, const size_t* caps,
                                    size_t* out_lens);
+/* Device-resident batch, asynchronous on `stream` (NULL = the context's stream). Input errors
+ * (non-digit bytes, leading zeros) and bound violations of the asynchronous entry points
+ * (this call and multiply_device without out_len) are collected in a stream-ordered error
+ * word of their own: decmul_gpu_check_errors(ctx, stream) synchronises the stream, clears the
+ * word and returns the matching code (DECMUL_EINVAL, DECMUL_ECORRUPT) for the calls since the
+ * last check; decmul_gpu_result_length does the same. Synchronous calls never see them. */
 int decmul_gpu_multiply_batch_device(decmul_gpu_ctx* ctx, size_t count, const char* d_xs, size_t x_stride,
                                      size_t nx, const char* d_ys, size_t y_stride, size_t ny, char* d_outs,
                                      size_t out_stride, unsigned long long* d_lens, void* stream);
+int decmul_gpu_check_errors(decmul_gpu_ctx* ctx, void* stream);
 
 /* ---- parity hooks on host arrays (conv.hpp:59-71) ----
  * p must be one of the supported primes (the reference pair or the large pair); n = 2^k or
@@ -186,6 +193,14 @@ typedef struct {
   size_t table_bytes;      /* device bytes held by cached twiddle tables */
 } decmul_gpu_stats;
 int decmul_gpu_get_stats(decmul_gpu_ctx* ctx, decmul_gpu_stats* out);
+/* Per-launch timing (diagnostics, bench.py's roofline): while enabled, a CUDA event follows every
+ * kernel the context enqueues. decmul_gpu_profile_report synchronises and writes one line per
+ * launch since the last enable/report, "name<TAB>ms<TAB>modmuls<TAB>hbm_bytes\n" (ms since the
+ * previous event on the product's stream; modmuls and bytes are the launch's algorithmic work),
+ * NUL-terminated to report (truncated to cap; *len = full length), and clears the records
+ * (report == NULL only returns *len and keeps them). */
+int decmul_gpu_profile(decmul_gpu_ctx* ctx, int enable);
+int decmul_gpu_profile_report(decmul_gpu_ctx* ctx, char* report, size_t cap, size_t* len);
 
 /* GPU self-test, replaces run_selftest (selftest.cpp:79-219; CLI `selftest [--inject-fault]`,
  * main.cpp:162): field identities, transform round trips, convolution vs a direct O(n^2)

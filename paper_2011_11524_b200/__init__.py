@@ -57,6 +57,7 @@ EXPORTED_SYMBOLS = [
     "decmul_gpu_get_stats", "decmul_gpu_shard_plan_create", "decmul_gpu_shard_pack", "decmul_gpu_shard_transform",
     "decmul_gpu_shard_reorder", "decmul_gpu_shard_carry_begin", "decmul_gpu_shard_carry_probe",
     "decmul_gpu_shard_carry_emit", "decmul_gpu_selftest", "decmul_gpu_multiply_batch_ptrs",
+    "decmul_gpu_check_errors", "decmul_gpu_profile", "decmul_gpu_profile_report",
 ]
 
 
@@ -236,6 +237,26 @@ class Context:
         s = _Stats()
         self._call("decmul_gpu_get_stats", C.byref(s))
         return dict(last_launches=s.last_launches, table_bytes=s.table_bytes)
+
+    def check_errors(self, stream: int = 0) -> None:
+        """Raise the errors of the asynchronous entry points since the last check (syncs stream)."""
+        self._call("decmul_gpu_check_errors", C.c_void_p(stream))
+
+    def profile(self, enable: bool = True) -> None:
+        """Per-launch CUDA-event timing of every kernel this context enqueues."""
+        self._call("decmul_gpu_profile", C.c_int(int(enable)))
+
+    def profile_report(self) -> list[tuple[str, float, float, float]]:
+        """[(kernel name, ms, algorithmic modmuls, algorithmic HBM bytes)] since the last report."""
+        n = C.c_size_t()
+        self._call("decmul_gpu_profile_report", None, C.c_size_t(0), C.byref(n))
+        buf = C.create_string_buffer(n.value + 1)
+        self._call("decmul_gpu_profile_report", buf, C.c_size_t(len(buf)), C.byref(n))
+        out = []
+        for line in buf.value.decode().splitlines():
+            name, ms, mm, by = line.split("\t")
+            out.append((name, float(ms), float(mm), float(by)))
+        return out
 
     # ---- multiply ----
     def multiply_text(self, x: bytes, y: bytes | None, forced_base_exp: int = 0) -> bytes:

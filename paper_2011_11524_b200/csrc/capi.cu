@@ -57,10 +57,29 @@ int guarded(decmul_gpu_ctx* ctx, F&& f) {
   return rc;
 }
 
+// The calling thread's current device is switched to the context's for the call and restored
+// after it, so contexts on different GPUs can be used from one thread (allocations, streams
+// and kernel attributes all follow the current device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+    }
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 #define LOCKED(ctx, ...)                                     \
   do {                                                       \
     if (!(ctx)) return DECMUL_EINVAL;                        \
     std::lock_guard<std::mutex> lock_((ctx)->mu);            \
+    DeviceGuard dev_((ctx)->eng->device());                  \
     return guarded((ctx), [&] { __VA_ARGS__; });             \
   } while (0)
 
@@ -72,13 +91,18 @@ int decmul_gpu_create(decmul_gpu_ctx** ctx, int device) {
   if (!ctx) return DECMUL_EINVAL;
   *ctx = nullptr;
   return guarded(nullptr, [&] {
+    DeviceGuard dev(device);
     auto c = std::make_unique<decmul_gpu_ctx>();
     c->eng = std::make_unique<dmg::Engine>(device);
     *ctx = c.release();
   });
 }
 
-void decmul_gpu_destroy(decmul_gpu_ctx* ctx) { delete ctx; }
+void decmul_gpu_destroy(decmul_gpu_ctx* ctx) {
+  if (!ctx) return;
+  DeviceGuard dev(ctx->eng->device());
+  delete ctx;
+}
 
 const char* decmul_gpu_last_error(const decmul_gpu_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_create_err.c_str();
@@ -332,6 +356,24 @@ int decmul_gpu_selftest(decmul_gpu_ctx* ctx, int inject_fault, char* report, siz
     std::string r;
     const int f = ctx->eng->selftest(inject_fault != 0, r);
     if (failures) *failures = f;
+    if (report && cap) {
+      const size_t n = r.size() < cap - 1 ? r.size() : cap - 1;
+      std::memcpy(report, r.data(), n);
+      report[n] = '\0';
+    }
+  });
+}
+
+int decmul_gpu_check_errors(decmul_gpu_ctx* ctx, void* stream) {
+  LOCKED(ctx, ctx->eng->check_async_errors(static_cast<cudaStream_t>(stream)));
+}
+
+int decmul_gpu_profile(decmul_gpu_ctx* ctx, int enable) { LOCKED(ctx, ctx->eng->profile_enable(enable != 0)); }
+
+int decmul_gpu_profile_report(decmul_gpu_ctx* ctx, char* report, size_t cap, size_t* len) {
+  LOCKED(ctx, {
+    const std::string r = ctx->eng->profile_report(report != nullptr);
+    if (len) *len = r.size();
     if (report && cap) {
       const size_t n = r.size() < cap - 1 ? r.size() : cap - 1;
       std::memcpy(report, r.data(), n);

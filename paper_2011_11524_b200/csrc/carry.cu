@@ -43,41 +43,51 @@ __device__ __forceinline__ void coeff_digits(const CarryArgs& a, long long i, u6
 // Coefficients are read and limb sums written in coalesced order (loc = j NT + tid);
 // each limb's 6-bit transfer map goes to shared memory as a byte, and each thread
 // then composes the maps of PERC consecutive limbs (one PERC-byte shared load).
-template <int NTC, int PERC>
+// FROM_S: the limb sums are already in a.s (the general small-base recovery); only the maps.
+template <int NTC, int PERC, bool FROM_S = false>
 __global__ void __launch_bounds__(NTC) k_carry_split(CarryArgs a) {
   pdl_wait();
   constexpr int CHC = NTC * PERC;
   typedef typename MapWord<PERC>::type Word;
-  __shared__ u64 d1s[CHC + 2], d2s[CHC + 2];
+  __shared__ u64 d1s[FROM_S ? 1 : CHC + 2], d2s[FROM_S ? 1 : CHC + 2];
   __shared__ __align__(8) unsigned char mp[CHC];
   __shared__ unsigned wsm[NTC / 32 + 1];
   const unsigned long long k0 = (unsigned long long)blockIdx.x * CHC;
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const u64 B = a.div.base;
-  u64 d0r[PERC];
+  if constexpr (FROM_S) {
 #pragma unroll
-  for (int j = 0; j < PERC; ++j) {
-    const int loc = j * NTC + threadIdx.x;
-    u64 d0, d1, d2;
-    coeff_digits(a, (long long)(k0 + loc), d0, d1, d2);
-    d0r[j] = d0;
-    d1s[loc + 2] = d1;
-    d2s[loc + 2] = d2;
-  }
-  if (threadIdx.x < 2) {
-    u64 d0, d1, d2;
-    coeff_digits(a, (long long)k0 - 2 + threadIdx.x, d0, d1, d2);
-    d1s[threadIdx.x] = d1;
-    d2s[threadIdx.x] = d2;
-  }
-  __syncthreads();
+    for (int j = 0; j < PERC; ++j) {
+      const int loc = j * NTC + threadIdx.x;
+      const unsigned long long k = k0 + loc;
+      mp[loc] = (unsigned char)(k < K ? limb_map(a.s[k], B) : kIdentityMap);
+    }
+  } else {
+    u64 d0r[PERC];
 #pragma unroll
-  for (int j = 0; j < PERC; ++j) {
-    const int loc = j * NTC + threadIdx.x;
-    const unsigned long long k = k0 + loc;
-    const u64 s = d0r[j] + d1s[loc + 1] + d2s[loc];
-    if (k < K) a.s[k] = s;
-    mp[loc] = (unsigned char)(k < K ? limb_map(s, B) : kIdentityMap);
+    for (int j = 0; j < PERC; ++j) {
+      const int loc = j * NTC + threadIdx.x;
+      u64 d0, d1, d2;
+      coeff_digits(a, (long long)(k0 + loc), d0, d1, d2);
+      d0r[j] = d0;
+      d1s[loc + 2] = d1;
+      d2s[loc + 2] = d2;
+    }
+    if (threadIdx.x < 2) {
+      u64 d0, d1, d2;
+      coeff_digits(a, (long long)k0 - 2 + threadIdx.x, d0, d1, d2);
+      d1s[threadIdx.x] = d1;
+      d2s[threadIdx.x] = d2;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < PERC; ++j) {
+      const int loc = j * NTC + threadIdx.x;
+      const unsigned long long k = k0 + loc;
+      const u64 s = d0r[j] + d1s[loc + 1] + d2s[loc];
+      if (k < K) a.s[k] = s;
+      mp[loc] = (unsigned char)(k < K ? limb_map(s, B) : kIdentityMap);
+    }
   }
   __syncthreads();
   const unsigned long long m8 = reinterpret_cast<const Word*>(mp)[threadIdx.x];
@@ -318,15 +328,78 @@ __global__ void k_carry_cin(unsigned* maps, unsigned nchunks, unsigned rank_cin)
   if (c < nchunks) maps[c] = map_apply(maps[c], rank_cin);
 }
 
+// ---- general recovery for small forced bases (lambda < 14) ----
+
+// Coefficient i = sum_j d_j B^j (D digits; the reference's recover_digits, decimal.cpp:154-189,
+// carries the whole 128-bit value instead); digit j is added into the limb sum s[i + j].
+__global__ void k_carry_scatter(CarryArgs a, int D) {
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < a.n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    u64 lo, hi;
+    crt2(a.z1[i], a.z2[i], a.p1, a.p2, a.p2_prime, a.r_tilde, lo, hi);
+    if (above_cap(lo, hi, a.coeff_cap_lo, a.coeff_cap_hi)) atomicOr(a.err, kErrCoeffBound);
+    for (int j = 0; j < D && (lo | hi); ++j) {
+      u64 qlo, qhi;
+      const u64 d = divmod_base(a.div, lo, hi, qlo, qhi);
+      if (d) atomicAdd(&a.s[i + j], (unsigned long long)d);
+      lo = qlo;
+      hi = qhi;
+    }
+  }
+}
+
+// t_k = s_k mod B + floor(s_{k-1} / B): the value sum s_k B^k is unchanged.
+__global__ void k_carry_normalize(const u64* __restrict__ s, u64* __restrict__ t, unsigned long long K, u64 B) {
+  for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < K;
+       k += (unsigned long long)gridDim.x * blockDim.x)
+    t[k] = s[k] % B + (k ? s[k - 1] / B : 0);
+}
+
 }  // namespace
+
+int launch_carry_general(const CarryArgs& a0, int D, int rounds, u64* tmp, unsigned long long K, cudaStream_t st) {
+  CarryArgs a = a0;
+  int launched = 0;
+  cudaMemsetAsync(a.s, 0, K * sizeof(u64), st);
+  {
+    const unsigned long long b = (a.n + 255) / 256;
+    k_carry_scatter<<<unsigned(b < 148ull * 16 ? (b ? b : 1) : 148ull * 16), 256, 0, st>>>(a, D);
+    ++launched;
+  }
+  prof_mark("k_carry_scatter", st, double(a.n), double(a.n) * 16 + double(K) * 8);
+  u64* src = a.s;
+  u64* dst = tmp;
+  for (int r = 0; r < rounds; ++r) {
+    const unsigned long long b = (K + 255) / 256;
+    k_carry_normalize<<<unsigned(b < 148ull * 16 ? b : 148ull * 16), 256, 0, st>>>(src, dst, K, a.div.base);
+    ++launched;
+    u64* t = src;
+    src = dst;
+    dst = t;
+  }
+  if (src != a.s) cudaMemcpyAsync(a.s, src, K * sizeof(u64), cudaMemcpyDeviceToDevice, st);
+  // the {0,1,2} scan over K limbs: n' + 2 = K with the sums already in s
+  a.n = K - 2;
+  a.tail = 1;
+  const unsigned nchunks = unsigned((K + CH - 1) / CH);
+  launch_pdl(k_carry_split<NT, PER, true>, dim3(nchunks), dim3(NT), 0, st, a);
+  launch_pdl(k_carry_scan<CH>, dim3(1), dim3(1024), 0, st, a, nchunks);
+  launch_pdl(k_carry_emit<NT, PER, false>, dim3(nchunks), dim3(NT), 0, st, a);
+  prof_mark("k_carry_general_scan_emit", st, 0, double(K) * 16);
+  return launched + 3;
+}
 
 template <int PERL>
 static int launch_carry_large(const CarryArgs& a, unsigned long long K, cudaStream_t st) {
   constexpr int CHL = NT * PERL;
   const unsigned nchunks = unsigned((K + CHL - 1) / CHL);
+  const double n = double(a.n), k = double(K);
   launch_pdl(k_carry_split<NT, PERL>, dim3(nchunks), dim3(NT), 0, st, a);
+  prof_mark("k_carry_split", st, n, 16 * n + 8 * k);
   launch_pdl(k_carry_scan<CHL>, dim3(1), dim3(1024), 0, st, a, nchunks);
+  prof_mark("k_carry_scan", st, 0, 8.0 * nchunks);
   launch_pdl(k_carry_emit<NT, PERL, false>, dim3(nchunks), dim3(NT), 0, st, a);
+  prof_mark("k_carry_emit", st, 0, 8 * k + k * a.base_exp);
   return 3;
 }
 
@@ -335,8 +408,11 @@ int launch_carry(const CarryArgs& a, cudaStream_t st) {
   const unsigned nchunks = unsigned((K + CH - 1) / CH);
   if (nchunks < 2 * 148) {  // small product: 512-limb chunks, no separate scan
     const unsigned ns = unsigned((K + kCarryChunkSmall - 1) / kCarryChunkSmall);
+    const double n = double(a.n), k = double(K);
     launch_pdl(k_carry_split<NT_SMALL, PER_SMALL>, dim3(ns), dim3(NT_SMALL), 0, st, a);
+    prof_mark("k_carry_split_small", st, n, 16 * n + 8 * k);
     launch_pdl(k_carry_emit<NT_SMALL, PER_SMALL, true>, dim3(ns), dim3(NT_SMALL), 0, st, a);
+    prof_mark("k_carry_emit_small", st, 0, 8 * k + k * a.base_exp);
     return 2;
   }
   // large products are throughput-bound: 8 limbs per thread (4 and 2 measured 0.7-4% slower)

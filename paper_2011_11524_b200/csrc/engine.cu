@@ -104,12 +104,17 @@ Engine::Engine(int device) : device_(device) {
     cuda_check(cudaEventCreateWithFlags(&done_ev_[i], cudaEventDisableTiming), "cudaEventCreate");
   }
   err_.ensure(1);
+  async_err_.ensure(1);
   meta_.ensure(4);
   cuda_check(cudaMemsetAsync(err_.ptr, 0, sizeof(unsigned), stream_), "memset");
+  cuda_check(cudaMemsetAsync(async_err_.ptr, 0, sizeof(unsigned), stream_), "memset");
+  cuda_check(cudaStreamSynchronize(stream_), "init");
 }
 
 Engine::~Engine() {
+  cudaSetDevice(device_);
   cudaStreamSynchronize(stream_);
+  for (auto& r : prof_) cudaEventDestroy(r.ev);
   for (auto s : pipe_) cudaStreamSynchronize(s);
   plans_.clear();
   for (auto s : pipe_) cudaStreamDestroy(s);
@@ -353,6 +358,7 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
       a.sb = L.sb;
       a.off = L.off;
       launch_radix3(false, a, np, st);
+      prof_mark("k_radix3_fwd", st, double(np) * 3.0 * double(L.S), double(np) * 48.0 * double(L.S));
     } else {
       PassArgs a{};
       const PassPlan& P = *pl[0]->passes[i];
@@ -372,6 +378,12 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
       a.tw_logS = L.tw_logS;
       a.tw_off = L.tw_off;
       launch_pass_fwd(P.logR, a, L.ncols, np, st);
+      if (prof_on_) {
+        char nm[64];
+        std::snprintf(nm, sizeof nm, "k_pass_fwd<%d,%s>", P.logR, L.S > 1 ? "rows" : "cols");
+        const double n = double(L.ncols) * P.R;
+        prof_mark(nm, st, np * (n / 2 * P.logR + (L.S > 1 ? n : 0)), np * 16 * n);
+      }
     }
     ++launches_;
   }
@@ -403,6 +415,12 @@ void Engine::pass_fused(const PrimePlan* pl[2], int np, u64* const data[2], cons
   a.tw_logS = 0;
   a.has_final_scale = any_table ? 0 : 1;
   launch_pass_fused(P.logR, a, L.ncols, np, st);
+  if (prof_on_) {
+    char nm[64];
+    std::snprintf(nm, sizeof nm, "k_pass_fused<%d>", P.logR);
+    const double n = double(L.ncols) * P.R;
+    prof_mark(nm, st, np * (n * P.logR + n + (a.has_final_scale ? n : 0)), np * (other ? 24 : 16) * n);
+  }
   ++launches_;
 }
 
@@ -429,6 +447,7 @@ void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std:
       a.sb = L.sb;
       a.off = L.off;
       launch_radix3(true, a, np, st);
+      prof_mark("k_radix3_inv", st, double(np) * 4.0 * double(L.S), double(np) * 48.0 * double(L.S));
     } else {
       PassArgs a{};
       const PassPlan& P = *pl[0]->passes[ii];
@@ -450,6 +469,12 @@ void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std:
       a.tw_off = L.tw_off;
       a.has_final_scale = (!any_table && ii == 0) ? 1 : 0;
       launch_pass_inv(P.logR, a, L.ncols, np, st);
+      if (prof_on_) {
+        char nm[64];
+        std::snprintf(nm, sizeof nm, "k_pass_inv<%d,%s>", P.logR, L.S > 1 ? "rows" : "cols");
+        const double n = double(L.ncols) * P.R;
+        prof_mark(nm, st, np * (n / 2 * P.logR + (L.S > 1 ? n : 0) + (a.has_final_scale ? n : 0)), np * 16 * n);
+      }
     }
     ++launches_;
   }
@@ -492,11 +517,17 @@ void Engine::transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2
   passes_inv(pl, np, data, 0, skip_last ? (m ? m - 1 : 0) : m, nullptr, st);
 }
 
-void Engine::check_err(cudaStream_t st) {
+void Engine::check_err(cudaStream_t st) { check_word(err_.ptr, st); }
+void Engine::check_async_errors(cudaStream_t st) { check_word(async_err_.ptr, st ? st : stream_); }
+
+void Engine::check_word(unsigned* word, cudaStream_t st) {
   unsigned e = 0;
-  cuda_check(cudaMemcpyAsync(&e, err_.ptr, sizeof e, cudaMemcpyDeviceToHost, st), "err readback");
+  cuda_check(cudaMemcpyAsync(&e, word, sizeof e, cudaMemcpyDeviceToHost, st), "err readback");
   cuda_check(cudaStreamSynchronize(st), "sync");
-  if (e) cuda_check(cudaMemsetAsync(err_.ptr, 0, sizeof(unsigned), st), "memset");
+  if (e) {
+    cuda_check(cudaMemsetAsync(word, 0, sizeof(unsigned), st), "memset");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+  }
   if (e & kErrBadDigit) throw std::invalid_argument("decimal: non-digit character");
   if (e & kErrLeadingZero) throw std::invalid_argument("decimal: leading zero");
   if (e & kErrCoeffBound)
@@ -521,8 +552,55 @@ void coeff_cap(unsigned be, std::size_t min_limbs, u64& lo, u64& hi) {
 
 }  // namespace
 
+const unsigned long long kOneLen = 1;  // product length of the zero short-circuit
+
+// Algorithmic modular multiplications of one product: T(2^k) = (N/2) k (+ N for
+// a six-step twiddle when N > 2^15), T(3c) = 8c + 3 T(c); M = 2 (3 T(N) + N) + N, squaring
+// 2 (2 T(N) + N) + N.
+static double alg_modmuls(std::size_t N, bool squaring) {
+  std::function<double(std::size_t)> T = [&](std::size_t m) -> double {
+    if (m % 3 == 0) return 8.0 * double(m / 3) + 3.0 * T(m / 3);
+    const int k = m > 1 ? __builtin_ctzll(m) : 0;
+    return double(m / 2) * k + (m > (std::size_t(1) << 15) ? double(m) : 0.0);
+  };
+  return 2.0 * ((squaring ? 2.0 : 3.0) * T(N) + double(N)) + double(N);
+}
+
+// Whether every coefficient c <= (B - 1)^2 min_limbs is < B^3, so three base-B digits and
+// {0,1,2} carries suffice (always for lambda >= 13: c < p1 p2 < 2^127 < 10^39).
+static bool carry3_exact(unsigned be, std::size_t min_limbs) {
+  if (be >= 13) return true;
+  const u128 B = pow10u(be), top = B - 1;
+  return top * top * (u128)min_limbs < B * B * B;
+}
+
+int Engine::recover(CarryArgs c, unsigned be, std::size_t min_limbs, bool allow_s_in_x, cudaStream_t st) {
+  (void)allow_s_in_x;
+  if (carry3_exact(be, min_limbs)) return launch_carry(c, st);
+  // D = base-B digits of the coefficient cap; normalisation rounds until every sum <= 3 (B - 1)
+  const u128 B = pow10u(be), cap = ((u128)c.coeff_cap_hi << 64) | c.coeff_cap_lo;
+  int D = 1;
+  for (u128 pw = B; pw <= cap; ++D) {
+    if (pw > ~(u128)0 / B) {
+      ++D;
+      break;
+    }
+    pw *= B;
+  }
+  int rounds = 0;
+  for (u128 bound = (u128)D * (B - 1); bound > 3 * (B - 1); ++rounds) bound = (B - 1) + bound / B;
+  const std::size_t K = c.n + std::size_t(D) + std::size_t(rounds);
+  const std::size_t s_words = (K + kCarryChunk - 1) / kCarryChunk * kCarryChunk;
+  S_.ensure(s_words);
+  S2_.ensure(s_words);
+  maps_.ensure(carry_map_words(K));
+  c.s = S_.ptr;
+  c.maps = maps_.ptr;
+  return launch_carry_general(c, D, rounds, S2_.ptr, K, st);
+}
+
 void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, bool squaring, char* dout,
-                         cudaStream_t st, const std::function<void()>& before_y) {
+                         cudaStream_t st, unsigned* err, const std::function<void()>& before_y) {
   const PrimePlan& P1 = prime_plan(pp.p1, pp.N);
   const PrimePlan& P2 = prime_plan(pp.p2, pp.N);
   const unsigned be = pp.base_exp;
@@ -531,9 +609,12 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   const DivB div = div_for(pow10u(be));
   u64 cap_lo, cap_hi;
   coeff_cap(be, std::min(lx, ly), cap_lo, cap_hi);
+  const bool carry3 = carry3_exact(be, std::min(lx, ly));
   launches_ = 0;
+  ProfScope prof_scope(this);
+  prof_mark(nullptr, st);
 
-  if (P1.small_ok && P2.small_ok) {
+  if (P1.small_ok && P2.small_ok && carry3) {
     if (before_y) before_y();
     SmallArgs a{};
     a.xs = dx;
@@ -566,10 +647,11 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
     a.div = div;
     a.coeff_cap_lo = cap_lo;
     a.coeff_cap_hi = cap_hi;
-    a.err = err_.ptr;
+    a.err = err;
     a.squaring = squaring ? 1 : 0;
     if (!launch_small(a, st)) throw CudaError("small kernel launch failed");
     cuda_check(cudaGetLastError(), "small kernel");
+    prof_mark("k_small", st, alg_modmuls(pp.N, squaring), double(2 * (pp.dx + pp.dy)));
     cuda_check(cudaMemcpyAsync(meta_.ptr + 2, lens_.ptr, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st),
                "meta");
     launches_ = 1;
@@ -587,7 +669,7 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   const std::size_t s_words = nchunks * kCarryChunk;
   const char* force_lean = std::getenv("DECMUL_FORCE_LEAN");  // test knob: lean plan at any size
   const bool lean = npad * sizeof(u64) >= (std::size_t(2) << 30) || (force_lean && force_lean[0] == '1');
-  const bool s_in_x = lean && !squaring;
+  const bool s_in_x = lean && !squaring && carry3;
   X_[0].ensure(s_in_x ? std::max(npad, s_words) : npad);
   X_[1].ensure(npad);
   if (!squaring) {
@@ -604,7 +686,8 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   u64* px = lean ? X_[1].ptr : Px_.ptr;
   u64* py = lean ? Y_[1].ptr : Py_.ptr;
 
-  launch_pack(dx, pp.dx, be, px, npad, err_.ptr, st);
+  launch_pack(dx, pp.dx, be, px, npad, err, st);
+  prof_mark("k_pack", st, 0, double(pp.dx) + 8.0 * npad);
   ++launches_;
   const PrimePlan* pl[2] = {&P1, &P2};
   auto forward = [&](const u64* packed, u64* const dst[2], bool include_last) {
@@ -623,6 +706,7 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
       transform_fused_last(pl, 2, X, nullptr, st);
     } else {
       for (int q = 0; q < 2; ++q) launch_pointwise(X[q], X[q], pp.N, pl[q]->p, pl[q]->pp, st);
+      prof_mark("k_pointwise", st, 2.0 * pp.N, 32.0 * pp.N);
       launches_ += 2;
     }
     transform_inverse(pl, 2, X, P1.last_pow2, st);
@@ -633,7 +717,8 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
     u64* Y[2] = {Y_[0].ptr, Y_[1].ptr};
     forward(px, X, true);
     if (before_y) before_y();
-    launch_pack(dy, pp.dy, be, py, npad, err_.ptr, st);
+    launch_pack(dy, pp.dy, be, py, npad, err, st);
+    prof_mark("k_pack", st, 0, double(pp.dy) + 8.0 * npad);
     ++launches_;
     forward(py, Y, !P1.last_pow2);
     if (P1.last_pow2) {
@@ -641,6 +726,7 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
       transform_fused_last(pl, 2, Y, oth, st);
     } else {
       for (int q = 0; q < 2; ++q) launch_pointwise(Y[q], X[q], pp.N, pl[q]->p, pl[q]->pp, st);
+      prof_mark("k_pointwise", st, 2.0 * pp.N, 48.0 * pp.N);
       launches_ += 2;
     }
     transform_inverse(pl, 2, Y, P1.last_pow2, st);
@@ -667,14 +753,14 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   c.base_exp = be;
   c.s = s_buf;
   c.maps = maps_.ptr;
-  c.err = err_.ptr;
+  c.err = err;
   const unsigned long long dsum = pp.dx + pp.dy;
   c.top_candidates[0] = dsum >= 2 ? (dsum - 2) / be : 0;
   c.top_candidates[1] = (dsum - 1) / be;
   c.meta = meta_.ptr;
   c.out = dout;
   c.tail = 1;
-  launches_ += launch_carry(c, st);
+  launches_ += recover(c, be, std::min(lx, ly), s_in_x, st);
   cuda_check(cudaGetLastError(), "product kernels");
 }
 
@@ -683,19 +769,24 @@ std::size_t Engine::multiply_device(const char* dx, std::size_t nx, const char* 
   if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
   if (!st) st = stream_;
   if (nx == 1 || ny == 1) {  // zero short-circuit (decimal.cpp:193), before any size checks
+    // both texts are validated first, as DecimalNumber::parse does for the reference's operands
+    launch_validate(dx, nx, err_.ptr, st);
+    if (!squaring) launch_validate(dy, ny, err_.ptr, st);
     char a = 0, b = 0;
-    if (nx == 1) cuda_check(cudaMemcpy(&a, dx, 1, cudaMemcpyDeviceToHost), "zero check");
-    if (ny == 1) cuda_check(cudaMemcpy(&b, dy, 1, cudaMemcpyDeviceToHost), "zero check");
+    if (nx == 1) cuda_check(cudaMemcpyAsync(&a, dx, 1, cudaMemcpyDeviceToHost, st), "zero check");
+    if (ny == 1) cuda_check(cudaMemcpyAsync(&b, dy, 1, cudaMemcpyDeviceToHost, st), "zero check");
+    check_err(st);  // synchronises st: a and b are valid after this
     if (a == '0' || b == '0') {
       if (cap < 1) throw std::length_error("multiply: output buffer too small");
       cuda_check(cudaMemcpyAsync(dout, "0", 1, cudaMemcpyHostToDevice, st), "zero");
-      if (sync) cuda_check(cudaStreamSynchronize(st), "sync");
+      cuda_check(cudaMemcpyAsync(meta_.ptr + 2, &kOneLen, sizeof kOneLen, cudaMemcpyHostToDevice, st), "meta");
+      cuda_check(cudaStreamSynchronize(st), "sync");
       return 1;
     }
   }
   const ProductPlan pp = plan_product(nx, ny, forced);
   if (cap < nx + ny) throw std::length_error("multiply: output buffer too small");
-  run_product(pp, dx, squaring ? dx : dy, squaring, dout, st);
+  run_product(pp, dx, squaring ? dx : dy, squaring, dout, st, sync ? err_.ptr : async_err_.ptr);
   if (!sync) return 0;
   unsigned long long len = 0;
   cuda_check(cudaMemcpyAsync(&len, meta_.ptr + 2, sizeof len, cudaMemcpyDeviceToHost, st), "len");
@@ -706,7 +797,7 @@ std::size_t Engine::multiply_device(const char* dx, std::size_t nx, const char* 
 std::size_t Engine::result_length() {
   unsigned long long len = 0;
   cuda_check(cudaMemcpyAsync(&len, meta_.ptr + 2, sizeof len, cudaMemcpyDeviceToHost, stream_), "len");
-  check_err(stream_);
+  check_word(async_err_.ptr, stream_);
   return std::size_t(len);
 }
 
@@ -732,7 +823,7 @@ std::size_t Engine::multiply_host(const char* x, std::size_t nx, const char* y, 
   stage_h2d(din_x_.ptr, x, nx, cs);
   cuda_check(cudaEventRecord(up_ev_[0], cs), "event");
   cuda_check(cudaStreamWaitEvent(st, up_ev_[0], 0), "wait");
-  run_product(pp, din_x_.ptr, squaring ? din_x_.ptr : din_y_.ptr, squaring, dout_.ptr, st, [&] {
+  run_product(pp, din_x_.ptr, squaring ? din_x_.ptr : din_y_.ptr, squaring, dout_.ptr, st, err_.ptr, [&] {
     if (squaring) return;
     stage_h2d(din_y_.ptr, y, ny, cs);
     cuda_check(cudaEventRecord(up_ev_[1], cs), "event");
@@ -749,7 +840,13 @@ std::size_t Engine::multiply_host(const char* x, std::size_t nx, const char* y, 
 void Engine::multiply_batch_device(std::size_t count, const char* dxs, std::size_t x_stride, std::size_t nx,
                                    const char* dys, std::size_t y_stride, std::size_t ny, char* douts,
                                    std::size_t out_stride, unsigned long long* dlens, cudaStream_t st) {
-  if (!st) st = stream_;
+  batch_device(count, dxs, x_stride, nx, dys, y_stride, ny, douts, out_stride, dlens, st ? st : stream_,
+               async_err_.ptr);
+}
+
+void Engine::batch_device(std::size_t count, const char* dxs, std::size_t x_stride, std::size_t nx, const char* dys,
+                          std::size_t y_stride, std::size_t ny, char* douts, std::size_t out_stride,
+                          unsigned long long* dlens, cudaStream_t st, unsigned* err) {
   if (count == 0) return;
   if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
   if (out_stride < nx + ny) throw std::length_error("multiply_batch: output stride too small");
@@ -759,7 +856,7 @@ void Engine::multiply_batch_device(std::size_t count, const char* dxs, std::size
   if (!(P1.small_ok && P2.small_ok)) {
     // large products: one after another through the pass engine
     for (std::size_t i = 0; i < count; ++i) {
-      run_product(pp, dxs + i * x_stride, dys + i * y_stride, false, douts + i * out_stride, st);
+      run_product(pp, dxs + i * x_stride, dys + i * y_stride, false, douts + i * out_stride, st, err);
       cuda_check(cudaMemcpyAsync(dlens + i, meta_.ptr + 2, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st),
                  "len");
     }
@@ -797,8 +894,10 @@ void Engine::multiply_batch_device(std::size_t count, const char* dxs, std::size
   a.r_tilde = cc.r_tilde;
   a.div = div_for(pow10u(be));
   coeff_cap(be, std::min(lx, ly), a.coeff_cap_lo, a.coeff_cap_hi);
-  a.err = err_.ptr;
+  a.err = err;
   a.squaring = 0;
+  ProfScope prof_scope(this);
+  prof_mark(nullptr, st);
   const std::size_t maxgrid = 1u << 30;
   for (std::size_t off = 0; off < count; off += maxgrid) {
     SmallArgs b = a;
@@ -811,6 +910,7 @@ void Engine::multiply_batch_device(std::size_t count, const char* dxs, std::size
   }
   launches_ = 1;
   cuda_check(cudaGetLastError(), "batch kernel");
+  prof_mark("k_small", st, double(count) * alg_modmuls(pp.N, false), double(count) * 2.0 * double(nx + ny));
 }
 
 void Engine::multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
@@ -831,8 +931,8 @@ void Engine::multiply_batch_host(std::size_t count, const char* xs, std::size_t 
   lens_.ensure(count);
   cuda_check(cudaMemcpyAsync(din_x_.ptr, xs, xb, cudaMemcpyHostToDevice, stream_), "h2d");
   cuda_check(cudaMemcpyAsync(din_y_.ptr, ys, yb, cudaMemcpyHostToDevice, stream_), "h2d");
-  multiply_batch_device(count, din_x_.ptr, x_stride, nx, din_y_.ptr, y_stride, ny, dout_.ptr, out_stride,
-                        lens_.ptr, stream_);
+  batch_device(count, din_x_.ptr, x_stride, nx, din_y_.ptr, y_stride, ny, dout_.ptr, out_stride, lens_.ptr,
+               stream_, err_.ptr);
   std::vector<unsigned long long> l(count);
   cuda_check(cudaMemcpyAsync(l.data(), lens_.ptr, count * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_),
              "d2h");
@@ -903,8 +1003,8 @@ void Engine::batch_host_pipelined(std::size_t count, const char* xs, std::size_t
     mark(up);
     cuda_check(cudaEventRecord(up_ev_[c], up), "event");
     cuda_check(cudaStreamWaitEvent(comp, up_ev_[c], 0), "wait");
-    multiply_batch_device(n, din_x_.ptr + c0 * x_stride, x_stride, nx, din_y_.ptr + c0 * y_stride, y_stride, ny,
-                          dout_.ptr + c0 * out_stride, out_stride, lens_.ptr + c0, comp);
+    batch_device(n, din_x_.ptr + c0 * x_stride, x_stride, nx, din_y_.ptr + c0 * y_stride, y_stride, ny,
+                 dout_.ptr + c0 * out_stride, out_stride, lens_.ptr + c0, comp, err_.ptr);
     launched += launches_;
     mark(comp);
     cuda_check(cudaEventRecord(done_ev_[c], comp), "event");
@@ -1092,7 +1192,7 @@ std::size_t Engine::pack(const char* digits, std::size_t nd, unsigned be, u64* l
 
 std::size_t Engine::recover_decimal(const u64* r1, const u64* r2, std::size_t n, u64 p1, u64 p2, unsigned be,
                                     std::size_t min_limbs, std::size_t dsum, char* out, std::size_t cap) {
-  if (be < 14 || be > 17) throw std::invalid_argument("recover_digits: base out of range");
+  if (be < 1 || be > 17) throw std::invalid_argument("recover_digits: base out of range");
   if (min_limbs < 1) throw std::invalid_argument("recover_digits: min_limbs must be >= 1");
   const CrtConsts cc = crt_consts(p1, p2);
   X_[0].ensure(n);
@@ -1123,7 +1223,7 @@ std::size_t Engine::recover_decimal(const u64* r1, const u64* r2, std::size_t n,
   c.meta = meta_.ptr;
   c.out = dout_.ptr;
   c.tail = 1;
-  launch_carry(c, st);
+  recover(c, be, min_limbs, false, st);
   cuda_check(cudaGetLastError(), "carry");
   unsigned long long len = 0;
   cuda_check(cudaMemcpyAsync(&len, meta_.ptr + 2, sizeof len, cudaMemcpyDeviceToHost, st), "len");
@@ -1158,6 +1258,53 @@ void Engine::transpose(int kind, u64* a, std::size_t n, std::size_t stride) {
   cuda_check(cudaGetLastError(), "transpose");
   cuda_check(cudaMemcpyAsync(a, X_[0].ptr, total * 8, cudaMemcpyDeviceToHost, st), "d2h");
   cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+// ---------------- per-launch profiling ----------------
+
+namespace {
+thread_local Engine* g_prof_engine = nullptr;
+}
+
+ProfScope::ProfScope(Engine* e) : prev(g_prof_engine) { g_prof_engine = e; }
+ProfScope::~ProfScope() { g_prof_engine = prev; }
+
+void prof_mark(const char* name, cudaStream_t st, double modmuls, double bytes) {
+  if (g_prof_engine) g_prof_engine->prof_record(name, st, modmuls, bytes);
+}
+
+void Engine::prof_record(const char* name, cudaStream_t st, double modmuls, double bytes) {
+  if (!prof_on_) return;
+  cudaEvent_t e;
+  cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+  cuda_check(cudaEventRecord(e, st), "cudaEventRecord");
+  prof_.push_back({name ? std::string(name) : std::string(), modmuls, bytes, e});
+}
+
+void Engine::profile_enable(bool on) {
+  cuda_check(cudaDeviceSynchronize(), "sync");
+  for (auto& r : prof_) cudaEventDestroy(r.ev);
+  prof_.clear();
+  prof_on_ = on;
+}
+
+std::string Engine::profile_report(bool clear) {
+  cuda_check(cudaDeviceSynchronize(), "sync");
+  std::string out;
+  char line[256];
+  for (std::size_t i = 0; i < prof_.size(); ++i) {
+    if (prof_[i].name.empty() || i == 0) continue;  // product-start marks
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, prof_[i - 1].ev, prof_[i].ev), "cudaEventElapsedTime");
+    std::snprintf(line, sizeof line, "%s\t%.6f\t%.6g\t%.6g\n", prof_[i].name.c_str(), double(ms), prof_[i].modmuls,
+                  prof_[i].bytes);
+    out += line;
+  }
+  if (clear) {
+    for (auto& r : prof_) cudaEventDestroy(r.ev);
+    prof_.clear();
+  }
+  return out;
 }
 
 }  // namespace dmg

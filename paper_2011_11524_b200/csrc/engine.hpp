@@ -228,6 +228,16 @@ class Engine {
   // Launch count of the last product (for the bench's gpu_launches claim).
   int last_launches() const { return launches_; }
 
+  // Per-launch profiling (decmul_gpu_profile_*): while on, every kernel this engine enqueues
+  // is followed by a CUDA event; report() syncs and returns "name<TAB>ms<TAB>modmuls<TAB>bytes"
+  // lines (one per launch, ms since the previous mark); clear drops the records.
+  void profile_enable(bool on);
+  std::string profile_report(bool clear);
+  void prof_record(const char* name, cudaStream_t st, double modmuls, double bytes);
+  // Stream-ordered error word of the asynchronous entry points (multiply_device without sync,
+  // multiply_batch_device): read and cleared by check_async_errors / result_length.
+  void check_async_errors(cudaStream_t st);
+
  private:
   void build_passes(PrimePlan& pl);
   void build_small_tables(PrimePlan& pl);
@@ -235,7 +245,11 @@ class Engine {
   // enqueued and before anything reads dy: the host path uploads y there, so the
   // upload overlaps x's transform.
   void run_product(const ProductPlan& pp, const char* dx, const char* dy, bool squaring, char* dout,
-                   cudaStream_t st, const std::function<void()>& before_y = nullptr);
+                   cudaStream_t st, unsigned* err, const std::function<void()>& before_y = nullptr);
+  // multiply_batch_device with an explicit error word (err_ for the synchronous host paths)
+  void batch_device(std::size_t count, const char* dxs, std::size_t x_stride, std::size_t nx, const char* dys,
+                    std::size_t y_stride, std::size_t ny, char* douts, std::size_t out_stride,
+                    unsigned long long* dlens, cudaStream_t st, unsigned* err);
   // Host <-> device copies for the host-buffer API: pinned or small buffers go straight
   // to DMA; large pageable ones are pipelined through a pinned ring (CopyPool threads
   // fill/drain slot c while the DMA engine moves slot c - 1). stage_h2d returns once the
@@ -259,6 +273,10 @@ class Engine {
                   const ShardGeom* sg, cudaStream_t st);
   CarryArgs carry_args(const ProductPlan& pp, const u64* z1, const u64* z2, std::size_t n, char* out) const;
   void check_err(cudaStream_t st);
+  void check_word(unsigned* word, cudaStream_t st);
+  // decimal recovery of a product's coefficients: the 3-digit {0,1,2}-carry pipeline when every
+  // coefficient is < B^3, else the general small-base path (forced lambda < 14)
+  int recover(CarryArgs c, unsigned be, std::size_t min_limbs, bool allow_s_in_x, cudaStream_t st);
 
   // H2D / compute / D2H pipeline of multiply_batch_host (one-CTA products)
   void batch_host_pipelined(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx, const char* ys,
@@ -281,11 +299,25 @@ class Engine {
   std::unique_ptr<CopyPool> copy_pool_;
   std::mutex mu_;
   std::map<std::pair<u64, std::size_t>, std::unique_ptr<PrimePlan>> plans_;
-  DevBuf<u64> X_[2], Y_[2], Px_, Py_, S_;
-  DevBuf<unsigned> maps_, err_;
+  DevBuf<u64> X_[2], Y_[2], Px_, Py_, S_, S2_;
+  DevBuf<unsigned> maps_, err_, async_err_;
   DevBuf<unsigned long long> meta_, lens_;
   DevBuf<char> din_x_, din_y_, dout_;
   int launches_ = 0;
+  struct ProfRec {
+    std::string name;
+    double modmuls, bytes;
+    cudaEvent_t ev;
+  };
+  bool prof_on_ = false;
+  std::vector<ProfRec> prof_;
+};
+
+// The engine whose launches the calling thread is currently enqueueing (prof_mark target).
+struct ProfScope {
+  explicit ProfScope(Engine* e);
+  ~ProfScope();
+  Engine* prev;
 };
 
 }  // namespace dmg

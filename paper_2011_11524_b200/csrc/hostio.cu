@@ -29,7 +29,8 @@ void CopyPool::copy(char* dst, const char* src, std::size_t n) {
     std::memcpy(dst, src, n);
     return;
   }
-  const std::size_t per = (n / parts + 4095) & ~std::size_t(4095);
+  // ceiling quotient, rounded up to 4 KiB: parts * per >= n, so the parts cover every byte
+  const std::size_t per = ((n + parts - 1) / parts + 4095) & ~std::size_t(4095);
   {
     std::lock_guard<std::mutex> lk(mu_);
     dst_ = dst;

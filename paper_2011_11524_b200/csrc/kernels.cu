@@ -597,6 +597,15 @@ __global__ void k_gather(const u64* src, u64* dst, const unsigned long long* map
     dst[i] = src[map[i]];
 }
 
+__global__ void k_validate(const char* __restrict__ d, unsigned long long n, unsigned* err) {
+  unsigned bad = 0;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    bad |= unsigned((unsigned char)d[i] - '0') > 9u;
+  if (bad) atomicOr(err, kErrBadDigit);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n > 1 && d[0] == '0') atomicOr(err, kErrLeadingZero);
+}
+
 int grid_for(unsigned long long n, int threads) {
   unsigned long long b = (n + threads - 1) / threads;
   const unsigned long long cap = 148ull * 16;
@@ -751,6 +760,9 @@ void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, un
   const unsigned long long ntiles = peers * rows * (nvec / tile);
   k_block_reorder<<<unsigned(ntiles < 148ull * 16 ? ntiles : 148ull * 16), 256, 0, st>>>(src, dst, peers, rows, width,
                                                                                           to_segments ? 1 : 0);
+}
+void launch_validate(const char* d, unsigned long long n, unsigned* err, cudaStream_t st) {
+  k_validate<<<grid_for(n, 256), 256, 0, st>>>(d, n, err);
 }
 void launch_pointwise(u64* a, const u64* b, unsigned long long n, u64 p, u64 pp, cudaStream_t st) {
   k_pointwise<<<grid_for(n, 256), 256, 0, st>>>(a, b, n, p, pp);

@@ -40,6 +40,12 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// Per-launch profiling (decmul_gpu_profile_*): when the calling thread's engine has profiling
+// on, records a CUDA event on st after the kernel just enqueued, tagged with its name and its
+// algorithmic work (modular multiplications, HBM bytes); name == nullptr marks the start of
+// a product. No-op otherwise.
+void prof_mark(const char* name, cudaStream_t st, double modmuls = 0, double bytes = 0);
+
 // Error bits raised by kernels (device flag, read by the host after a product).
 enum : unsigned {
   kErrBadDigit = 1u,
@@ -108,6 +114,9 @@ void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, un
 void launch_pointwise(u64* a, const u64* b, unsigned long long n, u64 p, u64 pp, cudaStream_t st);
 void launch_mont_scale(u64* a, unsigned long long n, u64 factor, u64 p, u64 pp, cudaStream_t st);
 void launch_gather(const u64* src, u64* dst, const unsigned long long* map, unsigned long long n, cudaStream_t st);
+// DecimalNumber::parse checks on device digits (decimal.cpp:29-36): non-digit bytes and a
+// leading zero raise kErrBadDigit / kErrLeadingZero in *err.
+void launch_validate(const char* d, unsigned long long n, unsigned* err, cudaStream_t st);
 
 // Carry pipeline (decimal recovery).
 struct CarryArgs {
@@ -136,6 +145,12 @@ constexpr int kCarryChunkSmall = 512;   // small products: 4x the CTAs
 inline std::size_t carry_map_words(std::size_t K) { return (K + kCarryChunkSmall - 1) / kCarryChunkSmall; }
 // Returns the number of kernels launched.
 int launch_carry(const CarryArgs& a, cudaStream_t st);
+// General recovery for small forced bases (lambda < 14, where a coefficient can need more than
+// three base-B digits): every coefficient's D base-B digits are added into the limb sums
+// s[i + j] (s zeroed first), then `rounds` normalisation passes t_k = s_k mod B + s_{k-1} / B
+// (ping-pong through tmp, result back in a.s) bring every sum to <= 3 (B - 1), so the {0,1,2}
+// carry scan of launch_carry applies to the K = n + D + rounds limbs. Returns kernels launched.
+int launch_carry_general(const CarryArgs& a, int D, int rounds, u64* tmp, unsigned long long K, cudaStream_t st);
 // Sharded carry: split + per-chunk exclusive prefix maps; *rank_map_dev gets the rank's composed map.
 void launch_carry_shard_begin(const CarryArgs& a, unsigned* rank_map_dev, cudaStream_t st);
 // z at the global limbs `cand` owned by this rank (others UINT64_MAX), given the carry into the rank.

@@ -34,3 +34,20 @@ def gen_digits(seed: int, n: int, mode: int = 0, chunk: int = 1 << 24) -> bytes:
                 d[0] = np.uint8(1 + int(v[0] % np.uint64(9)))
             out[a: a + len(i)] = d + 48
     return out.tobytes()
+
+
+def gen_digits_range(seed: int, n: int, start: int, stop: int, mode: int = 0) -> bytes:
+    """Digits [start, stop) of the n-digit operand gen_digits(seed, n, mode) (counter-based:
+    a slice costs only its own length)."""
+    if not 0 <= start <= stop <= n:
+        raise ValueError("gen_digits_range: bad range")
+    if mode == 1:
+        return b"9" * (stop - start)
+    with np.errstate(over="ignore"):
+        key = _mix(np.array([seed], dtype=np.uint64) + _G)[0]
+        i = np.arange(start, stop, dtype=np.uint64)
+        v = _mix(key + (i + np.uint64(1)) * _G)
+        d = (v % np.uint64(10)).astype(np.uint8)
+        if start == 0 and stop > 0:
+            d[0] = np.uint8(1 + int(v[0] % np.uint64(9)))
+    return (d + 48).tobytes()

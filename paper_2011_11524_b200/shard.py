@@ -1,9 +1,10 @@
 """Multi-GPU partitioning of the decimal-multiplication workload.
 
-Batches of independent products (config 2) shard with no data-path collective:
-rank r of a world of G owns products [r * count, (r + 1) * count) of the global
-stream (weak scaling; pair k is seeded (2k, 2k + 1)). The only cross-rank
-traffic is the timing reduction (max over ranks) done by the bench.
+Batches of independent products (config 2) shard with no data-path collective: the
+4096-product batch is split evenly, rank r of a world of G owning products
+[r * count, (r + 1) * count) with count = 4096 / G (strong scaling, as BASELINE config 2
+states; pair k is seeded (2k, 2k + 1)). The only cross-rank traffic is the timing
+reduction (max over ranks) done by the bench (bench.py uses batch_range).
 """
 from __future__ import annotations
 

@@ -1,5 +1,9 @@
-"""TEST INFRASTRUCTURE: exact SHA-256 goldens for BASELINE configs 3, 4 and 5 from the
-compiled reference (oracle/_ref), for tests/test_gpu_large.py.
+"""TEST INFRASTRUCTURE: exact SHA-256 goldens for BASELINE configs 1, 3, 4 and 5 from the
+compiled reference (oracle/_ref), for tests/test_gpu_large.py and bench.py's output check.
+
+* Config 1 (1e6 x 1e6 digits, seeds 0 and 1): the reference's own multiply.
+* Config "3x" (1e8 uniform digits, seed 2, times 1e8 nines): the non-squaring worst case
+  of SURVEY §8(d) cfg3, the reference's own multiply.
 
 * Config 3 (1e8 x 1e8 digits, seeds 0 and 1): the reference's own multiply (N = 2^24 is
   inside its cap).
@@ -76,9 +80,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--threads", type=int, default=9)
     ap.add_argument("--out", default=os.path.join(HERE, "golden_large.json"))
-    ap.add_argument("--configs", default="3,4", help="comma-separated: 3, 4, 5")
+    ap.add_argument("--configs", default="3,4", help="comma-separated: 1, 3, 3x, 4, 5")
     args = ap.parse_args()
-    todo = {int(c) for c in args.configs.split(",")}
+    todo = set(args.configs.split(","))
     port, ref = oracle.port(), oracle.ref()
     res = {}
 
@@ -89,7 +93,21 @@ def main():
     if os.path.exists(args.out):
         with open(args.out) as f:
             res = json.load(f)
-    if 3 in todo:
+    if "1" in todo:
+        x, y = port.gen_digits(0, 10**6), port.gen_digits(1, 10**6)
+        z = ref.multiply(x, y)
+        res["config1"] = dict(seeds=[0, 1], digits=[10**6, 10**6], length=len(z),
+                              sha256=hashlib.sha256(z).hexdigest(), method="reference multiply")
+        print("config 1", res["config1"], flush=True)
+    if "3x" in todo:
+        t = time.time()
+        x, y = port.gen_digits(2, 10**8), b"9" * 10**8
+        z = ref.multiply(x, y)
+        res["config3x"] = dict(seeds=[2, "nines"], digits=[10**8, 10**8], length=len(z),
+                               sha256=hashlib.sha256(z).hexdigest(), method="reference multiply")
+        print("config 3x", res["config3x"], f"{time.time() - t:.0f} s", flush=True)
+        del x, y, z
+    if "3" in todo:
         t = time.time()
         x, y = port.gen_digits(0, 10**8), port.gen_digits(1, 10**8)
         z = ref.multiply(x, y)
@@ -98,7 +116,7 @@ def main():
         print("config 3", res["config3"], f"{time.time() - t:.0f} s", flush=True)
         del x, y, z
     for cfg, (sx, sy, nx, ny) in ((4, (40, 41, 2 * 10**9, 10**9)), (5, (50, 51, 10**10, 10**10))):
-        if cfg not in todo:
+        if str(cfg) not in todo:
             continue
         t = time.time()
         x, y = port.gen_digits(sx, nx), port.gen_digits(sy, ny)

@@ -71,11 +71,25 @@ def test_squaring_paths(gpu, ref):
         assert gpu.multiply_text(s, bytes(s)) == want  # equal text, distinct buffers
 
 
-def test_every_forced_base(gpu, port):
+def test_every_forced_base(gpu, port, ref):
+    """MultiplyOptions::forced_base_exp 1..17 (the reference accepts every base its planner
+    admits, decimal.cpp:78-100). Below lambda = 13 a coefficient can need more than three
+    base-B digits, which takes the general recovery (digit scatter + normalisation rounds)."""
     x, y = inputs.gen_digits(1, 4211), inputs.gen_digits(2, 3999)
     want = port.schoolbook_multiply(x, y)
-    for be in (0, 14, 15, 16, 17):
-        assert gpu.multiply_text(x, y, forced_base_exp=be) == want
+    for be in [0] + list(range(1, 18)):
+        assert gpu.multiply_text(x, y, forced_base_exp=be) == want, be
+    # larger operands through the multi-pass engine, and squaring, at small bases
+    for be in (1, 2, 5, 9, 12, 13):
+        for nx, ny in ((60001, 50000), (200000, 150001)):
+            a, b = inputs.gen_digits(nx + be, nx), inputs.gen_digits(ny + be, ny)
+            assert gpu.multiply_text(a, b, forced_base_exp=be) == ref.multiply(a, b), (be, nx, ny)
+        a = inputs.gen_digits(be, 30000)
+        assert gpu.multiply_text(a, None, forced_base_exp=be) == ref.multiply(a, None), be
+    # worst-case magnitudes: all nines at a small base
+    n9 = b"9" * 20000
+    for be in (1, 3, 7):
+        assert gpu.multiply_text(n9, n9 + b"9", forced_base_exp=be) == ref.multiply(n9, n9 + b"9"), be
 
 
 def test_large_prime_pair_path(gpu, ref):
@@ -199,9 +213,10 @@ def test_pointwise_and_pack_hooks(gpu, port):
 
 def test_recover_decimal_hook(gpu, port):
     """CRT + carry + formatting on the device, from exact convolution residues."""
-    for nx, ny in ((100, 90), (5000, 5000), (40000, 35000)):
+    cases = [(100, 90, 0), (5000, 5000, 0), (40000, 35000, 0), (3000, 2000, 1), (3000, 2000, 6), (40000, 35000, 11)]
+    for nx, ny, forced in cases:
         x, y = inputs.gen_digits(nx, nx), inputs.gen_digits(ny, ny)
-        be, n = port.select_base_and_length(nx, ny)
+        be, n = port.select_base_and_length(nx, ny, forced)
         lx, ly = port.pack(x, be), port.pack(y, be)
         r1 = port.convolve_mod_p(P1, n, lx, ly)
         r2 = port.convolve_mod_p(P2, n, lx, ly)
@@ -277,3 +292,64 @@ def test_batch_mixed_sizes_pointer_arrays(gpu, ref):
     assert gpu.multiply_batch_mixed(xs, ys) == [ref.multiply(a, b) for a, b in zip(xs, ys)]
     with pytest.raises(ValueError, match="non-digit"):
         gpu.multiply_batch_mixed([b"12", b"3x4"], [b"5", b"6"])
+
+
+def test_async_error_word(gpu):
+    """Errors of the asynchronous entry points land in their own stream-ordered word: the
+    device batch reports bad digits at check_errors, and synchronous calls never see them."""
+    import torch
+
+    n, count = 10000, 8
+    xs = torch.full((count * n,), ord("7"), dtype=torch.uint8, device="cuda")
+    ys = torch.full((count * n,), ord("3"), dtype=torch.uint8, device="cuda")
+    xs[5 * n + 17] = ord("x")
+    outs = torch.empty(count * 2 * n, dtype=torch.uint8, device="cuda")
+    lens = torch.zeros(count, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    gpu.multiply_batch_device(count, xs.data_ptr(), n, ys.data_ptr(), n, outs.data_ptr(), 2 * n, lens.data_ptr(),
+                              stream=s)
+    assert gpu.multiply_text(b"12", b"34") == b"408"  # a synchronous call is unaffected
+    with pytest.raises(ValueError, match="non-digit"):
+        gpu.check_errors(s)
+    gpu.check_errors(s)  # cleared
+    xs[5 * n + 17] = ord("7")
+    gpu.multiply_batch_device(count, xs.data_ptr(), n, ys.data_ptr(), n, outs.data_ptr(), 2 * n, lens.data_ptr(),
+                              stream=s)
+    gpu.check_errors(s)
+    want = str(int("7" * n) * int("3" * n)).encode()
+    assert bytes(outs[:int(lens[0])].cpu().numpy()) == want
+
+
+def test_device_zero_short_circuit_validates(gpu):
+    """multiply_device's zero short-circuit reads the digit in stream order and validates
+    both operands as DecimalNumber::parse does (decimal.cpp:29-36, :193)."""
+    import torch
+
+    zero = torch.tensor([ord("0")], dtype=torch.uint8, device="cuda")
+    y = torch.tensor(list(b"12345"), dtype=torch.uint8, device="cuda")
+    out = torch.empty(8, dtype=torch.uint8, device="cuda")
+    assert gpu.multiply_device(zero.data_ptr(), 1, y.data_ptr(), 5, out.data_ptr(), 8) == 1
+    assert int(out[0]) == ord("0")
+    bad = torch.tensor(list(b"12a45"), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError, match="non-digit"):
+        gpu.multiply_device(zero.data_ptr(), 1, bad.data_ptr(), 5, out.data_ptr(), 8)
+    lead = torch.tensor(list(b"012"), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError, match="leading zero"):
+        gpu.multiply_device(lead.data_ptr(), 3, zero.data_ptr(), 1, out.data_ptr(), 8)
+    assert gpu.multiply_text(b"12", b"34") == b"408"
+
+
+def test_profile_report(gpu):
+    """Per-launch profiling (decmul_gpu_profile_*): every kernel of a product appears with its
+    algorithmic work, and the records clear after a report."""
+    x, y = inputs.gen_digits(3, 300000), inputs.gen_digits(4, 200000)
+    gpu.profile(True)
+    gpu.multiply_text(x, y)
+    rep = gpu.profile_report()
+    gpu.profile(False)
+    names = [r[0] for r in rep]
+    assert names[0] == "k_pack" and any(nm.startswith("k_pass_fused") for nm in names)
+    assert any(nm.startswith("k_carry") for nm in names)
+    assert all(ms >= 0 for _, ms, _, _ in rep)
+    assert sum(mm for _, _, mm, _ in rep) > 0
+    assert gpu.profile_report() == []

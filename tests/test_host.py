@@ -197,15 +197,49 @@ def test_two_rank_gloo_sharding(port):
 
 def test_bench_reference_arm_prints_one_json_line():
     """bench.py keeps stdout for exactly one JSON line (libraries' banners go to stderr);
-    the reference arm reports the reference's own refusal beyond its 3*2^24 cap."""
+    beyond the reference's 3*2^24 cap the reference arm times the reference's own multiply
+    on chunk pairs of the config's operands (here with small chunks to stay fast)."""
     import json
     import subprocess
     import sys
 
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "4"],
-                       capture_output=True, text=True, timeout=300)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "4",
+                        "--steps", "1", "--ref-chunk", "200000"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     lines = r.stdout.strip().splitlines()
     assert len(lines) == 1
     d = json.loads(lines[0])
-    assert d["impl"] == "reference" and "unavailable" in d
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "digits/s"
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["config"]["digits_x"] == 2 * 10**9
+
+
+def test_bench_reference_sample_is_the_configs_operands():
+    """The reference arm's chunk products are exact chunks of the config-4 operands (the
+    composed-reference decomposition, cut from the least significant end)."""
+    import bench
+
+    cfg = dict(bench.CONFIGS[4], nx=10**6, ny=5 * 10**5)
+    xs, ys, cores, sample = bench.reference_sample(cfg, 10**5, 4)
+    x = inputs.gen_digits(40, 10**6)
+    y = inputs.gen_digits(41, 5 * 10**5)
+    assert cores == 4 and len(xs) == 4
+    assert xs[0] == x[-10**5:].lstrip(b"0") and ys[1] == y[-2 * 10**5:-10**5].lstrip(b"0")
+
+
+def test_bench_nines_closed_form():
+    import bench
+
+    n, h = bench.nines_square_sha(5)
+    assert n == 10 and h == hashlib.sha256(str((10**5 - 1) ** 2).encode()).hexdigest()
+
+
+def test_copy_pool_covers_every_byte():
+    """The pageable <-> pinned staging copy split (csrc/hostio.cu CopyPool) over lengths
+    parts * 4096 * k + r, r = 0..4, and 1..4 worker threads (no GPU needed)."""
+    import subprocess
+
+    cpp = os.path.join(ROOT, "tests", "cpp")
+    subprocess.run(["make", "-s", "-C", cpp, "test_copypool"], check=True, capture_output=True)
+    r = subprocess.run([os.path.join(cpp, "test_copypool")], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "failures=0" in r.stdout, r.stdout + r.stderr
