@@ -42,7 +42,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def lib_path() -> str:
-    return os.path.join(HERE, "libdecmul_gpu.so")
+    """The in-tree library; DECMUL_GPU_LIB overrides the path (A/B timing of kernel variants)."""
+    return os.environ.get("DECMUL_GPU_LIB") or os.path.join(HERE, "libdecmul_gpu.so")
 
 
 # every function declared in include/decmul_gpu.h

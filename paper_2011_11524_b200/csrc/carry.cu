@@ -261,6 +261,32 @@ __global__ void __launch_bounds__(NTC) k_carry_emit(CarryArgs a) {
   char* sb = buf + (reinterpret_cast<unsigned long long>(g) & 15);
   // digits: each thread prints PERC consecutive limbs (a contiguous PERC lambda-byte run)
   const unsigned long long* sg = reinterpret_cast<const unsigned long long*>(a.s);
+  if constexpr (PERC == 8) {
+    // fast path: 8 full-width limbs below the top one -> one 8 lambda-byte run built in
+    // registers (SWAR) and stored as 32-bit words
+    const unsigned long long kg0 = a.k_off + cbase + threadIdx.x * PERC;
+    if (kg0 + 7 < top && be >= 14) {
+      u64 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // text order: the highest limb first
+        const int loc = threadIdx.x * PERC + 7 - j;
+        u64 x = sg[cbase + loc] + mp[loc];
+        if (x >= B) x -= B;
+        if (x >= B) x -= B;
+        v[j] = x;
+      }
+      char* dst = sb + (limb_pos(kg0 + 7, top, top_len, be) - start);
+      switch (be) {
+        case 14: print_run8<14>(dst, v); break;
+        case 15: print_run8<15>(dst, v); break;
+        case 16: print_run8<16>(dst, v); break;
+        default: print_run8<17>(dst, v); break;
+      }
+      __syncthreads();
+      cta_store_bytes(g, sb, unsigned(end - start), threadIdx.x, NTC);
+      return;
+    }
+  }
 #pragma unroll
   for (int j = 0; j < PERC; ++j) {
     const int loc = threadIdx.x * PERC + j;
@@ -326,6 +352,156 @@ __global__ void __launch_bounds__(1024) k_carry_probe(CarryArgs a, unsigned rank
 __global__ void k_carry_cin(unsigned* maps, unsigned nchunks, unsigned rank_cin) {
   const unsigned c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < nchunks) maps[c] = map_apply(maps[c], rank_cin);
+}
+
+// ---- inverse radix-3 pass fused with CRT and the digit split (large N = 3 S) ----
+
+// Coefficient k (0 <= k < 3 S) from the last inverse power-of-two pass's output: the inverse
+// radix-3 butterfly of column s = k mod S (reference three_row_inverse_columns,
+// conv.cpp:129-147, as k_radix3_inv computes it) for both primes, output row g = k / S.
+__device__ __forceinline__ void r3inv_load(const Radix3Args& r, unsigned long long s, u64 x[2][3]) {
+#pragma unroll
+  for (int pr = 0; pr < 2; ++pr) {
+#pragma unroll
+    for (int g = 0; g < 3; ++g) x[pr][g] = r.src[pr][g * r.S + s];
+  }
+}
+__device__ __forceinline__ void r3inv_from(const Radix3Args& r, unsigned long long s, const u64 x[2][3],
+                                           u64 out[2][3]) {
+  const unsigned long long L = 1ull << r.lbits, H = r.hrow;
+  const unsigned long long sl = s & (L - 1), sh = s >> r.lbits;
+#pragma unroll
+  for (int pr = 0; pr < 2; ++pr) {
+    const u64 p = r.p[pr];
+    const TwPair* __restrict__ lo = r.lo[pr];
+    const TwPair* __restrict__ hi = r.hi[pr];
+    const u64 y0 = shoup_mul(x[pr][0], hi[sh], p);  // lo[0][.] = 1
+    const u64 y1 = shoup_mul(shoup_mul(x[pr][1], lo[L + sl], p), hi[H + sh], p);
+    const u64 y2 = shoup_mul(shoup_mul(x[pr][2], lo[2 * L + sl], p), hi[2 * H + sh], p);
+    const u64 t = shoup_mul(mod_sub(y1, y2, p), r.lam[pr], p);
+    out[pr][0] = mod_add(mod_add(y0, y1, p), y2, p);
+    out[pr][1] = mod_add(mod_sub(y0, y2, p), t, p);
+    out[pr][2] = mod_sub(mod_sub(y0, y1, p), t, p);
+  }
+}
+__device__ __forceinline__ void r3inv_column(const Radix3Args& r, unsigned long long s, u64 out[2][3]) {
+  u64 x[2][3];
+  r3inv_load(r, s, x);
+  r3inv_from(r, s, x, out);
+}
+
+__device__ __forceinline__ void coeff_split(const CarryArgs& a, u64 r1, u64 r2, bool check, u64& d0, u64& d1,
+                                            u64& d2) {
+  u64 lo, hi;
+  crt2(r1, r2, a.p1, a.p2, a.p2_prime, a.r_tilde, lo, hi);
+  if (check && above_cap(lo, hi, a.coeff_cap_lo, a.coeff_cap_hi)) atomicOr(a.err, kErrCoeffBound);
+  split3(a.div, lo, hi, d0, d1, d2);
+}
+
+// d1, d2 of coefficient k (k < 0: zero)
+__device__ __forceinline__ void coeff_d12(const CarryArgs& a, const Radix3Args& r, long long k, u64& d1, u64& d2) {
+  d1 = d2 = 0;
+  if (k < 0) return;
+  u64 c[2][3];
+  const unsigned long long g = (unsigned long long)k / r.S;
+  r3inv_column(r, (unsigned long long)k - g * r.S, c);
+  u64 d0;
+  coeff_split(a, g == 0 ? c[0][0] : (g == 1 ? c[0][1] : c[0][2]), g == 0 ? c[1][0] : (g == 1 ? c[1][1] : c[1][2]),
+              false, d0, d1, d2);
+}
+
+// CTA b (< S / CH) takes columns [b CH, (b + 1) CH) and produces the limb sums and chunk maps of
+// the three chunks g S / CH + b (g = 0, 1, 2); the coefficient k's own digit d0 meets d1 of
+// k - 1 and d2 of k - 2 through warp shuffles, with the warp edges (and the chunk's two halo
+// coefficients) in shared memory. The last CTA (a.tail) forms the two trailing limbs N, N + 1.
+// Replaces k_radix3_inv + k_carry_split: the natural-order coefficients never touch HBM.
+__global__ void __launch_bounds__(NT) k_carry_split_r3(CarryArgs a, Radix3Args r) {
+  pdl_wait();
+  constexpr int NW = NT / 32;
+  __shared__ u64 e1[3][PER * NW + 1], e2a[3][PER * NW + 1], e2b[3][PER * NW + 1];
+  __shared__ __align__(8) unsigned char mp[3][CH];
+  __shared__ unsigned wsm[NT / 32 + 1];
+  const unsigned long long S = r.S, N = 3 * S;
+  const u64 B = a.div.base;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (blockIdx.x == S / CH) {  // tail chunk N / CH: limbs N, N + 1 (K = N + 2)
+    if (tid == 0) {
+      u64 d1a, d2a, d1b, d2b;
+      coeff_d12(a, r, (long long)N - 1, d1a, d2a);
+      coeff_d12(a, r, (long long)N - 2, d1b, d2b);
+      const u64 sN = d1a + d2b, sN1 = d2a;
+      a.s[N] = sN;
+      a.s[N + 1] = sN1;
+      a.maps[N / CH] = map_compose(limb_map(sN1, B), limb_map(sN, B));
+    }
+    return;
+  }
+  const unsigned long long s0 = (unsigned long long)blockIdx.x * CH;
+  if (tid < 6) {  // halo: coefficients k0 - 1 and k0 - 2 of each group's chunk
+    const int g = tid >> 1, which = tid & 1;
+    u64 d1, d2;
+    coeff_d12(a, r, (long long)(g * S + s0) - 1 - which, d1, d2);
+    if (which == 0) {
+      e1[g][0] = d1;
+      e2b[g][0] = d2;
+    } else {
+      e2a[g][0] = d2;
+    }
+  }
+  // round j + 1's six inputs are loaded while round j computes
+  u64 xin[2][3];
+  r3inv_load(r, s0 + tid, xin);
+#pragma unroll 1
+  for (int j = 0; j < PER; ++j) {
+    const unsigned long long s = s0 + j * NT + tid;
+    u64 c[2][3];
+    {
+      u64 cur[2][3];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) cur[q / 3][q % 3] = xin[q / 3][q % 3];
+      if (j + 1 < PER) r3inv_load(r, s + NT, xin);
+      r3inv_from(r, s, cur, c);
+    }
+    u64 d0[3], d1[3], d2[3];
+#pragma unroll
+    for (int g = 0; g < 3; ++g) {
+      coeff_split(a, c[0][g], c[1][g], true, d0[g], d1[g], d2[g]);
+      if (lane == 31) {
+        e1[g][1 + j * NW + w] = d1[g];
+        e2b[g][1 + j * NW + w] = d2[g];
+      } else if (lane == 30) {
+        e2a[g][1 + j * NW + w] = d2[g];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < 3; ++g) {
+      u64 p1 = __shfl_up_sync(0xffffffffu, d1[g], 1);
+      u64 p2 = __shfl_up_sync(0xffffffffu, d2[g], 2);
+      const int prev = j * NW + w;  // edge slot of the previous warp (0: the halo)
+      if (lane == 0) {
+        p1 = e1[g][prev];
+        p2 = e2a[g][prev];
+      } else if (lane == 1) {
+        p2 = e2b[g][prev];
+      }
+      const u64 sum = d0[g] + p1 + p2;
+      a.s[g * S + s] = sum;
+      mp[g][j * NT + tid] = (unsigned char)limb_map(sum, B);
+    }
+  }
+  __syncthreads();
+  // each group's chunk map: PER consecutive limbs per thread, then a block scan
+#pragma unroll
+  for (int g = 0; g < 3; ++g) {
+    const unsigned long long m8 = reinterpret_cast<const unsigned long long*>(mp[g])[tid];
+    unsigned agg = kIdentityMap;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
+    unsigned total;
+    block_scan_maps<NT>(agg, wsm, &total);
+    if (tid == 0) a.maps[(g * S + s0) / CH] = total;
+  }
 }
 
 // ---- general recovery for small forced bases (lambda < 14) ----
@@ -402,6 +578,21 @@ static int launch_carry_large(const CarryArgs& a, unsigned long long K, cudaStre
   prof_mark("k_carry_emit", st, 0, 8 * k + k * a.base_exp);
   return 3;
 }
+
+int launch_carry_r3(const CarryArgs& a, const Radix3Args& r, cudaStream_t st) {
+  const unsigned long long N = 3 * r.S, K = N + 2;
+  const unsigned nchunks = unsigned((K + CH - 1) / CH);  // S / CH column blocks + the tail chunk
+  const double n = double(N), k = double(K);
+  launch_pdl(k_carry_split_r3, dim3(unsigned(r.S / CH + 1)), dim3(NT), 0, st, a, r);
+  prof_mark("k_carry_split_r3", st, 2.0 * 6.0 * r.S + n, 16 * n + 8 * k);
+  launch_pdl(k_carry_scan<CH>, dim3(1), dim3(1024), 0, st, a, nchunks);
+  prof_mark("k_carry_scan", st, 0, 8.0 * nchunks);
+  launch_pdl(k_carry_emit<NT, PER, false>, dim3(nchunks), dim3(NT), 0, st, a);
+  prof_mark("k_carry_emit", st, 0, 8 * k + k * a.base_exp);
+  return 3;
+}
+
+bool carry_r3_fusable(unsigned long long S) { return S % CH == 0 && (3 * S + 2 + CH - 1) / CH >= 2 * 148; }
 
 int launch_carry(const CarryArgs& a, cudaStream_t st) {
   const unsigned long long K = a.n + (a.tail ? 2 : 0);

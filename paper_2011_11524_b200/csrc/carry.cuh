@@ -119,6 +119,71 @@ __device__ __forceinline__ void write_digits(char* out, u64 v, unsigned len) {
   }
 }
 
+// ---- eight limbs of a fixed width BE (14..17) as one text run, SWAR ----
+// Text bytes are accumulated in registers (all offsets compile-time after unrolling) as
+// 2 BE 32-bit words, then stored at the run's byte offset with funnel shifts: 2 BE word
+// stores plus at most 6 byte stores instead of 8 BE byte stores and per-digit divisions.
+struct TextAcc {
+  u64 acc = 0;  // pending bytes, the first at the lowest byte
+  int n = 0;    // pending byte count (< 4 between pushes)
+  int nw = 0;   // words emitted
+};
+template <int NW>
+__device__ __forceinline__ void text_push(TextAcc& t, unsigned (&W)[NW], unsigned x, int bytes) {
+  t.acc |= (u64)x << (8 * t.n);
+  t.n += bytes;
+  if (t.n >= 4) {
+    W[t.nw++] = unsigned(t.acc);
+    t.acc >>= 32;
+    t.n -= 4;
+  }
+}
+template <int NW>
+__device__ __forceinline__ void text_push8(TextAcc& t, unsigned (&W)[NW], u64 x, int bytes) {  // bytes <= 8
+  if (bytes > 4) {
+    text_push(t, W, unsigned(x), 4);
+    text_push(t, W, unsigned(x >> 32), bytes - 4);
+  } else {
+    text_push(t, W, unsigned(x), bytes);
+  }
+}
+
+template <int BE>
+__device__ __forceinline__ void print_run8(char* dst, const u64 (&v)[8]) {
+  static_assert(BE >= 14 && BE <= 17, "limb width");
+  unsigned W[2 * BE];
+  TextAcc t;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const u64 q = v[j] / 100000000ull;  // the digits above the low 8
+    const unsigned lo8 = unsigned(v[j] - q * 100000000ull);
+    if constexpr (BE == 17) {
+      const unsigned d = unsigned(q / 100000000ull);
+      text_push(t, W, 0x30u + d, 1);
+      text_push8(t, W, ascii8(unsigned(q - (u64)d * 100000000ull)), 8);
+    } else {
+      text_push8(t, W, ascii8(unsigned(q)) >> (8 * (16 - BE)), BE - 8);
+    }
+    text_push8(t, W, ascii8(lo8), 8);
+  }
+  // store the 8 BE bytes at dst (any alignment): aligned words via funnel shifts, the two
+  // partial words (shared with the neighbouring runs) byte by byte
+  const int ph = int(reinterpret_cast<unsigned long long>(dst) & 3);
+  unsigned* aw = reinterpret_cast<unsigned*>(dst - ph);
+  if (ph == 0) {
+#pragma unroll
+    for (int i = 0; i < 2 * BE; ++i) aw[i] = W[i];
+  } else {
+    const int sh = 8 * ph;
+    for (int b = 0; b < 4 - ph; ++b) dst[b] = char(W[0] >> (8 * b));
+#pragma unroll
+    for (int i = 1; i < 2 * BE; ++i) aw[i] = __funnelshift_l(W[i - 1], W[i], sh);
+    const unsigned last = W[2 * BE - 1] >> (32 - sh);
+    char* tail = reinterpret_cast<char*>(aw + 2 * BE);
+    for (int b = 0; b < ph; ++b) tail[b] = char(last >> (8 * b));
+  }
+}
+
 // Copy len bytes from shared s to global g with 16-byte stores in the aligned middle.
 // Requires (g mod 16) == (s mod 16): callers place the staged text at that offset.
 __device__ __forceinline__ void cta_store_bytes(char* g, const char* s, unsigned len, int tid, int nt) {

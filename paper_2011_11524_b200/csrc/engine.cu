@@ -599,6 +599,26 @@ int Engine::recover(CarryArgs c, unsigned be, std::size_t min_limbs, bool allow_
   return launch_carry_general(c, D, rounds, S2_.ptr, K, st);
 }
 
+void Engine::pack_radix3(const PrimePlan* pl[2], const char* digits, std::size_t nd, unsigned be, u64* const dst[2],
+                         unsigned* err, cudaStream_t st) {
+  const PassPlan& P = *pl[0]->passes[0];
+  Radix3Args a{};
+  for (int q = 0; q < 2; ++q) {
+    a.src[q] = nullptr;
+    a.dst[q] = dst[q];
+    a.lo[q] = pl[q]->passes[0]->r3_lo_fwd.ptr;
+    a.hi[q] = pl[q]->passes[0]->r3_hi_fwd.ptr;
+    a.p[q] = pl[q]->p;
+    a.lam[q] = pl[q]->lam;
+  }
+  a.S = P.S;
+  a.lbits = P.r3_lbits;
+  a.hrow = P.S >> a.lbits;
+  launch_pack_radix3(digits, nd, be, a, err, st);
+  ++launches_;
+  prof_mark("k_pack_radix3", st, 2.0 * double(P.S) * 5.0, double(nd) + 48.0 * double(P.S));
+}
+
 void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, bool squaring, char* dout,
                          cudaStream_t st, unsigned* err, const std::function<void()>& before_y) {
   const PrimePlan& P1 = prime_plan(pp.p1, pp.N);
@@ -676,8 +696,10 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
     Y_[0].ensure(npad);
     Y_[1].ensure(npad);
   }
+  // N = 3 S: the pack runs inside the first (radix-3) pass, no packed-limb buffer at all
+  const bool fuse_r3 = !P1.passes.empty() && P1.passes[0]->radix3;
   if (!s_in_x) S_.ensure(s_words);
-  if (!lean) {
+  if (!lean && !fuse_r3) {
     Px_.ensure(npad);
     if (!squaring) Py_.ensure(npad);
   }
@@ -686,11 +708,25 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   u64* px = lean ? X_[1].ptr : Px_.ptr;
   u64* py = lean ? Y_[1].ptr : Py_.ptr;
 
-  launch_pack(dx, pp.dx, be, px, npad, err, st);
-  prof_mark("k_pack", st, 0, double(pp.dx) + 8.0 * npad);
-  ++launches_;
   const PrimePlan* pl[2] = {&P1, &P2};
-  auto forward = [&](const u64* packed, u64* const dst[2], bool include_last) {
+  const std::size_t m = P1.passes.size();
+  // the inverse radix-3 pass runs inside the carry split (no natural-order coefficients in HBM)
+  const bool fuse_r3_carry = fuse_r3 && carry3 && carry_r3_fusable(P1.passes[0]->S);
+  auto inverse = [&](u64* const z[2]) {
+    passes_inv(pl, 2, z, fuse_r3_carry ? 1 : 0, P1.last_pow2 ? m - 1 : m, nullptr, st);
+  };
+  // digits -> forward transform (all passes, or all but the last when it is fused with the
+  // pointwise product)
+  auto load = [&](const char* dd, std::size_t nd, u64* packed, u64* const dst[2], bool include_last) {
+    if (fuse_r3) {
+      pack_radix3(pl, dd, nd, be, dst, err, st);
+      const u64* src[2] = {dst[0], dst[1]};
+      passes_fwd(pl, 2, src, dst, 1, include_last ? m : m - 1, nullptr, st);
+      return;
+    }
+    launch_pack(dd, nd, be, packed, npad, err, st);
+    prof_mark("k_pack", st, 0, double(nd) + 8.0 * npad);
+    ++launches_;
     if (lean) {
       transform_forward_packed(pl, dst, include_last, st);
     } else {
@@ -701,7 +737,7 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   u64* Z[2];
   if (squaring) {
     u64* X[2] = {X_[0].ptr, X_[1].ptr};
-    forward(px, X, !P1.last_pow2);
+    load(dx, pp.dx, px, X, !P1.last_pow2);
     if (P1.last_pow2) {
       transform_fused_last(pl, 2, X, nullptr, st);
     } else {
@@ -709,18 +745,15 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
       prof_mark("k_pointwise", st, 2.0 * pp.N, 32.0 * pp.N);
       launches_ += 2;
     }
-    transform_inverse(pl, 2, X, P1.last_pow2, st);
+    inverse(X);
     Z[0] = X[0];
     Z[1] = X[1];
   } else {
     u64* X[2] = {X_[0].ptr, X_[1].ptr};
     u64* Y[2] = {Y_[0].ptr, Y_[1].ptr};
-    forward(px, X, true);
+    load(dx, pp.dx, px, X, true);
     if (before_y) before_y();
-    launch_pack(dy, pp.dy, be, py, npad, err, st);
-    prof_mark("k_pack", st, 0, double(pp.dy) + 8.0 * npad);
-    ++launches_;
-    forward(py, Y, !P1.last_pow2);
+    load(dy, pp.dy, py, Y, !P1.last_pow2);
     if (P1.last_pow2) {
       const u64* oth[2] = {X[0], X[1]};
       transform_fused_last(pl, 2, Y, oth, st);
@@ -729,7 +762,7 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
       prof_mark("k_pointwise", st, 2.0 * pp.N, 48.0 * pp.N);
       launches_ += 2;
     }
-    transform_inverse(pl, 2, Y, P1.last_pow2, st);
+    inverse(Y);
     Z[0] = Y[0];
     Z[1] = Y[1];
   }
@@ -760,7 +793,24 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   c.meta = meta_.ptr;
   c.out = dout;
   c.tail = 1;
-  launches_ += recover(c, be, std::min(lx, ly), s_in_x, st);
+  if (fuse_r3_carry) {
+    const PassPlan& P0 = *P1.passes[0];
+    Radix3Args r{};
+    for (int q = 0; q < 2; ++q) {
+      r.src[q] = Z[q];
+      r.dst[q] = nullptr;
+      r.lo[q] = pl[q]->passes[0]->r3_lo_inv.ptr;
+      r.hi[q] = pl[q]->passes[0]->r3_hi_inv.ptr;
+      r.p[q] = pl[q]->p;
+      r.lam[q] = pl[q]->lam_inv;
+    }
+    r.S = P0.S;
+    r.lbits = P0.r3_lbits;
+    r.hrow = P0.S >> r.lbits;
+    launches_ += launch_carry_r3(c, r, st);
+  } else {
+    launches_ += recover(c, be, std::min(lx, ly), s_in_x, st);
+  }
   cuda_check(cudaGetLastError(), "product kernels");
 }
 

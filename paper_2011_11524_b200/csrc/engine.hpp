@@ -271,6 +271,9 @@ class Engine {
                   const ShardGeom* sg, cudaStream_t st);
   void passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std::size_t begin, std::size_t end,
                   const ShardGeom* sg, cudaStream_t st);
+  // digits -> the first (radix-3) pass's output of both primes, one fused kernel
+  void pack_radix3(const PrimePlan* pl[2], const char* digits, std::size_t nd, unsigned be, u64* const dst[2],
+                   unsigned* err, cudaStream_t st);
   CarryArgs carry_args(const ProductPlan& pp, const u64* z1, const u64* z2, std::size_t n, char* out) const;
   void check_err(cudaStream_t st);
   void check_word(unsigned* word, cudaStream_t st);

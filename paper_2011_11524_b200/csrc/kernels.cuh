@@ -107,6 +107,10 @@ void launch_gen_pass_table(TwPair* out, u64 root_m, u64 scale, int R, int logR, 
 void launch_pack(const char* digits, unsigned long long nd, unsigned base_exp, u64* limbs,
                  unsigned long long nlimbs_total, unsigned* err, cudaStream_t st, int row_bits = 63,
                  unsigned long long row_stride = 0, unsigned long long off = 0);
+// Pack fused with the forward radix-3 pass (N = 3 S, unsharded): digits -> pass 0's output
+// of both primes (a.dst), lo/hi/lam/p/lbits/hrow as for launch_radix3; a.src unused.
+void launch_pack_radix3(const char* digits, unsigned long long nd, unsigned base_exp, const Radix3Args& a,
+                        unsigned* err, cudaStream_t st);
 // Block reorder between the all-to-all layout [peer][row][c] and segment rows [row][peer][c]
 // (c < width, row < rows, peer < peers); to_segments selects the direction.
 void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, unsigned long long rows,
@@ -145,6 +149,12 @@ constexpr int kCarryChunkSmall = 512;   // small products: 4x the CTAs
 inline std::size_t carry_map_words(std::size_t K) { return (K + kCarryChunkSmall - 1) / kCarryChunkSmall; }
 // Returns the number of kernels launched.
 int launch_carry(const CarryArgs& a, cudaStream_t st);
+// Inverse radix-3 pass fused with the recovery (N = 3 S, unsharded, tail = 1): r holds the
+// radix-3 inverse arguments (r.src = the last inverse power-of-two pass's output of both
+// primes); a.z1/a.z2 are unused. Applies when carry_r3_fusable(S) (S a multiple of the carry
+// chunk and a large product). Returns kernels launched.
+int launch_carry_r3(const CarryArgs& a, const Radix3Args& r, cudaStream_t st);
+bool carry_r3_fusable(unsigned long long S);
 // General recovery for small forced bases (lambda < 14, where a coefficient can need more than
 // three base-B digits): every coefficient's D base-B digits are added into the limb sums
 // s[i + j] (s zeroed first), then `rounds` normalisation passes t_k = s_k mod B + s_{k-1} / B

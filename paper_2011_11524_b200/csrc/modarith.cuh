@@ -24,11 +24,30 @@ struct __align__(16) TwPair {  // Shoup form of one root-of-unity factor
 
 // Because p < 2^63, a value in [-p, p) is unambiguous as a signed 64-bit word:
 // corrections test the sign bit (reference words.hpp:38-45, adjust_signed).
+#ifndef DMG_CORR_FMA
+#define DMG_CORR_FMA 0
+#endif
 __device__ __forceinline__ u64 adjust_signed(u64 t, u64 p) {
+#if DMG_CORR_FMA
+  // t + s p with the sign bit s = hi(t) >> 31 taken as mul.hi(hi(t), 2) and s p added by
+  // mad.wide / mad.lo: ptxas emits IMAD.HI + IMAD.WIDE + IMAD (FMA pipe) + IADD3 + IADD3.X
+  // instead of ISETP + IADD3 + IADD3.X + 2 SEL (all ALU pipe, the transforms' binding pipe).
+  asm("{\n\t.reg .u32 tl, th, s, pl, ph;\n\t"
+      "mov.b64 {tl, th}, %0;\n\t"
+      "mov.b64 {pl, ph}, %1;\n\t"
+      "mul.hi.u32 s, th, 2;\n\t"
+      "mad.wide.u32 %0, s, pl, %0;\n\t"
+      "mov.b64 {tl, th}, %0;\n\t"
+      "mad.lo.u32 th, s, ph, th;\n\t"
+      "mov.b64 %0, {tl, th};\n\t}"
+      : "+l"(t)
+      : "l"(p));
+#else
   // sign test + predicated add (ptxas emits ISETP + IADD3 + 2 SEL) rather than the
   // mask form SHF + 2 LOP3 + IADD3 + IADD3.X: measured 0.6% (config 2) and 1.8%
   // (config 4) faster on B200.
   asm("{\n\t.reg .pred n;\n\tsetp.lt.s64 n, %0, 0;\n\t@n add.u64 %0, %0, %1;\n\t}" : "+l"(t) : "l"(p));
+#endif
   return t;
 }
 __device__ __forceinline__ u64 mod_add(u64 a, u64 b, u64 p) { return adjust_signed(a + b - p, p); }

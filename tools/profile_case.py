@@ -25,13 +25,19 @@ def main():
     s = torch.cuda.Stream()
     torch.cuda.set_stream(s)
     sp = s.cuda_stream
-    count, nx, ny, mode = cfg["count"], cfg["nx"], cfg["ny"], cfg["mode"]
+    count, nx, ny = cfg["count"], cfg["nx"], cfg["ny"]
+    (sx, sy), (mx, my) = cfg["seeds"], cfg["modes"]
+    mode = 1 if cfg["modes"] == (1, 1) else 0
     xs = torch.empty(count * nx, dtype=torch.uint8, device="cuda")
     ys = torch.empty(count * ny, dtype=torch.uint8, device="cuda")
     outs = torch.empty(count * (nx + ny), dtype=torch.uint8, device="cuda")
     lens = torch.zeros(count, dtype=torch.int64, device="cuda")
-    ctx.generate_digits(xs.data_ptr(), nx, 0, count=count, seed_step=2, mode=mode, stream=sp)
-    ctx.generate_digits(ys.data_ptr(), ny, 1, count=count, seed_step=2, mode=mode, stream=sp)
+    if count > 1:
+        ctx.generate_digits(xs.data_ptr(), nx, 0, count=count, seed_step=2, mode=mx, stream=sp)
+        ctx.generate_digits(ys.data_ptr(), ny, 1, count=count, seed_step=2, mode=my, stream=sp)
+    else:
+        ctx.generate_digits(xs.data_ptr(), nx, sx, mode=mx, stream=sp)
+        ctx.generate_digits(ys.data_ptr(), ny, sy, mode=my, stream=sp)
     for r in range(a.reps):
         torch.cuda.synchronize()
         t = time.perf_counter()
