@@ -57,14 +57,24 @@ namespace detail {
   }
 }
 
-// Process-wide context on the device named by DECMUL_DEVICE (default 0).
+// Process-wide context over every visible GPU (decmul_gpu_create_multi: large products shard,
+// batches fan out), or only the device named by DECMUL_DEVICE.
 inline decmul_gpu_ctx* context() {
   static std::once_flag once;
   static decmul_gpu_ctx* ctx = nullptr;
   static int rc = 0;
   std::call_once(once, [] {
-    const char* d = std::getenv("DECMUL_DEVICE");
-    rc = decmul_gpu_create(&ctx, d ? std::atoi(d) : 0);
+    if (const char* d = std::getenv("DECMUL_DEVICE")) {
+      rc = decmul_gpu_create(&ctx, std::atoi(d));
+      return;
+    }
+    int n = 0;
+    rc = decmul_gpu_device_count(&n);
+    if (rc) return;
+    std::vector<int> devs;
+    for (int i = 0; i < n; ++i) devs.push_back(i);
+    if (devs.empty()) devs.push_back(0);  // no GPU: creation fails loudly (DECMUL_ECUDA)
+    rc = decmul_gpu_create_multi(&ctx, devs.data(), int(devs.size()));
   });
   if (rc) throw_for(rc, decmul_gpu_last_error(nullptr));
   return ctx;

@@ -51,6 +51,13 @@ typedef struct {
 
 /* ---- context ---- */
 int decmul_gpu_create(decmul_gpu_ctx** ctx, int device);
+/* A context over n GPUs (multi-GPU fan-out hidden behind the context). Host-buffer
+ * calls use every device: uniform and mixed batches split into contiguous ranges per device; one
+ * product with a transform of >= 2^22 words is sharded (columns/rows of the six-step over the
+ * devices, the transposition as peer copies over NVLink). Device-pointer calls and the parity
+ * hooks run on devices[0]. devices may repeat (ranks sharing a GPU; tests). */
+int decmul_gpu_create_multi(decmul_gpu_ctx** ctx, const int* devices, int n);
+int decmul_gpu_context_devices(decmul_gpu_ctx* ctx, int* devices, int cap, int* n);
 void decmul_gpu_destroy(decmul_gpu_ctx* ctx);
 const char* decmul_gpu_last_error(const decmul_gpu_ctx* ctx); /* ctx may be NULL (create failures) */
 int decmul_gpu_device_count(int* count);
@@ -69,6 +76,12 @@ int decmul_gpu_plan(decmul_gpu_ctx* ctx, size_t digits_x, size_t digits_y, unsig
  * are detected as squaring too. forced_base_exp = MultiplyOptions::forced_base_exp. */
 int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
                         size_t cap, size_t* out_len, unsigned forced_base_exp, int alias);
+
+/* decmul_gpu_multiply sharded over the context's devices whatever the size (a product too
+ * small for the shard shape fails with DECMUL_EINVAL); what decmul_gpu_multiply does on its own
+ * for large products. Exposed for parity tests of the sharded path at small sizes. */
+int decmul_gpu_multiply_sharded(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
+                                size_t cap, size_t* out_len, int alias);
 
 /* Device-resident variant: digits in and out stay in HBM. stream = cudaStream_t (NULL = the
  * context's stream). If out_len is NULL the call is asynchronous (no host sync; read the

@@ -35,8 +35,8 @@ __all__ = [
 
 P1 = 9223372036015915009  # reference primes.hpp:30
 P2 = 9223372036166909953  # reference primes.hpp:31
-Q1 = 9223371938070528001  # find_primes(64, 30, 2) (primes.cpp:70-81): lengths beyond 3 * 2^24
-Q2 = 9223371941291753473
+Q1 = 9223371564408373249  # find_primes(64, 32, 2) (primes.cpp:70-81): lengths beyond 3 * 2^24
+Q2 = 9223371938070528001  # (both == 1 mod 2^32)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -58,7 +58,8 @@ EXPORTED_SYMBOLS = [
     "decmul_gpu_get_stats", "decmul_gpu_shard_plan_create", "decmul_gpu_shard_pack", "decmul_gpu_shard_transform",
     "decmul_gpu_shard_reorder", "decmul_gpu_shard_carry_begin", "decmul_gpu_shard_carry_probe",
     "decmul_gpu_shard_carry_emit", "decmul_gpu_selftest", "decmul_gpu_multiply_batch_ptrs",
-    "decmul_gpu_check_errors", "decmul_gpu_profile", "decmul_gpu_profile_report",
+    "decmul_gpu_check_errors", "decmul_gpu_profile", "decmul_gpu_profile_report", "decmul_gpu_create_multi",
+    "decmul_gpu_context_devices", "decmul_gpu_multiply_sharded",
 ]
 
 
@@ -193,17 +194,41 @@ class DecimalNumber:
 
 
 class Context:
-    """One device context (``decmul_gpu_ctx``): plan cache, workspace, stream."""
+    """A device context (``decmul_gpu_ctx``): plan cache, workspace, streams. ``devices`` (a
+    list) makes a multi-GPU context (decmul_gpu_create_multi): host-buffer products fan out
+    over the devices and large single products are sharded; device ids may repeat."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, devices: list[int] | None = None):
         lib = load_library()
         h = C.c_void_p()
-        rc = lib.decmul_gpu_create(C.byref(h), C.c_int(device))
+        if devices:
+            arr = (C.c_int * len(devices))(*devices)
+            rc = lib.decmul_gpu_create_multi(C.byref(h), arr, C.c_int(len(devices)))
+            device = devices[0]
+        else:
+            rc = lib.decmul_gpu_create(C.byref(h), C.c_int(device))
         if rc:
             _raise(rc, None)
         self._h = h
         self._lib = lib
         self.device = device
+
+    def devices(self) -> list[int]:
+        arr = (C.c_int * 64)()
+        n = C.c_int()
+        self._call("decmul_gpu_context_devices", arr, C.c_int(64), C.byref(n))
+        return list(arr[: n.value])
+
+    def multiply_sharded(self, x: bytes, y: bytes | None) -> bytes:
+        """The product sharded over the context's devices whatever its size (parity tests)."""
+        alias = y is None
+        y = x if alias else y
+        cap = len(x) + len(y) + 1
+        out = C.create_string_buffer(cap)
+        n = C.c_size_t()
+        self._call("decmul_gpu_multiply_sharded", x, C.c_size_t(len(x)), y, C.c_size_t(len(y)), out,
+                   C.c_size_t(cap), C.byref(n), C.c_int(int(alias)))
+        return out.raw[: n.value]
 
     def close(self):
         if getattr(self, "_h", None):

@@ -7,9 +7,11 @@
 
 #include "../../include/decmul_gpu.h"
 #include "engine.hpp"
+#include "multi.hpp"
 
 struct decmul_gpu_ctx {
-  std::unique_ptr<dmg::Engine> eng;
+  std::unique_ptr<dmg::MultiEngine> multi;  // one engine per device of the context
+  dmg::Engine* eng = nullptr;               // the first device's engine (device-pointer calls, hooks)
   std::mutex mu;
   std::string err;
 };
@@ -87,20 +89,32 @@ struct DeviceGuard {
 
 extern "C" {
 
-int decmul_gpu_create(decmul_gpu_ctx** ctx, int device) {
-  if (!ctx) return DECMUL_EINVAL;
+int decmul_gpu_create(decmul_gpu_ctx** ctx, int device) { return decmul_gpu_create_multi(ctx, &device, 1); }
+
+int decmul_gpu_create_multi(decmul_gpu_ctx** ctx, const int* devices, int n) {
+  if (!ctx || !devices || n < 1) return DECMUL_EINVAL;
   *ctx = nullptr;
   return guarded(nullptr, [&] {
-    DeviceGuard dev(device);
+    DeviceGuard dev(devices[0]);
     auto c = std::make_unique<decmul_gpu_ctx>();
-    c->eng = std::make_unique<dmg::Engine>(device);
+    c->multi = std::make_unique<dmg::MultiEngine>(devices, n);
+    c->eng = &c->multi->primary();
     *ctx = c.release();
+  });
+}
+
+int decmul_gpu_context_devices(decmul_gpu_ctx* ctx, int* devices, int cap, int* n) {
+  LOCKED(ctx, {
+    const std::vector<int> d = ctx->multi->devices();
+    if (n) *n = int(d.size());
+    for (int i = 0; devices && i < cap && i < int(d.size()); ++i) devices[i] = d[i];
   });
 }
 
 void decmul_gpu_destroy(decmul_gpu_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dev(ctx->eng->device());
+  ctx->eng = nullptr;
   delete ctx;
 }
 
@@ -157,7 +171,17 @@ int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const cha
       *out_len = 1;
       return;
     }
-    *out_len = ctx->eng->multiply_host(x, nx, y, ny, out, cap, forced, alias != 0);
+    *out_len = ctx->multi->multiply_host(x, nx, y, ny, out, cap, forced, alias != 0);
+  });
+}
+
+int decmul_gpu_multiply_sharded(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
+                                size_t cap, size_t* out_len, int alias) {
+  LOCKED(ctx, {
+    if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
+    if ((nx > 1 && x[0] == '0') || (ny > 1 && y[0] == '0')) throw std::invalid_argument("decimal: leading zero");
+    const bool sq = alias != 0 || (nx == ny && (x == y || std::memcmp(x, y, nx) == 0));
+    *out_len = ctx->multi->sharded_multiply(x, nx, y, ny, out, cap, sq);
   });
 }
 
@@ -181,13 +205,13 @@ int decmul_gpu_result_length(decmul_gpu_ctx* ctx, size_t* out_len) {
 int decmul_gpu_multiply_batch(decmul_gpu_ctx* ctx, size_t count, const char* xs, size_t x_stride, size_t nx,
                               const char* ys, size_t y_stride, size_t ny, char* outs, size_t out_stride,
                               size_t* out_lens) {
-  LOCKED(ctx, ctx->eng->multiply_batch_host(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, out_lens));
+  LOCKED(ctx, ctx->multi->multiply_batch_host(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, out_lens));
 }
 
 int decmul_gpu_multiply_batch_ptrs(decmul_gpu_ctx* ctx, size_t count, const char* const* xs, const size_t* nxs,
                                    const char* const* ys, const size_t* nys, char* const* outs, const size_t* caps,
                                    size_t* out_lens) {
-  LOCKED(ctx, ctx->eng->multiply_batch_ptrs(count, xs, nxs, ys, nys, outs, caps, out_lens));
+  LOCKED(ctx, ctx->multi->multiply_batch_ptrs(count, xs, nxs, ys, nys, outs, caps, out_lens));
 }
 
 int decmul_gpu_multiply_batch_device(decmul_gpu_ctx* ctx, size_t count, const char* d_xs, size_t x_stride,

@@ -261,41 +261,38 @@ __global__ void __launch_bounds__(NTC) k_carry_emit(CarryArgs a) {
   char* sb = buf + (reinterpret_cast<unsigned long long>(g) & 15);
   // digits: each thread prints PERC consecutive limbs (a contiguous PERC lambda-byte run)
   const unsigned long long* sg = reinterpret_cast<const unsigned long long*>(a.s);
-  if constexpr (PERC == 8) {
-    // fast path: 8 full-width limbs below the top one -> one 8 lambda-byte run built in
-    // registers (SWAR) and stored as 32-bit words
-    const unsigned long long kg0 = a.k_off + cbase + threadIdx.x * PERC;
-    if (kg0 + 7 < top && be >= 14) {
-      u64 v[8];
+  // fast path: 8 full-width limbs below the top one -> one 8 lambda-byte run built in registers
+  // (SWAR) and stored as 32-bit words; the chunk holding the top limb (or a lambda < 14 tail)
+  // prints limb by limb. Both paths end at the block's one barrier below.
+  const unsigned long long kg0 = a.k_off + cbase + threadIdx.x * PERC;
+  if (PERC == 8 && kg0 + 7 < top && be >= 14) {
+    u64 v[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {  // text order: the highest limb first
-        const int loc = threadIdx.x * PERC + 7 - j;
-        u64 x = sg[cbase + loc] + mp[loc];
-        if (x >= B) x -= B;
-        if (x >= B) x -= B;
-        v[j] = x;
-      }
-      char* dst = sb + (limb_pos(kg0 + 7, top, top_len, be) - start);
-      switch (be) {
-        case 14: print_run8<14>(dst, v); break;
-        case 15: print_run8<15>(dst, v); break;
-        case 16: print_run8<16>(dst, v); break;
-        default: print_run8<17>(dst, v); break;
-      }
-      __syncthreads();
-      cta_store_bytes(g, sb, unsigned(end - start), threadIdx.x, NTC);
-      return;
+    for (int j = 0; j < 8; ++j) {  // text order: the highest limb first
+      const int loc = threadIdx.x * PERC + 7 - j;
+      u64 x = sg[cbase + loc] + mp[loc];
+      if (x >= B) x -= B;
+      if (x >= B) x -= B;
+      v[j] = x;
     }
-  }
+    char* dst = sb + (limb_pos(kg0 + 7, top, top_len, be) - start);
+    switch (be) {
+      case 14: print_run8<14>(dst, v); break;
+      case 15: print_run8<15>(dst, v); break;
+      case 16: print_run8<16>(dst, v); break;
+      default: print_run8<17>(dst, v); break;
+    }
+  } else {
 #pragma unroll
-  for (int j = 0; j < PERC; ++j) {
-    const int loc = threadIdx.x * PERC + j;
-    const unsigned long long k = cbase + loc, kg = a.k_off + k;
-    if (kg > ghi) break;
-    u64 v = sg[k] + mp[loc];  // re-read from L1/L2 (this block just streamed it)
-    if (v >= B) v -= B;
-    if (v >= B) v -= B;
-    write_digits(sb + (limb_pos(kg, top, top_len, be) - start), v, kg == top ? top_len : be);
+    for (int j = 0; j < PERC; ++j) {
+      const int loc = threadIdx.x * PERC + j;
+      const unsigned long long k = cbase + loc, kg = a.k_off + k;
+      if (kg > ghi) break;
+      u64 v = sg[k] + mp[loc];  // re-read from L1/L2 (this block just streamed it)
+      if (v >= B) v -= B;
+      if (v >= B) v -= B;
+      write_digits(sb + (limb_pos(kg, top, top_len, be) - start), v, kg == top ? top_len : be);
+    }
   }
   __syncthreads();
   cta_store_bytes(g, sb, unsigned(end - start), threadIdx.x, NTC);
@@ -366,6 +363,7 @@ __device__ __forceinline__ void r3inv_load(const Radix3Args& r, unsigned long lo
     for (int g = 0; g < 3; ++g) x[pr][g] = r.src[pr][g * r.S + s];
   }
 }
+template <bool P32>
 __device__ __forceinline__ void r3inv_from(const Radix3Args& r, unsigned long long s, const u64 x[2][3],
                                            u64 out[2][3]) {
   const unsigned long long L = 1ull << r.lbits, H = r.hrow;
@@ -375,19 +373,20 @@ __device__ __forceinline__ void r3inv_from(const Radix3Args& r, unsigned long lo
     const u64 p = r.p[pr];
     const TwPair* __restrict__ lo = r.lo[pr];
     const TwPair* __restrict__ hi = r.hi[pr];
-    const u64 y0 = shoup_mul(x[pr][0], hi[sh], p);  // lo[0][.] = 1
-    const u64 y1 = shoup_mul(shoup_mul(x[pr][1], lo[L + sl], p), hi[H + sh], p);
-    const u64 y2 = shoup_mul(shoup_mul(x[pr][2], lo[2 * L + sl], p), hi[2 * H + sh], p);
-    const u64 t = shoup_mul(mod_sub(y1, y2, p), r.lam[pr], p);
+    const u64 y0 = shoup_mul<P32>(x[pr][0], hi[sh], p);  // lo[0][.] = 1
+    const u64 y1 = shoup_mul<P32>(shoup_mul<P32>(x[pr][1], lo[L + sl], p), hi[H + sh], p);
+    const u64 y2 = shoup_mul<P32>(shoup_mul<P32>(x[pr][2], lo[2 * L + sl], p), hi[2 * H + sh], p);
+    const u64 t = shoup_mul<P32>(mod_sub(y1, y2, p), r.lam[pr], p);
     out[pr][0] = mod_add(mod_add(y0, y1, p), y2, p);
     out[pr][1] = mod_add(mod_sub(y0, y2, p), t, p);
     out[pr][2] = mod_sub(mod_sub(y0, y1, p), t, p);
   }
 }
+template <bool P32>
 __device__ __forceinline__ void r3inv_column(const Radix3Args& r, unsigned long long s, u64 out[2][3]) {
   u64 x[2][3];
   r3inv_load(r, s, x);
-  r3inv_from(r, s, x, out);
+  r3inv_from<P32>(r, s, x, out);
 }
 
 __device__ __forceinline__ void coeff_split(const CarryArgs& a, u64 r1, u64 r2, bool check, u64& d0, u64& d1,
@@ -399,12 +398,13 @@ __device__ __forceinline__ void coeff_split(const CarryArgs& a, u64 r1, u64 r2, 
 }
 
 // d1, d2 of coefficient k (k < 0: zero)
+template <bool P32>
 __device__ __forceinline__ void coeff_d12(const CarryArgs& a, const Radix3Args& r, long long k, u64& d1, u64& d2) {
   d1 = d2 = 0;
   if (k < 0) return;
   u64 c[2][3];
   const unsigned long long g = (unsigned long long)k / r.S;
-  r3inv_column(r, (unsigned long long)k - g * r.S, c);
+  r3inv_column<P32>(r, (unsigned long long)k - g * r.S, c);
   u64 d0;
   coeff_split(a, g == 0 ? c[0][0] : (g == 1 ? c[0][1] : c[0][2]), g == 0 ? c[1][0] : (g == 1 ? c[1][1] : c[1][2]),
               false, d0, d1, d2);
@@ -415,6 +415,7 @@ __device__ __forceinline__ void coeff_d12(const CarryArgs& a, const Radix3Args& 
 // k - 1 and d2 of k - 2 through warp shuffles, with the warp edges (and the chunk's two halo
 // coefficients) in shared memory. The last CTA (a.tail) forms the two trailing limbs N, N + 1.
 // Replaces k_radix3_inv + k_carry_split: the natural-order coefficients never touch HBM.
+template <bool P32>
 __global__ void __launch_bounds__(NT) k_carry_split_r3(CarryArgs a, Radix3Args r) {
   pdl_wait();
   constexpr int NW = NT / 32;
@@ -427,8 +428,8 @@ __global__ void __launch_bounds__(NT) k_carry_split_r3(CarryArgs a, Radix3Args r
   if (blockIdx.x == S / CH) {  // tail chunk N / CH: limbs N, N + 1 (K = N + 2)
     if (tid == 0) {
       u64 d1a, d2a, d1b, d2b;
-      coeff_d12(a, r, (long long)N - 1, d1a, d2a);
-      coeff_d12(a, r, (long long)N - 2, d1b, d2b);
+      coeff_d12<P32>(a, r, (long long)N - 1, d1a, d2a);
+      coeff_d12<P32>(a, r, (long long)N - 2, d1b, d2b);
       const u64 sN = d1a + d2b, sN1 = d2a;
       a.s[N] = sN;
       a.s[N + 1] = sN1;
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(NT) k_carry_split_r3(CarryArgs a, Radix3Args r
   if (tid < 6) {  // halo: coefficients k0 - 1 and k0 - 2 of each group's chunk
     const int g = tid >> 1, which = tid & 1;
     u64 d1, d2;
-    coeff_d12(a, r, (long long)(g * S + s0) - 1 - which, d1, d2);
+    coeff_d12<P32>(a, r, (long long)(g * S + s0) - 1 - which, d1, d2);
     if (which == 0) {
       e1[g][0] = d1;
       e2b[g][0] = d2;
@@ -460,7 +461,7 @@ __global__ void __launch_bounds__(NT) k_carry_split_r3(CarryArgs a, Radix3Args r
 #pragma unroll
       for (int q = 0; q < 6; ++q) cur[q / 3][q % 3] = xin[q / 3][q % 3];
       if (j + 1 < PER) r3inv_load(r, s + NT, xin);
-      r3inv_from(r, s, cur, c);
+      r3inv_from<P32>(r, s, cur, c);
     }
     u64 d0[3], d1[3], d2[3];
 #pragma unroll
@@ -583,7 +584,8 @@ int launch_carry_r3(const CarryArgs& a, const Radix3Args& r, cudaStream_t st) {
   const unsigned long long N = 3 * r.S, K = N + 2;
   const unsigned nchunks = unsigned((K + CH - 1) / CH);  // S / CH column blocks + the tail chunk
   const double n = double(N), k = double(K);
-  launch_pdl(k_carry_split_r3, dim3(unsigned(r.S / CH + 1)), dim3(NT), 0, st, a, r);
+  launch_pdl(r.p32 ? k_carry_split_r3<true> : k_carry_split_r3<false>, dim3(unsigned(r.S / CH + 1)), dim3(NT), 0, st,
+             a, r);
   prof_mark("k_carry_split_r3", st, 2.0 * 6.0 * r.S + n, 16 * n + 8 * k);
   launch_pdl(k_carry_scan<CH>, dim3(1), dim3(1024), 0, st, a, nchunks);
   prof_mark("k_carry_scan", st, 0, 8.0 * nchunks);

@@ -16,6 +16,22 @@ namespace {
 
 TwPair shoup_pair(const HostField& F, u64 w) { return TwPair{w, F.shoup(w)}; }
 
+// Factorised inter-pass twiddle tables for a pass whose full R x S table would take more than
+// 4 GB per direction... per prime (config 5's first power-of-two pass: 8 GB; config 4 keeps its
+// 1 GB tables: the second Shoup product per element costs more than the table read saves).
+// DECMUL_FACTOR_TABLES=1 factorises every pass with S > 1 (tests), =0 none.
+bool factor_tables(std::size_t entries) {
+  if (const char* e = std::getenv("DECMUL_FACTOR_TABLES")) return e[0] == '1';
+  return entries * sizeof(TwPair) > (std::size_t(4) << 30);
+}
+
+// every prime of a launch == 1 mod 2^32: the kernels' shoup_mul<true> instantiation
+bool p32_of(const PrimePlan* const pl[2], int np) {
+  for (int q = 0; q < np; ++q)
+    if (!prime_p32(pl[q]->p)) return false;
+  return true;
+}
+
 u64 recip_of(u64 d) {  // reference make_div_by_const (decimal.hpp:93-104), for a normalized divisor
   return u64(~(u128)0 / d - ((u128)1 << 64));
 }
@@ -216,12 +232,34 @@ void Engine::build_passes(PrimePlan& pl) {
       cuda_check(cudaStreamSynchronize(stream_), "radix-3 tables");
     } else if (ps.S > 1) {
       const std::size_t cnt = std::size_t(ps.R) * ps.S;
-      ps.tw_fwd.ensure(cnt);
-      ps.tw_inv.ensure(cnt);
       const u64 scale = int(i) == last_table ? pl.conv_scale : 1;
-      launch_gen_pass_table(ps.tw_fwd.ptr, F.to_mont(wM), F.to_mont(1), ps.R, ps.logR, ps.S, pl.p, recip, stream_);
-      launch_gen_pass_table(ps.tw_inv.ptr, F.to_mont(F.inv(wM)), F.to_mont(scale), ps.R, ps.logR, ps.S, pl.p, recip,
-                            stream_);
+      if (factor_all_ || factor_tables(cnt)) {
+        // omega_M^{f s} = omega_M^{f (s mod L)} * (omega_M^L)^{f (s / L)}: R (L + S / L) pairs instead
+        // of R S, for one more Shoup product per element of the pass (memory-bound plans only)
+        const int lb = std::max(kTileLogW, (ps.logS + 1) / 2);
+        const std::size_t L = std::size_t(1) << lb, H = ps.S / L;
+        ps.tw_lbits = lb;
+        ps.tw_fwd.ensure(std::size_t(ps.R) * L);
+        ps.tw_inv.ensure(std::size_t(ps.R) * L);
+        ps.hi_fwd.ensure(std::size_t(ps.R) * H);
+        ps.hi_inv.ensure(std::size_t(ps.R) * H);
+        const u64 wMi = F.inv(wM);
+        // lo: exponents f sl mod M over R x L; hi: (omega^L)^{f sh} mod M / L over R x H
+        launch_gen_pass_table(ps.tw_fwd.ptr, F.to_mont(wM), F.to_mont(1), ps.R, ps.logR, L, pl.p, recip, stream_,
+                              std::size_t(ps.R) * ps.S);
+        launch_gen_pass_table(ps.tw_inv.ptr, F.to_mont(wMi), F.to_mont(1), ps.R, ps.logR, L, pl.p, recip, stream_,
+                              std::size_t(ps.R) * ps.S);
+        launch_gen_pass_table(ps.hi_fwd.ptr, F.to_mont(F.pow(wM, L)), F.to_mont(1), ps.R, ps.logR, H, pl.p, recip,
+                              stream_, std::size_t(ps.R) * ps.S / L);
+        launch_gen_pass_table(ps.hi_inv.ptr, F.to_mont(F.pow(wMi, L)), F.to_mont(scale), ps.R, ps.logR, H, pl.p,
+                              recip, stream_, std::size_t(ps.R) * ps.S / L);
+      } else {
+        ps.tw_fwd.ensure(cnt);
+        ps.tw_inv.ensure(cnt);
+        launch_gen_pass_table(ps.tw_fwd.ptr, F.to_mont(wM), F.to_mont(1), ps.R, ps.logR, ps.S, pl.p, recip, stream_);
+        launch_gen_pass_table(ps.tw_inv.ptr, F.to_mont(F.inv(wM)), F.to_mont(scale), ps.R, ps.logR, ps.S, pl.p,
+                              recip, stream_);
+      }
       cuda_check(cudaGetLastError(), "gen table");
     }
     if (!ps.radix3) {
@@ -285,8 +323,8 @@ std::size_t Engine::table_bytes() const {
   std::size_t b = 0;
   for (const auto& kv : plans_)
     for (const auto& ps : kv.second->passes)
-      b += (ps->tw_fwd.n + ps->tw_inv.n + ps->dft_fwd.n + ps->dft_inv.n + ps->r3_lo_fwd.n + ps->r3_hi_fwd.n +
-            ps->r3_lo_inv.n + ps->r3_hi_inv.n) *
+      b += (ps->tw_fwd.n + ps->tw_inv.n + ps->hi_fwd.n + ps->hi_inv.n + ps->dft_fwd.n + ps->dft_inv.n +
+            ps->r3_lo_fwd.n + ps->r3_hi_fwd.n + ps->r3_lo_inv.n + ps->r3_hi_inv.n) *
            sizeof(TwPair);
   return b;
 }
@@ -357,6 +395,7 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
       a.cb = L.cb;
       a.sb = L.sb;
       a.off = L.off;
+      a.p32 = p32_of(pl, np);
       launch_radix3(false, a, np, st);
       prof_mark("k_radix3_fwd", st, double(np) * 3.0 * double(L.S), double(np) * 48.0 * double(L.S));
     } else {
@@ -369,14 +408,17 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
         a.dft_fwd[q] = Pq.dft_fwd.ptr;
         a.dft_inv[q] = Pq.dft_inv.ptr;
         a.pass_tw[q] = Pq.S > 1 ? Pq.tw_fwd.ptr : nullptr;
+        a.pass_hi[q] = Pq.hi_fwd.ptr;
         a.p[q] = pl[q]->p;
         a.pp[q] = pl[q]->pp;
       }
+      a.tw_lbits = P.tw_lbits;
       a.S = L.S;
       a.logS = L.logS;
       a.G = L.groups;
       a.tw_logS = L.tw_logS;
       a.tw_off = L.tw_off;
+      a.p32 = p32_of(pl, np);
       launch_pass_fwd(P.logR, a, L.ncols, np, st);
       if (prof_on_) {
         char nm[64];
@@ -414,6 +456,7 @@ void Engine::pass_fused(const PrimePlan* pl[2], int np, u64* const data[2], cons
   a.G = L.groups;
   a.tw_logS = 0;
   a.has_final_scale = any_table ? 0 : 1;
+  a.p32 = p32_of(pl, np);
   launch_pass_fused(P.logR, a, L.ncols, np, st);
   if (prof_on_) {
     char nm[64];
@@ -446,6 +489,7 @@ void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std:
       a.cb = L.cb;
       a.sb = L.sb;
       a.off = L.off;
+      a.p32 = p32_of(pl, np);
       launch_radix3(true, a, np, st);
       prof_mark("k_radix3_inv", st, double(np) * 4.0 * double(L.S), double(np) * 48.0 * double(L.S));
     } else {
@@ -458,6 +502,7 @@ void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std:
         a.dft_fwd[q] = Pq.dft_fwd.ptr;
         a.dft_inv[q] = Pq.dft_inv.ptr;
         a.pass_tw[q] = Pq.S > 1 ? Pq.tw_inv.ptr : nullptr;
+        a.pass_hi[q] = Pq.hi_inv.ptr;
         a.final_scale[q] = pl[q]->final_scale;
         a.p[q] = pl[q]->p;
         a.pp[q] = pl[q]->pp;
@@ -468,6 +513,8 @@ void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std:
       a.tw_logS = L.tw_logS;
       a.tw_off = L.tw_off;
       a.has_final_scale = (!any_table && ii == 0) ? 1 : 0;
+      a.p32 = p32_of(pl, np);
+      a.tw_lbits = P.tw_lbits;
       launch_pass_inv(P.logR, a, L.ncols, np, st);
       if (prof_on_) {
         char nm[64];
@@ -614,6 +661,7 @@ void Engine::pack_radix3(const PrimePlan* pl[2], const char* digits, std::size_t
   a.S = P.S;
   a.lbits = P.r3_lbits;
   a.hrow = P.S >> a.lbits;
+  a.p32 = p32_of(pl, 2);
   launch_pack_radix3(digits, nd, be, a, err, st);
   ++launches_;
   prof_mark("k_pack_radix3", st, 2.0 * double(P.S) * 5.0, double(nd) + 48.0 * double(P.S));
@@ -807,6 +855,7 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
     r.S = P0.S;
     r.lbits = P0.r3_lbits;
     r.hrow = P0.S >> r.lbits;
+    r.p32 = p32_of(pl, 2);
     launches_ += launch_carry_r3(c, r, st);
   } else {
     launches_ += recover(c, be, std::min(lx, ly), s_in_x, st);
@@ -1525,6 +1574,64 @@ void Engine::shard_carry_emit(const ShardPlan& sp, int q, unsigned rank_cin, uns
   launches_ += 2;
   cuda_check(cudaGetLastError(), "shard emit");
   check_err(st);
+}
+
+void Engine::shard_pack_compact(const ShardPlan& sp, const char* d_compact, std::size_t nd_compact, u64* d_out,
+                                cudaStream_t st) {
+  // the compacted slice is a digit string whose limb i (from the end) is this rank's local limb i
+  launch_pack(d_compact, nd_compact, sp.pp.base_exp, d_out, sp.geom.local_len, err_.ptr, st, 63, 0, 0, false);
+  ++launches_;
+  cuda_check(cudaGetLastError(), "shard pack");
+}
+
+void Engine::shard_carry_begin_async(const ShardPlan& sp, int q, const u64* z1, const u64* z2, const u64 h1[2],
+                                     const u64 h2[2], u64* s_buf, unsigned* maps_buf, unsigned* h_rank_map,
+                                     cudaStream_t st) {
+  CarryArgs c = carry_args(sp.pp, z1, z2, sp.geom.local_len, nullptr);
+  c.k_off = std::size_t(q) * sp.geom.local_len;
+  c.halo1[0] = h1[0];
+  c.halo1[1] = h1[1];
+  c.halo2[0] = h2[0];
+  c.halo2[1] = h2[1];
+  c.tail = q == sp.geom.G - 1;
+  c.s = s_buf;
+  c.maps = maps_buf;
+  shard_.tmp.ensure(4);
+  unsigned* rmap = reinterpret_cast<unsigned*>(shard_.tmp.ptr);
+  launch_carry_shard_begin(c, rmap, st);
+  launches_ += 2;
+  cuda_check(cudaGetLastError(), "shard carry");
+  cuda_check(cudaMemcpyAsync(h_rank_map, rmap, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "rank map");
+}
+
+void Engine::shard_carry_probe_async(const ShardPlan& sp, int q, unsigned rank_cin, const u64* z1, const u64* z2,
+                                     const u64* s_buf, unsigned* maps_buf, u64* h_z, cudaStream_t st) {
+  CarryArgs c = carry_args(sp.pp, z1, z2, sp.geom.local_len, nullptr);
+  c.k_off = std::size_t(q) * sp.geom.local_len;
+  c.tail = q == sp.geom.G - 1;
+  c.s = const_cast<u64*>(s_buf);
+  c.maps = maps_buf;
+  shard_.tmp.ensure(4);
+  u64* zd = reinterpret_cast<u64*>(shard_.tmp.ptr) + 2;
+  launch_carry_shard_probe(c, rank_cin, zd, st);
+  ++launches_;
+  cuda_check(cudaGetLastError(), "shard probe");
+  cuda_check(cudaMemcpyAsync(h_z, zd, 2 * sizeof(u64), cudaMemcpyDeviceToHost, st), "probe");
+}
+
+void Engine::shard_carry_emit_async(const ShardPlan& sp, int q, unsigned rank_cin, unsigned long long top,
+                                    unsigned top_len, const u64* z1, const u64* z2, const u64* s_buf,
+                                    unsigned* maps_buf, char* d_out, cudaStream_t st) {
+  CarryArgs c = carry_args(sp.pp, z1, z2, sp.geom.local_len, d_out);
+  c.k_off = std::size_t(q) * sp.geom.local_len;
+  c.tail = q == sp.geom.G - 1;
+  c.s = const_cast<u64*>(s_buf);
+  c.maps = maps_buf;
+  const unsigned long long meta[3] = {top, top_len, top_len + top * sp.pp.base_exp};
+  cuda_check(cudaMemcpyAsync(meta_.ptr, meta, sizeof meta, cudaMemcpyHostToDevice, st), "meta");
+  launch_carry_shard_emit(c, rank_cin, st);
+  launches_ += 2;
+  cuda_check(cudaGetLastError(), "shard emit");
 }
 
 DivB div_for(u64 base) { return div_for_impl(base); }

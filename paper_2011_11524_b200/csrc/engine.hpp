@@ -52,7 +52,10 @@ struct PassPlan {
   int logR = 0, R = 0;
   unsigned long long S = 0;
   int logS = 0;
-  DevBuf<TwPair> tw_fwd, tw_inv;    // R x S inter-pass twiddles (power-of-two passes, S > 1)
+  DevBuf<TwPair> tw_fwd, tw_inv;    // R x S inter-pass twiddles (power-of-two passes, S > 1), or the
+                                    // factorised lo tables R x 2^tw_lbits when tw_lbits > 0
+  DevBuf<TwPair> hi_fwd, hi_inv;    // factorised: R x S / 2^tw_lbits (the inverse carries the scale)
+  int tw_lbits = 0;
   DevBuf<TwPair> dft_fwd, dft_inv;  // omega_R^{+-k}, k < R/2
   // radix-3 passes: omega_N^{+-f s} = lo[f][s mod 2^lbits] * hi[f][s >> lbits]
   DevBuf<TwPair> r3_lo_fwd, r3_hi_fwd, r3_lo_inv, r3_hi_inv;
@@ -153,6 +156,14 @@ class CopyPool {
   bool stop_ = false;
 };
 
+// One rank's device buffers of a sharded product driven inside the library (multi.cu).
+struct ShardBufs {
+  DevBuf<u64> X[2], Y[2], P, R, S;
+  DevBuf<unsigned> M;
+  DevBuf<char> dx, dy, dout;
+  DevBuf<unsigned long long> tmp;  // halo words, rank maps, probes
+};
+
 class Engine {
  public:
   explicit Engine(int device);
@@ -210,6 +221,24 @@ class Engine {
   void shard_carry_emit(const ShardPlan& sp, int q, unsigned rank_cin, unsigned long long top, unsigned top_len,
                         const u64* z1, const u64* z2, const u64* s_buf, unsigned* maps_buf, char* d_out,
                         cudaStream_t st);
+
+  // async forms for the in-library multi-device driver (multi.cu): no host sync; results land
+  // in the caller's pinned host memory once st completes
+  void shard_pack_compact(const ShardPlan& sp, const char* d_compact, std::size_t nd_compact, u64* d_out,
+                          cudaStream_t st);
+  void shard_carry_begin_async(const ShardPlan& sp, int q, const u64* z1, const u64* z2, const u64 h1[2],
+                               const u64 h2[2], u64* s_buf, unsigned* maps_buf, unsigned* h_rank_map,
+                               cudaStream_t st);
+  void shard_carry_probe_async(const ShardPlan& sp, int q, unsigned rank_cin, const u64* z1, const u64* z2,
+                               const u64* s_buf, unsigned* maps_buf, u64* h_z, cudaStream_t st);
+  void shard_carry_emit_async(const ShardPlan& sp, int q, unsigned rank_cin, unsigned long long top,
+                              unsigned top_len, const u64* z1, const u64* z2, const u64* s_buf, unsigned* maps_buf,
+                              char* d_out, cudaStream_t st);
+  ShardBufs& shard_bufs() { return shard_; }
+  // every pass with S > 1 gets factorised twiddle tables (ranks of a sharded context: table
+  // memory independent of N)
+  void set_factor_all(bool on) { factor_all_ = on; }
+  void check_errors_sync(cudaStream_t st) { check_err(st); }
 
   const PrimePlan& prime_plan(u64 p, std::size_t N);
   // Length of the last product (after its stream was synchronised); raises its errors.
@@ -314,6 +343,8 @@ class Engine {
   };
   bool prof_on_ = false;
   std::vector<ProfRec> prof_;
+  ShardBufs shard_;
+  bool factor_all_ = false;
 };
 
 // The engine whose launches the calling thread is currently enqueueing (prof_mark target).

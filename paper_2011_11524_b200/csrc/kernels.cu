@@ -30,12 +30,13 @@ template <int LOGR, bool ROWS, int TW>
 struct Geom {
   unsigned long long base, s0;
   unsigned long long S, tw_col;
-  int logS, tw_logS;
+  int logS, tw_logS, tw_lb;
   __device__ __forceinline__ Geom(const PassArgs& a) {
     const unsigned long long tile = blockIdx.x / a.np;
     S = a.S;
     logS = a.logS;
     tw_logS = a.tw_logS;
+    tw_lb = a.tw_lbits;
     if (ROWS) {
       // group-fastest tile order: the G groups share the twiddle rows T[f][s0..s0+15],
       // so consecutive CTAs reuse them from L2 instead of re-streaming them from HBM
@@ -55,6 +56,16 @@ struct Geom {
   // inter-pass twiddle omega_M^{f s} for the element at row r (frequency bitrev(r) after DIF)
   __device__ __forceinline__ const TwPair& tw(const TwPair* T, int r, int w) const {
     return T[((unsigned long long)bitrev(r, LOGR) << tw_logS) + tw_col + w];
+  }
+  // v omega_M^{f s}: one Shoup product with the full R x S table, or two with the factorised
+  // tables lo[f][s mod 2^lb] * hi[f][s >> lb] (tw_lb > 0; hi carries the scale)
+  template <bool P32>
+  __device__ __forceinline__ u64 twist(u64 v, const TwPair* T, const TwPair* Hi, int r, int w, u64 p) const {
+    const unsigned long long f = (unsigned long long)bitrev(r, LOGR);
+    if (tw_lb == 0) return shoup_mul<P32>(v, T[(f << tw_logS) + tw_col + w], p);
+    const unsigned long long s = tw_col + w;
+    v = shoup_mul<P32>(v, T[(f << tw_lb) + (s & ((1ull << tw_lb) - 1))], p);
+    return shoup_mul<P32>(v, Hi[(f << (tw_logS - tw_lb)) + (s >> tw_lb)], p);
   }
 };
 
@@ -138,7 +149,7 @@ constexpr int pass_min_blocks(int logr, int tw) {
 // Forward pass: column DIFs, then the inter-pass twiddle omega_M^{f s} (row passes).
 // The first round reads HBM into registers and the last round writes HBM from
 // registers; shared memory carries only the rounds in between.
-template <int LOGR, bool ROWS, int TW>
+template <int LOGR, bool ROWS, int TW, bool P32>
 __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_fwd(PassArgs a) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
   // first round's HBM loads above that barrier (config 5 +5%)
@@ -152,8 +163,9 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   const u64* src = a.src[pr];
   u64* dst = a.dst[pr];
   const TwPair* __restrict__ T = a.pass_tw[pr];
+  const TwPair* __restrict__ Hi = a.pass_hi[pr];
   const Geom<LOGR, ROWS, TW> G(a);
-  if constexpr (ROWS) {
+  if (ROWS && a.tw_lbits == 0) {
     // The twiddles are applied in the epilogue, after the DIF; start pulling the tile's
     // rows T[f][s0 .. s0 + TW) (TW pairs = TW * 16 bytes each) into L2 now so those
     // loads hit L2 instead of DRAM (large-S passes stream a table of N / 3 .. N pairs).
@@ -176,17 +188,17 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << E1];
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i, w)];
-      dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>>(v, j0, tw, p);
+      dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>, P32>(v, j0, tw, p);
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) {
-        if (ROWS) v[i] = shoup_mul(v[i], G.tw(T, base + i, w), p);
+        if (ROWS) v[i] = G.template twist<P32>(v[i], T, Hi, base + i, w, p);
         dst[G.at(base + i, w)] = v[i];
       }
     }
     return;
   } else {
     if constexpr (kStageFwd<ROWS, TW>) {
-      dif_rounds_smem<LOGR, LOGR, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
+      dif_rounds_smem<LOGR, LOGR, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>, P32>{p, tw}, tid, NTK);
     } else {
       constexpr int ST1 = 1 << (LOGR - E1);
       for (int g = tid; g < (R >> E1) * TW; g += NTK) {
@@ -196,12 +208,12 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
         u64 v[1 << E1];
 #pragma unroll
         for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i * ST1, w)];
-        dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>>(v, j0, tw, p);
+        dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>, P32>(v, j0, tw, p);
 #pragma unroll
         for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
       }
       __syncthreads();
-      dif_rounds_smem<LOGR, LOGR - E1, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
+      dif_rounds_smem<LOGR, LOGR - E1, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>, P32>{p, tw}, tid, NTK);
     }
     for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
@@ -210,10 +222,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i, w)];
-      dif_regs<LOGR, EL, EL, kSwzTables<ROWS>>(v, 0, tw, p);
+      dif_regs<LOGR, EL, EL, kSwzTables<ROWS>, P32>(v, 0, tw, p);
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
-        if (ROWS) v[i] = shoup_mul(v[i], G.tw(T, base + i, w), p);
+        if (ROWS) v[i] = G.template twist<P32>(v[i], T, Hi, base + i, w, p);
         dst[G.at(base + i, w)] = v[i];
       }
     }
@@ -230,7 +242,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
 constexpr int pass_inv_min_blocks(int logr, int tw) {
   return (logr == 9 && tw == kTileW) ? DMG_INV_MINB9 : pass_min_blocks(logr, tw);
 }
-template <int LOGR, bool ROWS, int TW>
+template <int LOGR, bool ROWS, int TW, bool P32>
 __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LOGR, TW)) k_pass_inv(PassArgs a) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
   // first round's HBM loads above that barrier (config 5 +5%)
@@ -246,6 +258,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   const u64* src = a.src[pr];
   u64* dst = a.dst[pr];
   const TwPair* __restrict__ T = a.pass_tw[pr];
+  const TwPair* __restrict__ Hi = a.pass_hi[pr];
   const TwPair sc = a.final_scale[pr];
   const Geom<LOGR, ROWS, TW> G(a);
   const TileLayout<LOGR, ROWS, TW> L;
@@ -262,13 +275,13 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
 #pragma unroll
     for (int i = 0; i < (1 << E1); ++i) {
       v[i] = STAGE ? sm[L(base + i, w)] : src[G.at(base + i, w)];
-      if (ROWS) v[i] = shoup_mul(v[i], G.tw(T, base + i, w), p);
+      if (ROWS) v[i] = G.template twist<P32>(v[i], T, Hi, base + i, w, p);
     }
-    dit_regs<LOGR, 0, E1, kSwzTables<ROWS>>(v, 0, tw, p);
+    dit_regs<LOGR, 0, E1, kSwzTables<ROWS>, P32>(v, 0, tw, p);
 #pragma unroll
     for (int i = 0; i < (1 << E1); ++i) {
       if constexpr (LOGR == E1) {
-        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
+        if (a.has_final_scale) v[i] = shoup_mul<P32>(v[i], sc, p);
         dst[G.at(base + i, w)] = v[i];
       } else {
         sm[L(base + i, w)] = v[i];
@@ -277,7 +290,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   }
   if constexpr (LOGR > E1) {
     __syncthreads();
-    dit_rounds_smem<LOGR, E1, AL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
+    dit_rounds_smem<LOGR, E1, AL, TW>(sm, L, UniformField<kSwzTables<ROWS>, P32>{p, tw}, tid, NTK);
     constexpr int STL = 1 << AL;
     for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
@@ -286,10 +299,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i * STL, w)];
-      dit_regs<LOGR, AL, EL, kSwzTables<ROWS>>(v, j0, tw, p);
+      dit_regs<LOGR, AL, EL, kSwzTables<ROWS>, P32>(v, j0, tw, p);
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
-        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
+        if (a.has_final_scale) v[i] = shoup_mul<P32>(v[i], sc, p);
         dst[G.at(base + i * STL, w)] = v[i];
       }
     }
@@ -301,7 +314,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
 // conv.cpp:205-208, :299-305) and the first inverse pass. The last DIF round
 // and the first DIT round act on the same 8-element groups, so DIF -> pointwise
 // -> DIT happens in registers.
-template <int LOGR, int TW>
+template <int LOGR, int TW, bool P32>
 __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_fused(PassArgs a) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
   // first round's HBM loads above that barrier (config 5 +5%)
@@ -328,7 +341,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   if constexpr (STAGE) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if constexpr (STAGE) {
-    dif_rounds_smem<LOGR, LOGR, EM, TW>(sm, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
+    dif_rounds_smem<LOGR, LOGR, EM, TW>(sm, L, UniformField<kSwzTables<false>, P32>{p, twf}, tid, NTK);
   } else if constexpr (LOGR > EM) {
     constexpr int ST1 = 1 << (LOGR - E1);
     for (int g = tid; g < (R >> E1) * TW; g += NTK) {
@@ -338,12 +351,12 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << E1];
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i * ST1, w)];
-      dif_regs<LOGR, LOGR, E1, kSwzTables<false>>(v, j0, twf, p);
+      dif_regs<LOGR, LOGR, E1, kSwzTables<false>, P32>(v, j0, twf, p);
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
     }
     __syncthreads();
-    dif_rounds_smem<LOGR, LOGR - E1, EM, TW>(sm, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
+    dif_rounds_smem<LOGR, LOGR - E1, EM, TW>(sm, L, UniformField<kSwzTables<false>, P32>{p, twf}, tid, NTK);
   }
   for (int g = tid; g < (R >> EM) * TW; g += NTK) {
     int w, q, j0, base;
@@ -352,14 +365,14 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
     u64 v[1 << EM];
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) v[i] = LOGR > EM ? sm[L(base + i, w)] : src[G.at(base + i, w)];
-    dif_regs<LOGR, EM, EM, kSwzTables<false>>(v, 0, twf, p);
+    dif_regs<LOGR, EM, EM, kSwzTables<false>, P32>(v, 0, twf, p);
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) v[i] = mont_mul(v[i], oth ? oth[G.at(base + i, w)] : v[i], p, pp);
-    dit_regs<LOGR, 0, EM, kSwzTables<false>>(v, 0, twi, p);
+    dit_regs<LOGR, 0, EM, kSwzTables<false>, P32>(v, 0, twi, p);
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) {
       if constexpr (LOGR == EM) {
-        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
+        if (a.has_final_scale) v[i] = shoup_mul<P32>(v[i], sc, p);
         dst[G.at(base + i, w)] = v[i];
       } else {
         sm[L(base + i, w)] = v[i];
@@ -368,7 +381,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   }
   if constexpr (LOGR > EM) {
     __syncthreads();
-    dit_rounds_smem<LOGR, EM, AL, TW>(sm, L, UniformField<kSwzTables<false>>{p, twi}, tid, NTK);
+    dit_rounds_smem<LOGR, EM, AL, TW>(sm, L, UniformField<kSwzTables<false>, P32>{p, twi}, tid, NTK);
     constexpr int STL = 1 << AL;
     for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
@@ -377,10 +390,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i * STL, w)];
-      dit_regs<LOGR, AL, EL, kSwzTables<false>>(v, j0, twi, p);
+      dit_regs<LOGR, AL, EL, kSwzTables<false>, P32>(v, j0, twi, p);
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
-        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
+        if (a.has_final_scale) v[i] = shoup_mul<P32>(v[i], sc, p);
         dst[G.at(base + i * STL, w)] = v[i];
       }
     }
@@ -389,6 +402,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
 
 // Radix-3 pass (reference three_row_forward_columns conv.cpp:109-125, with the
 // length-3 DFT written with one multiplication: omega_3^2 = -1 - omega_3).
+template <bool P32>
 __global__ void k_radix3_fwd(Radix3Args a) {
   pdl_wait();
   const int pr = blockIdx.y;  // select, not index: keeps the parameter block out of local memory
@@ -405,18 +419,19 @@ __global__ void k_radix3_fwd(Radix3Args a) {
     const unsigned long long sg = ((s >> a.cb) << a.sb) + a.off + (s & ((1ull << a.cb) - 1));  // global column
     const unsigned long long sl = sg & (L - 1), sh = sg >> a.lbits;
     const u64 x0 = src[s], x1 = src[S + s], x2 = src[2 * S + s];
-    const u64 t = shoup_mul(mod_sub(x1, x2, p), lam, p);
+    const u64 t = shoup_mul<P32>(mod_sub(x1, x2, p), lam, p);
     const u64 y0 = mod_add(mod_add(x0, x1, p), x2, p);
     const u64 y1 = mod_add(mod_sub(x0, x2, p), t, p);
     const u64 y2 = mod_sub(mod_sub(x0, x1, p), t, p);
     dst[s] = y0;
-    dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hi[H + sh], p);
-    dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
+    dst[S + s] = shoup_mul<P32>(shoup_mul<P32>(y1, lo[L + sl], p), hi[H + sh], p);
+    dst[2 * S + s] = shoup_mul<P32>(shoup_mul<P32>(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
   }
 }
 
 // Inverse radix-3 pass (conv.cpp:129-147): twiddle (with the convolution scale
 // folded into the hi table when this is the first inverse pass) then length-3 IDFT*.
+template <bool P32>
 __global__ void k_radix3_inv(Radix3Args a) {
   pdl_wait();
   const int pr = blockIdx.y;  // select, not index: keeps the parameter block out of local memory
@@ -432,10 +447,10 @@ __global__ void k_radix3_inv(Radix3Args a) {
        s += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long sg = ((s >> a.cb) << a.sb) + a.off + (s & ((1ull << a.cb) - 1));  // global column
     const unsigned long long sl = sg & (L - 1), sh = sg >> a.lbits;
-    const u64 y0 = shoup_mul(src[s], hi[sh], p);  // lo[0][.] = 1
-    const u64 y1 = shoup_mul(shoup_mul(src[S + s], lo[L + sl], p), hi[H + sh], p);
-    const u64 y2 = shoup_mul(shoup_mul(src[2 * S + s], lo[2 * L + sl], p), hi[2 * H + sh], p);
-    const u64 t = shoup_mul(mod_sub(y1, y2, p), lam, p);
+    const u64 y0 = shoup_mul<P32>(src[s], hi[sh], p);  // lo[0][.] = 1
+    const u64 y1 = shoup_mul<P32>(shoup_mul<P32>(src[S + s], lo[L + sl], p), hi[H + sh], p);
+    const u64 y2 = shoup_mul<P32>(shoup_mul<P32>(src[2 * S + s], lo[2 * L + sl], p), hi[2 * H + sh], p);
+    const u64 t = shoup_mul<P32>(mod_sub(y1, y2, p), lam, p);
     dst[s] = mod_add(mod_add(y0, y1, p), y2, p);
     dst[S + s] = mod_add(mod_sub(y0, y2, p), t, p);
     dst[2 * S + s] = mod_sub(mod_sub(y0, y1, p), t, p);
@@ -523,7 +538,7 @@ __device__ __forceinline__ long long pack_stage(const char* __restrict__ d, unsi
 
 // Limb t0 + threadIdx.x (0 past the string's last limb) from a span staged by pack_stage.
 // Raises kErrLeadingZero in *err and ORs the non-digit flag of its bytes into bad.
-template <int NG>
+template <int NG, bool LEAD = true>
 __device__ __forceinline__ u64 pack_parse(const char* __restrict__ d, unsigned long long nd, unsigned be,
                                           unsigned long long t0, const char* smem, long long g0, unsigned* err,
                                           unsigned& bad) {
@@ -534,11 +549,13 @@ __device__ __forceinline__ u64 pack_parse(const char* __restrict__ d, unsigned l
   const long long end = (long long)nd - (long long)(t * be);
   const long long begin = end > (long long)be ? end - (long long)be : 0;
   const u64 limb = parse_digits<NG>(smem + 32, int(begin - g0), int(end - begin), bad);
-  if (begin == 0 && nd > 1 && d[0] == '0') atomicOr(err, kErrLeadingZero);
+  if (LEAD && begin == 0 && nd > 1 && d[0] == '0') atomicOr(err, kErrLeadingZero);
   return limb;
 }
 
-template <bool ROWMAP, int NG>
+// LEAD: d is the whole operand (its leading zero is an error); false for a rank's compacted
+// digit slices (multi.cu), whose first digit may be 0.
+template <bool ROWMAP, int NG, bool LEAD = true>
 __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d, unsigned long long nd, unsigned be,
                                                      u64* __restrict__ limbs, unsigned long long total, unsigned* err,
                                                      int row_bits, unsigned long long row_stride,
@@ -554,7 +571,7 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d,
     const unsigned long long t0 = ROWMAP ? (i0 >> row_bits) * row_stride + off + (i0 & rmask) : i0;
     const long long g0 = pack_stage(d, nd, be, t0, smem);
     __syncthreads();
-    const u64 limb = pack_parse<NG>(d, nd, be, t0, smem, g0, err, bad);
+    const u64 limb = pack_parse<NG, LEAD>(d, nd, be, t0, smem, g0, err, bad);
     __syncthreads();
     const unsigned long long li = i0 + threadIdx.x;
     if (li < total) limbs[li] = limb;
@@ -568,7 +585,7 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d,
 // (factorised lo * hi as in k_radix3_fwd) for both primes, and writes pass 0's output.
 // The packed limbs never touch HBM (the separate pack wrote 8 B and the radix-3 pass read
 // them back per limb).
-template <int NG>
+template <int NG, bool P32>
 __global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restrict__ d, unsigned long long nd,
                                                            unsigned be, Radix3Args a, unsigned* err) {
   pdl_wait();
@@ -612,13 +629,13 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restri
       const TwPair* __restrict__ hi = a.hi[pr];
       u64* dst = a.dst[pr];
       // limbs are < 10^17 < p: canonical residues of both primes
-      const u64 t = shoup_mul(mod_sub(x1, x2, p), lam, p);
+      const u64 t = shoup_mul<P32>(mod_sub(x1, x2, p), lam, p);
       const u64 y0 = mod_add(mod_add(x0, x1, p), x2, p);
       const u64 y1 = mod_add(mod_sub(x0, x2, p), t, p);
       const u64 y2 = mod_sub(mod_sub(x0, x1, p), t, p);
       dst[s] = y0;
-      dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hi[H + sh], p);
-      dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
+      dst[S + s] = shoup_mul<P32>(shoup_mul<P32>(y1, lo[L + sl], p), hi[H + sh], p);
+      dst[2 * S + s] = shoup_mul<P32>(shoup_mul<P32>(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -742,25 +759,42 @@ template <int LOGR, int TW>
 void pass_fwd_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
   const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) / 2 * 16;
-  if (a.S > 1)
-    launch_pass_kernel<k_pass_fwd<LOGR, true, TW>, TW, NTK>(a, ncols, np, sm, st);
-  else
-    launch_pass_kernel<k_pass_fwd<LOGR, false, TW>, TW, NTK>(a, ncols, np, sm, st);
+  if (a.p32) {
+    if (a.S > 1)
+      launch_pass_kernel<k_pass_fwd<LOGR, true, TW, true>, TW, NTK>(a, ncols, np, sm, st);
+    else
+      launch_pass_kernel<k_pass_fwd<LOGR, false, TW, true>, TW, NTK>(a, ncols, np, sm, st);
+  } else {
+    if (a.S > 1)
+      launch_pass_kernel<k_pass_fwd<LOGR, true, TW, false>, TW, NTK>(a, ncols, np, sm, st);
+    else
+      launch_pass_kernel<k_pass_fwd<LOGR, false, TW, false>, TW, NTK>(a, ncols, np, sm, st);
+  }
 }
 template <int LOGR, int TW>
 void pass_inv_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
   const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) / 2 * 16;
-  if (a.S > 1)
-    launch_pass_kernel<k_pass_inv<LOGR, true, TW>, TW, NTK>(a, ncols, np, sm, st);
-  else
-    launch_pass_kernel<k_pass_inv<LOGR, false, TW>, TW, NTK>(a, ncols, np, sm, st);
+  if (a.p32) {
+    if (a.S > 1)
+      launch_pass_kernel<k_pass_inv<LOGR, true, TW, true>, TW, NTK>(a, ncols, np, sm, st);
+    else
+      launch_pass_kernel<k_pass_inv<LOGR, false, TW, true>, TW, NTK>(a, ncols, np, sm, st);
+  } else {
+    if (a.S > 1)
+      launch_pass_kernel<k_pass_inv<LOGR, true, TW, false>, TW, NTK>(a, ncols, np, sm, st);
+    else
+      launch_pass_kernel<k_pass_inv<LOGR, false, TW, false>, TW, NTK>(a, ncols, np, sm, st);
+  }
 }
 template <int LOGR, int TW>
 void pass_fused_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
   const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) * 16;
-  launch_pass_kernel<k_pass_fused<LOGR, TW>, TW, NTK>(a, ncols, np, sm, st);
+  if (a.p32)
+    launch_pass_kernel<k_pass_fused<LOGR, TW, true>, TW, NTK>(a, ncols, np, sm, st);
+  else
+    launch_pass_kernel<k_pass_fused<LOGR, TW, false>, TW, NTK>(a, ncols, np, sm, st);
 }
 
 template <int LOGR>
@@ -814,13 +848,13 @@ void launch_pass_fused(int logR, const PassArgs& a, unsigned long long ncols, in
 void launch_radix3(bool inverse, const Radix3Args& a, int np, cudaStream_t st) {
   const int g = grid_for(a.S, 256);
   if (inverse)
-    launch_pdl(k_radix3_inv, dim3(g, np), dim3(256), 0, st, a);
+    launch_pdl(a.p32 ? k_radix3_inv<true> : k_radix3_inv<false>, dim3(g, np), dim3(256), 0, st, a);
   else
-    launch_pdl(k_radix3_fwd, dim3(g, np), dim3(256), 0, st, a);
+    launch_pdl(a.p32 ? k_radix3_fwd<true> : k_radix3_fwd<false>, dim3(g, np), dim3(256), 0, st, a);
 }
 
 void launch_gen_pass_table(TwPair* out, u64 root_mont, u64 scale_mont, int R, int /*logR*/, unsigned long long S,
-                           u64 p, u64 recip, cudaStream_t st) {
+                           u64 p, u64 recip, cudaStream_t st, unsigned long long order) {
   GenArgs g;
   g.out = out;
   g.root_mont = root_mont;
@@ -835,15 +869,18 @@ void launch_gen_pass_table(TwPair* out, u64 root_mont, u64 scale_mont, int R, in
   g.recip = recip;
   g.R = R;
   g.S = S;
-  g.M = (unsigned long long)R * S;
-  k_gen_table<<<grid_for(g.M, 256), 256, 0, st>>>(g);
+  g.M = order ? order : (unsigned long long)R * S;  // order of the root (exponents reduced mod M)
+  k_gen_table<<<grid_for((unsigned long long)R * S, 256), 256, 0, st>>>(g);
 }
 
 void launch_pack(const char* digits, unsigned long long nd, unsigned be, u64* limbs, unsigned long long total,
                  unsigned* err, cudaStream_t st, int row_bits, unsigned long long row_stride,
-                 unsigned long long off) {
+                 unsigned long long off, bool lead_check) {
   if (row_bits < 8)
     k_pack_rows<<<grid_for(total, 256), 256, 0, st>>>(digits, nd, be, limbs, total, err, row_bits, row_stride, off);
+  else if (!lead_check)
+    launch_pdl(be > 16 ? k_pack<false, 5, false> : k_pack<false, 4, false>, dim3(grid_for(total, 256)), dim3(256), 0,
+               st, digits, nd, be, limbs, total, err, row_bits, row_stride, off);
   else
     launch_pdl(row_bits >= 63 ? (be > 16 ? k_pack<false, 5> : k_pack<false, 4>)
                               : (be > 16 ? k_pack<true, 5> : k_pack<true, 4>),
@@ -852,8 +889,9 @@ void launch_pack(const char* digits, unsigned long long nd, unsigned be, u64* li
 }
 void launch_pack_radix3(const char* digits, unsigned long long nd, unsigned be, const Radix3Args& a, unsigned* err,
                         cudaStream_t st) {
-  launch_pdl(be > 16 ? k_pack_radix3<5> : k_pack_radix3<4>, dim3(grid_for(a.S, kPackLimbs)), dim3(kPackLimbs), 0, st,
-             digits, nd, be, a, err);
+  auto fn = a.p32 ? (be > 16 ? k_pack_radix3<5, true> : k_pack_radix3<4, true>)
+                  : (be > 16 ? k_pack_radix3<5, false> : k_pack_radix3<4, false>);
+  launch_pdl(fn, dim3(grid_for(a.S, kPackLimbs)), dim3(kPackLimbs), 0, st, digits, nd, be, a, err);
 }
 void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, unsigned long long rows,
                           unsigned long long width, bool to_segments, cudaStream_t st) {

@@ -13,6 +13,12 @@ constexpr int kTileLogW = 4;  // 16 columns per pass tile: one 128 B row segment
 constexpr int kTileW = 1 << kTileLogW;
 constexpr int kPassThreads = 256;
 constexpr int kMaxPassLog = 9;  // radix of one pass <= 512 (64 KiB tile)
+// p == 1 (mod 2^32): the transforms use the cheaper q p of shoup_mul<true>
+#ifndef DMG_NO_P32
+inline bool prime_p32(u64 p) { return (p & 0xffffffffull) == 1; }
+#else
+inline bool prime_p32(u64) { return false; }  // A/B: the generic reduction for every prime
+#endif
 
 // ---- programmatic dependent launch (PDL) for the product's kernel chain ----
 // Chain kernels are launched with programmatic stream serialization: the next grid is
@@ -62,6 +68,8 @@ struct PassArgs {
   const TwPair* dft_fwd[2];  // omega_R^k, k < R/2
   const TwPair* dft_inv[2];  // omega_R^-k, k < R/2
   const TwPair* pass_tw[2];  // T[f][s] = omega_M^{+-f s} (* scale), R x S; nullptr when S == 1
+                             // (tw_lbits > 0: the factorised lo[f][s mod 2^tw_lbits], R x 2^tw_lbits)
+  const TwPair* pass_hi[2];  // factorised: hi[f][s >> tw_lbits] (* scale), R x S / 2^tw_lbits
   TwPair final_scale[2];   // fused single-pass transforms: (c, c') applied after the inverse
   u64 p[2], pp[2];
   unsigned long long S;    // column stride (elements)
@@ -73,6 +81,8 @@ struct PassArgs {
   // Column-sharded pass (this rank owns columns [tw_off, tw_off + S) of a global S' = 2^tw_logS).
   int tw_logS;
   unsigned long long tw_off;
+  int p32;                 // every prime of the launch is == 1 mod 2^32 (shoup_mul<true>)
+  int tw_lbits;            // 0: full R x S twiddle table; else the factorised pair (see pass_tw)
 };
 
 // Radix-3 pass over N = 3 S. The twiddle omega_N^{+-f s} (times the convolution
@@ -92,6 +102,7 @@ struct Radix3Args {
   // Unsharded: cb = sb = 0, off = 0 (s = l).
   int cb, sb;
   unsigned long long off;
+  int p32;              // both primes == 1 mod 2^32
 };
 
 // Launchers (kernels.cu).
@@ -100,13 +111,15 @@ void launch_pass_inv(int logR, const PassArgs& a, unsigned long long ncols, int 
 void launch_pass_fused(int logR, const PassArgs& a, unsigned long long ncols, int nprimes, cudaStream_t st);
 void launch_radix3(bool inverse, const Radix3Args& a, int nprimes, cudaStream_t st);
 
+// out[f][s] = root^(f s mod order) * scale (Shoup pairs), f < R, s < S; order 0 = R S.
 void launch_gen_pass_table(TwPair* out, u64 root_m, u64 scale, int R, int logR, unsigned long long S, u64 p,
-                           u64 recip, cudaStream_t st);
+                           u64 recip, cudaStream_t st, unsigned long long order = 0);
 // Local limb i is global limb ((i >> row_bits) * row_stride) + off + (i & (2^row_bits - 1)):
 // unsharded packs use row_bits = 63, off = 0 (limb i = i). Sharded packs need 2^row_bits >= 256.
+// lead_check false (unsharded map only): no leading-zero check (a rank's compacted digit slices).
 void launch_pack(const char* digits, unsigned long long nd, unsigned base_exp, u64* limbs,
                  unsigned long long nlimbs_total, unsigned* err, cudaStream_t st, int row_bits = 63,
-                 unsigned long long row_stride = 0, unsigned long long off = 0);
+                 unsigned long long row_stride = 0, unsigned long long off = 0, bool lead_check = true);
 // Pack fused with the forward radix-3 pass (N = 3 S, unsharded): digits -> pass 0's output
 // of both primes (a.dst), lo/hi/lam/p/lbits/hrow as for launch_radix3; a.src unused.
 void launch_pack_radix3(const char* digits, unsigned long long nd, unsigned base_exp, const Radix3Args& a,

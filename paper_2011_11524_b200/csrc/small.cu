@@ -40,6 +40,7 @@ __device__ unsigned long long g_phase_cycles[12];
 constexpr int NT = 256;  // 8 warps, 3 CTAs/SM at <= 85 registers; measured fastest of 192/256/320/384(x3) and 512(x2)
 
 struct SmallField {
+  static constexpr bool kP32 = false;
   static constexpr bool kSwz = true;  // tables stored at tw_slot(k) (ntt_tile.cuh)
   u64 p0, p1;
   const TwPair* t0;

@@ -79,17 +79,21 @@ def test_config3_uniform_fingerprints(gpu, port, ref):
 
 
 def test_config3_uniform_times_nines(gpu, port, ref):
-    """Non-squaring worst case: one operand all nines."""
+    """Non-squaring worst case at config-3 size: 1e8 uniform digits (seed 2) times 1e8 nines
+    (SURVEY §8(d) cfg3), against the SHA-256 of the reference's own product
+    (tests/golden/golden_large.json config3x, also equal to the closed form x 10^n - x)."""
     import torch
 
-    n = 3 * 10**7
+    n = 10**8
     x = torch.empty(n, dtype=torch.uint8, device="cuda")
     y = torch.empty(n, dtype=torch.uint8, device="cuda")
-    gpu.generate_digits(x.data_ptr(), n, 5)
+    gpu.generate_digits(x.data_ptr(), n, 2)
     gpu.generate_digits(y.data_ptr(), n, 0, mode=1)
     out = torch.empty(2 * n, dtype=torch.uint8, device="cuda")
     ln = gpu.multiply_device(x.data_ptr(), n, y.data_ptr(), n, out.data_ptr(), 2 * n)
     hx, hy, hz = bytes(x.cpu().numpy()), bytes(y.cpu().numpy()), bytes(out[:ln].cpu().numpy())
+    g = large_golden("config3x")
+    assert g["seeds"] == [2, "nines"] and (len(hz), sha(hz)) == (g["length"], g["sha256"])
     _check_fingerprints(port, ref, hx, hy, hz)
 
 
@@ -128,6 +132,8 @@ def test_config5_ten_billion_digits(gpu, port, ref):
     assert plan["large_pair"] and plan["length"] == 3 << 29 and plan["base_exp"] == 14
     x, y, out, ln = _device_product(gpu, n, n, 50, 51)
     assert ln in (2 * n - 1, 2 * n)
+    # the first power-of-two pass (R = 256, S = 2^21) uses factorised twiddle tables
+    assert gpu.stats()["table_bytes"] < 4 << 30
     z = out[:ln]
     assert int(z[0]) != ord("0")
     with open(GOLDEN_LARGE) as f:

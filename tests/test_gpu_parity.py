@@ -123,6 +123,27 @@ def test_lean_memory_plan(gpu, ref):
         os.environ.pop("DECMUL_FORCE_LARGE_PAIR", None)
 
 
+def test_factorised_pass_tables(gpu, ref):
+    """Factorised inter-pass twiddles lo[f][s mod L] * hi[f][s / L] (config 5's memory plan)
+    forced at small sizes for both prime pairs, every pass with S > 1, forward and inverse."""
+    import paper_2011_11524_b200 as dm2
+
+    os.environ["DECMUL_FACTOR_TABLES"] = "1"
+    try:
+        for large in (False, True):
+            if large:
+                os.environ["DECMUL_FORCE_LARGE_PAIR"] = "1"
+            ctx = dm2.Context(0)  # fresh plans: tables are built per context
+            for nx, ny in ((70000, 50000), (300001, 250000), (1200000, 1100000)):
+                x, y = inputs.gen_digits(nx + 3, nx), inputs.gen_digits(ny + 4, ny)
+                assert ctx.multiply_text(x, y) == ref.multiply(x, y), (large, nx, ny)
+            assert ctx.multiply_text(x, None) == ref.multiply(x, None), large
+            ctx.close()
+    finally:
+        os.environ.pop("DECMUL_FACTOR_TABLES", None)
+        os.environ.pop("DECMUL_FORCE_LARGE_PAIR", None)
+
+
 def test_errors_match_reference_types(gpu):
     with pytest.raises(ValueError, match="non-digit"):
         gpu.multiply_text(b"12a4" * 1000, b"5" * 100)

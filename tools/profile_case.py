@@ -19,8 +19,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--digits", type=int, default=0, help="override both operand sizes (single products)")
     a = ap.parse_args()
-    cfg = bench.CONFIGS[a.config]
+    cfg = dict(bench.CONFIGS[a.config])
+    if a.digits:
+        cfg.update(nx=a.digits, ny=a.digits)
     ctx = dm.Context(0)
     s = torch.cuda.Stream()
     torch.cuda.set_stream(s)
