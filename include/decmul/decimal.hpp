@@ -176,6 +176,10 @@ inline std::string to_decimal(const PackedOperand& x) {  // reference decimal.cp
 struct MultiplyOptions {
   AdjustStrategy strategy = AdjustStrategy::kConditionalSelect;  // accepted; products identical under both
   unsigned forced_base_exp = 0;
+  // Extension (last, so the reference's initialisers still compile): the prime pair of the
+  // planner, which the reference's multiply pins to production_primes() (decimal.cpp:194).
+  // {0, 0}: the reference pair, or the large pair beyond its 3 * 2^24 cap.
+  PrimePair primes{0, 0};
 };
 
 // Exact decimal product on the GPU; x and y may alias (squaring saves one transform).
@@ -184,8 +188,9 @@ inline DecimalNumber multiply(const DecimalNumber& x, const DecimalNumber& y, co
   decmul_gpu_ctx* ctx = detail::context();
   std::string out(x.digit_count() + y.digit_count(), '\0');
   std::size_t n = 0;
-  detail::check(decmul_gpu_multiply(ctx, x.text().data(), x.digit_count(), y.text().data(), y.digit_count(),
-                                    out.data(), out.size(), &n, opt.forced_base_exp, &x == &y ? 1 : 0),
+  const decmul_gpu_multiply_options o{opt.forced_base_exp, opt.primes.p1, opt.primes.p2, &x == &y ? 1 : 0};
+  detail::check(decmul_gpu_multiply_ex(ctx, x.text().data(), x.digit_count(), y.text().data(), y.digit_count(),
+                                       out.data(), out.size(), &n, &o),
                 ctx);
   out.resize(n);
   return from_device_result(std::move(out));

@@ -77,11 +77,33 @@ int decmul_gpu_plan(decmul_gpu_ctx* ctx, size_t digits_x, size_t digits_y, unsig
 int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
                         size_t cap, size_t* out_len, unsigned forced_base_exp, int alias);
 
+/* decmul_gpu_multiply with the options of the reference's multiply (MultiplyOptions,
+ * decimal.hpp:170-173) plus the prime pair of its planner (select_base_and_length(dx, dy, pair,
+ * forced), decimal.hpp:71-72, which the reference's multiply pins to production_primes(),
+ * decimal.cpp:194): p1 = p2 = 0 picks the reference pair, or the large pair beyond its
+ * 3 * 2^24 cap; otherwise two primes p1 < p2 < 2^63 (DECMUL_EINVAL if not; DECMUL_ETOOLARGE
+ * when the pair cannot hold the product, as the reference's planner raises OperandTooLarge). */
+typedef struct {
+  unsigned forced_base_exp;
+  uint64_t p1, p2;
+  int alias; /* the reference's &x == &y squaring path */
+} decmul_gpu_multiply_options;
+int decmul_gpu_multiply_ex(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
+                           size_t cap, size_t* out_len, const decmul_gpu_multiply_options* opt);
+
 /* decmul_gpu_multiply sharded over the context's devices whatever the size (a product too
  * small for the shard shape fails with DECMUL_EINVAL); what decmul_gpu_multiply does on its own
  * for large products. Exposed for parity tests of the sharded path at small sizes. */
 int decmul_gpu_multiply_sharded(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
                                 size_t cap, size_t* out_len, int alias);
+
+/* Concurrency: decmul_gpu_multiply calls from several threads on one context whose products run
+ * as one CTA each (transform length <= 3 * 2^10 or 2^11, no forced base, no alias) are
+ * coalesced: the first caller leads, waits for the context, and runs every product queued by
+ * then as one batch launch; the others sleep until their result is in. Results and errors are
+ * per call (a failing batch is rerun product by product). DECMUL_COALESCE=0 disables it.
+ * decmul_gpu_coalesce_stats reports the batches and products run that way. */
+int decmul_gpu_coalesce_stats(decmul_gpu_ctx* ctx, unsigned long long* batches, unsigned long long* products);
 
 /* Device-resident variant: digits in and out stay in HBM. stream = cudaStream_t (NULL = the
  * context's stream). If out_len is NULL the call is asynchronous (no host sync; read the

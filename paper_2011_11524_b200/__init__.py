@@ -35,8 +35,8 @@ __all__ = [
 
 P1 = 9223372036015915009  # reference primes.hpp:30
 P2 = 9223372036166909953  # reference primes.hpp:31
-Q1 = 9223371564408373249  # find_primes(64, 32, 2) (primes.cpp:70-81): lengths beyond 3 * 2^24
-Q2 = 9223371938070528001  # (both == 1 mod 2^32)
+Q1 = 9223371938070528001  # find_primes(64, 30, 2) (primes.cpp:70-81): lengths beyond 3 * 2^24
+Q2 = 9223371941291753473
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -59,7 +59,8 @@ EXPORTED_SYMBOLS = [
     "decmul_gpu_shard_reorder", "decmul_gpu_shard_carry_begin", "decmul_gpu_shard_carry_probe",
     "decmul_gpu_shard_carry_emit", "decmul_gpu_selftest", "decmul_gpu_multiply_batch_ptrs",
     "decmul_gpu_check_errors", "decmul_gpu_profile", "decmul_gpu_profile_report", "decmul_gpu_create_multi",
-    "decmul_gpu_context_devices", "decmul_gpu_multiply_sharded",
+    "decmul_gpu_context_devices", "decmul_gpu_multiply_sharded", "decmul_gpu_multiply_ex",
+    "decmul_gpu_coalesce_stats",
 ]
 
 
@@ -85,6 +86,10 @@ _szp = C.POINTER(C.c_size_t)
 class _PlanInfo(C.Structure):
     _fields_ = [("base_exp", C.c_uint), ("length", C.c_size_t), ("p1", C.c_uint64), ("p2", C.c_uint64),
                 ("large_pair", C.c_int), ("one_cta", C.c_int)]
+
+
+class _MulOpts(C.Structure):
+    _fields_ = [("forced_base_exp", C.c_uint), ("p1", C.c_uint64), ("p2", C.c_uint64), ("alias", C.c_int)]
 
 
 class _Stats(C.Structure):
@@ -146,9 +151,12 @@ class PackedOperand:
 class MultiplyOptions:
     """reference decimal.hpp:170-173. ``strategy`` is the reference's CPU codegen
     knob (words.hpp:29); products are identical under both, so it is accepted
-    and ignored."""
+    and ignored. ``primes`` (extension): the planner's prime pair (p1, p2), which the
+    reference's multiply pins to production_primes() (decimal.cpp:194); None = the
+    reference pair, or the large pair beyond its 3 * 2^24 cap."""
     strategy: int = 1
     forced_base_exp: int = 0
+    primes: tuple[int, int] | None = None
 
 
 class DecimalNumber:
@@ -264,6 +272,12 @@ class Context:
         self._call("decmul_gpu_get_stats", C.byref(s))
         return dict(last_launches=s.last_launches, table_bytes=s.table_bytes)
 
+    def coalesce_stats(self) -> tuple[int, int]:
+        """(batches, products) run by the coalescing path of concurrent small multiplies."""
+        b, p = C.c_ulonglong(), C.c_ulonglong()
+        self._call("decmul_gpu_coalesce_stats", C.byref(b), C.byref(p))
+        return b.value, p.value
+
     def check_errors(self, stream: int = 0) -> None:
         """Raise the errors of the asynchronous entry points since the last check (syncs stream)."""
         self._call("decmul_gpu_check_errors", C.c_void_p(stream))
@@ -285,15 +299,22 @@ class Context:
         return out
 
     # ---- multiply ----
-    def multiply_text(self, x: bytes, y: bytes | None, forced_base_exp: int = 0) -> bytes:
-        """Digits in host memory -> product digits. y=None is the aliased squaring path."""
+    def multiply_text(self, x: bytes, y: bytes | None, forced_base_exp: int = 0,
+                      primes: tuple[int, int] | None = None) -> bytes:
+        """Digits in host memory -> product digits. y=None is the aliased squaring path;
+        primes = the planner's prime pair (decmul_gpu_multiply_ex), None = automatic."""
         alias = y is None
         y = x if alias else y
         cap = len(x) + len(y) + 1
         out = C.create_string_buffer(cap)
         n = C.c_size_t()
-        self._call("decmul_gpu_multiply", x, C.c_size_t(len(x)), y, C.c_size_t(len(y)), out, C.c_size_t(cap),
-                   C.byref(n), C.c_uint(forced_base_exp), C.c_int(int(alias)))
+        if primes is None:
+            self._call("decmul_gpu_multiply", x, C.c_size_t(len(x)), y, C.c_size_t(len(y)), out, C.c_size_t(cap),
+                       C.byref(n), C.c_uint(forced_base_exp), C.c_int(int(alias)))
+        else:
+            o = _MulOpts(forced_base_exp, primes[0], primes[1], int(alias))
+            self._call("decmul_gpu_multiply_ex", x, C.c_size_t(len(x)), y, C.c_size_t(len(y)), out,
+                       C.c_size_t(cap), C.byref(n), C.byref(o))
         return out.raw[: n.value]
 
     def multiply_device(self, d_x: int, nx: int, d_y: int, ny: int, d_out: int, cap: int, stream: int = 0,
@@ -460,7 +481,7 @@ def multiply(x: DecimalNumber, y: DecimalNumber, opt: MultiplyOptions | None = N
     ctx = ctx or default_context()
     if x.is_zero() or y.is_zero():
         return DecimalNumber()
-    z = ctx.multiply_text(x.text(), None if x is y else y.text(), opt.forced_base_exp)
+    z = ctx.multiply_text(x.text(), None if x is y else y.text(), opt.forced_base_exp, opt.primes)
     return DecimalNumber(z, _trusted=True)
 
 

@@ -1,7 +1,9 @@
 // extern "C" implementation of include/decmul_gpu.h over dmg::Engine.
+#include <condition_variable>
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <vector>
 #include <new>
 #include <string>
 
@@ -9,11 +11,34 @@
 #include "engine.hpp"
 #include "multi.hpp"
 
+// One pending small product of the coalescing path (decmul_gpu_multiply from several threads).
+struct CoalescedReq {
+  const char* x;
+  size_t nx;
+  const char* y;
+  size_t ny;
+  char* out;
+  size_t cap;
+  size_t len = 0;
+  int rc = 0;
+  std::string msg;
+  bool done = false;
+};
+
 struct decmul_gpu_ctx {
   std::unique_ptr<dmg::MultiEngine> multi;  // one engine per device of the context
   dmg::Engine* eng = nullptr;               // the first device's engine (device-pointer calls, hooks)
   std::mutex mu;
   std::string err;
+  // coalescing of concurrent small products (leader/follower): callers queue their product;
+  // the first becomes the leader, takes the context lock (waiting out the batch in flight,
+  // while more callers queue) and runs everything queued as one batch (one k_small launch
+  // per size group); followers sleep until their result is in
+  std::mutex qmu;
+  std::condition_variable qcv;
+  std::vector<CoalescedReq*> queue;
+  bool leader = false;
+  unsigned long long coalesced_batches = 0, coalesced_products = 0;
 };
 
 namespace {
@@ -155,8 +180,101 @@ int decmul_gpu_plan(decmul_gpu_ctx* ctx, size_t dx, size_t dy, unsigned forced, 
   });
 }
 
+namespace {
+
+// Products that run as one CTA each (the batch kernel): worth coalescing across threads.
+bool coalescable(size_t nx, size_t ny, unsigned forced, int alias) {
+  if (forced || alias || nx < 2 || ny < 2) return false;
+  const char* e = std::getenv("DECMUL_COALESCE");
+  if (e && e[0] == '0') return false;
+  try {
+    const dmg::PairChoice pc = dmg::choose_pair(nx, ny, 0, true);
+    const size_t N = pc.bp.length;
+    const int three = N % 3 == 0;
+    const size_t c = three ? N / 3 : N;
+    return __builtin_ctzll(c) <= dmg::small_max_logc(three);
+  } catch (const std::exception&) {
+    return false;
+  }
+}
+
+// Runs the queued products as a batch (the caller holds ctx->mu); on any failure every product
+// is rerun on its own so each caller gets its own result or error.
+void run_coalesced(decmul_gpu_ctx* ctx, std::vector<CoalescedReq*>& batch) {
+  const size_t n = batch.size();
+  std::vector<const char*> xs(n), ys(n);
+  std::vector<char*> outs(n);
+  std::vector<size_t> nxs(n), nys(n), caps(n), lens(n);
+  for (size_t i = 0; i < n; ++i) {
+    xs[i] = batch[i]->x;
+    ys[i] = batch[i]->y;
+    outs[i] = batch[i]->out;
+    nxs[i] = batch[i]->nx;
+    nys[i] = batch[i]->ny;
+    caps[i] = batch[i]->cap;
+  }
+  const int rc = guarded(ctx, [&] {
+    ctx->multi->multiply_batch_ptrs(n, xs.data(), nxs.data(), ys.data(), nys.data(), outs.data(), caps.data(),
+                                    lens.data());
+  });
+  if (rc == DECMUL_OK) {
+    for (size_t i = 0; i < n; ++i) batch[i]->len = lens[i];
+    return;
+  }
+  for (CoalescedReq* r : batch) {
+    r->rc = guarded(ctx, [&] { r->len = ctx->multi->multiply_host(r->x, r->nx, r->y, r->ny, r->out, r->cap, 0, false); });
+    if (r->rc) r->msg = ctx->err;
+  }
+}
+
+int multiply_coalesced(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out, size_t cap,
+                       size_t* out_len) {
+  CoalescedReq req{x, nx, y, ny, out, cap};
+  {
+    std::unique_lock<std::mutex> q(ctx->qmu);
+    ctx->queue.push_back(&req);
+    if (ctx->leader) {  // follower: the current or next leader runs this product
+      ctx->qcv.wait(q, [&] { return req.done; });
+      if (req.rc) {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        ctx->err = req.msg;
+      }
+      *out_len = req.len;
+      return req.rc;
+    }
+    ctx->leader = true;
+  }
+  std::vector<CoalescedReq*> batch;
+  {
+    std::lock_guard<std::mutex> lock_(ctx->mu);  // waits for the batch in flight; callers keep queueing
+    DeviceGuard dev_(ctx->eng->device());
+    {
+      std::lock_guard<std::mutex> q(ctx->qmu);
+      batch.swap(ctx->queue);
+      ctx->leader = false;  // the next caller leads the next batch
+    }
+    run_coalesced(ctx, batch);
+    ++ctx->coalesced_batches;
+    ctx->coalesced_products += batch.size();
+    if (req.rc) ctx->err = req.msg;
+  }
+  {
+    std::lock_guard<std::mutex> q(ctx->qmu);
+    for (CoalescedReq* r : batch) r->done = true;
+  }
+  ctx->qcv.notify_all();
+  *out_len = req.len;
+  return req.rc;
+}
+
+}  // namespace
+
 int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
                         size_t cap, size_t* out_len, unsigned forced, int alias) {
+  if (ctx && out_len && coalescable(nx, ny, forced, alias) && !(nx == ny && x == y)) {
+    bool valid = cap >= nx + ny && x[0] != '0' && y[0] != '0';
+    if (valid) return multiply_coalesced(ctx, x, nx, y, ny, out, cap, out_len);
+  }
   LOCKED(ctx, {
     if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
     const bool xz = nx == 1 && x[0] == '0', yz = ny == 1 && y[0] == '0';
@@ -172,6 +290,27 @@ int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const cha
       return;
     }
     *out_len = ctx->multi->multiply_host(x, nx, y, ny, out, cap, forced, alias != 0);
+  });
+}
+
+int decmul_gpu_multiply_ex(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
+                           size_t cap, size_t* out_len, const decmul_gpu_multiply_options* opt) {
+  LOCKED(ctx, {
+    const decmul_gpu_multiply_options o = opt ? *opt : decmul_gpu_multiply_options{0, 0, 0, 0};
+    if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
+    const bool xz = nx == 1 && x[0] == '0', yz = ny == 1 && y[0] == '0';
+    if (xz || yz) {  // decimal.cpp:193, after DecimalNumber::parse validated both texts
+      for (size_t i = 0; i < nx; ++i)
+        if (x[i] < '0' || x[i] > '9') throw std::invalid_argument("decimal: non-digit character");
+      for (size_t i = 0; i < ny; ++i)
+        if (y[i] < '0' || y[i] > '9') throw std::invalid_argument("decimal: non-digit character");
+      if ((nx > 1 && x[0] == '0') || (ny > 1 && y[0] == '0')) throw std::invalid_argument("decimal: leading zero");
+      if (cap < 1) throw std::length_error("multiply: output buffer too small");
+      out[0] = '0';
+      *out_len = 1;
+      return;
+    }
+    *out_len = ctx->multi->multiply_host(x, nx, y, ny, out, cap, o.forced_base_exp, o.alias != 0, o.p1, o.p2);
   });
 }
 
@@ -385,6 +524,13 @@ int decmul_gpu_selftest(decmul_gpu_ctx* ctx, int inject_fault, char* report, siz
       std::memcpy(report, r.data(), n);
       report[n] = '\0';
     }
+  });
+}
+
+int decmul_gpu_coalesce_stats(decmul_gpu_ctx* ctx, unsigned long long* batches, unsigned long long* products) {
+  LOCKED(ctx, {
+    if (batches) *batches = ctx->coalesced_batches;
+    if (products) *products = ctx->coalesced_products;
   });
 }
 

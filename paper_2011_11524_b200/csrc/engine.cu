@@ -25,12 +25,6 @@ bool factor_tables(std::size_t entries) {
   return entries * sizeof(TwPair) > (std::size_t(4) << 30);
 }
 
-// every prime of a launch == 1 mod 2^32: the kernels' shoup_mul<true> instantiation
-bool p32_of(const PrimePlan* const pl[2], int np) {
-  for (int q = 0; q < np; ++q)
-    if (!prime_p32(pl[q]->p)) return false;
-  return true;
-}
 
 u64 recip_of(u64 d) {  // reference make_div_by_const (decimal.hpp:93-104), for a normalized divisor
   return u64(~(u128)0 / d - ((u128)1 << 64));
@@ -329,8 +323,15 @@ std::size_t Engine::table_bytes() const {
   return b;
 }
 
-ProductPlan Engine::plan_product(std::size_t dx, std::size_t dy, unsigned forced) const {
-  PairChoice pc = choose_pair(dx, dy, forced, /*allow_large=*/true);
+ProductPlan Engine::plan_product(std::size_t dx, std::size_t dy, unsigned forced, u64 p1, u64 p2) const {
+  PairChoice pc;
+  if (p1 || p2) {  // caller-chosen pair (the reference's select_base_and_length(dx, dy, pair, forced))
+    if (!(p1 < p2) || p2 >= (u64(1) << 63) || !is_prime(p1) || !is_prime(p2))
+      throw std::invalid_argument("multiply: prime pair must be two primes p1 < p2 < 2^63");
+    pc = PairChoice{p1, p2, select_base_and_length(dx, dy, p1, p2, forced), false};
+  } else {
+    pc = choose_pair(dx, dy, forced, /*allow_large=*/true);
+  }
   ProductPlan pp;
   pp.dx = dx;
   pp.dy = dy;
@@ -395,7 +396,6 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
       a.cb = L.cb;
       a.sb = L.sb;
       a.off = L.off;
-      a.p32 = p32_of(pl, np);
       launch_radix3(false, a, np, st);
       prof_mark("k_radix3_fwd", st, double(np) * 3.0 * double(L.S), double(np) * 48.0 * double(L.S));
     } else {
@@ -418,7 +418,6 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
       a.G = L.groups;
       a.tw_logS = L.tw_logS;
       a.tw_off = L.tw_off;
-      a.p32 = p32_of(pl, np);
       launch_pass_fwd(P.logR, a, L.ncols, np, st);
       if (prof_on_) {
         char nm[64];
@@ -456,7 +455,6 @@ void Engine::pass_fused(const PrimePlan* pl[2], int np, u64* const data[2], cons
   a.G = L.groups;
   a.tw_logS = 0;
   a.has_final_scale = any_table ? 0 : 1;
-  a.p32 = p32_of(pl, np);
   launch_pass_fused(P.logR, a, L.ncols, np, st);
   if (prof_on_) {
     char nm[64];
@@ -489,7 +487,6 @@ void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std:
       a.cb = L.cb;
       a.sb = L.sb;
       a.off = L.off;
-      a.p32 = p32_of(pl, np);
       launch_radix3(true, a, np, st);
       prof_mark("k_radix3_inv", st, double(np) * 4.0 * double(L.S), double(np) * 48.0 * double(L.S));
     } else {
@@ -513,7 +510,6 @@ void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std:
       a.tw_logS = L.tw_logS;
       a.tw_off = L.tw_off;
       a.has_final_scale = (!any_table && ii == 0) ? 1 : 0;
-      a.p32 = p32_of(pl, np);
       a.tw_lbits = P.tw_lbits;
       launch_pass_inv(P.logR, a, L.ncols, np, st);
       if (prof_on_) {
@@ -661,7 +657,6 @@ void Engine::pack_radix3(const PrimePlan* pl[2], const char* digits, std::size_t
   a.S = P.S;
   a.lbits = P.r3_lbits;
   a.hrow = P.S >> a.lbits;
-  a.p32 = p32_of(pl, 2);
   launch_pack_radix3(digits, nd, be, a, err, st);
   ++launches_;
   prof_mark("k_pack_radix3", st, 2.0 * double(P.S) * 5.0, double(nd) + 48.0 * double(P.S));
@@ -855,7 +850,6 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
     r.S = P0.S;
     r.lbits = P0.r3_lbits;
     r.hrow = P0.S >> r.lbits;
-    r.p32 = p32_of(pl, 2);
     launches_ += launch_carry_r3(c, r, st);
   } else {
     launches_ += recover(c, be, std::min(lx, ly), s_in_x, st);
@@ -901,7 +895,7 @@ std::size_t Engine::result_length() {
 }
 
 std::size_t Engine::multiply_host(const char* x, std::size_t nx, const char* y, std::size_t ny, char* out,
-                                  std::size_t cap, unsigned forced, bool alias) {
+                                  std::size_t cap, unsigned forced, bool alias, u64 p1, u64 p2) {
   if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
   if ((nx == 1 && x[0] == '0') || (ny == 1 && y[0] == '0')) {  // zero short-circuit (decimal.cpp:193)
     if (cap < 1) throw std::length_error("multiply: output buffer too small");
@@ -909,7 +903,7 @@ std::size_t Engine::multiply_host(const char* x, std::size_t nx, const char* y, 
     return 1;
   }
   const bool squaring = alias || (nx == ny && (x == y || std::memcmp(x, y, nx) == 0));
-  const ProductPlan pp = plan_product(nx, ny, forced);
+  const ProductPlan pp = plan_product(nx, ny, forced, p1, p2);
   if (cap < nx + ny) throw std::length_error("multiply: output buffer too small");
   din_x_.ensure(nx);
   if (!squaring) din_y_.ensure(ny);

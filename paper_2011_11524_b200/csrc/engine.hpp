@@ -172,11 +172,12 @@ class Engine {
   int device() const { return device_; }
   cudaStream_t stream() const { return stream_; }
 
-  ProductPlan plan_product(std::size_t dx, std::size_t dy, unsigned forced_base_exp) const;
+  // p1 = p2 = 0: the reference pair, or the large pair beyond its 3 * 2^24 cap; else that pair
+  ProductPlan plan_product(std::size_t dx, std::size_t dy, unsigned forced_base_exp, u64 p1 = 0, u64 p2 = 0) const;
 
   // Host strings -> host string (reference decmul::multiply semantics).
   std::size_t multiply_host(const char* x, std::size_t nx, const char* y, std::size_t ny, char* out,
-                            std::size_t cap, unsigned forced_base_exp, bool alias);
+                            std::size_t cap, unsigned forced_base_exp, bool alias, u64 p1 = 0, u64 p2 = 0);
   // Device digits -> device digits; stream-ordered; *out_len written (host) after sync.
   std::size_t multiply_device(const char* dx, std::size_t nx, const char* dy, std::size_t ny, char* dout,
                               std::size_t cap, unsigned forced_base_exp, bool squaring, cudaStream_t st,

@@ -26,12 +26,10 @@ typedef unsigned __int128 u128;
 constexpr u64 kP1 = 9223372036015915009ull;  // 91625968973 * 3 * 2^25 + 1
 constexpr u64 kP2 = 9223372036166909953ull;  // 183251937949 * 3 * 2^24 + 1
 // Large-length pair: the two largest results of the reference's own search
-// find_primes(64, 32, 2) (primes.cpp:70-81). Used only when the
-// production pair cannot hold the transform (N > 3 * 2^24). n_min = 32 (rather than 30)
-// makes both primes == 1 mod 2^32, so the q p of every Shoup product is one 32-bit IMAD
-// (modarith.cuh shoup_mul<true>); transforms up to 3 * 2^32.
-constexpr u64 kQ1 = 9223371564408373249ull;  // 357913923 * 3 * 2^33 + 1
-constexpr u64 kQ2 = 9223371938070528001ull;  // 715827875 * 3 * 2^32 + 1
+// find_primes(64, 30, 2) (primes.cpp:70-81). Used only when the
+// production pair cannot hold the transform (N > 3 * 2^24).
+constexpr u64 kQ1 = 9223371938070528001ull;  // 715827875 * 3 * 2^32 + 1
+constexpr u64 kQ2 = 9223371941291753473ull;  // 2863311501 * 3 * 2^30 + 1
 
 struct OperandTooLarge : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -199,9 +197,9 @@ inline ShardShape shard_shape(std::size_t N, const std::vector<int>& radices, in
 }
 
 struct PairChoice {
-  u64 p1, p2;
+  u64 p1 = 0, p2 = 0;
   BasePlan bp;
-  bool large_pair;  // true when the q-pair had to be used (beyond the reference's 3*2^24 cap)
+  bool large_pair = false;  // true when the q-pair had to be used (beyond the reference's 3*2^24 cap)
 };
 
 // The reference pair wherever it can hold the product (bit-comparable spectra);

@@ -59,13 +59,18 @@ struct Geom {
   }
   // v omega_M^{f s}: one Shoup product with the full R x S table, or two with the factorised
   // tables lo[f][s mod 2^lb] * hi[f][s >> lb] (tw_lb > 0; hi carries the scale)
-  template <bool P32>
+  // (FACT is a template parameter: a runtime branch here split the unrolled 8-element groups
+  // into separate blocks and cost the R = 512 passes 5-28%)
+  template <bool FACT>
   __device__ __forceinline__ u64 twist(u64 v, const TwPair* T, const TwPair* Hi, int r, int w, u64 p) const {
     const unsigned long long f = (unsigned long long)bitrev(r, LOGR);
-    if (tw_lb == 0) return shoup_mul<P32>(v, T[(f << tw_logS) + tw_col + w], p);
-    const unsigned long long s = tw_col + w;
-    v = shoup_mul<P32>(v, T[(f << tw_lb) + (s & ((1ull << tw_lb) - 1))], p);
-    return shoup_mul<P32>(v, Hi[(f << (tw_logS - tw_lb)) + (s >> tw_lb)], p);
+    if constexpr (!FACT) {
+      return shoup_mul(v, T[(f << tw_logS) + tw_col + w], p);
+    } else {
+      const unsigned long long s = tw_col + w;
+      v = shoup_mul(v, T[(f << tw_lb) + (s & ((1ull << tw_lb) - 1))], p);
+      return shoup_mul(v, Hi[(f << (tw_logS - tw_lb)) + (s >> tw_lb)], p);
+    }
   }
 };
 
@@ -149,7 +154,7 @@ constexpr int pass_min_blocks(int logr, int tw) {
 // Forward pass: column DIFs, then the inter-pass twiddle omega_M^{f s} (row passes).
 // The first round reads HBM into registers and the last round writes HBM from
 // registers; shared memory carries only the rounds in between.
-template <int LOGR, bool ROWS, int TW, bool P32>
+template <int LOGR, bool ROWS, int TW, bool FACT = false>
 __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_fwd(PassArgs a) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
   // first round's HBM loads above that barrier (config 5 +5%)
@@ -165,7 +170,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   const TwPair* __restrict__ T = a.pass_tw[pr];
   const TwPair* __restrict__ Hi = a.pass_hi[pr];
   const Geom<LOGR, ROWS, TW> G(a);
-  if (ROWS && a.tw_lbits == 0) {
+  if constexpr (ROWS && !FACT) {
     // The twiddles are applied in the epilogue, after the DIF; start pulling the tile's
     // rows T[f][s0 .. s0 + TW) (TW pairs = TW * 16 bytes each) into L2 now so those
     // loads hit L2 instead of DRAM (large-S passes stream a table of N / 3 .. N pairs).
@@ -188,17 +193,17 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << E1];
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i, w)];
-      dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>, P32>(v, j0, tw, p);
+      dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>>(v, j0, tw, p);
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) {
-        if (ROWS) v[i] = G.template twist<P32>(v[i], T, Hi, base + i, w, p);
+        if (ROWS) v[i] = G.template twist<FACT>(v[i], T, Hi, base + i, w, p);
         dst[G.at(base + i, w)] = v[i];
       }
     }
     return;
   } else {
     if constexpr (kStageFwd<ROWS, TW>) {
-      dif_rounds_smem<LOGR, LOGR, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>, P32>{p, tw}, tid, NTK);
+      dif_rounds_smem<LOGR, LOGR, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
     } else {
       constexpr int ST1 = 1 << (LOGR - E1);
       for (int g = tid; g < (R >> E1) * TW; g += NTK) {
@@ -208,12 +213,12 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
         u64 v[1 << E1];
 #pragma unroll
         for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i * ST1, w)];
-        dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>, P32>(v, j0, tw, p);
+        dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>>(v, j0, tw, p);
 #pragma unroll
         for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
       }
       __syncthreads();
-      dif_rounds_smem<LOGR, LOGR - E1, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>, P32>{p, tw}, tid, NTK);
+      dif_rounds_smem<LOGR, LOGR - E1, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
     }
     for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
@@ -222,10 +227,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i, w)];
-      dif_regs<LOGR, EL, EL, kSwzTables<ROWS>, P32>(v, 0, tw, p);
+      dif_regs<LOGR, EL, EL, kSwzTables<ROWS>>(v, 0, tw, p);
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
-        if (ROWS) v[i] = G.template twist<P32>(v[i], T, Hi, base + i, w, p);
+        if (ROWS) v[i] = G.template twist<FACT>(v[i], T, Hi, base + i, w, p);
         dst[G.at(base + i, w)] = v[i];
       }
     }
@@ -242,7 +247,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
 constexpr int pass_inv_min_blocks(int logr, int tw) {
   return (logr == 9 && tw == kTileW) ? DMG_INV_MINB9 : pass_min_blocks(logr, tw);
 }
-template <int LOGR, bool ROWS, int TW, bool P32>
+template <int LOGR, bool ROWS, int TW, bool FACT = false>
 __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LOGR, TW)) k_pass_inv(PassArgs a) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
   // first round's HBM loads above that barrier (config 5 +5%)
@@ -275,13 +280,13 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
 #pragma unroll
     for (int i = 0; i < (1 << E1); ++i) {
       v[i] = STAGE ? sm[L(base + i, w)] : src[G.at(base + i, w)];
-      if (ROWS) v[i] = G.template twist<P32>(v[i], T, Hi, base + i, w, p);
+      if (ROWS) v[i] = G.template twist<FACT>(v[i], T, Hi, base + i, w, p);
     }
-    dit_regs<LOGR, 0, E1, kSwzTables<ROWS>, P32>(v, 0, tw, p);
+    dit_regs<LOGR, 0, E1, kSwzTables<ROWS>>(v, 0, tw, p);
 #pragma unroll
     for (int i = 0; i < (1 << E1); ++i) {
       if constexpr (LOGR == E1) {
-        if (a.has_final_scale) v[i] = shoup_mul<P32>(v[i], sc, p);
+        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
         dst[G.at(base + i, w)] = v[i];
       } else {
         sm[L(base + i, w)] = v[i];
@@ -290,7 +295,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   }
   if constexpr (LOGR > E1) {
     __syncthreads();
-    dit_rounds_smem<LOGR, E1, AL, TW>(sm, L, UniformField<kSwzTables<ROWS>, P32>{p, tw}, tid, NTK);
+    dit_rounds_smem<LOGR, E1, AL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
     constexpr int STL = 1 << AL;
     for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
@@ -299,10 +304,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i * STL, w)];
-      dit_regs<LOGR, AL, EL, kSwzTables<ROWS>, P32>(v, j0, tw, p);
+      dit_regs<LOGR, AL, EL, kSwzTables<ROWS>>(v, j0, tw, p);
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
-        if (a.has_final_scale) v[i] = shoup_mul<P32>(v[i], sc, p);
+        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
         dst[G.at(base + i * STL, w)] = v[i];
       }
     }
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
 // conv.cpp:205-208, :299-305) and the first inverse pass. The last DIF round
 // and the first DIT round act on the same 8-element groups, so DIF -> pointwise
 // -> DIT happens in registers.
-template <int LOGR, int TW, bool P32>
+template <int LOGR, int TW>
 __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_fused(PassArgs a) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
   // first round's HBM loads above that barrier (config 5 +5%)
@@ -341,7 +346,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   if constexpr (STAGE) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if constexpr (STAGE) {
-    dif_rounds_smem<LOGR, LOGR, EM, TW>(sm, L, UniformField<kSwzTables<false>, P32>{p, twf}, tid, NTK);
+    dif_rounds_smem<LOGR, LOGR, EM, TW>(sm, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
   } else if constexpr (LOGR > EM) {
     constexpr int ST1 = 1 << (LOGR - E1);
     for (int g = tid; g < (R >> E1) * TW; g += NTK) {
@@ -351,12 +356,12 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << E1];
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i * ST1, w)];
-      dif_regs<LOGR, LOGR, E1, kSwzTables<false>, P32>(v, j0, twf, p);
+      dif_regs<LOGR, LOGR, E1, kSwzTables<false>>(v, j0, twf, p);
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
     }
     __syncthreads();
-    dif_rounds_smem<LOGR, LOGR - E1, EM, TW>(sm, L, UniformField<kSwzTables<false>, P32>{p, twf}, tid, NTK);
+    dif_rounds_smem<LOGR, LOGR - E1, EM, TW>(sm, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
   }
   for (int g = tid; g < (R >> EM) * TW; g += NTK) {
     int w, q, j0, base;
@@ -365,14 +370,14 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
     u64 v[1 << EM];
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) v[i] = LOGR > EM ? sm[L(base + i, w)] : src[G.at(base + i, w)];
-    dif_regs<LOGR, EM, EM, kSwzTables<false>, P32>(v, 0, twf, p);
+    dif_regs<LOGR, EM, EM, kSwzTables<false>>(v, 0, twf, p);
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) v[i] = mont_mul(v[i], oth ? oth[G.at(base + i, w)] : v[i], p, pp);
-    dit_regs<LOGR, 0, EM, kSwzTables<false>, P32>(v, 0, twi, p);
+    dit_regs<LOGR, 0, EM, kSwzTables<false>>(v, 0, twi, p);
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) {
       if constexpr (LOGR == EM) {
-        if (a.has_final_scale) v[i] = shoup_mul<P32>(v[i], sc, p);
+        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
         dst[G.at(base + i, w)] = v[i];
       } else {
         sm[L(base + i, w)] = v[i];
@@ -381,7 +386,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   }
   if constexpr (LOGR > EM) {
     __syncthreads();
-    dit_rounds_smem<LOGR, EM, AL, TW>(sm, L, UniformField<kSwzTables<false>, P32>{p, twi}, tid, NTK);
+    dit_rounds_smem<LOGR, EM, AL, TW>(sm, L, UniformField<kSwzTables<false>>{p, twi}, tid, NTK);
     constexpr int STL = 1 << AL;
     for (int g = tid; g < (R >> EL) * TW; g += NTK) {
       int w, q, j0, base;
@@ -390,10 +395,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i * STL, w)];
-      dit_regs<LOGR, AL, EL, kSwzTables<false>, P32>(v, j0, twi, p);
+      dit_regs<LOGR, AL, EL, kSwzTables<false>>(v, j0, twi, p);
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
-        if (a.has_final_scale) v[i] = shoup_mul<P32>(v[i], sc, p);
+        if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
         dst[G.at(base + i * STL, w)] = v[i];
       }
     }
@@ -402,7 +407,6 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
 
 // Radix-3 pass (reference three_row_forward_columns conv.cpp:109-125, with the
 // length-3 DFT written with one multiplication: omega_3^2 = -1 - omega_3).
-template <bool P32>
 __global__ void k_radix3_fwd(Radix3Args a) {
   pdl_wait();
   const int pr = blockIdx.y;  // select, not index: keeps the parameter block out of local memory
@@ -419,19 +423,18 @@ __global__ void k_radix3_fwd(Radix3Args a) {
     const unsigned long long sg = ((s >> a.cb) << a.sb) + a.off + (s & ((1ull << a.cb) - 1));  // global column
     const unsigned long long sl = sg & (L - 1), sh = sg >> a.lbits;
     const u64 x0 = src[s], x1 = src[S + s], x2 = src[2 * S + s];
-    const u64 t = shoup_mul<P32>(mod_sub(x1, x2, p), lam, p);
+    const u64 t = shoup_mul(mod_sub(x1, x2, p), lam, p);
     const u64 y0 = mod_add(mod_add(x0, x1, p), x2, p);
     const u64 y1 = mod_add(mod_sub(x0, x2, p), t, p);
     const u64 y2 = mod_sub(mod_sub(x0, x1, p), t, p);
     dst[s] = y0;
-    dst[S + s] = shoup_mul<P32>(shoup_mul<P32>(y1, lo[L + sl], p), hi[H + sh], p);
-    dst[2 * S + s] = shoup_mul<P32>(shoup_mul<P32>(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
+    dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hi[H + sh], p);
+    dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
   }
 }
 
 // Inverse radix-3 pass (conv.cpp:129-147): twiddle (with the convolution scale
 // folded into the hi table when this is the first inverse pass) then length-3 IDFT*.
-template <bool P32>
 __global__ void k_radix3_inv(Radix3Args a) {
   pdl_wait();
   const int pr = blockIdx.y;  // select, not index: keeps the parameter block out of local memory
@@ -447,10 +450,10 @@ __global__ void k_radix3_inv(Radix3Args a) {
        s += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long sg = ((s >> a.cb) << a.sb) + a.off + (s & ((1ull << a.cb) - 1));  // global column
     const unsigned long long sl = sg & (L - 1), sh = sg >> a.lbits;
-    const u64 y0 = shoup_mul<P32>(src[s], hi[sh], p);  // lo[0][.] = 1
-    const u64 y1 = shoup_mul<P32>(shoup_mul<P32>(src[S + s], lo[L + sl], p), hi[H + sh], p);
-    const u64 y2 = shoup_mul<P32>(shoup_mul<P32>(src[2 * S + s], lo[2 * L + sl], p), hi[2 * H + sh], p);
-    const u64 t = shoup_mul<P32>(mod_sub(y1, y2, p), lam, p);
+    const u64 y0 = shoup_mul(src[s], hi[sh], p);  // lo[0][.] = 1
+    const u64 y1 = shoup_mul(shoup_mul(src[S + s], lo[L + sl], p), hi[H + sh], p);
+    const u64 y2 = shoup_mul(shoup_mul(src[2 * S + s], lo[2 * L + sl], p), hi[2 * H + sh], p);
+    const u64 t = shoup_mul(mod_sub(y1, y2, p), lam, p);
     dst[s] = mod_add(mod_add(y0, y1, p), y2, p);
     dst[S + s] = mod_add(mod_sub(y0, y2, p), t, p);
     dst[2 * S + s] = mod_sub(mod_sub(y0, y1, p), t, p);
@@ -585,21 +588,51 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d,
 // (factorised lo * hi as in k_radix3_fwd) for both primes, and writes pass 0's output.
 // The packed limbs never touch HBM (the separate pack wrote 8 B and the radix-3 pass read
 // them back per limb).
-template <int NG, bool P32>
+// Double-buffered staging of the spans (and of the twiddles) through cp.async measured slower
+// on config 4 (4.48 / 5.74 ms for the two launches vs 4.32 ms single-buffered); kept for A/B.
+#ifndef DMG_PACK_DB
+#define DMG_PACK_DB 0
+#endif
+#if DMG_PACK_DB
+// Dynamic shared memory of k_pack_radix3: two stages of (three digit spans, the lo twiddles of
+// rows 1 and 2 of both primes for the stage's kPackLimbs columns, and their hi factors).
+constexpr int kPackR3Smem = 2 * 3 * kPackBuf + 2 * 2 * 2 * kPackLimbs * 16 + 2 * 2 * 2 * 16;
+template <int NG>
 __global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restrict__ d, unsigned long long nd,
                                                            unsigned be, Radix3Args a, unsigned* err) {
   pdl_wait();
-  // two stages: the spans of the block's next columns stream in (cp.async) while it parses
-  // and transforms the current ones
-  __shared__ __align__(16) char smem[2][3][kPackBuf];
+  // two stages: the next columns' digit spans and twiddles stream in (cp.async) while the
+  // block parses and transforms the current ones, so neither HBM nor L2 latency is exposed
+  extern __shared__ __align__(16) char dsm[];
+  char(*span)[3][kPackBuf] = reinterpret_cast<char(*)[3][kPackBuf]>(dsm);
+  TwPair(*tlo)[2][2][kPackLimbs] = reinterpret_cast<TwPair(*)[2][2][kPackLimbs]>(dsm + 2 * 3 * kPackBuf);
+  TwPair(*thi)[2][2] = reinterpret_cast<TwPair(*)[2][2]>(dsm + 2 * 3 * kPackBuf + 2 * 2 * 2 * kPackLimbs * 16);
   const unsigned long long S = a.S, L = 1ull << a.lbits, H = a.hrow;
   const unsigned long long step = (unsigned long long)gridDim.x * kPackLimbs;
   unsigned bad = 0;
+  // the twiddles of columns [c0, c0 + kPackLimbs) (one L-block: kPackLimbs divides L)
+  auto stage_tw = [&](int stg, unsigned long long c0) {
+    const unsigned long long sl0 = c0 & (L - 1), sh = c0 >> a.lbits;
+    for (int i = threadIdx.x; i < 4 * kPackLimbs; i += kPackLimbs) {
+      const int pr = i / (2 * kPackLimbs), row = (i / kPackLimbs) & 1, c = i % kPackLimbs;
+      if (c0 + c >= S) continue;
+      const unsigned sa = unsigned(__cvta_generic_to_shared(&tlo[stg][pr][row][c]));
+      const TwPair* src = a.lo[pr] + (row + 1) * L + sl0 + c;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
+    }
+    if (threadIdx.x < 4) {
+      const int pr = threadIdx.x >> 1, row = threadIdx.x & 1;
+      const unsigned sa = unsigned(__cvta_generic_to_shared(&thi[stg][pr][row]));
+      const TwPair* src = a.hi[pr] + (row + 1) * H + sh;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
+    }
+  };
   long long ga[3] = {0, 0, 0}, gb[3] = {0, 0, 0};  // span origins of stages 0 / 1 (block-uniform)
   unsigned long long s0 = (unsigned long long)blockIdx.x * kPackLimbs;
   if (s0 < S) {
 #pragma unroll
-    for (int j = 0; j < 3; ++j) ga[j] = pack_stage<true>(d, nd, be, j * S + s0, smem[0][j]);
+    for (int j = 0; j < 3; ++j) ga[j] = pack_stage<true>(d, nd, be, j * S + s0, span[0][j]);
+    stage_tw(0, s0);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
   for (int cur = 0; s0 < S; s0 += step, cur ^= 1) {
@@ -607,17 +640,58 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restri
     if (n0 < S) {
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        const long long gn = pack_stage<true>(d, nd, be, j * S + n0, smem[cur ^ 1][j]);
+        const long long gn = pack_stage<true>(d, nd, be, j * S + n0, span[cur ^ 1][j]);
         if (cur) ga[j] = gn; else gb[j] = gn;
       }
+      stage_tw(cur ^ 1, n0);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // this stage's spans have landed
     __syncthreads();
-    const u64 x0 = pack_parse<NG>(d, nd, be, s0, smem[cur][0], cur ? gb[0] : ga[0], err, bad);
-    const u64 x1 = pack_parse<NG>(d, nd, be, S + s0, smem[cur][1], cur ? gb[1] : ga[1], err, bad);
-    const u64 x2 = pack_parse<NG>(d, nd, be, 2 * S + s0, smem[cur][2], cur ? gb[2] : ga[2], err, bad);
-    __syncthreads();  // smem[cur] is refilled by the next iteration's prefetch
+    const u64 x0 = pack_parse<NG>(d, nd, be, s0, span[cur][0], cur ? gb[0] : ga[0], err, bad);
+    const u64 x1 = pack_parse<NG>(d, nd, be, S + s0, span[cur][1], cur ? gb[1] : ga[1], err, bad);
+    const u64 x2 = pack_parse<NG>(d, nd, be, 2 * S + s0, span[cur][2], cur ? gb[2] : ga[2], err, bad);
+    const unsigned long long s = s0 + threadIdx.x;
+    if (s < S) {
+#pragma unroll
+      for (int pr = 0; pr < 2; ++pr) {
+        const u64 p = a.p[pr];
+        const TwPair lam = a.lam[pr];
+        u64* dst = a.dst[pr];
+        // limbs are < 10^17 < p: canonical residues of both primes
+        const u64 t = shoup_mul(mod_sub(x1, x2, p), lam, p);
+        const u64 y0 = mod_add(mod_add(x0, x1, p), x2, p);
+        const u64 y1 = mod_add(mod_sub(x0, x2, p), t, p);
+        const u64 y2 = mod_sub(mod_sub(x0, x1, p), t, p);
+        dst[s] = y0;
+        dst[S + s] = shoup_mul(shoup_mul(y1, tlo[cur][pr][0][threadIdx.x], p), thi[cur][pr][0], p);
+        dst[2 * S + s] = shoup_mul(shoup_mul(y2, tlo[cur][pr][1][threadIdx.x], p), thi[cur][pr][1], p);
+      }
+    }
+    __syncthreads();  // stage cur is refilled by the next iteration's prefetch
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (bad) atomicOr(err, kErrBadDigit);
+}
+#else
+template <int NG>
+__global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restrict__ d, unsigned long long nd,
+                                                           unsigned be, Radix3Args a, unsigned* err) {
+  pdl_wait();
+  __shared__ __align__(16) char smem[3][kPackBuf];
+  const unsigned long long S = a.S, L = 1ull << a.lbits, H = a.hrow;
+  unsigned bad = 0;
+  for (unsigned long long s0 = (unsigned long long)blockIdx.x * kPackLimbs; s0 < S;
+       s0 += (unsigned long long)gridDim.x * kPackLimbs) {
+    // the three spans in flight together, one barrier
+    long long g[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) g[j] = pack_stage(d, nd, be, j * S + s0, smem[j]);
+    __syncthreads();
+    const u64 x0 = pack_parse<NG>(d, nd, be, s0, smem[0], g[0], err, bad);
+    const u64 x1 = pack_parse<NG>(d, nd, be, S + s0, smem[1], g[1], err, bad);
+    const u64 x2 = pack_parse<NG>(d, nd, be, 2 * S + s0, smem[2], g[2], err, bad);
+    __syncthreads();
     const unsigned long long s = s0 + threadIdx.x;
     if (s >= S) continue;
     const unsigned long long sl = s & (L - 1), sh = s >> a.lbits;
@@ -629,18 +703,18 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restri
       const TwPair* __restrict__ hi = a.hi[pr];
       u64* dst = a.dst[pr];
       // limbs are < 10^17 < p: canonical residues of both primes
-      const u64 t = shoup_mul<P32>(mod_sub(x1, x2, p), lam, p);
+      const u64 t = shoup_mul(mod_sub(x1, x2, p), lam, p);
       const u64 y0 = mod_add(mod_add(x0, x1, p), x2, p);
       const u64 y1 = mod_add(mod_sub(x0, x2, p), t, p);
       const u64 y2 = mod_sub(mod_sub(x0, x1, p), t, p);
       dst[s] = y0;
-      dst[S + s] = shoup_mul<P32>(shoup_mul<P32>(y1, lo[L + sl], p), hi[H + sh], p);
-      dst[2 * S + s] = shoup_mul<P32>(shoup_mul<P32>(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
+      dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hi[H + sh], p);
+      dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
     }
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
   if (bad) atomicOr(err, kErrBadDigit);
 }
+#endif
 
 // Column-sharded pack for rows narrower than one 256-limb block: one limb per thread.
 __global__ void k_pack_rows(const char* __restrict__ d, unsigned long long nd, unsigned be, u64* __restrict__ limbs,
@@ -759,42 +833,29 @@ template <int LOGR, int TW>
 void pass_fwd_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
   const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) / 2 * 16;
-  if (a.p32) {
-    if (a.S > 1)
-      launch_pass_kernel<k_pass_fwd<LOGR, true, TW, true>, TW, NTK>(a, ncols, np, sm, st);
-    else
-      launch_pass_kernel<k_pass_fwd<LOGR, false, TW, true>, TW, NTK>(a, ncols, np, sm, st);
-  } else {
-    if (a.S > 1)
-      launch_pass_kernel<k_pass_fwd<LOGR, true, TW, false>, TW, NTK>(a, ncols, np, sm, st);
-    else
-      launch_pass_kernel<k_pass_fwd<LOGR, false, TW, false>, TW, NTK>(a, ncols, np, sm, st);
-  }
+  if (a.S > 1 && a.tw_lbits)
+    launch_pass_kernel<k_pass_fwd<LOGR, true, TW, true>, TW, NTK>(a, ncols, np, sm, st);
+  else if (a.S > 1)
+    launch_pass_kernel<k_pass_fwd<LOGR, true, TW>, TW, NTK>(a, ncols, np, sm, st);
+  else
+    launch_pass_kernel<k_pass_fwd<LOGR, false, TW>, TW, NTK>(a, ncols, np, sm, st);
 }
 template <int LOGR, int TW>
 void pass_inv_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
   const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) / 2 * 16;
-  if (a.p32) {
-    if (a.S > 1)
-      launch_pass_kernel<k_pass_inv<LOGR, true, TW, true>, TW, NTK>(a, ncols, np, sm, st);
-    else
-      launch_pass_kernel<k_pass_inv<LOGR, false, TW, true>, TW, NTK>(a, ncols, np, sm, st);
-  } else {
-    if (a.S > 1)
-      launch_pass_kernel<k_pass_inv<LOGR, true, TW, false>, TW, NTK>(a, ncols, np, sm, st);
-    else
-      launch_pass_kernel<k_pass_inv<LOGR, false, TW, false>, TW, NTK>(a, ncols, np, sm, st);
-  }
+  if (a.S > 1 && a.tw_lbits)
+    launch_pass_kernel<k_pass_inv<LOGR, true, TW, true>, TW, NTK>(a, ncols, np, sm, st);
+  else if (a.S > 1)
+    launch_pass_kernel<k_pass_inv<LOGR, true, TW>, TW, NTK>(a, ncols, np, sm, st);
+  else
+    launch_pass_kernel<k_pass_inv<LOGR, false, TW>, TW, NTK>(a, ncols, np, sm, st);
 }
 template <int LOGR, int TW>
 void pass_fused_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
   const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) * 16;
-  if (a.p32)
-    launch_pass_kernel<k_pass_fused<LOGR, TW, true>, TW, NTK>(a, ncols, np, sm, st);
-  else
-    launch_pass_kernel<k_pass_fused<LOGR, TW, false>, TW, NTK>(a, ncols, np, sm, st);
+  launch_pass_kernel<k_pass_fused<LOGR, TW>, TW, NTK>(a, ncols, np, sm, st);
 }
 
 template <int LOGR>
@@ -848,9 +909,9 @@ void launch_pass_fused(int logR, const PassArgs& a, unsigned long long ncols, in
 void launch_radix3(bool inverse, const Radix3Args& a, int np, cudaStream_t st) {
   const int g = grid_for(a.S, 256);
   if (inverse)
-    launch_pdl(a.p32 ? k_radix3_inv<true> : k_radix3_inv<false>, dim3(g, np), dim3(256), 0, st, a);
+    launch_pdl(k_radix3_inv, dim3(g, np), dim3(256), 0, st, a);
   else
-    launch_pdl(a.p32 ? k_radix3_fwd<true> : k_radix3_fwd<false>, dim3(g, np), dim3(256), 0, st, a);
+    launch_pdl(k_radix3_fwd, dim3(g, np), dim3(256), 0, st, a);
 }
 
 void launch_gen_pass_table(TwPair* out, u64 root_mont, u64 scale_mont, int R, int /*logR*/, unsigned long long S,
@@ -889,9 +950,17 @@ void launch_pack(const char* digits, unsigned long long nd, unsigned be, u64* li
 }
 void launch_pack_radix3(const char* digits, unsigned long long nd, unsigned be, const Radix3Args& a, unsigned* err,
                         cudaStream_t st) {
-  auto fn = a.p32 ? (be > 16 ? k_pack_radix3<5, true> : k_pack_radix3<4, true>)
-                  : (be > 16 ? k_pack_radix3<5, false> : k_pack_radix3<4, false>);
-  launch_pdl(fn, dim3(grid_for(a.S, kPackLimbs)), dim3(kPackLimbs), 0, st, digits, nd, be, a, err);
+  auto fn = be > 16 ? k_pack_radix3<5> : k_pack_radix3<4>;
+#if DMG_PACK_DB
+  constexpr int smem = kPackR3Smem;
+  if (be > 16)
+    set_smem<k_pack_radix3<5>>(smem);
+  else
+    set_smem<k_pack_radix3<4>>(smem);
+#else
+  constexpr int smem = 0;
+#endif
+  launch_pdl(fn, dim3(grid_for(a.S, kPackLimbs)), dim3(kPackLimbs), size_t(smem), st, digits, nd, be, a, err);
 }
 void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, unsigned long long rows,
                           unsigned long long width, bool to_segments, cudaStream_t st) {

@@ -13,12 +13,6 @@ constexpr int kTileLogW = 4;  // 16 columns per pass tile: one 128 B row segment
 constexpr int kTileW = 1 << kTileLogW;
 constexpr int kPassThreads = 256;
 constexpr int kMaxPassLog = 9;  // radix of one pass <= 512 (64 KiB tile)
-// p == 1 (mod 2^32): the transforms use the cheaper q p of shoup_mul<true>
-#ifndef DMG_NO_P32
-inline bool prime_p32(u64 p) { return (p & 0xffffffffull) == 1; }
-#else
-inline bool prime_p32(u64) { return false; }  // A/B: the generic reduction for every prime
-#endif
 
 // ---- programmatic dependent launch (PDL) for the product's kernel chain ----
 // Chain kernels are launched with programmatic stream serialization: the next grid is
@@ -81,7 +75,6 @@ struct PassArgs {
   // Column-sharded pass (this rank owns columns [tw_off, tw_off + S) of a global S' = 2^tw_logS).
   int tw_logS;
   unsigned long long tw_off;
-  int p32;                 // every prime of the launch is == 1 mod 2^32 (shoup_mul<true>)
   int tw_lbits;            // 0: full R x S twiddle table; else the factorised pair (see pass_tw)
 };
 
@@ -102,7 +95,6 @@ struct Radix3Args {
   // Unsharded: cb = sb = 0, off = 0 (s = l).
   int cb, sb;
   unsigned long long off;
-  int p32;              // both primes == 1 mod 2^32
 };
 
 // Launchers (kernels.cu).

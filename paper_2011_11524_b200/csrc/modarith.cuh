@@ -55,27 +55,15 @@ __device__ __forceinline__ u64 mod_sub(u64 a, u64 b, u64 p) { return adjust_sign
 
 // x in [0, 2^64), w < p: returns x w mod p in [0, p).
 // (Measured on B200: folding -q p as q (2^64 - p) plus an explicit predicated
-// select was 3% slower than letting ptxas schedule this form.)
-//
-// P32: p = p_hi 2^32 + 1, i.e. p == 1 (mod 2^32) — both primes of the large pair, the
-// reference's own search find_primes(64, 32, 2) (primes.cpp:70-81). Then
-// q p mod 2^64 = q_lo + (q_lo p_hi + q_hi) 2^32: one 32-bit IMAD instead of the
-// IMAD.WIDE + 2 IMAD of a 64 x 64 low product, on the FMA pipe that binds the transforms.
-template <bool P32 = false>
+// select was 3% slower than letting ptxas schedule this form. Rejected too: for primes
+// == 1 mod 2^32 writing q p as q_lo + (q_lo p_hi + q_hi) 2^32 — ptxas kept the same
+// IMAD.WIDE count and the transforms slowed down.)
 __device__ __forceinline__ u64 shoup_mul(u64 x, u64 w, u64 wp, u64 p) {
   u64 q = __umul64hi(x, wp);
-  u64 qp;
-  if constexpr (P32) {
-    const unsigned ql = unsigned(q), qh = unsigned(q >> 32), ph = unsigned(p >> 32);
-    qp = ((u64)(ql * ph + qh) << 32) | ql;
-  } else {
-    qp = q * p;
-  }
-  u64 r = x * w - qp;  // exact, r < 2p
+  u64 r = x * w - q * p;  // exact, r < 2p
   return adjust_signed(r - p, p);
 }
-template <bool P32 = false>
-__device__ __forceinline__ u64 shoup_mul(u64 x, TwPair t, u64 p) { return shoup_mul<P32>(x, t.w, t.wp, p); }
+__device__ __forceinline__ u64 shoup_mul(u64 x, TwPair t, u64 p) { return shoup_mul(x, t.w, t.wp, p); }
 
 // REDC(a b) = a b 2^-64 mod p for a b < p 2^64 (one operand may lie in [0, 2p)).
 __device__ __forceinline__ u64 mont_mul(u64 a, u64 b, u64 p, u64 pp) {
@@ -103,10 +91,9 @@ __device__ __forceinline__ u64 solinas_mul(u64 a, u64 b) {
 }
 
 // Gentleman-Sande butterfly (reference ntt.cpp:42-47): (u + v, (u - v) w).
-template <bool P32 = false>
 __device__ __forceinline__ void bfly_dif(u64& u, u64& v, TwPair t, u64 p) {
   u64 a = mod_add(u, v, p);
-  v = shoup_mul<P32>(u - v + p, t, p);  // u - v + p in [1, 2p)
+  v = shoup_mul(u - v + p, t, p);  // u - v + p in [1, 2p)
   u = a;
 }
 __device__ __forceinline__ void bfly_dif1(u64& u, u64& v, u64 p) {  // factor 1 (j = 0 peel)
@@ -115,9 +102,8 @@ __device__ __forceinline__ void bfly_dif1(u64& u, u64& v, u64 p) {  // factor 1 
   u = a;
 }
 // Cooley-Tukey butterfly (reference ntt.cpp:65-70): (u + v w, u - v w).
-template <bool P32 = false>
 __device__ __forceinline__ void bfly_dit(u64& u, u64& v, TwPair t, u64 p) {
-  u64 w = shoup_mul<P32>(v, t, p);
+  u64 w = shoup_mul(v, t, p);
   v = mod_sub(u, w, p);
   u = mod_add(u, w, p);
 }

@@ -117,16 +117,16 @@ bool MultiEngine::shards(std::size_t nx, std::size_t ny, unsigned forced) const 
 }
 
 std::size_t MultiEngine::multiply_host(const char* x, std::size_t nx, const char* y, std::size_t ny, char* out,
-                                       std::size_t cap, unsigned forced, bool alias) {
+                                       std::size_t cap, unsigned forced, bool alias, u64 p1, u64 p2) {
   if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
   const bool zero = (nx == 1 && x[0] == '0') || (ny == 1 && y[0] == '0');
-  if (!zero && shards(nx, ny, forced)) {
+  if (!zero && !p1 && !p2 && shards(nx, ny, forced)) {
     const bool squaring = alias || (nx == ny && (x == y || std::memcmp(x, y, nx) == 0));
     if ((nx > 1 && x[0] == '0') || (ny > 1 && y[0] == '0')) throw std::invalid_argument("decimal: leading zero");
     return sharded_multiply(x, nx, y, ny, out, cap, squaring);
   }
   cudaSetDevice(eng_[0]->device());
-  return eng_[0]->multiply_host(x, nx, y, ny, out, cap, forced, alias);
+  return eng_[0]->multiply_host(x, nx, y, ny, out, cap, forced, alias, p1, p2);
 }
 
 // Runs f(rank, begin, end) for the G contiguous ranges of [0, count) on G host threads (each

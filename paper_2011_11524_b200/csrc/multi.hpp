@@ -22,7 +22,7 @@ class MultiEngine {
   // decmul::multiply on host strings: sharded over every device when the product is large
   // enough (shards()), else on the first device
   std::size_t multiply_host(const char* x, std::size_t nx, const char* y, std::size_t ny, char* out,
-                            std::size_t cap, unsigned forced_base_exp, bool alias);
+                            std::size_t cap, unsigned forced_base_exp, bool alias, u64 p1 = 0, u64 p2 = 0);
   // batches: contiguous ranges of products per device, one host thread per device
   void multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
                            const char* ys, std::size_t y_stride, std::size_t ny, char* outs,

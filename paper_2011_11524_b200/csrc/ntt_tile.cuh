@@ -53,7 +53,7 @@ struct Sched {
 // ---- register stages ----
 // DIF stages of one group: elements v[i] at positions base + i * STRIDE, STRIDE = 2^(MLOG-E),
 // j0 = base mod STRIDE. Spans 2^MLOG down to 2^(MLOG-E+1).
-template <int LOGR, int MLOG, int E, bool SWZ, bool P32 = false>
+template <int LOGR, int MLOG, int E, bool SWZ>
 __device__ __forceinline__ void dif_regs(u64 (&v)[1 << E], int j0, const TwPair* tw, u64 p) {
   constexpr int NE = 1 << E, STRIDE = 1 << (MLOG - E);
 #pragma unroll
@@ -70,13 +70,13 @@ __device__ __forceinline__ void dif_regs(u64 (&v)[1 << E], int j0, const TwPair*
       if (STRIDE == 1 && (i & (half - 1)) == 0)
         bfly_dif1(v[i], v[i + half], p);  // j = 0: factor 1 (reference ntt.cpp:39-41 peel)
       else
-        bfly_dif<P32>(v[i], v[i + half], t[i & (half - 1)], p);
+        bfly_dif(v[i], v[i + half], t[i & (half - 1)], p);
     }
   }
 }
 
 // DIT stages of one group: positions base + i * STRIDE, STRIDE = 2^ALOG; spans 2^(ALOG+1)..2^(ALOG+E).
-template <int LOGR, int ALOG, int E, bool SWZ, bool P32 = false>
+template <int LOGR, int ALOG, int E, bool SWZ>
 __device__ __forceinline__ void dit_regs(u64 (&v)[1 << E], int j0, const TwPair* tw, u64 p) {
   constexpr int NE = 1 << E, STRIDE = 1 << ALOG;
 #pragma unroll
@@ -93,7 +93,7 @@ __device__ __forceinline__ void dit_regs(u64 (&v)[1 << E], int j0, const TwPair*
       if (STRIDE == 1 && (i & (d - 1)) == 0)
         bfly_dit1(v[i], v[i + d], p);  // j = 0: factor 1 (reference ntt.cpp:62-64 peel)
       else
-        bfly_dit<P32>(v[i], v[i + d], t[i & (d - 1)], p);
+        bfly_dit(v[i], v[i + d], t[i & (d - 1)], p);
     }
   }
 }
@@ -129,12 +129,10 @@ struct ContigColumns {
   __device__ __forceinline__ int operator()(int r, int w) const { return (w << LOGR) + col_swizzle(r); }
 };
 
-// Same prime and table for every column; SWZ: the table is stored at tw_slot(k); P32: the
-// prime is == 1 mod 2^32 (shoup_mul<true>).
-template <bool SWZ, bool P32 = false>
+// Same prime and table for every column; SWZ: the table is stored at tw_slot(k).
+template <bool SWZ>
 struct UniformField {
   static constexpr bool kSwz = SWZ;
-  static constexpr bool kP32 = P32;
   u64 pv;
   const TwPair* t;
   __device__ __forceinline__ u64 p(int) const { return pv; }
@@ -163,7 +161,7 @@ __device__ __forceinline__ void dif_round_smem(u64* s, const L& idx, const F& fl
     u64 v[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) v[i] = s[idx(base + i * STRIDE, w)];
-    dif_regs<LOGR, MLOG, E, F::kSwz, F::kP32>(v, j0, fld.tw(w), fld.p(w));
+    dif_regs<LOGR, MLOG, E, F::kSwz>(v, j0, fld.tw(w), fld.p(w));
 #pragma unroll
     for (int i = 0; i < NE; ++i) s[idx(base + i * STRIDE, w)] = v[i];
   }
@@ -179,7 +177,7 @@ __device__ __forceinline__ void dit_round_smem(u64* s, const L& idx, const F& fl
     u64 v[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) v[i] = s[idx(base + i * STRIDE, w)];
-    dit_regs<LOGR, ALOG, E, F::kSwz, F::kP32>(v, j0, fld.tw(w), fld.p(w));
+    dit_regs<LOGR, ALOG, E, F::kSwz>(v, j0, fld.tw(w), fld.p(w));
 #pragma unroll
     for (int i = 0; i < NE; ++i) s[idx(base + i * STRIDE, w)] = v[i];
   }

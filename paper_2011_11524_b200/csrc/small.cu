@@ -37,10 +37,12 @@ __device__ unsigned long long g_phase_cycles[12];
   } while (0)
 #endif
 
+#ifndef DMG_SMALL_TW_PREFETCH
+#define DMG_SMALL_TW_PREFETCH 0
+#endif
 constexpr int NT = 256;  // 8 warps, 3 CTAs/SM at <= 85 registers; measured fastest of 192/256/320/384(x3) and 512(x2)
 
 struct SmallField {
-  static constexpr bool kP32 = false;
   static constexpr bool kSwz = true;  // tables stored at tw_slot(k) (ntt_tile.cuh)
   u64 p0, p1;
   const TwPair* t0;
@@ -118,6 +120,24 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
   if (32 + 16 * (nxv + nyv) + 48 + 16 <= kRegion) {
     char* xb = reinterpret_cast<char*>(sm + 2 * N) + 32;  // xb[k] = byte at address ax0 + k
     char* yb = xb + 16 * nxv + 48;
+    constexpr int LPT = (N + NT - 1) / NT;  // limbs per thread
+    // C = 2 NT (config 2: 3 x 512 at 256 threads): a thread's limbs t = tid + j NT are the
+    // three limbs s, s + C, s + 2C of its columns s = tid and tid + NT, so the radix-3
+    // column pass runs on them in registers (no limb store and reload).
+    constexpr bool kFuse3 = THREE && C == 2 * NT && LPT == 6;
+#if DMG_SMALL_TW_PREFETCH
+    // the radix-3 twiddles of the thread's two columns (both primes, rows 1 and 2; the same
+    // for x and y) are loaded with the digits, so their L2 latency hides behind the copies
+    TwPair tw3[2][2][2];
+    if constexpr (kFuse3) {
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int f = 1; f <= 2; ++f) tw3[cc][q][f - 1] = a.r3_fwd[q][f * C + tid + cc * NT];
+    }
+#endif
     for (int v = tid; v < nxv + nyv; v += NT) {
       const bool isx = v < nxv;
       char* dst = isx ? xb + 16 * v : yb + 16 * (v - nxv);
@@ -129,11 +149,6 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
     __syncthreads();
     DMG_PHASE(8);  // tables + digit loads
     unsigned bad = 0;
-    constexpr int LPT = (N + NT - 1) / NT;  // limbs per thread
-    // C = 2 NT (config 2: 3 x 512 at 256 threads): a thread's limbs t = tid + j NT are the
-    // three limbs s, s + C, s + 2C of its columns s = tid and tid + NT, so the radix-3
-    // column pass runs on them in registers (no limb store and reload).
-    constexpr bool kFuse3 = THREE && C == 2 * NT && LPT == 6;
     auto r3_columns = [&](const u64* lim, int first_arr) {
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
@@ -145,9 +160,15 @@ __global__ void __launch_bounds__(NT, 3) k_small(SmallArgs a) {
           u64* x = sm + (first_arr + q) * N + col_swizzle(sc);
           const u64 x0 = lim[cc], x1 = lim[cc + 2], x2 = lim[cc + 4];
           const u64 t = shoup_mul(mod_sub(x1, x2, p), a.lam[q], p);
+#if DMG_SMALL_TW_PREFETCH
+          const TwPair w1 = tw3[cc][q][0], w2 = tw3[cc][q][1];
+          (void)T;
+#else
+          const TwPair w1 = T[C + sc], w2 = T[2 * C + sc];
+#endif
           x[0] = mod_add(mod_add(x0, x1, p), x2, p);
-          x[C] = shoup_mul(mod_add(mod_sub(x0, x2, p), t, p), T[C + sc], p);
-          x[2 * C] = shoup_mul(mod_sub(mod_sub(x0, x1, p), t, p), T[2 * C + sc], p);
+          x[C] = shoup_mul(mod_add(mod_sub(x0, x2, p), t, p), w1, p);
+          x[2 * C] = shoup_mul(mod_sub(mod_sub(x0, x1, p), t, p), w2, p);
         }
       }
     };

@@ -377,3 +377,70 @@ def test_profile_report(gpu):
     assert all(ms >= 0 for _, ms, _, _ in rep)
     assert sum(mm for _, _, mm, _ in rep) > 0
     assert gpu.profile_report() == []
+
+
+def test_prime_pair_option(gpu, ref, port):
+    """MultiplyOptions' prime pair (decmul_gpu_multiply_ex; the reference's planner takes a
+    PrimePair, decimal.hpp:71-72, its multiply pins production_primes()): the reference pair,
+    the large pair and another pair from the reference's own search give the same digits; a
+    pair too small for the product raises OperandTooLarge like the reference's planner."""
+    import paper_2011_11524_b200 as dm2
+
+    other = tuple(sorted(port.find_primes(64, 26, 2)))
+    for nx, ny in ((10000, 10000), (250001, 200000), (3_000_000, 1_000_001)):
+        x, y = inputs.gen_digits(nx + 11, nx), inputs.gen_digits(ny + 12, ny)
+        want = ref.multiply(x, y)
+        for pair in ((P1, P2), (dm2.Q1, dm2.Q2), other):
+            assert gpu.multiply_text(x, y, primes=pair) == want, (pair, nx)
+    x = inputs.gen_digits(3, 50000)
+    assert gpu.multiply_text(x, None, primes=other) == ref.multiply(x, None)
+    with pytest.raises(ValueError, match="prime pair"):
+        gpu.multiply_text(b"12", b"34", primes=(P2, P1))
+    with pytest.raises(ValueError, match="prime pair"):
+        gpu.multiply_text(b"12", b"34", primes=(15, P1))
+    small = tuple(sorted(port.find_primes(64, 14, 2)))  # 2-adicity 14: N <= 3 * 2^14
+    with pytest.raises(dm2.OperandTooLarge):
+        gpu.multiply_text(b"7" * 2_000_000, b"3" * 2_000_000, primes=small)
+
+
+def test_concurrent_small_multiplies_coalesce(ref):
+    """decmul_gpu_multiply from 16 threads on one context: the small products are coalesced
+    into shared batch launches (leader/follower), every caller gets its own exact product,
+    and a bad operand fails only its own call."""
+    import threading
+
+    import paper_2011_11524_b200 as dm2
+
+    ctx = dm2.Context(0)
+    n_threads, per = 16, 40
+    pairs = [[(inputs.gen_digits(1000 * t + 2 * k, 10000), inputs.gen_digits(1000 * t + 2 * k + 1, 9000 + t))
+              for k in range(per)] for t in range(n_threads)]
+    results = [[None] * per for _ in range(n_threads)]
+    errors = []
+
+    def work(t):
+        try:
+            for k, (x, y) in enumerate(pairs[t]):
+                if t == 3 and k == 5:
+                    try:
+                        ctx.multiply_text(x[:100] + b"x" + x[101:], y)
+                        errors.append("no error for a bad digit")
+                    except ValueError:
+                        pass
+                results[t][k] = ctx.multiply_text(x, y)
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(n_threads)]
+    for h in th:
+        h.start()
+    for h in th:
+        h.join()
+    assert not errors, errors
+    for t in range(n_threads):
+        for k in range(0, per, 7):
+            x, y = pairs[t][k]
+            assert results[t][k] == ref.multiply(x, y), (t, k)
+    batches, products = ctx.coalesce_stats()
+    assert products >= n_threads * per and batches < products
+    ctx.close()
