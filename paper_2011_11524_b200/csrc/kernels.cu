@@ -23,6 +23,13 @@ namespace {
 constexpr int W = kTileW;
 constexpr int NT = kPassThreads;
 
+// bit reversal of a compile-time index (unrolled register groups)
+constexpr int crev(int i, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((i >> b) & 1) << (bits - 1 - b);
+  return r;
+}
+
 // Tile geometry. Row passes (S >= 16): one group g, 16 adjacent columns s0..s0+15;
 // element (r, w) at g R S + r S + s0 + w. Column passes (S == 1): 16 adjacent
 // groups, each a contiguous run of R words; element (r, w) at (c0 + w) R + r.
@@ -61,6 +68,33 @@ struct Geom {
   // tables lo[f][s mod 2^lb] * hi[f][s >> lb] (tw_lb > 0; hi carries the scale)
   // (FACT is a template parameter: a runtime branch here split the unrolled 8-element groups
   // into separate blocks and cost the R = 512 passes 5-28%)
+  // The same for the 2^E elements base + i of one register group (base = q 2^E, STRIDE 1):
+  // f_i = bitrev(base + i) = bitrev(i, E) 2^(LOGR - E) + bitrev(q, LOGR - E), so every row pointer
+  // is one per-group base plus a compile-time multiple of a per-kernel stride (the per-element
+  // bit reversal, shift and 64-bit index sum cost ~10 instructions per element in the epilogue).
+  template <int E, bool FACT>
+  __device__ __forceinline__ void twist_group(u64 (&v)[1 << E], const TwPair* T, const TwPair* Hi, int q, int w,
+                                              u64 p) const {
+    const unsigned long long f0 = (unsigned long long)bitrev(q, LOGR - E);
+    const unsigned long long s = tw_col + w;
+    if constexpr (!FACT) {
+      const TwPair* t0 = T + (f0 << tw_logS) + s;
+      const unsigned long long fs = 1ull << (LOGR - E + tw_logS);
+#pragma unroll
+      for (int i = 0; i < (1 << E); ++i) v[i] = shoup_mul(v[i], t0[(unsigned long long)crev(i, E) * fs], p);
+    } else {
+      const TwPair* l0 = T + (f0 << tw_lb) + (s & ((1ull << tw_lb) - 1));
+      const TwPair* h0 = Hi + (f0 << (tw_logS - tw_lb)) + (s >> tw_lb);
+      const unsigned long long fl = 1ull << (LOGR - E + tw_lb), fh = 1ull << (LOGR - E + tw_logS - tw_lb);
+#pragma unroll
+      for (int i = 0; i < (1 << E); ++i) {
+        const unsigned long long k = (unsigned long long)crev(i, E);
+        v[i] = shoup_mul(shoup_mul(v[i], l0[k * fl], p), h0[k * fh], p);
+      }
+    }
+  }
+  // element stride between consecutive rows of the tile
+  __device__ __forceinline__ unsigned long long row_stride() const { return ROWS ? (1ull << logS) : 1ull; }
   template <bool FACT>
   __device__ __forceinline__ u64 twist(u64 v, const TwPair* T, const TwPair* Hi, int r, int w, u64 p) const {
     const unsigned long long f = (unsigned long long)bitrev(r, LOGR);
@@ -141,14 +175,20 @@ __device__ __forceinline__ void group_coords(int g, int& w, int& q) {
 // Minimum resident CTAs per SM requested from ptxas (launch bounds), measured per shape:
 //  * R = 256: tiles use 34 KB of shared memory, so registers limit occupancy; capping them
 //    at 64 (4 CTAs/SM) is 1-2% faster on configs 3-5 than ptxas's own choice (80: 3 CTAs);
-//  * R = 512, 16-column tiles (68 KB, at most 3 CTAs/SM): no cap at all (1) lets ptxas use
-//    up to 124 registers at 2 CTAs/SM — faster on config 4 than 3 CTAs at <= 85;
+//  * R = 512, 16-column tiles (68 KB, at most 3 CTAs/SM): 3 (DMG_FWD_MINB9) for the forward
+//    pass; the fused/inverse ones below;
 //  * R = 512, 4-column tiles (small transforms, config 1): 3;
 //  * smaller radices: ptxas's default (0 = unspecified). NB an explicit 1 is not the
 //    default: it let ptxas double the registers of the R = 128 passes (6 -> 4 CTAs/SM,
 //    config 5 +2.6%).
+// R = 512 forward row passes: 3 CTAs/SM (<= 85 registers). The grouped epilogue addressing
+// (Geom::twist_group) let ptxas grow an unconstrained kernel to 106 registers (2 CTAs/SM);
+// capped, config 4's forward passes run 13.30 -> 12.75 ms.
+#ifndef DMG_FWD_MINB9
+#define DMG_FWD_MINB9 3
+#endif
 constexpr int pass_min_blocks(int logr, int tw) {
-  return logr == 9 ? (tw == kTileW ? 1 : 3) : (logr == 8 ? 4 : 0);
+  return logr == 9 ? (tw == kTileW ? DMG_FWD_MINB9 : 3) : (logr == 8 ? 4 : 0);
 }
 
 // Forward pass: column DIFs, then the inter-pass twiddle omega_M^{f s} (row passes).
@@ -194,11 +234,11 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i, w)];
       dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>>(v, j0, tw, p);
+      if constexpr (ROWS) G.template twist_group<E1, FACT>(v, T, Hi, q, w, p);
+      u64* d = dst + G.at(base, w);
+      const unsigned long long es = G.row_stride();
 #pragma unroll
-      for (int i = 0; i < (1 << E1); ++i) {
-        if (ROWS) v[i] = G.template twist<FACT>(v[i], T, Hi, base + i, w, p);
-        dst[G.at(base + i, w)] = v[i];
-      }
+      for (int i = 0; i < (1 << E1); ++i) d[i * es] = v[i];
     }
     return;
   } else {
@@ -228,11 +268,11 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i, w)];
       dif_regs<LOGR, EL, EL, kSwzTables<ROWS>>(v, 0, tw, p);
+      if constexpr (ROWS) G.template twist_group<EL, FACT>(v, T, Hi, q, w, p);
+      u64* d = dst + G.at(base, w);
+      const unsigned long long es = G.row_stride();
 #pragma unroll
-      for (int i = 0; i < (1 << EL); ++i) {
-        if (ROWS) v[i] = G.template twist<FACT>(v[i], T, Hi, base + i, w, p);
-        dst[G.at(base + i, w)] = v[i];
-      }
+      for (int i = 0; i < (1 << EL); ++i) d[i * es] = v[i];
     }
   }
 }
@@ -277,11 +317,16 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
     group_coords<LOGR, ROWS, E1, TW>(g, w, q);
     dit_group<0, E1>(q, j0, base);
     u64 v[1 << E1];
+    if constexpr (STAGE) {
 #pragma unroll
-    for (int i = 0; i < (1 << E1); ++i) {
-      v[i] = STAGE ? sm[L(base + i, w)] : src[G.at(base + i, w)];
-      if (ROWS) v[i] = G.template twist<FACT>(v[i], T, Hi, base + i, w, p);
+      for (int i = 0; i < (1 << E1); ++i) v[i] = sm[L(base + i, w)];
+    } else {
+      const u64* s0 = src + G.at(base, w);
+      const unsigned long long es = G.row_stride();
+#pragma unroll
+      for (int i = 0; i < (1 << E1); ++i) v[i] = s0[i * es];
     }
+    if constexpr (ROWS) G.template twist_group<E1, FACT>(v, T, Hi, q, w, p);
     dit_regs<LOGR, 0, E1, kSwzTables<ROWS>>(v, 0, tw, p);
 #pragma unroll
     for (int i = 0; i < (1 << E1); ++i) {

@@ -27,6 +27,9 @@ struct __align__(16) TwPair {  // Shoup form of one root-of-unity factor
 #ifndef DMG_CORR_FMA
 #define DMG_CORR_FMA 0
 #endif
+#ifndef DMG_CORR_PRED32
+#define DMG_CORR_PRED32 1
+#endif
 __device__ __forceinline__ u64 adjust_signed(u64 t, u64 p) {
 #if DMG_CORR_FMA
   // t + s p with the sign bit s = hi(t) >> 31 taken as mul.hi(hi(t), 2) and s p added by
@@ -42,6 +45,21 @@ __device__ __forceinline__ u64 adjust_signed(u64 t, u64 p) {
       "mov.b64 %0, {tl, th};\n\t}"
       : "+l"(t)
       : "l"(p));
+#elif DMG_CORR_PRED32
+  // 32-bit halves: the low add is predicated in place, ptxas selects only the high word
+  // (ISETP + @P IADD3 + IADD3.X + SEL: 4 instructions after the subtraction, not 5).
+  // Measured against the 64-bit predicated form below: config 3 -2.9%, config 4 -0.4%.
+  // (The FMA-pipe form above, on every site or only after Shoup products, was 5-16% slower:
+  // the transforms are issue-bound and IMAD.WIDE is the costlier slot.)
+  asm("{\n\t.reg .u32 tl, th, pl, ph;\n\t.reg .pred n;\n\t"
+      "mov.b64 {tl, th}, %0;\n\t"
+      "mov.b64 {pl, ph}, %1;\n\t"
+      "setp.lt.s32 n, th, 0;\n\t"
+      "@n add.cc.u32 tl, tl, pl;\n\t"
+      "@n addc.u32 th, th, ph;\n\t"
+      "mov.b64 %0, {tl, th};\n\t}"
+      : "+l"(t)
+      : "l"(p));
 #else
   // sign test + predicated add (ptxas emits ISETP + IADD3 + 2 SEL) rather than the
   // mask form SHF + 2 LOP3 + IADD3 + IADD3.X: measured 0.6% (config 2) and 1.8%
@@ -50,6 +68,23 @@ __device__ __forceinline__ u64 adjust_signed(u64 t, u64 p) {
 #endif
   return t;
 }
+// The same correction on the FMA pipe: s = sign bit by IMAD.HI, t += s p by IMAD.WIDE + IMAD.
+__device__ __forceinline__ u64 adjust_fma(u64 t, u64 p) {
+  asm("{\n\t.reg .u32 tl, th, s, pl, ph;\n\t"
+      "mov.b64 {tl, th}, %0;\n\t"
+      "mov.b64 {pl, ph}, %1;\n\t"
+      "mul.hi.u32 s, th, 2;\n\t"
+      "mad.wide.u32 %0, s, pl, %0;\n\t"
+      "mov.b64 {tl, th}, %0;\n\t"
+      "mad.lo.u32 th, s, ph, th;\n\t"
+      "mov.b64 %0, {tl, th};\n\t}"
+      : "+l"(t)
+      : "l"(p));
+  return t;
+}
+#ifndef DMG_SHOUP_CORR_FMA
+#define DMG_SHOUP_CORR_FMA 0
+#endif
 __device__ __forceinline__ u64 mod_add(u64 a, u64 b, u64 p) { return adjust_signed(a + b - p, p); }
 __device__ __forceinline__ u64 mod_sub(u64 a, u64 b, u64 p) { return adjust_signed(a - b, p); }
 
@@ -58,10 +93,43 @@ __device__ __forceinline__ u64 mod_sub(u64 a, u64 b, u64 p) { return adjust_sign
 // select was 3% slower than letting ptxas schedule this form. Rejected too: for primes
 // == 1 mod 2^32 writing q p as q_lo + (q_lo p_hi + q_hi) 2^32 — ptxas kept the same
 // IMAD.WIDE count and the transforms slowed down.)
+#ifndef DMG_SHOUP_FOLD
+#define DMG_SHOUP_FOLD 0
+#endif
 __device__ __forceinline__ u64 shoup_mul(u64 x, u64 w, u64 wp, u64 p) {
+#if DMG_SHOUP_FOLD
+  // p = 2^63 - c with c < 2^32 (both production primes): r - p = x w - (q + 1) p
+  // = x w + (q + 1) c + (q + 1) 2^63 mod 2^64, with (q + 1) 2^63 = (q_lo + 1) 2^63: one wide and
+  // four plain 32-bit multiply-adds instead of the full q p product and its negation
+  const u64 q = __umul64hi(x, wp);
+  const unsigned c = 0u - unsigned(p);
+  u64 r;
+  asm("{\n\t.reg .u32 xl, xh, wl, wh, ql, qh, rl, rh;\n\t.reg .u64 k, tt;\n\t"
+      "mov.b64 {xl, xh}, %1;\n\t"
+      "mov.b64 {wl, wh}, %2;\n\t"
+      "mov.b64 {ql, qh}, %3;\n\t"
+      "cvt.u64.u32 k, %4;\n\t"
+      "add.u64 k, k, 0x8000000000000000;\n\t"
+      "mad.wide.u32 tt, ql, %4, k;\n\t"
+      "mad.wide.u32 tt, xl, wl, tt;\n\t"
+      "mov.b64 {rl, rh}, tt;\n\t"
+      "mad.lo.u32 rh, xl, wh, rh;\n\t"
+      "mad.lo.u32 rh, xh, wl, rh;\n\t"
+      "mad.lo.u32 rh, qh, %4, rh;\n\t"
+      "mad.lo.u32 rh, ql, 0x80000000, rh;\n\t"
+      "mov.b64 %0, {rl, rh};\n\t}"
+      : "=l"(r)
+      : "l"(x), "l"(w), "l"(q), "r"(c));
+  return adjust_signed(r, p);
+#else
   u64 q = __umul64hi(x, wp);
   u64 r = x * w - q * p;  // exact, r < 2p
+#if DMG_SHOUP_CORR_FMA
+  return adjust_fma(r - p, p);
+#else
   return adjust_signed(r - p, p);
+#endif
+#endif
 }
 __device__ __forceinline__ u64 shoup_mul(u64 x, TwPair t, u64 p) { return shoup_mul(x, t.w, t.wp, p); }
 
