@@ -375,6 +375,15 @@ PassLocal Engine::local_pass(const PrimePlan& pl, std::size_t i, const ShardGeom
   return L;
 }
 
+// Whether inverse pass i may leave its outputs in [0, 2p): only when the pass that consumes
+// them next is an inverse power-of-two row pass (it starts with a Shoup twiddle product, which
+// takes any input below 2^64). The radix-3 passes, the carry and the parity hooks need [0, p).
+static bool inverse_lazy_ok(const PrimePlan& pl, std::size_t i) {
+  if (i == 0) return false;
+  const PassPlan& nx = *pl.passes[i - 1];
+  return !nx.radix3 && nx.S > 1;
+}
+
 void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2], std::size_t begin,
                         std::size_t end, const ShardGeom* sg, cudaStream_t st) {
   for (std::size_t i = begin; i < end; ++i) {
@@ -455,6 +464,7 @@ void Engine::pass_fused(const PrimePlan* pl[2], int np, u64* const data[2], cons
   a.G = L.groups;
   a.tw_logS = 0;
   a.has_final_scale = any_table ? 0 : 1;
+  a.lazy_out = inverse_lazy_ok(*pl[0], m - 1) ? 1 : 0;
   launch_pass_fused(P.logR, a, L.ncols, np, st);
   if (prof_on_) {
     char nm[64];
@@ -510,6 +520,7 @@ void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std:
       a.tw_logS = L.tw_logS;
       a.tw_off = L.tw_off;
       a.has_final_scale = (!any_table && ii == 0) ? 1 : 0;
+      a.lazy_out = inverse_lazy_ok(*pl[0], ii) ? 1 : 0;
       a.tw_lbits = P.tw_lbits;
       launch_pass_inv(P.logR, a, L.ncols, np, st);
       if (prof_on_) {

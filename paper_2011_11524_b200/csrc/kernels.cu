@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << E1];
 #pragma unroll
       for (int i = 0; i < (1 << E1); ++i) v[i] = src[G.at(base + i, w)];
-      dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>>(v, j0, tw, p);
+      dif_regs<LOGR, LOGR, E1, kSwzTables<ROWS>, ROWS>(v, j0, tw, p);  // lazy: twiddled next
       if constexpr (ROWS) G.template twist_group<E1, FACT>(v, T, Hi, q, w, p);
       u64* d = dst + G.at(base, w);
       const unsigned long long es = G.row_stride();
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i, w)];
-      dif_regs<LOGR, EL, EL, kSwzTables<ROWS>>(v, 0, tw, p);
+      dif_regs<LOGR, EL, EL, kSwzTables<ROWS>, ROWS>(v, 0, tw, p);  // lazy: twiddled next
       if constexpr (ROWS) G.template twist_group<EL, FACT>(v, T, Hi, q, w, p);
       u64* d = dst + G.at(base, w);
       const unsigned long long es = G.row_stride();
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
 constexpr int pass_inv_min_blocks(int logr, int tw) {
   return (logr == 9 && tw == kTileW) ? DMG_INV_MINB9 : pass_min_blocks(logr, tw);
 }
-template <int LOGR, bool ROWS, int TW, bool FACT = false>
+template <int LOGR, bool ROWS, int TW, bool FACT = false, bool LZO = false>
 __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LOGR, TW)) k_pass_inv(PassArgs a) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
   // first round's HBM loads above that barrier (config 5 +5%)
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
       for (int i = 0; i < (1 << E1); ++i) v[i] = s0[i * es];
     }
     if constexpr (ROWS) G.template twist_group<E1, FACT>(v, T, Hi, q, w, p);
-    dit_regs<LOGR, 0, E1, kSwzTables<ROWS>>(v, 0, tw, p);
+    dit_regs<LOGR, 0, E1, kSwzTables<ROWS>, LZO && LOGR == E1>(v, 0, tw, p);
 #pragma unroll
     for (int i = 0; i < (1 << E1); ++i) {
       if constexpr (LOGR == E1) {
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i * STL, w)];
-      dit_regs<LOGR, AL, EL, kSwzTables<ROWS>>(v, j0, tw, p);
+      dit_regs<LOGR, AL, EL, kSwzTables<ROWS>, LZO>(v, j0, tw, p);
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
         if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
 // conv.cpp:205-208, :299-305) and the first inverse pass. The last DIF round
 // and the first DIT round act on the same 8-element groups, so DIF -> pointwise
 // -> DIT happens in registers.
-template <int LOGR, int TW>
+template <int LOGR, int TW, bool LZO = false>
 __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_fused(PassArgs a) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
   // first round's HBM loads above that barrier (config 5 +5%)
@@ -415,10 +415,12 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
     u64 v[1 << EM];
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) v[i] = LOGR > EM ? sm[L(base + i, w)] : src[G.at(base + i, w)];
-    dif_regs<LOGR, EM, EM, kSwzTables<false>>(v, 0, twf, p);
+    // the last DIF stage stays lazy ([0, 2p)): REDC takes a b < p 2^64 with the other factor
+    // canonical (the other operand's spectrum, or the reduced copy when squaring)
+    dif_regs<LOGR, EM, EM, kSwzTables<false>, true>(v, 0, twf, p);
 #pragma unroll
-    for (int i = 0; i < (1 << EM); ++i) v[i] = mont_mul(v[i], oth ? oth[G.at(base + i, w)] : v[i], p, pp);
-    dit_regs<LOGR, 0, EM, kSwzTables<false>>(v, 0, twi, p);
+    for (int i = 0; i < (1 << EM); ++i) v[i] = mont_mul(v[i], oth ? oth[G.at(base + i, w)] : reduce_2p(v[i], p), p, pp);
+    dit_regs<LOGR, 0, EM, kSwzTables<false>, LZO && LOGR == EM>(v, 0, twi, p);
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) {
       if constexpr (LOGR == EM) {
@@ -440,7 +442,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       u64 v[1 << EL];
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i * STL, w)];
-      dit_regs<LOGR, AL, EL, kSwzTables<false>>(v, j0, twi, p);
+      dit_regs<LOGR, AL, EL, kSwzTables<false>, LZO>(v, j0, twi, p);
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
         if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
@@ -889,8 +891,12 @@ template <int LOGR, int TW>
 void pass_inv_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
   const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) / 2 * 16;
-  if (a.S > 1 && a.tw_lbits)
+  if (a.S > 1 && a.tw_lbits && a.lazy_out)
+    launch_pass_kernel<k_pass_inv<LOGR, true, TW, true, true>, TW, NTK>(a, ncols, np, sm, st);
+  else if (a.S > 1 && a.tw_lbits)
     launch_pass_kernel<k_pass_inv<LOGR, true, TW, true>, TW, NTK>(a, ncols, np, sm, st);
+  else if (a.S > 1 && a.lazy_out)
+    launch_pass_kernel<k_pass_inv<LOGR, true, TW, false, true>, TW, NTK>(a, ncols, np, sm, st);
   else if (a.S > 1)
     launch_pass_kernel<k_pass_inv<LOGR, true, TW>, TW, NTK>(a, ncols, np, sm, st);
   else
@@ -900,7 +906,10 @@ template <int LOGR, int TW>
 void pass_fused_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
   const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) * 16;
-  launch_pass_kernel<k_pass_fused<LOGR, TW>, TW, NTK>(a, ncols, np, sm, st);
+  if (a.lazy_out)
+    launch_pass_kernel<k_pass_fused<LOGR, TW, true>, TW, NTK>(a, ncols, np, sm, st);
+  else
+    launch_pass_kernel<k_pass_fused<LOGR, TW>, TW, NTK>(a, ncols, np, sm, st);
 }
 
 template <int LOGR>

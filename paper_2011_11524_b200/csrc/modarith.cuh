@@ -158,6 +158,12 @@ __device__ __forceinline__ u64 solinas_mul(u64 a, u64 b) {
   return r;
 }
 
+// Shoup product left in [0, 2p) (no final correction), for consumers that accept it.
+__device__ __forceinline__ u64 shoup_mul_lazy(u64 x, TwPair t, u64 p) {
+  u64 q = __umul64hi(x, t.wp);
+  return x * t.w - q * p;
+}
+
 // Gentleman-Sande butterfly (reference ntt.cpp:42-47): (u + v, (u - v) w).
 __device__ __forceinline__ void bfly_dif(u64& u, u64& v, TwPair t, u64 p) {
   u64 a = mod_add(u, v, p);
@@ -180,6 +186,33 @@ __device__ __forceinline__ void bfly_dit1(u64& u, u64& v, u64 p) {
   v = mod_sub(u, w, p);
   u = mod_add(u, w, p);
 }
+
+// Lazy butterflies of a final stage: outputs in [0, 2p) instead of [0, p), for a consumer that
+// accepts any input below 2p (a Shoup product, or one operand of a REDC product against a
+// canonical one). p < 2^63, so 2p - 1 still fits the word; nothing uses these values as
+// inputs of another add or subtract.
+__device__ __forceinline__ void bfly_dif_lz(u64& u, u64& v, TwPair t, u64 p) {
+  const u64 a = u + v;
+  v = shoup_mul_lazy(u - v + p, t, p);
+  u = a;
+}
+__device__ __forceinline__ void bfly_dif1_lz(u64& u, u64& v, u64 p) {
+  const u64 a = u + v;
+  v = u - v + p;
+  u = a;
+}
+__device__ __forceinline__ void bfly_dit_lz(u64& u, u64& v, TwPair t, u64 p) {
+  const u64 w = shoup_mul(v, t, p);
+  v = u - w + p;
+  u = u + w;
+}
+__device__ __forceinline__ void bfly_dit1_lz(u64& u, u64& v, u64 p) {
+  const u64 w = v;
+  v = u - w + p;
+  u = u + w;
+}
+// [0, 2p) -> [0, p)
+__device__ __forceinline__ u64 reduce_2p(u64 a, u64 p) { return adjust_signed(a - p, p); }
 
 // ---- two-word division by the constant limb base B = 10^lambda ----
 // Restates the reciprocal scheme of reference decimal.hpp:93-146 (make_div_by_const,

@@ -53,7 +53,9 @@ struct Sched {
 // ---- register stages ----
 // DIF stages of one group: elements v[i] at positions base + i * STRIDE, STRIDE = 2^(MLOG-E),
 // j0 = base mod STRIDE. Spans 2^MLOG down to 2^(MLOG-E+1).
-template <int LOGR, int MLOG, int E, bool SWZ>
+// LZ: the last stage's outputs stay in [0, 2p) (modarith.cuh lazy butterflies) for a consumer
+// that accepts them (the inter-pass twiddle, the pointwise REDC).
+template <int LOGR, int MLOG, int E, bool SWZ, bool LZ = false>
 __device__ __forceinline__ void dif_regs(u64 (&v)[1 << E], int j0, const TwPair* tw, u64 p) {
   constexpr int NE = 1 << E, STRIDE = 1 << (MLOG - E);
 #pragma unroll
@@ -67,16 +69,23 @@ __device__ __forceinline__ void dif_regs(u64 (&v)[1 << E], int j0, const TwPair*
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
       if (i & half) continue;
-      if (STRIDE == 1 && (i & (half - 1)) == 0)
-        bfly_dif1(v[i], v[i + half], p);  // j = 0: factor 1 (reference ntt.cpp:39-41 peel)
-      else
+      const bool lz = LZ && st == E - 1;
+      if (STRIDE == 1 && (i & (half - 1)) == 0) {  // j = 0: factor 1 (reference ntt.cpp:39-41 peel)
+        if (lz)
+          bfly_dif1_lz(v[i], v[i + half], p);
+        else
+          bfly_dif1(v[i], v[i + half], p);
+      } else if (lz) {
+        bfly_dif_lz(v[i], v[i + half], t[i & (half - 1)], p);
+      } else {
         bfly_dif(v[i], v[i + half], t[i & (half - 1)], p);
+      }
     }
   }
 }
 
 // DIT stages of one group: positions base + i * STRIDE, STRIDE = 2^ALOG; spans 2^(ALOG+1)..2^(ALOG+E).
-template <int LOGR, int ALOG, int E, bool SWZ>
+template <int LOGR, int ALOG, int E, bool SWZ, bool LZ = false>
 __device__ __forceinline__ void dit_regs(u64 (&v)[1 << E], int j0, const TwPair* tw, u64 p) {
   constexpr int NE = 1 << E, STRIDE = 1 << ALOG;
 #pragma unroll
@@ -90,10 +99,17 @@ __device__ __forceinline__ void dit_regs(u64 (&v)[1 << E], int j0, const TwPair*
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
       if (i & d) continue;
-      if (STRIDE == 1 && (i & (d - 1)) == 0)
-        bfly_dit1(v[i], v[i + d], p);  // j = 0: factor 1 (reference ntt.cpp:62-64 peel)
-      else
+      const bool lz = LZ && st == E - 1;
+      if (STRIDE == 1 && (i & (d - 1)) == 0) {  // j = 0: factor 1 (reference ntt.cpp:62-64 peel)
+        if (lz)
+          bfly_dit1_lz(v[i], v[i + d], p);
+        else
+          bfly_dit1(v[i], v[i + d], p);
+      } else if (lz) {
+        bfly_dit_lz(v[i], v[i + d], t[i & (d - 1)], p);
+      } else {
         bfly_dit(v[i], v[i + d], t[i & (d - 1)], p);
+      }
     }
   }
 }
