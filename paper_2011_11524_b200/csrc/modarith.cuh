@@ -211,6 +211,21 @@ __device__ __forceinline__ void bfly_dit1_lz(u64& u, u64& v, u64 p) {
   v = u - w + p;
   u = u + w;
 }
+// Cooley-Tukey butterfly with per-output laziness: LU / LV leave u + v w / u - v w in [0, 2p)
+// (for outputs that the next stage only multiplies). v may be anything below 2^64 (it is
+// multiplied first); u must be canonical.
+template <bool LU, bool LV>
+__device__ __forceinline__ void bfly_dit_m(u64& u, u64& v, TwPair t, u64 p) {
+  const u64 w = shoup_mul(v, t, p);
+  v = LV ? u - w + p : mod_sub(u, w, p);
+  u = LU ? u + w : mod_add(u, w, p);
+}
+template <bool LU, bool LV>
+__device__ __forceinline__ void bfly_dit1_m(u64& u, u64& v, u64 p) {  // factor 1: v canonical
+  const u64 w = v;
+  v = LV ? u - w + p : mod_sub(u, w, p);
+  u = LU ? u + w : mod_add(u, w, p);
+}
 // [0, 2p) -> [0, p)
 __device__ __forceinline__ u64 reduce_2p(u64 a, u64 p) { return adjust_signed(a - p, p); }
 

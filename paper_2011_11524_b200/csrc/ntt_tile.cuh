@@ -99,16 +99,26 @@ __device__ __forceinline__ void dit_regs(u64 (&v)[1 << E], int j0, const TwPair*
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
       if (i & d) continue;
-      const bool lz = LZ && st == E - 1;
-      if (STRIDE == 1 && (i & (d - 1)) == 0) {  // j = 0: factor 1 (reference ntt.cpp:62-64 peel)
-        if (lz)
-          bfly_dit1_lz(v[i], v[i + d], p);
-        else
-          bfly_dit1(v[i], v[i + d], p);
-      } else if (lz) {
-        bfly_dit_lz(v[i], v[i + d], t[i & (d - 1)], p);
+      // Outputs that the next stage of this group only multiplies stay lazy ([0, 2p)): both
+      // outputs of a pair whose bit st + 1 is set are v inputs of stage st + 1, except the u
+      // output when its consumer is the j = 0 peel (no multiplication). The last stage's
+      // outputs leave the group: lazy only if the pass's consumer allows it (LZ).
+      const bool last = st == E - 1;
+      const bool is_v = !last && (i & (2 * d)) != 0;
+      const bool peel = STRIDE == 1 && (i & (d - 1)) == 0;
+      const bool next_peel = STRIDE == 1 && (i & (2 * d - 1)) == 0;
+      const bool lu = last ? LZ : (is_v && !next_peel);
+      const bool lv = last ? LZ : is_v;
+      // (j = 0: factor 1, reference ntt.cpp:62-64 peel)
+      if (lu && lv) {
+        if (peel) bfly_dit1_m<true, true>(v[i], v[i + d], p);
+        else bfly_dit_m<true, true>(v[i], v[i + d], t[i & (d - 1)], p);
+      } else if (lv) {
+        if (peel) bfly_dit1_m<false, true>(v[i], v[i + d], p);
+        else bfly_dit_m<false, true>(v[i], v[i + d], t[i & (d - 1)], p);
       } else {
-        bfly_dit(v[i], v[i + d], t[i & (d - 1)], p);
+        if (peel) bfly_dit1(v[i], v[i + d], p);
+        else bfly_dit(v[i], v[i + d], t[i & (d - 1)], p);
       }
     }
   }
