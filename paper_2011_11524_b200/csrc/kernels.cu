@@ -635,111 +635,78 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d,
 // (factorised lo * hi as in k_radix3_fwd) for both primes, and writes pass 0's output.
 // The packed limbs never touch HBM (the separate pack wrote 8 B and the radix-3 pass read
 // them back per limb).
-// Double-buffered staging of the spans (and of the twiddles) through cp.async measured slower
-// on config 4 (4.48 / 5.74 ms for the two launches vs 4.32 ms single-buffered); kept for A/B.
-#ifndef DMG_PACK_DB
-#define DMG_PACK_DB 0
-#endif
-#if DMG_PACK_DB
-// Dynamic shared memory of k_pack_radix3: two stages of (three digit spans, the lo twiddles of
-// rows 1 and 2 of both primes for the stage's kPackLimbs columns, and their hi factors).
-constexpr int kPackR3Smem = 2 * 3 * kPackBuf + 2 * 2 * 2 * kPackLimbs * 16 + 2 * 2 * 2 * 16;
+// The block's three spans are staged with 16-byte loads; in span-local coordinates thread t's
+// limb always ends at byte (kPackLimbs - t) lambda, so the parse needs no 64-bit index
+// arithmetic (only the block holding the string's head clips). Rows past the last limb are
+// skipped block-uniformly (config 4's y fills one of the three rows, x two).
+// (Rejected: double-buffered cp.async staging of the spans and twiddles, 4.48 / 5.74 ms for the
+// two config-4 launches vs 4.32 single-buffered.)
 template <int NG>
-__global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restrict__ d, unsigned long long nd,
-                                                           unsigned be, Radix3Args a, unsigned* err) {
-  pdl_wait();
-  // two stages: the next columns' digit spans and twiddles stream in (cp.async) while the
-  // block parses and transforms the current ones, so neither HBM nor L2 latency is exposed
-  extern __shared__ __align__(16) char dsm[];
-  char(*span)[3][kPackBuf] = reinterpret_cast<char(*)[3][kPackBuf]>(dsm);
-  TwPair(*tlo)[2][2][kPackLimbs] = reinterpret_cast<TwPair(*)[2][2][kPackLimbs]>(dsm + 2 * 3 * kPackBuf);
-  TwPair(*thi)[2][2] = reinterpret_cast<TwPair(*)[2][2]>(dsm + 2 * 3 * kPackBuf + 2 * 2 * 2 * kPackLimbs * 16);
-  const unsigned long long S = a.S, L = 1ull << a.lbits, H = a.hrow;
-  const unsigned long long step = (unsigned long long)gridDim.x * kPackLimbs;
-  unsigned bad = 0;
-  // the twiddles of columns [c0, c0 + kPackLimbs) (one L-block: kPackLimbs divides L)
-  auto stage_tw = [&](int stg, unsigned long long c0) {
-    const unsigned long long sl0 = c0 & (L - 1), sh = c0 >> a.lbits;
-    for (int i = threadIdx.x; i < 4 * kPackLimbs; i += kPackLimbs) {
-      const int pr = i / (2 * kPackLimbs), row = (i / kPackLimbs) & 1, c = i % kPackLimbs;
-      if (c0 + c >= S) continue;
-      const unsigned sa = unsigned(__cvta_generic_to_shared(&tlo[stg][pr][row][c]));
-      const TwPair* src = a.lo[pr] + (row + 1) * L + sl0 + c;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
-    }
-    if (threadIdx.x < 4) {
-      const int pr = threadIdx.x >> 1, row = threadIdx.x & 1;
-      const unsigned sa = unsigned(__cvta_generic_to_shared(&thi[stg][pr][row]));
-      const TwPair* src = a.hi[pr] + (row + 1) * H + sh;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src) : "memory");
-    }
-  };
-  long long ga[3] = {0, 0, 0}, gb[3] = {0, 0, 0};  // span origins of stages 0 / 1 (block-uniform)
-  unsigned long long s0 = (unsigned long long)blockIdx.x * kPackLimbs;
-  if (s0 < S) {
-#pragma unroll
-    for (int j = 0; j < 3; ++j) ga[j] = pack_stage<true>(d, nd, be, j * S + s0, span[0][j]);
-    stage_tw(0, s0);
+__device__ __forceinline__ u64 r3_row_limb(const char* __restrict__ d, unsigned long long nd, long long hi,
+                                           unsigned be, const char* buf, unsigned* err, unsigned& bad) {
+  // hi = string end (exclusive) of the block's first limb; the span starts at hi - 256 be
+  const int t = threadIdx.x;
+  const long long base = hi - (long long)kPackLimbs * be;  // string position of span byte 0
+  const int o = int((reinterpret_cast<unsigned long long>(d) + (unsigned long long)base) & 15);
+  const int e = (kPackLimbs - t) * int(be);  // limb end, span-local
+  int b = e - int(be);
+  if (base < 0) {  // the string's head: limbs may be short or absent
+    const int b0 = int(-base);
+    if (e <= b0) return 0;
+    if (b < b0) b = b0;
+    const u64 v = parse_digits<NG>(buf + 32, o + b, e - b, bad);
+    if (b == b0 && nd > 1 && d[0] == '0') atomicOr(err, kErrLeadingZero);  // the most significant limb
+    return v;
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int cur = 0; s0 < S; s0 += step, cur ^= 1) {
-    const unsigned long long n0 = s0 + step;
-    if (n0 < S) {
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const long long gn = pack_stage<true>(d, nd, be, j * S + n0, span[cur ^ 1][j]);
-        if (cur) ga[j] = gn; else gb[j] = gn;
-      }
-      stage_tw(cur ^ 1, n0);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_group 1;" ::: "memory");  // this stage's spans have landed
-    __syncthreads();
-    const u64 x0 = pack_parse<NG>(d, nd, be, s0, span[cur][0], cur ? gb[0] : ga[0], err, bad);
-    const u64 x1 = pack_parse<NG>(d, nd, be, S + s0, span[cur][1], cur ? gb[1] : ga[1], err, bad);
-    const u64 x2 = pack_parse<NG>(d, nd, be, 2 * S + s0, span[cur][2], cur ? gb[2] : ga[2], err, bad);
-    const unsigned long long s = s0 + threadIdx.x;
-    if (s < S) {
-#pragma unroll
-      for (int pr = 0; pr < 2; ++pr) {
-        const u64 p = a.p[pr];
-        const TwPair lam = a.lam[pr];
-        u64* dst = a.dst[pr];
-        // limbs are < 10^17 < p: canonical residues of both primes
-        const u64 t = shoup_mul(mod_sub(x1, x2, p), lam, p);
-        const u64 y0 = mod_add(mod_add(x0, x1, p), x2, p);
-        const u64 y1 = mod_add(mod_sub(x0, x2, p), t, p);
-        const u64 y2 = mod_sub(mod_sub(x0, x1, p), t, p);
-        dst[s] = y0;
-        dst[S + s] = shoup_mul(shoup_mul(y1, tlo[cur][pr][0][threadIdx.x], p), thi[cur][pr][0], p);
-        dst[2 * S + s] = shoup_mul(shoup_mul(y2, tlo[cur][pr][1][threadIdx.x], p), thi[cur][pr][1], p);
-      }
-    }
-    __syncthreads();  // stage cur is refilled by the next iteration's prefetch
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  if (bad) atomicOr(err, kErrBadDigit);
+  if (base + b == 0 && nd > 1 && d[0] == '0') atomicOr(err, kErrLeadingZero);
+  return parse_digits<NG>(buf + 32, o + b, int(be), bad);
 }
-#else
+__device__ __forceinline__ void r3_row_stage(const char* __restrict__ d, unsigned long long nd, long long hi,
+                                             unsigned be, char* buf) {
+  const long long base = hi - (long long)kPackLimbs * be;
+  const int o = int((reinterpret_cast<unsigned long long>(d) + (unsigned long long)base) & 15);
+  const long long g0 = base - o;  // 16-byte aligned in the address space
+  const int nvec = (o + kPackLimbs * int(be) + 15) >> 4;
+  char* dst = buf + 32;
+  for (int v = threadIdx.x; v < nvec; v += kPackLimbs) {
+    const long long g = g0 + 16LL * v;
+    if (g >= 0 && g + 16 <= (long long)nd) {
+      reinterpret_cast<uint4*>(dst)[v] = *reinterpret_cast<const uint4*>(d + g);
+    } else {
+      for (int k = 0; k < 16; ++k) dst[v * 16 + k] = (g + k >= 0 && g + k < (long long)nd) ? d[g + k] : '0';
+    }
+  }
+}
+
 template <int NG>
 __global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restrict__ d, unsigned long long nd,
                                                            unsigned be, Radix3Args a, unsigned* err) {
   pdl_wait();
   __shared__ __align__(16) char smem[3][kPackBuf];
   const unsigned long long S = a.S, L = 1ull << a.lbits, H = a.hrow;
+  const unsigned long long nl = (nd + be - 1) / be;  // limbs of the string
   unsigned bad = 0;
   for (unsigned long long s0 = (unsigned long long)blockIdx.x * kPackLimbs; s0 < S;
        s0 += (unsigned long long)gridDim.x * kPackLimbs) {
-    // the three spans in flight together, one barrier
-    long long g[3];
+    bool live[3];
+    long long hi[3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) g[j] = pack_stage(d, nd, be, j * S + s0, smem[j]);
-    __syncthreads();
-    const u64 x0 = pack_parse<NG>(d, nd, be, s0, smem[0], g[0], err, bad);
-    const u64 x1 = pack_parse<NG>(d, nd, be, S + s0, smem[1], g[1], err, bad);
-    const u64 x2 = pack_parse<NG>(d, nd, be, 2 * S + s0, smem[2], g[2], err, bad);
+    for (int j = 0; j < 3; ++j) {
+      const unsigned long long t0 = j * S + s0;  // the block's first limb of row j
+      live[j] = t0 < nl;
+      hi[j] = (long long)nd - (long long)(t0 * be);
+      if (live[j]) r3_row_stage(d, nd, hi[j], be, smem[j]);
+    }
     __syncthreads();
     const unsigned long long s = s0 + threadIdx.x;
+    u64 x[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      x[j] = 0;
+      // limbs past the string's end inside a live block: its last block may be partial
+      if (live[j] && j * S + s < nl) x[j] = r3_row_limb<NG>(d, nd, hi[j], be, smem[j], err, bad);
+    }
+    __syncthreads();
     if (s >= S) continue;
     const unsigned long long sl = s & (L - 1), sh = s >> a.lbits;
 #pragma unroll
@@ -747,21 +714,20 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restri
       const u64 p = a.p[pr];
       const TwPair lam = a.lam[pr];
       const TwPair* __restrict__ lo = a.lo[pr];
-      const TwPair* __restrict__ hi = a.hi[pr];
+      const TwPair* __restrict__ hiw = a.hi[pr];
       u64* dst = a.dst[pr];
       // limbs are < 10^17 < p: canonical residues of both primes
-      const u64 t = shoup_mul(mod_sub(x1, x2, p), lam, p);
-      const u64 y0 = mod_add(mod_add(x0, x1, p), x2, p);
-      const u64 y1 = mod_add(mod_sub(x0, x2, p), t, p);
-      const u64 y2 = mod_sub(mod_sub(x0, x1, p), t, p);
+      const u64 t = shoup_mul(mod_sub(x[1], x[2], p), lam, p);
+      const u64 y0 = mod_add(mod_add(x[0], x[1], p), x[2], p);
+      const u64 y1 = mod_add(mod_sub(x[0], x[2], p), t, p);
+      const u64 y2 = mod_sub(mod_sub(x[0], x[1], p), t, p);
       dst[s] = y0;
-      dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hi[H + sh], p);
-      dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
+      dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hiw[H + sh], p);
+      dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hiw[2 * H + sh], p);
     }
   }
   if (bad) atomicOr(err, kErrBadDigit);
 }
-#endif
 
 // Column-sharded pack for rows narrower than one 256-limb block: one limb per thread.
 __global__ void k_pack_rows(const char* __restrict__ d, unsigned long long nd, unsigned be, u64* __restrict__ limbs,
@@ -1005,16 +971,7 @@ void launch_pack(const char* digits, unsigned long long nd, unsigned be, u64* li
 void launch_pack_radix3(const char* digits, unsigned long long nd, unsigned be, const Radix3Args& a, unsigned* err,
                         cudaStream_t st) {
   auto fn = be > 16 ? k_pack_radix3<5> : k_pack_radix3<4>;
-#if DMG_PACK_DB
-  constexpr int smem = kPackR3Smem;
-  if (be > 16)
-    set_smem<k_pack_radix3<5>>(smem);
-  else
-    set_smem<k_pack_radix3<4>>(smem);
-#else
-  constexpr int smem = 0;
-#endif
-  launch_pdl(fn, dim3(grid_for(a.S, kPackLimbs)), dim3(kPackLimbs), size_t(smem), st, digits, nd, be, a, err);
+  launch_pdl(fn, dim3(grid_for(a.S, kPackLimbs)), dim3(kPackLimbs), 0, st, digits, nd, be, a, err);
 }
 void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, unsigned long long rows,
                           unsigned long long width, bool to_segments, cudaStream_t st) {

@@ -363,6 +363,26 @@ def test_device_zero_short_circuit_validates(gpu):
     assert gpu.multiply_text(b"12", b"34") == b"408"
 
 
+def test_errors_in_fused_pack_radix3(gpu, ref):
+    """Digit validation inside the pack fused with the radix-3 pass (N = 3 2^k multi-pass
+    transforms): a leading zero, a non-digit anywhere, and operand lengths that leave the
+    most significant limb short, against the reference."""
+    n = 300001
+    x, y = inputs.gen_digits(7, n), inputs.gen_digits(8, n - 2)
+    assert gpu.plan(n, n - 2)["length"] % 3 == 0 and not gpu.plan(n, n - 2)["one_cta"]
+    with pytest.raises(ValueError, match="leading zero"):
+        gpu.multiply_text(b"0" + x[1:], y)
+    for pos in (0, 17, n // 2, n - 1):
+        bad = bytearray(x)
+        bad[pos] = ord(":")
+        with pytest.raises(ValueError, match="non-digit"):
+            gpu.multiply_text(bytes(bad), y)
+    for extra in range(0, 17):
+        xs = x[: n - extra]
+        assert gpu.multiply_text(xs, y) == ref.multiply(xs, y)
+    assert gpu.multiply_text(b"12", b"34") == b"408"
+
+
 def test_profile_report(gpu):
     """Per-launch profiling (decmul_gpu_profile_*): every kernel of a product appears with its
     algorithmic work, and the records clear after a report."""
