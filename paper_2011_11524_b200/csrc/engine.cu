@@ -440,7 +440,7 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
 }
 
 void Engine::pass_fused(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
-                        const ShardGeom* sg, cudaStream_t st) {
+                        const ShardGeom* sg, cudaStream_t st, bool two) {
   const std::size_t m = pl[0]->passes.size();
   const PassPlan& P = *pl[0]->passes[m - 1];
   const PassLocal L = local_pass(*pl[0], m - 1, sg);
@@ -465,12 +465,14 @@ void Engine::pass_fused(const PrimePlan* pl[2], int np, u64* const data[2], cons
   a.tw_logS = 0;
   a.has_final_scale = any_table ? 0 : 1;
   a.lazy_out = inverse_lazy_ok(*pl[0], m - 1) ? 1 : 0;
+  a.two = two ? 1 : 0;
   launch_pass_fused(P.logR, a, L.ncols, np, st);
   if (prof_on_) {
     char nm[64];
-    std::snprintf(nm, sizeof nm, "k_pass_fused<%d>", P.logR);
+    std::snprintf(nm, sizeof nm, two ? "k_pass_fused2<%d>" : "k_pass_fused<%d>", P.logR);
     const double n = double(L.ncols) * P.R;
-    prof_mark(nm, st, np * (n * P.logR + n + (a.has_final_scale ? n : 0)), np * (other ? 24 : 16) * n);
+    prof_mark(nm, st, np * (n * P.logR * (two ? 1.5 : 1.0) + n + (a.has_final_scale ? n : 0)),
+              np * (other ? 24 : 16) * n);
   }
   ++launches_;
 }
@@ -805,12 +807,17 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
   } else {
     u64* X[2] = {X_[0].ptr, X_[1].ptr};
     u64* Y[2] = {Y_[0].ptr, Y_[1].ptr};
-    load(dx, pp.dx, px, X, true);
+    // two-operand fused last pass (x's last forward pass inside the pointwise kernel) when the
+    // transform has at least two passes (DECMUL_FUSE2=0: x's last pass as its own launch)
+    const char* f2 = std::getenv("DECMUL_FUSE2");
+    // (R = 512: two 64 KB tiles would leave one CTA per SM)
+    const bool two = P1.last_pow2 && m >= 2 && P1.passes[m - 1]->logR <= 8 && !(f2 && f2[0] == '0');
+    load(dx, pp.dx, px, X, !two);
     if (before_y) before_y();
     load(dy, pp.dy, py, Y, !P1.last_pow2);
     if (P1.last_pow2) {
       const u64* oth[2] = {X[0], X[1]};
-      transform_fused_last(pl, 2, Y, oth, st);
+      pass_fused(pl, 2, Y, oth, nullptr, st, two);
     } else {
       for (int q = 0; q < 2; ++q) launch_pointwise(Y[q], X[q], pp.N, pl[q]->p, pl[q]->pp, st);
       prof_mark("k_pointwise", st, 2.0 * pp.N, 48.0 * pp.N);

@@ -297,8 +297,9 @@ class Engine {
   PassLocal local_pass(const PrimePlan& pl, std::size_t i, const ShardGeom* sg) const;
   void passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2], std::size_t begin,
                   std::size_t end, const ShardGeom* sg, cudaStream_t st);
+  // two: other[] holds the first operand before its last forward pass (run inside the kernel)
   void pass_fused(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
-                  const ShardGeom* sg, cudaStream_t st);
+                  const ShardGeom* sg, cudaStream_t st, bool two = false);
   void passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std::size_t begin, std::size_t end,
                   const ShardGeom* sg, cudaStream_t st);
   // digits -> the first (radix-3) pass's output of both primes, one fused kernel

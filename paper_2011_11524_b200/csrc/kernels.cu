@@ -364,8 +364,17 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
 // conv.cpp:205-208, :299-305) and the first inverse pass. The last DIF round
 // and the first DIT round act on the same 8-element groups, so DIF -> pointwise
 // -> DIT happens in registers.
-template <int LOGR, int TW, bool LZO = false>
-__global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_fused(PassArgs a) {
+// TWO: a.other holds the first operand BEFORE its last forward pass (not its spectrum); the
+// CTA stages that tile too and runs its whole DIF in shared memory, so the first operand's
+// last pass needs no launch (and its spectrum no HBM round trip): the standalone column pass
+// ran at ~0.5 instructions per cycle against the fused kernel's ~0.66.
+// (Two tiles of R = 256 x 16 take 64 KB: three CTAs per SM by shared memory, so TWO
+// kernels get the 85 registers of a 3-CTA bound instead of R = 256's 64.)
+constexpr int fused_min_blocks(int logr, int tw, bool two) {
+  return two && logr == 8 && tw == kTileW ? 3 : pass_min_blocks(logr, tw);
+}
+template <int LOGR, int TW, bool LZO = false, bool TWO = false>
+__global__ void __launch_bounds__(pass_threads(LOGR, TW), fused_min_blocks(LOGR, TW, TWO)) k_pass_fused(PassArgs a) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
   // first round's HBM loads above that barrier (config 5 +5%)
   pdl_wait();
@@ -374,7 +383,8 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   constexpr int EL = Sched<LOGR>::rem ? Sched<LOGR>::rem : EM;
   constexpr int AL = LOGR - EL;
   extern __shared__ __align__(16) u64 sm[];
-  TwPair* twf = reinterpret_cast<TwPair*>(sm + R * TW);
+  u64* smx = sm + R * TW;  // TWO: the first operand's tile
+  TwPair* twf = reinterpret_cast<TwPair*>(sm + (TWO ? 2 : 1) * R * TW);
   TwPair* twi = twf + R / 2;
   const int pr = int(blockIdx.x % a.np), tid = threadIdx.x;
   const u64 p = a.p[pr], pp = a.pp[pr];
@@ -386,10 +396,12 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   const ContigColumns<LOGR> L;
   constexpr bool STAGE = kStageFwd<false, TW> && LOGR > EM;
   if constexpr (STAGE) stage_tile<LOGR, false, TW, NTK>(sm, src, G, L, tid);
+  if constexpr (TWO) stage_tile<LOGR, false, TW, NTK>(smx, oth, G, L, tid);
   load_table<LOGR, NTK, kSwzTables<false>>(twf, a.dft_fwd[pr]);
   load_table<LOGR, NTK, kSwzTables<false>>(twi, a.dft_inv[pr]);
-  if constexpr (STAGE) asm volatile("cp.async.wait_all;" ::: "memory");
+  if constexpr (STAGE || TWO) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  if constexpr (TWO) tile_dif<LOGR, TW>(smx, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
   if constexpr (STAGE) {
     dif_rounds_smem<LOGR, LOGR, EM, TW>(sm, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
   } else if constexpr (LOGR > EM) {
@@ -419,7 +431,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
     // canonical (the other operand's spectrum, or the reduced copy when squaring)
     dif_regs<LOGR, EM, EM, kSwzTables<false>, true>(v, 0, twf, p);
 #pragma unroll
-    for (int i = 0; i < (1 << EM); ++i) v[i] = mont_mul(v[i], oth ? oth[G.at(base + i, w)] : reduce_2p(v[i], p), p, pp);
+    for (int i = 0; i < (1 << EM); ++i) {
+      const u64 o = TWO ? smx[L(base + i, w)] : (oth ? oth[G.at(base + i, w)] : reduce_2p(v[i], p));
+      v[i] = mont_mul(v[i], o, p, pp);
+    }
     dit_regs<LOGR, 0, EM, kSwzTables<false>, LZO && LOGR == EM>(v, 0, twi, p);
 #pragma unroll
     for (int i = 0; i < (1 << EM); ++i) {
@@ -871,8 +886,13 @@ void pass_inv_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_
 template <int LOGR, int TW>
 void pass_fused_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
-  const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) * 16;
-  if (a.lazy_out)
+  const int sm = (1 << LOGR) * TW * 8 * (a.two ? 2 : 1) + (1 << LOGR) * 16;
+  if (a.two) {
+    if (a.lazy_out)
+      launch_pass_kernel<k_pass_fused<LOGR, TW, true, true>, TW, NTK>(a, ncols, np, sm, st);
+    else
+      launch_pass_kernel<k_pass_fused<LOGR, TW, false, true>, TW, NTK>(a, ncols, np, sm, st);
+  } else if (a.lazy_out)
     launch_pass_kernel<k_pass_fused<LOGR, TW, true>, TW, NTK>(a, ncols, np, sm, st);
   else
     launch_pass_kernel<k_pass_fused<LOGR, TW>, TW, NTK>(a, ncols, np, sm, st);

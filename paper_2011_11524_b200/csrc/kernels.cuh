@@ -78,6 +78,7 @@ struct PassArgs {
   int tw_lbits;            // 0: full R x S twiddle table; else the factorised pair (see pass_tw)
   int lazy_out;            // inverse / fused passes: outputs may stay in [0, 2p) (the next pass is an
                            // inverse row pass, whose first step is a Shoup twiddle product)
+  int two;                 // fused pass: other = the first operand before its last forward pass
 };
 
 // Radix-3 pass over N = 3 S. The twiddle omega_N^{+-f s} (times the convolution
