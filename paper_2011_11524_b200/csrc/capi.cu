@@ -235,6 +235,7 @@ int multiply_coalesced(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char
     ctx->queue.push_back(&req);
     if (ctx->leader) {  // follower: the current or next leader runs this product
       ctx->qcv.wait(q, [&] { return req.done; });
+      q.unlock();  // before taking ctx->mu: a leader holds mu while it takes qmu to swap the queue
       if (req.rc) {
         std::lock_guard<std::mutex> lk(ctx->mu);
         ctx->err = req.msg;

@@ -26,6 +26,14 @@ bool factor_tables(std::size_t entries) {
 }
 
 
+// Unfactorised inverse radix-3 twiddle rows (2 S pairs per prime, 4.3 GB in all for config
+// 4's S = 2^26) save the fused carry kernel one Shoup product per twiddle; larger transforms
+// keep only the factorised tables. DECMUL_R3_FULL=0/1 overrides (tests, A/B).
+bool r3_full_tables(std::size_t S) {
+  if (const char* e = std::getenv("DECMUL_R3_FULL")) return e[0] == '1';
+  return S <= (std::size_t(1) << 26);
+}
+
 u64 recip_of(u64 d) {  // reference make_div_by_const (decimal.hpp:93-104), for a normalized divisor
   return u64(~(u128)0 / d - ((u128)1 << 64));
 }
@@ -223,6 +231,17 @@ void Engine::build_passes(PrimePlan& pl) {
       upload(ps.r3_hi_fwd, hf, stream_);
       upload(ps.r3_lo_inv, li, stream_);
       upload(ps.r3_hi_inv, hi, stream_);
+      ps.r3_r0_inv = shoup_pair(F, scale);
+      if (i == 0 && r3_full_tables(ps.S)) {
+        // rows 1, 2 of omega_N^{-f s} scale (N = M = 3 S), generated on the device. Inverse only:
+        // with them the fused pack turned HBM-bound (config 4: 4.17 -> 4.66 ms) while the
+        // carry split gained (3.29 -> 3.12 ms).
+        ps.r3_full_inv.ensure(2 * ps.S);
+        launch_gen_pass_table(ps.r3_full_inv.ptr, F.to_mont(wMi), F.to_mont(scale), 2, 0, ps.S, pl.p, recip, stream_, M,
+                              1);
+        cuda_check(cudaGetLastError(), "gen radix-3 table");
+        ps.r3_full_ok = true;
+      }
       cuda_check(cudaStreamSynchronize(stream_), "radix-3 tables");
     } else if (ps.S > 1) {
       const std::size_t cnt = std::size_t(ps.R) * ps.S;
@@ -375,13 +394,13 @@ PassLocal Engine::local_pass(const PrimePlan& pl, std::size_t i, const ShardGeom
   return L;
 }
 
-// Whether inverse pass i may leave its outputs in [0, 2p): only when the pass that consumes
-// them next is an inverse power-of-two row pass (it starts with a Shoup twiddle product, which
-// takes any input below 2^64). The radix-3 passes, the carry and the parity hooks need [0, p).
+// Whether inverse pass i may leave its outputs in [0, 2p): yes unless it is the last inverse
+// pass (pass 0), whose outputs the carry and the parity hooks read as residues in [0, p).
 static bool inverse_lazy_ok(const PrimePlan& pl, std::size_t i) {
-  if (i == 0) return false;
-  const PassPlan& nx = *pl.passes[i - 1];
-  return !nx.radix3 && nx.S > 1;
+  // every inverse pass below the last starts by multiplying each input (a power-of-two row
+  // pass by its twiddle, the radix-3 pass / fused carry by its twiddle or the scale)
+  (void)pl;
+  return i > 0;
 }
 
 void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2], std::size_t begin,
@@ -664,9 +683,11 @@ void Engine::pack_radix3(const PrimePlan* pl[2], const char* digits, std::size_t
     a.dst[q] = dst[q];
     a.lo[q] = pl[q]->passes[0]->r3_lo_fwd.ptr;
     a.hi[q] = pl[q]->passes[0]->r3_hi_fwd.ptr;
+    a.full[q] = nullptr;  // factorised forward twiddles (see build_passes)
     a.p[q] = pl[q]->p;
     a.lam[q] = pl[q]->lam;
   }
+  if (!a.full[0] || !a.full[1]) a.full[0] = a.full[1] = nullptr;
   a.S = P.S;
   a.lbits = P.r3_lbits;
   a.hrow = P.S >> a.lbits;
@@ -862,9 +883,12 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
       r.dst[q] = nullptr;
       r.lo[q] = pl[q]->passes[0]->r3_lo_inv.ptr;
       r.hi[q] = pl[q]->passes[0]->r3_hi_inv.ptr;
+      r.full[q] = pl[q]->passes[0]->r3_full_ok ? pl[q]->passes[0]->r3_full_inv.ptr : nullptr;
+      r.r0[q] = pl[q]->passes[0]->r3_r0_inv;
       r.p[q] = pl[q]->p;
       r.lam[q] = pl[q]->lam_inv;
     }
+    if (!r.full[0] || !r.full[1]) r.full[0] = r.full[1] = nullptr;
     r.S = P0.S;
     r.lbits = P0.r3_lbits;
     r.hrow = P0.S >> r.lbits;

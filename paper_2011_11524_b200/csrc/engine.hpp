@@ -60,6 +60,11 @@ struct PassPlan {
   // radix-3 passes: omega_N^{+-f s} = lo[f][s mod 2^lbits] * hi[f][s >> lbits]
   DevBuf<TwPair> r3_lo_fwd, r3_hi_fwd, r3_lo_inv, r3_hi_inv;
   int r3_lbits = 0;
+  // unfactorised inverse rows f = 1, 2 (2 S pairs, carrying the scale) for the fused carry
+  // kernel when they fit (r3_full_ok), and the inverse's row-0 factor (the scale)
+  DevBuf<TwPair> r3_full_inv;
+  bool r3_full_ok = false;
+  TwPair r3_r0_inv{};
 };
 
 // Transform plan for one prime and one length N = 2^k or 3*2^k (root chosen

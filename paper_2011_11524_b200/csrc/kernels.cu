@@ -539,7 +539,7 @@ struct GenArgs {
   u64 root_mont, one_mont, scale_mont;  // Montgomery forms
   u64 p, pp, d_norm, recip;
   unsigned shift;
-  int R;
+  int R, f_off;
   unsigned long long S, M;
 };
 
@@ -547,7 +547,7 @@ __global__ void k_gen_table(GenArgs g) {
   const unsigned long long total = (unsigned long long)g.R * g.S;
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long f = i / g.S, s = i % g.S;
+    const unsigned long long f = i / g.S + g.f_off, s = i % g.S;
     const unsigned long long e = (f * s) % g.M;  // exponent of omega_M (root_mont may be omega^-1)
     u64 w = mont_pow_dev(g.root_mont, e, g.one_mont, g.p, g.pp);
     w = mont_mul(w, g.scale_mont, g.p, g.pp);  // Montgomery form of omega^e * scale
@@ -693,7 +693,7 @@ __device__ __forceinline__ void r3_row_stage(const char* __restrict__ d, unsigne
   }
 }
 
-template <int NG>
+template <int NG, bool FULL>
 __global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restrict__ d, unsigned long long nd,
                                                            unsigned be, Radix3Args a, unsigned* err) {
   pdl_wait();
@@ -737,8 +737,14 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restri
       const u64 y1 = mod_add(mod_sub(x[0], x[2], p), t, p);
       const u64 y2 = mod_sub(mod_sub(x[0], x[1], p), t, p);
       dst[s] = y0;
-      dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hiw[H + sh], p);
-      dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hiw[2 * H + sh], p);
+      if constexpr (FULL) {
+        const TwPair* __restrict__ full = a.full[pr];
+        dst[S + s] = shoup_mul(y1, full[s], p);
+        dst[2 * S + s] = shoup_mul(y2, full[S + s], p);
+      } else {
+        dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hiw[H + sh], p);
+        dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hiw[2 * H + sh], p);
+      }
     }
   }
   if (bad) atomicOr(err, kErrBadDigit);
@@ -955,8 +961,9 @@ void launch_radix3(bool inverse, const Radix3Args& a, int np, cudaStream_t st) {
 }
 
 void launch_gen_pass_table(TwPair* out, u64 root_mont, u64 scale_mont, int R, int /*logR*/, unsigned long long S,
-                           u64 p, u64 recip, cudaStream_t st, unsigned long long order) {
+                           u64 p, u64 recip, cudaStream_t st, unsigned long long order, int f_off) {
   GenArgs g;
+  g.f_off = f_off;
   g.out = out;
   g.root_mont = root_mont;
   g.scale_mont = scale_mont;
@@ -970,7 +977,7 @@ void launch_gen_pass_table(TwPair* out, u64 root_mont, u64 scale_mont, int R, in
   g.recip = recip;
   g.R = R;
   g.S = S;
-  g.M = order ? order : (unsigned long long)R * S;  // order of the root (exponents reduced mod M)
+  g.M = order ? order : (unsigned long long)(R + f_off) * S;  // order of the root (exponents reduced mod M)
   k_gen_table<<<grid_for((unsigned long long)R * S, 256), 256, 0, st>>>(g);
 }
 
@@ -990,7 +997,8 @@ void launch_pack(const char* digits, unsigned long long nd, unsigned be, u64* li
 }
 void launch_pack_radix3(const char* digits, unsigned long long nd, unsigned be, const Radix3Args& a, unsigned* err,
                         cudaStream_t st) {
-  auto fn = be > 16 ? k_pack_radix3<5> : k_pack_radix3<4>;
+  auto fn = a.full[0] ? (be > 16 ? k_pack_radix3<5, true> : k_pack_radix3<4, true>)
+                      : (be > 16 ? k_pack_radix3<5, false> : k_pack_radix3<4, false>);
   launch_pdl(fn, dim3(grid_for(a.S, kPackLimbs)), dim3(kPackLimbs), 0, st, digits, nd, be, a, err);
 }
 void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, unsigned long long rows,

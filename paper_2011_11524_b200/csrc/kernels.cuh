@@ -98,6 +98,11 @@ struct Radix3Args {
   // Unsharded: cb = sb = 0, off = 0 (s = l).
   int cb, sb;
   unsigned long long off;
+  // Unfactorised rows f = 1, 2 (full[(f - 1) S + s], the inverse's carrying the scale) and the
+  // inverse's row-0 factor (the scale): one Shoup product per twiddle instead of two. Only the
+  // fused pack / carry kernels use them (nullptr: the factorised lo * hi).
+  const TwPair* full[2];
+  TwPair r0[2];
 };
 
 // Launchers (kernels.cu).
@@ -107,8 +112,9 @@ void launch_pass_fused(int logR, const PassArgs& a, unsigned long long ncols, in
 void launch_radix3(bool inverse, const Radix3Args& a, int nprimes, cudaStream_t st);
 
 // out[f][s] = root^(f s mod order) * scale (Shoup pairs), f < R, s < S; order 0 = R S.
+// f_off: rows f_off .. f_off + R - 1 (out[f - f_off][s]).
 void launch_gen_pass_table(TwPair* out, u64 root_m, u64 scale, int R, int logR, unsigned long long S, u64 p,
-                           u64 recip, cudaStream_t st, unsigned long long order = 0);
+                           u64 recip, cudaStream_t st, unsigned long long order = 0, int f_off = 0);
 // Local limb i is global limb ((i >> row_bits) * row_stride) + off + (i & (2^row_bits - 1)):
 // unsharded packs use row_bits = 63, off = 0 (limb i = i). Sharded packs need 2^row_bits >= 256.
 // lead_check false (unsharded map only): no leading-zero check (a rank's compacted digit slices).

@@ -144,6 +144,29 @@ def test_factorised_pass_tables(gpu, ref):
         os.environ.pop("DECMUL_FORCE_LARGE_PAIR", None)
 
 
+def test_radix3_twiddle_tables_both_forms(ref):
+    """The fused pack / carry kernels with unfactorised radix-3 twiddle rows (config 4's plan)
+    and with the factorised lo * hi pair (config 5's), forced at small N = 3 2^k sizes
+    (multi-pass, the fused carry included), squaring and not, both prime pairs."""
+    for full in ("1", "0"):
+        os.environ["DECMUL_R3_FULL"] = full
+        try:
+            for large in (False, True):
+                if large:
+                    os.environ["DECMUL_FORCE_LARGE_PAIR"] = "1"
+                ctx = dm.Context(0)  # fresh plans under the knobs
+                for nx, ny in ((300001, 250000), (1400000, 1200000), (5000000, 4000001)):
+                    assert ctx.plan(nx, ny)["length"] % 3 == 0
+                    x, y = inputs.gen_digits(nx + 3, nx), inputs.gen_digits(ny + 4, ny)
+                    assert ctx.multiply_text(x, y) == ref.multiply(x, y), (full, large, nx, ny)
+                    assert ctx.multiply_text(x, None) == ref.multiply(x, None), (full, large, nx)
+                ctx.close()
+                os.environ.pop("DECMUL_FORCE_LARGE_PAIR", None)
+        finally:
+            os.environ.pop("DECMUL_R3_FULL", None)
+            os.environ.pop("DECMUL_FORCE_LARGE_PAIR", None)
+
+
 def test_errors_match_reference_types(gpu):
     with pytest.raises(ValueError, match="non-digit"):
         gpu.multiply_text(b"12a4" * 1000, b"5" * 100)
@@ -426,7 +449,8 @@ def test_prime_pair_option(gpu, ref, port):
 def test_concurrent_small_multiplies_coalesce(ref):
     """decmul_gpu_multiply from 16 threads on one context: the small products are coalesced
     into shared batch launches (leader/follower), every caller gets its own exact product,
-    and a bad operand fails only its own call."""
+    and a bad operand fails only its own call (also when the failing caller is a follower
+    while the next leader holds the context: the lock-order case that once deadlocked)."""
     import threading
 
     import paper_2011_11524_b200 as dm2
@@ -441,7 +465,7 @@ def test_concurrent_small_multiplies_coalesce(ref):
     def work(t):
         try:
             for k, (x, y) in enumerate(pairs[t]):
-                if t == 3 and k == 5:
+                if k % 8 == t % 8:  # failing calls from every thread (followers' error path)
                     try:
                         ctx.multiply_text(x[:100] + b"x" + x[101:], y)
                         errors.append("no error for a bad digit")
