@@ -39,12 +39,75 @@ __device__ __forceinline__ void coeff_digits(const CarryArgs& a, long long i, u6
   split3(a.div, lo, hi, d0, d1, d2);
 }
 
+// Phase 2 (one block of NTB threads): exclusive scan of chunk maps -> chunk carry-ins (stored
+// in place), then the top limb, its digit count and the output length. Reads bypass L1
+// (__ldcg): in the last-block form the other CTAs' writes are only ordered through L2.
+template <int NTB, int CHC>
+__device__ __forceinline__ void scan_chunks_top(const CarryArgs& a, unsigned nchunks, unsigned* wsm, u64* zc) {
+  const unsigned per = (nchunks + NTB - 1) / NTB;
+  const unsigned c0 = threadIdx.x * per;
+  unsigned agg = kIdentityMap;
+  for (unsigned c = c0; c < c0 + per && c < nchunks; ++c) agg = map_compose(__ldcg(a.maps + c), agg);
+  unsigned pre = block_scan_maps<NTB>(agg, wsm, nullptr);
+  unsigned carry = map_apply(pre, 0);
+  for (unsigned c = c0; c < c0 + per && c < nchunks; ++c) {
+    const unsigned m = __ldcg(a.maps + c);
+    a.maps[c] = carry;  // chunk carry-in
+    carry = map_apply(m, carry);
+  }
+  __syncthreads();
+  __threadfence_block();
+  // z at the two candidate top limbs: carry-in of the chunk, then the maps of
+  // the limbs before the candidate inside its chunk.
+  const u64 B = a.div.base;
+  for (int t = 0; t < 2; ++t) {
+    const unsigned long long k = a.top_candidates[t];
+    const unsigned long long cs = k / CHC * CHC;
+    unsigned m = kIdentityMap;
+    const unsigned long long len = k - cs;  // ordered contiguous segments, one per thread
+    const unsigned long long seg = (len + NTB - 1) / NTB;
+    const unsigned long long j0 = cs + threadIdx.x * seg;
+    for (unsigned long long j = j0; j < j0 + seg && j < k; ++j) m = map_compose(limb_map(__ldcg(a.s + j), B), m);
+    block_scan_maps<NTB>(m, wsm, &m);
+    if (threadIdx.x == 0) {
+      const unsigned cin = a.maps[k / CHC];
+      const unsigned c = map_apply(m, cin);
+      u64 v = __ldcg(a.s + k) + c;
+      v -= (v >= B ? B : 0);
+      v -= (v >= B ? B : 0);
+      zc[t] = v;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long top;
+    u64 z;
+    if (zc[1] != 0) {
+      top = a.top_candidates[1];
+      z = zc[1];
+    } else if (zc[0] != 0) {
+      top = a.top_candidates[0];
+      z = zc[0];
+    } else {
+      top = 0;
+      z = 0;
+    }
+    const unsigned len = decimal_len(z);
+    a.meta[0] = top;
+    a.meta[1] = len;
+    a.meta[2] = len + top * a.base_exp;
+  }
+}
+
 // Phase 1: s_k for the chunk's limbs and the chunk's composed transfer map.
 // Coefficients are read and limb sums written in coalesced order (loc = j NT + tid);
 // each limb's 6-bit transfer map goes to shared memory as a byte, and each thread
 // then composes the maps of PERC consecutive limbs (one PERC-byte shared load).
 // FROM_S: the limb sums are already in a.s (the general small-base recovery); only the maps.
-template <int NTC, int PERC, bool FROM_S = false>
+// LASTSCAN (small products): the last CTA to finish (a.ticket) runs phase 2 itself, so the
+// chain is split -> emit with no one-block scan launch in between (which, like an emit that
+// re-derived every chunk carry-in and the top limb per CTA, cost config 1 several us).
+template <int NTC, int PERC, bool FROM_S = false, bool LASTSCAN = false>
 __global__ void __launch_bounds__(NTC) k_carry_split(CarryArgs a) {
   pdl_wait();
   constexpr int CHC = NTC * PERC;
@@ -97,104 +160,32 @@ __global__ void __launch_bounds__(NTC) k_carry_split(CarryArgs a) {
   unsigned total;
   block_scan_maps<NTC>(agg, wsm, &total);
   if (threadIdx.x == 0) a.maps[blockIdx.x] = total;
+  if constexpr (LASTSCAN) {
+    __shared__ unsigned is_last;
+    __shared__ u64 zc[2];
+    __threadfence();  // this CTA's limb sums and chunk map, before its ticket
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (is_last) {
+      __threadfence();
+      scan_chunks_top<NTC, CHC>(a, gridDim.x, wsm, zc);
+      if (threadIdx.x == 0) *a.ticket = 0;  // ready for the next product
+    }
+  }
 }
 
-// Phase 2 (one block): exclusive scan of chunk maps -> chunk carry-ins (stored in
-// place), then the top limb, its digit count and the output length.
 template <int CHC>
 __global__ void __launch_bounds__(1024) k_carry_scan(CarryArgs a, unsigned nchunks) {
   pdl_wait();
   __shared__ unsigned wsm[1024 / 32 + 1];
   __shared__ u64 zc[2];
-  const unsigned per = (nchunks + 1023) / 1024;
-  const unsigned c0 = threadIdx.x * per;
-  unsigned agg = kIdentityMap;
-  for (unsigned c = c0; c < c0 + per && c < nchunks; ++c) agg = map_compose(a.maps[c], agg);
-  unsigned pre = block_scan_maps<1024>(agg, wsm, nullptr);
-  unsigned carry = map_apply(pre, 0);
-  for (unsigned c = c0; c < c0 + per && c < nchunks; ++c) {
-    const unsigned m = a.maps[c];
-    a.maps[c] = carry;  // chunk carry-in
-    carry = map_apply(m, carry);
-  }
-  __syncthreads();
-  __threadfence_block();
-  // z at the two candidate top limbs: carry-in of the chunk, then the maps of
-  // the limbs before the candidate inside its chunk.
-  const u64 B = a.div.base;
-  for (int t = 0; t < 2; ++t) {
-    const unsigned long long k = a.top_candidates[t];
-    const unsigned long long cs = k / CHC * CHC;
-    unsigned m = kIdentityMap;
-    const unsigned long long len = k - cs;  // ordered contiguous segments, one per thread
-    const unsigned long long seg = (len + 1023) / 1024;
-    const unsigned long long j0 = cs + threadIdx.x * seg;
-    for (unsigned long long j = j0; j < j0 + seg && j < k; ++j) m = map_compose(limb_map(a.s[j], B), m);
-    const unsigned before = block_scan_maps<1024>(m, wsm, &m);
-    (void)before;
-    if (threadIdx.x == 0) {
-      const unsigned cin = a.maps[k / CHC];
-      const unsigned c = map_apply(m, cin);
-      u64 v = a.s[k] + c;
-      v -= (v >= B ? B : 0);
-      v -= (v >= B ? B : 0);
-      zc[t] = v;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    unsigned long long top;
-    u64 z;
-    if (zc[1] != 0) {
-      top = a.top_candidates[1];
-      z = zc[1];
-    } else if (zc[0] != 0) {
-      top = a.top_candidates[0];
-      z = zc[0];
-    } else {
-      top = 0;
-      z = 0;
-    }
-    const unsigned len = decimal_len(z);
-    a.meta[0] = top;
-    a.meta[1] = len;
-    a.meta[2] = len + top * a.base_exp;
-  }
-}
-
-// z (final value) of limb k given its chunk's carry-in: compose the maps of the limbs
-// before k inside its chunk (block-wide, ordered segments).
-template <int NTB, int CHC>
-__device__ __forceinline__ u64 limb_value(const CarryArgs& a, unsigned long long k, unsigned chunk_cin,
-                                          unsigned* wsm) {
-  const u64 B = a.div.base;
-  const unsigned long long cs = k / CHC * CHC, len = k - cs, seg = (len + NTB - 1) / NTB;
-  const unsigned long long j0 = cs + threadIdx.x * seg;
-  unsigned m = kIdentityMap;
-  for (unsigned long long j = j0; j < j0 + seg && j < k; ++j) m = map_compose(limb_map(a.s[j], B), m);
-  block_scan_maps<NTB>(m, wsm, &m);
-  u64 v = a.s[k] + map_apply(m, chunk_cin);
-  v -= (v >= B ? B : 0);
-  v -= (v >= B ? B : 0);
-  return v;
-}
-
-// Composition of chunk maps [0, c) applied to 0: the carry into chunk c (block-wide).
-template <int NTB>
-__device__ __forceinline__ unsigned chunk_carry_in(const unsigned* maps, unsigned c, unsigned* wsm) {
-  const unsigned per = (c + NTB - 1) / NTB, c0 = threadIdx.x * per;
-  unsigned agg = kIdentityMap;
-  for (unsigned i = c0; i < c0 + per && i < c; ++i) agg = map_compose(maps[i], agg);
-  unsigned total;
-  block_scan_maps<NTB>(agg, wsm, &total);
-  return map_apply(total, 0);
+  scan_chunks_top<1024, CHC>(a, nchunks, wsm, zc);
 }
 
 // Phase 3: apply carries and print each limb at its place in the output string.
 // The chunk's digits are staged in shared memory and stored as 16-byte vectors.
-// SELF (small products): no phase 2 — every CTA derives its chunk carry-in and the
-// top limb from the chunk maps itself (a few thousand maps at most).
-template <int NTC, int PERC, bool SELF>
+template <int NTC, int PERC>
 __global__ void __launch_bounds__(NTC) k_carry_emit(CarryArgs a) {
   pdl_wait();
   constexpr int CHC = NTC * PERC;
@@ -203,27 +194,10 @@ __global__ void __launch_bounds__(NTC) k_carry_emit(CarryArgs a) {
   __shared__ __align__(16) char buf[CHC * 17 + 32];
   __shared__ __align__(8) unsigned char mp[CHC];  // limb maps, then limb carry-ins
   const unsigned long long cbase = (unsigned long long)blockIdx.x * CHC;
-  unsigned long long top;
-  unsigned top_len, chunk_cin;
-  if constexpr (SELF) {
-    const unsigned long long k0 = a.top_candidates[0], k1 = a.top_candidates[1];
-    const u64 z0 = limb_value<NTC, CHC>(a, k0, chunk_carry_in<NTC>(a.maps, unsigned(k0 / CHC), wsm), wsm);
-    const u64 z1 = limb_value<NTC, CHC>(a, k1, chunk_carry_in<NTC>(a.maps, unsigned(k1 / CHC), wsm), wsm);
-    top = z1 != 0 ? k1 : (z0 != 0 ? k0 : 0);
-    top_len = decimal_len(z1 != 0 ? z1 : z0);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      a.meta[0] = top;
-      a.meta[1] = top_len;
-      a.meta[2] = top_len + top * a.base_exp;
-    }
-    if (cbase > top) return;  // uniform per block
-    chunk_cin = chunk_carry_in<NTC>(a.maps, blockIdx.x, wsm);
-  } else {
-    top = a.meta[0];
-    top_len = unsigned(a.meta[1]);
-    if (a.k_off + cbase > top) return;  // nothing of this chunk is printed (uniform per block)
-    chunk_cin = a.maps[blockIdx.x];
-  }
+  const unsigned long long top = a.meta[0];
+  const unsigned top_len = unsigned(a.meta[1]);
+  if (a.k_off + cbase > top) return;  // nothing of this chunk is printed (uniform per block)
+  const unsigned chunk_cin = a.maps[blockIdx.x];
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const u64 B = a.div.base;
   // coalesced limb sums (loc = j NTC + tid); their maps to shared memory
@@ -570,7 +544,7 @@ int launch_carry_general(const CarryArgs& a0, int D, int rounds, u64* tmp, unsig
   const unsigned nchunks = unsigned((K + CH - 1) / CH);
   launch_pdl(k_carry_split<NT, PER, true>, dim3(nchunks), dim3(NT), 0, st, a);
   launch_pdl(k_carry_scan<CH>, dim3(1), dim3(1024), 0, st, a, nchunks);
-  launch_pdl(k_carry_emit<NT, PER, false>, dim3(nchunks), dim3(NT), 0, st, a);
+  launch_pdl(k_carry_emit<NT, PER>, dim3(nchunks), dim3(NT), 0, st, a);
   prof_mark("k_carry_general_scan_emit", st, 0, double(K) * 16);
   return launched + 3;
 }
@@ -584,7 +558,7 @@ static int launch_carry_large(const CarryArgs& a, unsigned long long K, cudaStre
   prof_mark("k_carry_split", st, n, 16 * n + 8 * k);
   launch_pdl(k_carry_scan<CHL>, dim3(1), dim3(1024), 0, st, a, nchunks);
   prof_mark("k_carry_scan", st, 0, 8.0 * nchunks);
-  launch_pdl(k_carry_emit<NT, PERL, false>, dim3(nchunks), dim3(NT), 0, st, a);
+  launch_pdl(k_carry_emit<NT, PERL>, dim3(nchunks), dim3(NT), 0, st, a);
   prof_mark("k_carry_emit", st, 0, 8 * k + k * a.base_exp);
   return 3;
 }
@@ -598,7 +572,7 @@ int launch_carry_r3(const CarryArgs& a, const Radix3Args& r, cudaStream_t st) {
   prof_mark("k_carry_split_r3", st, 2.0 * 6.0 * r.S + n, 16 * n + 8 * k);
   launch_pdl(k_carry_scan<CH>, dim3(1), dim3(1024), 0, st, a, nchunks);
   prof_mark("k_carry_scan", st, 0, 8.0 * nchunks);
-  launch_pdl(k_carry_emit<NT, PER, false>, dim3(nchunks), dim3(NT), 0, st, a);
+  launch_pdl(k_carry_emit<NT, PER>, dim3(nchunks), dim3(NT), 0, st, a);
   prof_mark("k_carry_emit", st, 0, 8 * k + k * a.base_exp);
   return 3;
 }
@@ -611,9 +585,9 @@ int launch_carry(const CarryArgs& a, cudaStream_t st) {
   if (nchunks < 2 * 148) {  // small product: 512-limb chunks, no separate scan
     const unsigned ns = unsigned((K + kCarryChunkSmall - 1) / kCarryChunkSmall);
     const double n = double(a.n), k = double(K);
-    launch_pdl(k_carry_split<NT_SMALL, PER_SMALL>, dim3(ns), dim3(NT_SMALL), 0, st, a);
+    launch_pdl(k_carry_split<NT_SMALL, PER_SMALL, false, true>, dim3(ns), dim3(NT_SMALL), 0, st, a);
     prof_mark("k_carry_split_small", st, n, 16 * n + 8 * k);
-    launch_pdl(k_carry_emit<NT_SMALL, PER_SMALL, true>, dim3(ns), dim3(NT_SMALL), 0, st, a);
+    launch_pdl(k_carry_emit<NT_SMALL, PER_SMALL>, dim3(ns), dim3(NT_SMALL), 0, st, a);
     prof_mark("k_carry_emit_small", st, 0, 8 * k + k * a.base_exp);
     return 2;
   }
@@ -636,7 +610,7 @@ void launch_carry_shard_emit(const CarryArgs& a, unsigned rank_cin, cudaStream_t
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const unsigned nchunks = unsigned((K + CH - 1) / CH);
   k_carry_cin<<<(nchunks + 255) / 256, 256, 0, st>>>(a.maps, nchunks, rank_cin);
-  k_carry_emit<NT, PER, false><<<nchunks, NT, 0, st>>>(a);
+  k_carry_emit<NT, PER><<<nchunks, NT, 0, st>>>(a);
 }
 
 }  // namespace dmg

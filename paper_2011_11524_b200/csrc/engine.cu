@@ -123,7 +123,9 @@ Engine::Engine(int device) : device_(device) {
   }
   err_.ensure(1);
   async_err_.ensure(1);
+  ticket_.ensure(1);
   meta_.ensure(4);
+  cuda_check(cudaMemsetAsync(ticket_.ptr, 0, sizeof(unsigned), stream_), "memset");
   cuda_check(cudaMemsetAsync(err_.ptr, 0, sizeof(unsigned), stream_), "memset");
   cuda_check(cudaMemsetAsync(async_err_.ptr, 0, sizeof(unsigned), stream_), "memset");
   cuda_check(cudaStreamSynchronize(stream_), "init");
@@ -651,6 +653,7 @@ static bool carry3_exact(unsigned be, std::size_t min_limbs) {
 
 int Engine::recover(CarryArgs c, unsigned be, std::size_t min_limbs, bool allow_s_in_x, cudaStream_t st) {
   (void)allow_s_in_x;
+  c.ticket = ticket_.ptr;
   if (carry3_exact(be, min_limbs)) return launch_carry(c, st);
   // D = base-B digits of the coefficient cap; normalisation rounds until every sum <= 3 (B - 1)
   const u128 B = pow10u(be), cap = ((u128)c.coeff_cap_hi << 64) | c.coeff_cap_lo;
