@@ -73,7 +73,10 @@ int decmul_gpu_plan(decmul_gpu_ctx* ctx, size_t digits_x, size_t digits_y, unsig
  * x, y: most-significant-first ASCII digits (the DecimalNumber text, decimal.hpp:26-38).
  * out receives the product digits (cap >= nx + ny); *out_len its length.
  * alias != 0 is the reference's &x == &y squaring path (decimal.cpp:198); equal texts
- * are detected as squaring too. forced_base_exp = MultiplyOptions::forced_base_exp. */
+ * are detected as squaring too. forced_base_exp = MultiplyOptions::forced_base_exp.
+ * Products past the largest transform the large pair holds (N > 3 * 2^30 limbs; the reference
+ * raises OperandTooLarge past 3 * 2^24) run as a block convolution: block products of 6e9
+ * digits fanned out over the context's devices and summed on the host (csrc/blocked.cu). */
 int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
                         size_t cap, size_t* out_len, unsigned forced_base_exp, int alias);
 

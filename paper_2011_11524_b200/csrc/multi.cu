@@ -120,6 +120,10 @@ std::size_t MultiEngine::multiply_host(const char* x, std::size_t nx, const char
                                        std::size_t cap, unsigned forced, bool alias, u64 p1, u64 p2) {
   if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
   const bool zero = (nx == 1 && x[0] == '0') || (ny == 1 && y[0] == '0');
+  if (!zero && !p1 && !p2) {  // past the largest transform: block convolution (blocked.cu)
+    const std::size_t K = block_digits(nx, ny, forced);
+    if (K) return blocked_multiply(x, nx, y, ny, out, cap, forced, K);
+  }
   if (!zero && !p1 && !p2 && shards(nx, ny, forced)) {
     const bool squaring = alias || (nx == ny && (x == y || std::memcmp(x, y, nx) == 0));
     if ((nx > 1 && x[0] == '0') || (ny > 1 && y[0] == '0')) throw std::invalid_argument("decimal: leading zero");
@@ -127,30 +131,6 @@ std::size_t MultiEngine::multiply_host(const char* x, std::size_t nx, const char
   }
   cudaSetDevice(eng_[0]->device());
   return eng_[0]->multiply_host(x, nx, y, ny, out, cap, forced, alias, p1, p2);
-}
-
-// Runs f(rank, begin, end) for the G contiguous ranges of [0, count) on G host threads (each
-// engine on its own device); rethrows the first failure.
-template <class F>
-void MultiEngine::fan_out(std::size_t count, F&& f) {
-  const std::size_t G = eng_.size();
-  std::vector<std::exception_ptr> errs(G);
-  std::vector<std::thread> th;
-  for (std::size_t q = 0; q < G; ++q) {
-    const std::size_t b = count * q / G, e = count * (q + 1) / G;
-    if (b == e) continue;
-    th.emplace_back([&, q, b, e] {
-      try {
-        cuda_check(cudaSetDevice(eng_[q]->device()), "cudaSetDevice");
-        f(*eng_[q], b, e);
-      } catch (...) {
-        errs[q] = std::current_exception();
-      }
-    });
-  }
-  for (auto& t : th) t.join();
-  for (auto& e : errs)
-    if (e) std::rethrow_exception(e);
 }
 
 void MultiEngine::multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,

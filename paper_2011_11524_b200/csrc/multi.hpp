@@ -1,7 +1,9 @@
 // Multi-device context (see multi.cu): one Engine per device of the context; batches fan out
 // over the devices, one large product is sharded over them.
 #pragma once
+#include <exception>
 #include <memory>
+#include <thread>
 #include <vector>
 
 #include "engine.hpp"
@@ -34,6 +36,13 @@ class MultiEngine {
   // the sharded product itself (any size the shard shape admits)
   std::size_t sharded_multiply(const char* x, std::size_t nx, const char* y, std::size_t ny, char* out,
                                std::size_t cap, bool squaring);
+  // block convolution (blocked.cu): products past the largest transform as sums of block
+  // products of K digits each, fanned out over the devices; block_digits: the K multiply_host
+  // uses (0 = one ordinary product)
+  static constexpr std::size_t kBlockDigits = 6000000000ull;
+  std::size_t block_digits(std::size_t nx, std::size_t ny, unsigned forced) const;
+  std::size_t blocked_multiply(const char* x, std::size_t nx, const char* y, std::size_t ny, char* out,
+                               std::size_t cap, unsigned forced, std::size_t K);
 
  private:
   template <class F>
@@ -48,5 +57,29 @@ class MultiEngine {
   static constexpr std::size_t kPinnedWords = 7 * 64;  // halo, rank maps, probes of up to 64 ranks
   u64* pinned_ = nullptr;
 };
+
+// Runs f(rank, begin, end) for the G contiguous ranges of [0, count) on G host threads (each
+// engine on its own device); rethrows the first failure.
+template <class F>
+inline void MultiEngine::fan_out(std::size_t count, F&& f) {
+  const std::size_t G = eng_.size();
+  std::vector<std::exception_ptr> errs(G);
+  std::vector<std::thread> th;
+  for (std::size_t q = 0; q < G; ++q) {
+    const std::size_t b = count * q / G, e = count * (q + 1) / G;
+    if (b == e) continue;
+    th.emplace_back([&, q, b, e] {
+      try {
+        cuda_check(cudaSetDevice(eng_[q]->device()), "cudaSetDevice");
+        f(*eng_[q], b, e);
+      } catch (...) {
+        errs[q] = std::current_exception();
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
 
 }  // namespace dmg

@@ -167,6 +167,38 @@ def test_radix3_twiddle_tables_both_forms(ref):
             os.environ.pop("DECMUL_FORCE_LARGE_PAIR", None)
 
 
+def test_block_convolution_fallback(ref):
+    """Products past the largest transform run as sums of block products (SURVEY §7 D1
+    fallback, blocked.cu), forced at small sizes with DECMUL_BLOCK_DIGITS: ragged blocks,
+    leading zeros and all-zero blocks inside an operand, squaring, one and two engines."""
+    def with_zeros(seed, n, runs):
+        d = bytearray(inputs.gen_digits(seed, n))
+        for start, length in runs:
+            d[start:start + length] = b"0" * length
+        return bytes(d)
+
+    os.environ["DECMUL_BLOCK_DIGITS"] = "7000"
+    try:
+        for devices in ([0], [0, 0]):
+            ctx = dm.Context(devices=devices)
+            cases = [(inputs.gen_digits(11, 30001), inputs.gen_digits(12, 17000)),
+                     (with_zeros(13, 50000, [(8000, 7000), (43000 - 5, 3000)]), with_zeros(14, 21001, [(1, 9000)])),
+                     (inputs.gen_digits(15, 6999), inputs.gen_digits(16, 70000)),
+                     (b"9" * 28000, b"9" * 28000)]
+            for x, y in cases:
+                assert ctx.multiply_text(x, y) == ref.multiply(x, y), (devices, len(x), len(y))
+            x = inputs.gen_digits(17, 40000)
+            assert ctx.multiply_text(x, None) == ref.multiply(x, None)
+            with pytest.raises(ValueError, match="non-digit"):
+                ctx.multiply_text(x[:30000] + b"/" + x[30001:], x)
+            with pytest.raises(ValueError, match="leading zero"):
+                ctx.multiply_text(b"0" + x[1:], x)
+            assert ctx.multiply_text(b"0", x) == b"0"
+            ctx.close()
+    finally:
+        os.environ.pop("DECMUL_BLOCK_DIGITS", None)
+
+
 def test_errors_match_reference_types(gpu):
     with pytest.raises(ValueError, match="non-digit"):
         gpu.multiply_text(b"12a4" * 1000, b"5" * 100)
