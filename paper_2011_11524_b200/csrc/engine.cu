@@ -406,11 +406,13 @@ static bool inverse_lazy_ok(const PrimePlan& pl, std::size_t i) {
 }
 
 void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2], std::size_t begin,
-                        std::size_t end, const ShardGeom* sg, cudaStream_t st) {
+                        std::size_t end, const ShardGeom* sg, cudaStream_t st, const u64* const src_b[2],
+                        u64* const dst_b[2]) {
   for (std::size_t i = begin; i < end; ++i) {
     const bool first = i == begin;
     const PassLocal L = local_pass(*pl[0], i, sg);
     if (pl[0]->passes[i]->radix3) {
+      if (src_b) throw std::logic_error("two-operand passes: power-of-two passes only");
       Radix3Args a{};
       for (int q = 0; q < np; ++q) {
         a.src[q] = first ? src[q] : dst[q];
@@ -441,7 +443,12 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
         a.pass_hi[q] = Pq.hi_fwd.ptr;
         a.p[q] = pl[q]->p;
         a.pp[q] = pl[q]->pp;
+        if (src_b) {
+          a.src_b[q] = first ? src_b[q] : dst_b[q];
+          a.dst_b[q] = dst_b[q];
+        }
       }
+      a.nops = src_b ? 2 : 1;
       a.tw_lbits = P.tw_lbits;
       a.S = L.S;
       a.logS = L.logS;
@@ -453,7 +460,7 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
         char nm[64];
         std::snprintf(nm, sizeof nm, "k_pass_fwd<%d,%s>", P.logR, L.S > 1 ? "rows" : "cols");
         const double n = double(L.ncols) * P.R;
-        prof_mark(nm, st, np * (n / 2 * P.logR + (L.S > 1 ? n : 0)), np * 16 * n);
+        prof_mark(nm, st, a.nops * np * (n / 2 * P.logR + (L.S > 1 ? n : 0)), a.nops * np * 16 * n);
       }
     }
     ++launches_;
@@ -836,9 +843,22 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
     const char* f2 = std::getenv("DECMUL_FUSE2");
     // (R = 512: two 64 KB tiles would leave one CTA per SM)
     const bool two = P1.last_pow2 && m >= 2 && P1.passes[m - 1]->logR <= 8 && !(f2 && f2[0] == '0');
-    load(dx, pp.dx, px, X, !two);
-    if (before_y) before_y();
-    load(dy, pp.dy, py, Y, !P1.last_pow2);
+    // small transforms are launch-latency bound: both operands share the pack launch and each
+    // forward pass launch (blockIdx.y = operand); larger ones keep y's upload overlapping x's work
+    const bool paired = two && !lean && !fuse_r3 && pp.N <= (std::size_t(1) << 21);
+    if (paired) {
+      if (before_y) before_y();
+      launch_pack2(dx, pp.dx, px, dy, pp.dy, py, be, npad, err, st);
+      prof_mark("k_pack2", st, 0, double(pp.dx + pp.dy) + 16.0 * npad);
+      ++launches_;
+      const u64* sx[2] = {px, px};
+      const u64* sy[2] = {py, py};
+      passes_fwd(pl, 2, sx, X, 0, m - 1, nullptr, st, sy, Y);
+    } else {
+      load(dx, pp.dx, px, X, !two);
+      if (before_y) before_y();
+      load(dy, pp.dy, py, Y, !P1.last_pow2);
+    }
     if (P1.last_pow2) {
       const u64* oth[2] = {X[0], X[1]};
       pass_fused(pl, 2, Y, oth, nullptr, st, two);

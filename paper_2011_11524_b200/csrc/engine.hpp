@@ -300,8 +300,10 @@ class Engine {
                             cudaStream_t st);
   void transform_inverse(const PrimePlan* pl[2], int np, u64* const data[2], bool skip_last, cudaStream_t st);
   PassLocal local_pass(const PrimePlan& pl, std::size_t i, const ShardGeom* sg) const;
+  // src_b / dst_b: a second operand in the same launches (power-of-two passes only)
   void passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2], std::size_t begin,
-                  std::size_t end, const ShardGeom* sg, cudaStream_t st);
+                  std::size_t end, const ShardGeom* sg, cudaStream_t st, const u64* const src_b[2] = nullptr,
+                  u64* const dst_b[2] = nullptr);
   // two: other[] holds the first operand before its last forward pass (run inside the kernel)
   void pass_fused(const PrimePlan* pl[2], int np, u64* const data[2], const u64* const other[2],
                   const ShardGeom* sg, cudaStream_t st, bool two = false);

@@ -205,8 +205,8 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   TwPair* tw = reinterpret_cast<TwPair*>(sm + R * TW);
   const int pr = int(blockIdx.x % a.np), tid = threadIdx.x;
   const u64 p = a.p[pr];
-  const u64* src = a.src[pr];
-  u64* dst = a.dst[pr];
+  const u64* src = blockIdx.y ? a.src_b[pr] : a.src[pr];  // blockIdx.y: the second operand
+  u64* dst = blockIdx.y ? a.dst_b[pr] : a.dst[pr];
   const TwPair* __restrict__ T = a.pass_tw[pr];
   const TwPair* __restrict__ Hi = a.pass_hi[pr];
   const Geom<LOGR, ROWS, TW> G(a);
@@ -620,12 +620,19 @@ __device__ __forceinline__ u64 pack_parse(const char* __restrict__ d, unsigned l
 
 // LEAD: d is the whole operand (its leading zero is an error); false for a rank's compacted
 // digit slices (multi.cu), whose first digit may be 0.
+// blockIdx.y == 1: the second operand of a two-operand launch (d2, nd2 -> limbs2, unsharded).
 template <bool ROWMAP, int NG, bool LEAD = true>
 __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d, unsigned long long nd, unsigned be,
                                                      u64* __restrict__ limbs, unsigned long long total, unsigned* err,
                                                      int row_bits, unsigned long long row_stride,
-                                                     unsigned long long off) {
+                                                     unsigned long long off, const char* __restrict__ d2,
+                                                     unsigned long long nd2, u64* __restrict__ limbs2) {
   pdl_wait();
+  if (blockIdx.y) {
+    d = d2;
+    nd = nd2;
+    limbs = limbs2;
+  }
   __shared__ __align__(16) char smem[kPackBuf];
   const unsigned long long rmask = row_bits >= 63 ? ~0ull : (1ull << row_bits) - 1;
   unsigned bad = 0;
@@ -852,7 +859,7 @@ void launch_pass_kernel(const PassArgs& a, unsigned long long ncols, int np, int
   set_smem<FN>(smem);
   PassArgs b = a;
   b.np = np;
-  launch_pdl(FN, dim3(unsigned((ncols + TW - 1) / TW * np)), dim3(NTK), size_t(smem), st, b);
+  launch_pdl(FN, dim3(unsigned((ncols + TW - 1) / TW * np), a.nops > 1 ? 2 : 1), dim3(NTK), size_t(smem), st, b);
 }
 
 // Tile width: 16 columns (128 B row segments) normally; 4 when a pass would otherwise
@@ -984,16 +991,22 @@ void launch_gen_pass_table(TwPair* out, u64 root_mont, u64 scale_mont, int R, in
 void launch_pack(const char* digits, unsigned long long nd, unsigned be, u64* limbs, unsigned long long total,
                  unsigned* err, cudaStream_t st, int row_bits, unsigned long long row_stride,
                  unsigned long long off, bool lead_check) {
+  const char* nd2 = nullptr;
   if (row_bits < 8)
     k_pack_rows<<<grid_for(total, 256), 256, 0, st>>>(digits, nd, be, limbs, total, err, row_bits, row_stride, off);
   else if (!lead_check)
     launch_pdl(be > 16 ? k_pack<false, 5, false> : k_pack<false, 4, false>, dim3(grid_for(total, 256)), dim3(256), 0,
-               st, digits, nd, be, limbs, total, err, row_bits, row_stride, off);
+               st, digits, nd, be, limbs, total, err, row_bits, row_stride, off, nd2, 0ull, (u64*)nullptr);
   else
     launch_pdl(row_bits >= 63 ? (be > 16 ? k_pack<false, 5> : k_pack<false, 4>)
                               : (be > 16 ? k_pack<true, 5> : k_pack<true, 4>),
                dim3(grid_for(total, 256)), dim3(256), 0, st, digits, nd, be, limbs, total, err, row_bits, row_stride,
-               off);
+               off, nd2, 0ull, (u64*)nullptr);
+}
+void launch_pack2(const char* dx, unsigned long long nx, u64* limbs_x, const char* dy, unsigned long long ny,
+                  u64* limbs_y, unsigned be, unsigned long long total, unsigned* err, cudaStream_t st) {
+  launch_pdl(be > 16 ? k_pack<false, 5> : k_pack<false, 4>, dim3(grid_for(total, 256), 2), dim3(256), 0, st, dx, nx, be,
+             limbs_x, total, err, 63, 0ull, 0ull, dy, ny, limbs_y);
 }
 void launch_pack_radix3(const char* digits, unsigned long long nd, unsigned be, const Radix3Args& a, unsigned* err,
                         cudaStream_t st) {

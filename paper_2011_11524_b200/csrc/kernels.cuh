@@ -79,6 +79,9 @@ struct PassArgs {
   int lazy_out;            // inverse / fused passes: outputs may stay in [0, 2p) (the next pass is an
                            // inverse row pass, whose first step is a Shoup twiddle product)
   int two;                 // fused pass: other = the first operand before its last forward pass
+  int nops;                // forward passes: 2 = a second operand in the same launch (blockIdx.y = 1)
+  const u64* src_b[2];     // the second operand's input / output (nops == 2)
+  u64* dst_b[2];
 };
 
 // Radix-3 pass over N = 3 S. The twiddle omega_N^{+-f s} (times the convolution
@@ -121,6 +124,9 @@ void launch_gen_pass_table(TwPair* out, u64 root_m, u64 scale, int R, int logR, 
 void launch_pack(const char* digits, unsigned long long nd, unsigned base_exp, u64* limbs,
                  unsigned long long nlimbs_total, unsigned* err, cudaStream_t st, int row_bits = 63,
                  unsigned long long row_stride = 0, unsigned long long off = 0, bool lead_check = true);
+// Both operands of a product in one launch (blockIdx.y = operand; unsharded, leading-zero check).
+void launch_pack2(const char* dx, unsigned long long nx, u64* limbs_x, const char* dy, unsigned long long ny,
+                  u64* limbs_y, unsigned base_exp, unsigned long long nlimbs_total, unsigned* err, cudaStream_t st);
 // Pack fused with the forward radix-3 pass (N = 3 S, unsharded): digits -> pass 0's output
 // of both primes (a.dst), lo/hi/lam/p/lbits/hrow as for launch_radix3; a.src unused.
 void launch_pack_radix3(const char* digits, unsigned long long nd, unsigned base_exp, const Radix3Args& a,

@@ -447,7 +447,7 @@ def test_profile_report(gpu):
     rep = gpu.profile_report()
     gpu.profile(False)
     names = [r[0] for r in rep]
-    assert names[0] == "k_pack" and any(nm.startswith("k_pass_fused") for nm in names)
+    assert names[0].startswith("k_pack") and any(nm.startswith("k_pass_fused") for nm in names)
     assert any(nm.startswith("k_carry") for nm in names)
     assert all(ms >= 0 for _, ms, _, _ in rep)
     assert sum(mm for _, _, mm, _ in rep) > 0
