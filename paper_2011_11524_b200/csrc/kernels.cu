@@ -657,20 +657,25 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack(const char* __restrict__ d,
 // (factorised lo * hi as in k_radix3_fwd) for both primes, and writes pass 0's output.
 // The packed limbs never touch HBM (the separate pack wrote 8 B and the radix-3 pass read
 // them back per limb).
-// The block's three spans are staged with 16-byte loads; in span-local coordinates thread t's
-// limb always ends at byte (kPackLimbs - t) lambda, so the parse needs no 64-bit index
+// The block's three spans are staged with 16-byte loads; in span-local coordinates column c's
+// limb always ends at byte (kR3Cols - c) lambda, so the parse needs no 64-bit index
 // arithmetic (only the block holding the string's head clips). Rows past the last limb are
 // skipped block-uniformly (config 4's y fills one of the three rows, x two).
 // (Rejected: double-buffered cp.async staging of the spans and twiddles, 4.48 / 5.74 ms for the
 // two config-4 launches vs 4.32 single-buffered.)
+// CB = kR3Cols columns per block, two per thread (c = t, t + 256): the per-iteration work
+// (span bounds, staging set-up, barriers) is shared by two columns and the two columns'
+// arithmetic interleaves.
+constexpr int kR3Cols = 2 * kPackLimbs;
+constexpr int kR3Buf = kR3Cols * 17 + 96;
+
+// Limb of column c of a block whose row span ends at string position hi (exclusive).
 template <int NG>
 __device__ __forceinline__ u64 r3_row_limb(const char* __restrict__ d, unsigned long long nd, long long hi,
-                                           unsigned be, const char* buf, unsigned* err, unsigned& bad) {
-  // hi = string end (exclusive) of the block's first limb; the span starts at hi - 256 be
-  const int t = threadIdx.x;
-  const long long base = hi - (long long)kPackLimbs * be;  // string position of span byte 0
+                                           unsigned be, const char* buf, int c, unsigned* err, unsigned& bad) {
+  const long long base = hi - (long long)kR3Cols * be;  // string position of span byte 0
   const int o = int((reinterpret_cast<unsigned long long>(d) + (unsigned long long)base) & 15);
-  const int e = (kPackLimbs - t) * int(be);  // limb end, span-local
+  const int e = (kR3Cols - c) * int(be);  // limb end, span-local
   int b = e - int(be);
   if (base < 0) {  // the string's head: limbs may be short or absent
     const int b0 = int(-base);
@@ -685,72 +690,81 @@ __device__ __forceinline__ u64 r3_row_limb(const char* __restrict__ d, unsigned 
 }
 __device__ __forceinline__ void r3_row_stage(const char* __restrict__ d, unsigned long long nd, long long hi,
                                              unsigned be, char* buf) {
-  const long long base = hi - (long long)kPackLimbs * be;
+  const long long base = hi - (long long)kR3Cols * be;
   const int o = int((reinterpret_cast<unsigned long long>(d) + (unsigned long long)base) & 15);
-  const long long g0 = base - o;  // 16-byte aligned in the address space
-  const int nvec = (o + kPackLimbs * int(be) + 15) >> 4;
-  char* dst = buf + 32;
+  const char* g0 = d + (base - o);  // 16-byte aligned in the address space
+  const int nvec = (o + kR3Cols * int(be) + 15) >> 4;
+  // vectors [vlo, vhi) lie wholly inside the string; the few others go byte by byte
+  const long long first = base - o;
+  const int vlo = first >= 0 ? 0 : int((-first + 15) >> 4);
+  const long long room = (long long)nd - first;
+  const int vhi = room >= 16LL * nvec ? nvec : (room < 16 ? 0 : int(room >> 4));
+  uint4* dst = reinterpret_cast<uint4*>(buf + 32);
   for (int v = threadIdx.x; v < nvec; v += kPackLimbs) {
-    const long long g = g0 + 16LL * v;
-    if (g >= 0 && g + 16 <= (long long)nd) {
-      reinterpret_cast<uint4*>(dst)[v] = *reinterpret_cast<const uint4*>(d + g);
+    if (v >= vlo && v < vhi) {
+      dst[v] = reinterpret_cast<const uint4*>(g0)[v];
     } else {
-      for (int k = 0; k < 16; ++k) dst[v * 16 + k] = (g + k >= 0 && g + k < (long long)nd) ? d[g + k] : '0';
+      const long long g = first + 16LL * v;
+      char* db = buf + 32 + 16 * v;
+      for (int k = 0; k < 16; ++k) db[k] = (g + k >= 0 && g + k < (long long)nd) ? d[g + k] : '0';
     }
   }
 }
 
-template <int NG, bool FULL>
+template <int NG>
 __global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restrict__ d, unsigned long long nd,
                                                            unsigned be, Radix3Args a, unsigned* err) {
   pdl_wait();
-  __shared__ __align__(16) char smem[3][kPackBuf];
+  __shared__ __align__(16) char smem[3][kR3Buf];
   const unsigned long long S = a.S, L = 1ull << a.lbits, H = a.hrow;
   const unsigned long long nl = (nd + be - 1) / be;  // limbs of the string
+  const long long SB = (long long)(S * be);           // digits per row of limbs
   unsigned bad = 0;
-  for (unsigned long long s0 = (unsigned long long)blockIdx.x * kPackLimbs; s0 < S;
-       s0 += (unsigned long long)gridDim.x * kPackLimbs) {
+  for (unsigned long long s0 = (unsigned long long)blockIdx.x * kR3Cols; s0 < S;
+       s0 += (unsigned long long)gridDim.x * kR3Cols) {
     bool live[3];
     long long hi[3];
+    hi[0] = (long long)nd - (long long)(s0 * be);
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const unsigned long long t0 = j * S + s0;  // the block's first limb of row j
-      live[j] = t0 < nl;
-      hi[j] = (long long)nd - (long long)(t0 * be);
+      if (j) hi[j] = hi[j - 1] - SB;
+      live[j] = j * S + s0 < nl;  // the block's first limb of row j
       if (live[j]) r3_row_stage(d, nd, hi[j], be, smem[j]);
     }
     __syncthreads();
-    const unsigned long long s = s0 + threadIdx.x;
-    u64 x[3];
+    u64 x[2][3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      x[j] = 0;
-      // limbs past the string's end inside a live block: its last block may be partial
-      if (live[j] && j * S + s < nl) x[j] = r3_row_limb<NG>(d, nd, hi[j], be, smem[j], err, bad);
+    for (int h = 0; h < 2; ++h) {
+      const int c = threadIdx.x + h * kPackLimbs;
+      const unsigned long long s = s0 + c;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        x[h][j] = 0;
+        // limbs past the string's end inside a live block: its last block may be partial
+        if (live[j] && j * S + s < nl) x[h][j] = r3_row_limb<NG>(d, nd, hi[j], be, smem[j], c, err, bad);
+      }
     }
     __syncthreads();
-    if (s >= S) continue;
-    const unsigned long long sl = s & (L - 1), sh = s >> a.lbits;
 #pragma unroll
-    for (int pr = 0; pr < 2; ++pr) {
-      const u64 p = a.p[pr];
-      const TwPair lam = a.lam[pr];
-      const TwPair* __restrict__ lo = a.lo[pr];
-      const TwPair* __restrict__ hiw = a.hi[pr];
-      u64* dst = a.dst[pr];
-      // limbs are < 10^17 < p: canonical residues of both primes
-      const u64 t = shoup_mul(mod_sub(x[1], x[2], p), lam, p);
-      const u64 y0 = mod_add(mod_add(x[0], x[1], p), x[2], p);
-      const u64 y1 = mod_add(mod_sub(x[0], x[2], p), t, p);
-      const u64 y2 = mod_sub(mod_sub(x[0], x[1], p), t, p);
-      dst[s] = y0;
-      if constexpr (FULL) {
-        const TwPair* __restrict__ full = a.full[pr];
-        dst[S + s] = shoup_mul(y1, full[s], p);
-        dst[2 * S + s] = shoup_mul(y2, full[S + s], p);
-      } else {
-        dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hiw[H + sh], p);
-        dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hiw[2 * H + sh], p);
+    for (int h = 0; h < 2; ++h) {
+      const unsigned long long s = s0 + threadIdx.x + h * kPackLimbs;
+      if (s >= S) continue;
+      const unsigned long long sl = s & (L - 1), sh = s >> a.lbits;
+#pragma unroll
+      for (int pr = 0; pr < 2; ++pr) {
+        const u64 p = a.p[pr];
+        const TwPair lam = a.lam[pr];
+        const TwPair* __restrict__ lo = a.lo[pr];
+        const TwPair* __restrict__ hiw = a.hi[pr];
+        u64* dst = a.dst[pr] + s;
+        // limbs are < 10^17 < p: canonical residues of both primes
+        const u64 t = shoup_mul(mod_sub(x[h][1], x[h][2], p), lam, p);
+        const u64 y0 = mod_add(mod_add(x[h][0], x[h][1], p), x[h][2], p);
+        const u64 y1 = mod_add(mod_sub(x[h][0], x[h][2], p), t, p);
+        const u64 y2 = mod_sub(mod_sub(x[h][0], x[h][1], p), t, p);
+        dst[0] = y0;
+        dst[S] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hiw[H + sh], p);
+        dst[2 * S] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hiw[2 * H + sh], p);
       }
     }
   }
@@ -1010,9 +1024,8 @@ void launch_pack2(const char* dx, unsigned long long nx, u64* limbs_x, const cha
 }
 void launch_pack_radix3(const char* digits, unsigned long long nd, unsigned be, const Radix3Args& a, unsigned* err,
                         cudaStream_t st) {
-  auto fn = a.full[0] ? (be > 16 ? k_pack_radix3<5, true> : k_pack_radix3<4, true>)
-                      : (be > 16 ? k_pack_radix3<5, false> : k_pack_radix3<4, false>);
-  launch_pdl(fn, dim3(grid_for(a.S, kPackLimbs)), dim3(kPackLimbs), 0, st, digits, nd, be, a, err);
+  auto fn = be > 16 ? k_pack_radix3<5> : k_pack_radix3<4>;
+  launch_pdl(fn, dim3(grid_for(a.S, kR3Cols)), dim3(kPackLimbs), 0, st, digits, nd, be, a, err);
 }
 void launch_block_reorder(const u64* src, u64* dst, unsigned long long peers, unsigned long long rows,
                           unsigned long long width, bool to_segments, cudaStream_t st) {
