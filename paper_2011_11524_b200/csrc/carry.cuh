@@ -148,13 +148,17 @@ __device__ __forceinline__ void text_push8(TextAcc& t, unsigned (&W)[NW], u64 x,
   }
 }
 
-template <int BE>
-__device__ __forceinline__ void print_run8(char* dst, const u64 (&v)[8]) {
+// NL limbs of width BE (highest first) as one text run of NL BE bytes at dst (any alignment):
+// the text is built in registers as 32-bit words, stored as aligned words (funnel shifts) with
+// the partial words at both ends (shared with the neighbouring runs) byte by byte.
+template <int BE, int NL>
+__device__ __forceinline__ void print_run(char* dst, const u64 (&v)[NL]) {
   static_assert(BE >= 14 && BE <= 17, "limb width");
-  unsigned W[2 * BE];
+  constexpr int TB = NL * BE, NWF = TB / 4, REM = TB % 4;
+  unsigned W[NWF + 2];
   TextAcc t;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
+  for (int j = 0; j < NL; ++j) {
     const u64 q = v[j] / 100000000ull;  // the digits above the low 8
     const unsigned lo8 = unsigned(v[j] - q * 100000000ull);
     if constexpr (BE == 17) {
@@ -166,22 +170,27 @@ __device__ __forceinline__ void print_run8(char* dst, const u64 (&v)[8]) {
     }
     text_push8(t, W, ascii8(lo8), 8);
   }
-  // store the 8 BE bytes at dst (any alignment): aligned words via funnel shifts, the two
-  // partial words (shared with the neighbouring runs) byte by byte
+  const unsigned tail = unsigned(t.acc);  // the last REM bytes
   const int ph = int(reinterpret_cast<unsigned long long>(dst) & 3);
   unsigned* aw = reinterpret_cast<unsigned*>(dst - ph);
   if (ph == 0) {
 #pragma unroll
-    for (int i = 0; i < 2 * BE; ++i) aw[i] = W[i];
+    for (int i = 0; i < NWF; ++i) aw[i] = W[i];
+    for (int b = 0; b < REM; ++b) dst[4 * NWF + b] = char(tail >> (8 * b));
   } else {
     const int sh = 8 * ph;
     for (int b = 0; b < 4 - ph; ++b) dst[b] = char(W[0] >> (8 * b));
 #pragma unroll
-    for (int i = 1; i < 2 * BE; ++i) aw[i] = __funnelshift_l(W[i - 1], W[i], sh);
-    const unsigned last = W[2 * BE - 1] >> (32 - sh);
-    char* tail = reinterpret_cast<char*>(aw + 2 * BE);
-    for (int b = 0; b < ph; ++b) tail[b] = char(last >> (8 * b));
+    for (int i = 1; i < NWF; ++i) aw[i] = __funnelshift_l(W[i - 1], W[i], sh);
+    // the last ph bytes of W[NWF - 1], then the REM tail bytes
+    const u64 rest = (u64)(W[NWF - 1] >> (32 - sh)) | ((u64)tail << sh);
+    char* e = dst + (4 * NWF - ph);
+    for (int b = 0; b < ph + REM; ++b) e[b] = char(rest >> (8 * b));
   }
+}
+template <int BE>
+__device__ __forceinline__ void print_run8(char* dst, const u64 (&v)[8]) {
+  print_run<BE, 8>(dst, v);
 }
 
 // Copy len bytes from shared s to global g with 16-byte stores in the aligned middle.
