@@ -99,6 +99,22 @@ __device__ __forceinline__ void scan_chunks_top(const CarryArgs& a, unsigned nch
   }
 }
 
+// Per-limb in-chunk exclusive prefix maps (a.pm, one byte per limb): `pre` is the composition
+// of the earlier threads' limbs, m8 this thread's PERC limb maps; the emit then applies
+// pm[k] to the chunk's carry-in instead of recomputing every limb's map and scanning again.
+template <int PERC, class Word>
+__device__ __forceinline__ void store_prefix_maps(unsigned char* pm, unsigned long long first, unsigned pre,
+                                                  unsigned long long m8) {
+  unsigned long long out = 0;
+  unsigned c = pre;
+#pragma unroll
+  for (int j = 0; j < PERC; ++j) {
+    out |= (unsigned long long)c << (8 * j);
+    c = map_compose(unsigned(m8 >> (8 * j)) & 63u, c);
+  }
+  *reinterpret_cast<Word*>(pm + first) = Word(out);
+}
+
 // Phase 1: s_k for the chunk's limbs and the chunk's composed transfer map.
 // Coefficients are read and limb sums written in coalesced order (loc = j NT + tid);
 // each limb's 6-bit transfer map goes to shared memory as a byte, and each thread
@@ -158,8 +174,9 @@ __global__ void __launch_bounds__(NTC) k_carry_split(CarryArgs a) {
 #pragma unroll
   for (int j = 0; j < PERC; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
   unsigned total;
-  block_scan_maps<NTC>(agg, wsm, &total);
+  const unsigned pre = block_scan_maps<NTC>(agg, wsm, &total);
   if (threadIdx.x == 0) a.maps[blockIdx.x] = total;
+  if (a.pm) store_prefix_maps<PERC, Word>(a.pm, k0 + threadIdx.x * PERC, pre, m8);
   if constexpr (LASTSCAN) {
     __shared__ unsigned is_last;
     __shared__ u64 zc[2];
@@ -200,27 +217,36 @@ __global__ void __launch_bounds__(NTC) k_carry_emit(CarryArgs a) {
   const unsigned chunk_cin = a.maps[blockIdx.x];
   const unsigned long long K = a.n + (a.tail ? 2 : 0);
   const u64 B = a.div.base;
-  // coalesced limb sums (loc = j NTC + tid); their maps to shared memory
-  u64 s[PERC];
-#pragma unroll
-  for (int j = 0; j < PERC; ++j) {
-    const unsigned long long k = cbase + j * NTC + threadIdx.x;
-    s[j] = k < K ? a.s[k] : 0;
-    mp[j * NTC + threadIdx.x] = (unsigned char)limb_map(s[j], B);
-  }
-  __syncthreads();
-  // each thread: PERC consecutive limbs -> composed map -> block scan -> per-limb carry-ins
-  unsigned long long m8 = reinterpret_cast<const Word*>(mp)[threadIdx.x];
-  unsigned agg = kIdentityMap;
-#pragma unroll
-  for (int j = 0; j < PERC; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
-  const unsigned pre = block_scan_maps<NTC>(agg, wsm, nullptr);  // ends with a barrier
-  unsigned c = map_apply(pre, chunk_cin);
   unsigned long long cin8 = 0;
+  if (a.pm) {
+    // the split stored every limb's in-chunk prefix map: carry-in = prefix applied to the
+    // chunk's carry-in (no limb maps, no block scan here)
+    const unsigned long long p8 = *reinterpret_cast<const Word*>(a.pm + cbase + threadIdx.x * PERC);
 #pragma unroll
-  for (int j = 0; j < PERC; ++j) {
-    cin8 |= (unsigned long long)c << (8 * j);
-    c = map_apply(unsigned(m8 >> (8 * j)) & 63u, c);
+    for (int j = 0; j < PERC; ++j)
+      cin8 |= (unsigned long long)map_apply(unsigned(p8 >> (8 * j)) & 63u, chunk_cin) << (8 * j);
+  } else {
+    // coalesced limb sums (loc = j NTC + tid); their maps to shared memory
+    u64 s[PERC];
+#pragma unroll
+    for (int j = 0; j < PERC; ++j) {
+      const unsigned long long k = cbase + j * NTC + threadIdx.x;
+      s[j] = k < K ? a.s[k] : 0;
+      mp[j * NTC + threadIdx.x] = (unsigned char)limb_map(s[j], B);
+    }
+    __syncthreads();
+    // each thread: PERC consecutive limbs -> composed map -> block scan -> per-limb carry-ins
+    unsigned long long m8 = reinterpret_cast<const Word*>(mp)[threadIdx.x];
+    unsigned agg = kIdentityMap;
+#pragma unroll
+    for (int j = 0; j < PERC; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
+    const unsigned pre = block_scan_maps<NTC>(agg, wsm, nullptr);  // ends with a barrier
+    unsigned c = map_apply(pre, chunk_cin);
+#pragma unroll
+    for (int j = 0; j < PERC; ++j) {
+      cin8 |= (unsigned long long)c << (8 * j);
+      c = map_apply(unsigned(m8 >> (8 * j)) & 63u, c);
+    }
   }
   reinterpret_cast<Word*>(mp)[threadIdx.x] = Word(cin8);
   __syncthreads();
@@ -417,6 +443,10 @@ __global__ void __launch_bounds__(NT) k_carry_split_r3(CarryArgs a, Radix3Args r
       a.s[N] = sN;
       a.s[N + 1] = sN1;
       a.maps[N / CH] = map_compose(limb_map(sN1, B), limb_map(sN, B));
+      if (a.pm) {  // in-chunk prefixes of the tail chunk's two limbs
+        a.pm[N] = (unsigned char)kIdentityMap;
+        a.pm[N + 1] = (unsigned char)limb_map(sN, B);
+      }
     }
     return;
   }
@@ -483,8 +513,9 @@ __global__ void __launch_bounds__(NT) k_carry_split_r3(CarryArgs a, Radix3Args r
 #pragma unroll
     for (int j = 0; j < PER; ++j) agg = map_compose(unsigned(m8 >> (8 * j)) & 63u, agg);
     unsigned total;
-    block_scan_maps<NT>(agg, wsm, &total);
+    const unsigned pre = block_scan_maps<NT>(agg, wsm, &total);
     if (tid == 0) a.maps[(g * S + s0) / CH] = total;
+    if (a.pm) store_prefix_maps<PER, unsigned long long>(a.pm, g * S + s0 + tid * PER, pre, m8);
   }
 }
 

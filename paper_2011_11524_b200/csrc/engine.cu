@@ -661,7 +661,11 @@ static bool carry3_exact(unsigned be, std::size_t min_limbs) {
 int Engine::recover(CarryArgs c, unsigned be, std::size_t min_limbs, bool allow_s_in_x, cudaStream_t st) {
   (void)allow_s_in_x;
   c.ticket = ticket_.ptr;
-  if (carry3_exact(be, min_limbs)) return launch_carry(c, st);
+  if (carry3_exact(be, min_limbs)) {
+    pm_.ensure((c.n + 2 + 2 * kCarryChunk) / kCarryChunk * kCarryChunk);
+    c.pm = pm_.ptr;
+    return launch_carry(c, st);
+  }
   // D = base-B digits of the coefficient cap; normalisation rounds until every sum <= 3 (B - 1)
   const u128 B = pow10u(be), cap = ((u128)c.coeff_cap_hi << 64) | c.coeff_cap_lo;
   int D = 1;
@@ -681,6 +685,8 @@ int Engine::recover(CarryArgs c, unsigned be, std::size_t min_limbs, bool allow_
   maps_.ensure(carry_map_words(K));
   c.s = S_.ptr;
   c.maps = maps_.ptr;
+  pm_.ensure((K + 2 * kCarryChunk) / kCarryChunk * kCarryChunk);
+  c.pm = pm_.ptr;
   return launch_carry_general(c, D, rounds, S2_.ptr, K, st);
 }
 
@@ -915,6 +921,8 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
     r.S = P0.S;
     r.lbits = P0.r3_lbits;
     r.hrow = P0.S >> r.lbits;
+    pm_.ensure((pp.N + 2 + 2 * kCarryChunk) / kCarryChunk * kCarryChunk);
+    c.pm = pm_.ptr;
     launches_ += launch_carry_r3(c, r, st);
   } else {
     launches_ += recover(c, be, std::min(lx, ly), s_in_x, st);

@@ -342,6 +342,7 @@ class Engine {
   std::map<std::pair<u64, std::size_t>, std::unique_ptr<PrimePlan>> plans_;
   DevBuf<u64> X_[2], Y_[2], Px_, Py_, S_, S2_;
   DevBuf<unsigned> maps_, err_, async_err_, ticket_;  // ticket_: the small carry's last-CTA counter
+  DevBuf<unsigned char> pm_;                         // per-limb prefix maps of the carry (split -> emit)
   DevBuf<unsigned long long> meta_, lens_;
   DevBuf<char> din_x_, din_y_, dout_;
   int launches_ = 0;

@@ -162,6 +162,7 @@ struct CarryArgs {
   u64 halo1[2], halo2[2];  // residues of global coefficients k_off - 2, k_off - 1 (zeros on the first rank)
   int tail;                // this rank also emits the two trailing limbs N, N + 1 (last rank)
   unsigned* ticket;        // small products: CTA completion counter of the split (0 between uses)
+  unsigned char* pm;       // optional, K bytes: per-limb in-chunk exclusive prefix maps (split -> emit)
 };
 constexpr int kCarryChunk = 2048;       // limbs per carry chunk (large products, shards)
 constexpr int kCarryThreads = 256;
