@@ -364,7 +364,9 @@ __device__ __forceinline__ void r3inv_load(const Radix3Args& r, unsigned long lo
   }
 }
 // (the inputs are only multiplied before the length-3 DFT: they may be lazy, [0, 2p))
-template <bool FULL>
+// PRE: the merged twiddles omega_{3 R1}^{-f r} from r.pinv, one Shoup product
+// per element; else the factorised lo * hi.
+template <bool PRE>
 __device__ __forceinline__ void r3inv_from(const Radix3Args& r, unsigned long long s, const u64 x[2][3],
                                            u64 out[2][3]) {
   const unsigned long long L = 1ull << r.lbits, H = r.hrow;
@@ -372,15 +374,15 @@ __device__ __forceinline__ void r3inv_from(const Radix3Args& r, unsigned long lo
 #pragma unroll
   for (int pr = 0; pr < 2; ++pr) {
     const u64 p = r.p[pr];
-    const TwPair* __restrict__ lo = r.lo[pr];
-    const TwPair* __restrict__ hi = r.hi[pr];
     u64 y0, y1, y2;
-    if constexpr (FULL) {
-      const TwPair* __restrict__ full = r.full[pr];
-      y0 = shoup_mul(x[pr][0], r.r0[pr], p);
-      y1 = shoup_mul(x[pr][1], full[s], p);
-      y2 = shoup_mul(x[pr][2], full[r.S + s], p);
+    if constexpr (PRE) {
+      const TwPair* __restrict__ pv = r.pinv[pr] + (s >> r.pre_shift);
+      y0 = shoup_mul(x[pr][0], pv[0], p);
+      y1 = shoup_mul(x[pr][1], pv[r.pre_rows], p);
+      y2 = shoup_mul(x[pr][2], pv[2 * r.pre_rows], p);
     } else {
+      const TwPair* __restrict__ lo = r.lo[pr];
+      const TwPair* __restrict__ hi = r.hi[pr];
       y0 = shoup_mul(x[pr][0], hi[sh], p);  // lo[0][.] = 1
       y1 = shoup_mul(shoup_mul(x[pr][1], lo[L + sl], p), hi[H + sh], p);
       y2 = shoup_mul(shoup_mul(x[pr][2], lo[2 * L + sl], p), hi[2 * H + sh], p);
@@ -391,11 +393,11 @@ __device__ __forceinline__ void r3inv_from(const Radix3Args& r, unsigned long lo
     out[pr][2] = mod_sub(mod_sub(y0, y1, p), t, p);
   }
 }
-template <bool FULL>
+template <bool PRE>
 __device__ __forceinline__ void r3inv_column(const Radix3Args& r, unsigned long long s, u64 out[2][3]) {
   u64 x[2][3];
   r3inv_load(r, s, x);
-  r3inv_from<FULL>(r, s, x, out);
+  r3inv_from<PRE>(r, s, x, out);
 }
 
 __device__ __forceinline__ void coeff_split(const CarryArgs& a, u64 r1, u64 r2, bool check, u64& d0, u64& d1,
@@ -407,13 +409,13 @@ __device__ __forceinline__ void coeff_split(const CarryArgs& a, u64 r1, u64 r2, 
 }
 
 // d1, d2 of coefficient k (k < 0: zero)
-template <bool FULL>
+template <bool PRE>
 __device__ __forceinline__ void coeff_d12(const CarryArgs& a, const Radix3Args& r, long long k, u64& d1, u64& d2) {
   d1 = d2 = 0;
   if (k < 0) return;
   u64 c[2][3];
   const unsigned long long g = (unsigned long long)k / r.S;
-  r3inv_column<FULL>(r, (unsigned long long)k - g * r.S, c);
+  r3inv_column<PRE>(r, (unsigned long long)k - g * r.S, c);
   u64 d0;
   coeff_split(a, g == 0 ? c[0][0] : (g == 1 ? c[0][1] : c[0][2]), g == 0 ? c[1][0] : (g == 1 ? c[1][1] : c[1][2]),
               false, d0, d1, d2);
@@ -424,7 +426,7 @@ __device__ __forceinline__ void coeff_d12(const CarryArgs& a, const Radix3Args& 
 // k - 1 and d2 of k - 2 through warp shuffles, with the warp edges (and the chunk's two halo
 // coefficients) in shared memory. The last CTA (a.tail) forms the two trailing limbs N, N + 1.
 // Replaces k_radix3_inv + k_carry_split: the natural-order coefficients never touch HBM.
-template <bool FULL>
+template <bool PRE>
 __global__ void __launch_bounds__(NT) k_carry_split_r3(CarryArgs a, Radix3Args r) {
   pdl_wait();
   constexpr int NW = NT / 32;
@@ -437,8 +439,8 @@ __global__ void __launch_bounds__(NT) k_carry_split_r3(CarryArgs a, Radix3Args r
   if (blockIdx.x == S / CH) {  // tail chunk N / CH: limbs N, N + 1 (K = N + 2)
     if (tid == 0) {
       u64 d1a, d2a, d1b, d2b;
-      coeff_d12<FULL>(a, r, (long long)N - 1, d1a, d2a);
-      coeff_d12<FULL>(a, r, (long long)N - 2, d1b, d2b);
+      coeff_d12<PRE>(a, r, (long long)N - 1, d1a, d2a);
+      coeff_d12<PRE>(a, r, (long long)N - 2, d1b, d2b);
       const u64 sN = d1a + d2b, sN1 = d2a;
       a.s[N] = sN;
       a.s[N + 1] = sN1;
@@ -454,7 +456,7 @@ __global__ void __launch_bounds__(NT) k_carry_split_r3(CarryArgs a, Radix3Args r
   if (tid < 6) {  // halo: coefficients k0 - 1 and k0 - 2 of each group's chunk
     const int g = tid >> 1, which = tid & 1;
     u64 d1, d2;
-    coeff_d12<FULL>(a, r, (long long)(g * S + s0) - 1 - which, d1, d2);
+    coeff_d12<PRE>(a, r, (long long)(g * S + s0) - 1 - which, d1, d2);
     if (which == 0) {
       e1[g][0] = d1;
       e2b[g][0] = d2;
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(NT) k_carry_split_r3(CarryArgs a, Radix3Args r
 #pragma unroll
       for (int q = 0; q < 6; ++q) cur[q / 3][q % 3] = xin[q / 3][q % 3];
       if (j + 1 < PER) r3inv_load(r, s + NT, xin);
-      r3inv_from<FULL>(r, s, cur, c);
+      r3inv_from<PRE>(r, s, cur, c);
     }
     u64 d0[3], d1[3], d2[3];
 #pragma unroll
@@ -598,7 +600,7 @@ int launch_carry_r3(const CarryArgs& a, const Radix3Args& r, cudaStream_t st) {
   const unsigned long long N = 3 * r.S, K = N + 2;
   const unsigned nchunks = unsigned((K + CH - 1) / CH);  // S / CH column blocks + the tail chunk
   const double n = double(N), k = double(K);
-  launch_pdl(r.full[0] ? k_carry_split_r3<true> : k_carry_split_r3<false>, dim3(unsigned(r.S / CH + 1)), dim3(NT), 0,
+  launch_pdl(r.pinv[0] ? k_carry_split_r3<true> : k_carry_split_r3<false>, dim3(unsigned(r.S / CH + 1)), dim3(NT), 0,
              st, a, r);
   prof_mark("k_carry_split_r3", st, 2.0 * 6.0 * r.S + n, 16 * n + 8 * k);
   launch_pdl(k_carry_scan<CH>, dim3(1), dim3(1024), 0, st, a, nchunks);

@@ -26,12 +26,12 @@ bool factor_tables(std::size_t entries) {
 }
 
 
-// Unfactorised inverse radix-3 twiddle rows (2 S pairs per prime, 4.3 GB in all for config
-// 4's S = 2^26) save the fused carry kernel one Shoup product per twiddle; larger transforms
-// keep only the factorised tables. DECMUL_R3_FULL=0/1 overrides (tests, A/B).
-bool r3_full_tables(std::size_t S) {
-  if (const char* e = std::getenv("DECMUL_R3_FULL")) return e[0] == '1';
-  return S <= (std::size_t(1) << 26);
+// Radix-3 twiddles merged into pass 1 (PassArgs::pre): the radix-3 passes run twiddle-free
+// forward and with a 3 x R1 table inverse; pass 1 gets one twiddle table per radix-3 row.
+// DECMUL_R3_MERGE=0 keeps the factorised lo * hi twiddles in the radix-3 passes (tests, A/B).
+bool r3_merge_enabled() {
+  const char* e = std::getenv("DECMUL_R3_MERGE");
+  return !(e && e[0] == '0');
 }
 
 u64 recip_of(u64 d) {  // reference make_div_by_const (decimal.hpp:93-104), for a normalized divisor
@@ -200,6 +200,29 @@ void Engine::build_passes(PrimePlan& pl) {
     if (ps->radix3 || ps->S > 1) last_table = int(i);
     pl.passes.push_back(std::move(ps));
   }
+  // merged radix-3 twiddles need pass 1 to be a staged row pass (S1 > 1, 16 <= R1)
+  pl.r3_merged = pl.passes.size() >= 2 && pl.passes[0]->radix3 && pl.passes[1]->S > 1 && pl.passes[1]->logR >= 4 &&
+                 r3_merge_enabled();
+  if (pl.r3_merged) {
+    // pre[f R1 + r] = omega_{3 R1}^{f r}; pinv[f R1 + r] = omega_{3 R1}^{-f r} (the convolution
+    // scale rides on the highest pass with a table, never pass 0 here: pass 1 has S > 1)
+    const int R1 = pl.passes[1]->R;
+    const u64 w = F.pow(pl.xi, pl.N / (3 * std::size_t(R1))), wi = F.inv(w);
+    std::vector<TwPair> pre(3 * R1), pinv(3 * R1);
+    for (int f = 0; f < 3; ++f) {
+      const u64 sf = F.pow(w, f), sfi = F.pow(wi, f);
+      u64 a = 1, b = last_table == 0 ? pl.conv_scale : 1;
+      for (int r = 0; r < R1; ++r) {
+        pre[f * R1 + r] = shoup_pair(F, a);
+        pinv[f * R1 + r] = shoup_pair(F, b);
+        a = F.mul(a, sf);
+        b = F.mul(b, sfi);
+      }
+    }
+    upload(pl.r3_pre, pre, stream_);
+    upload(pl.r3_pinv, pinv, stream_);
+    cuda_check(cudaStreamSynchronize(stream_), "radix-3 merged tables");
+  }
   for (std::size_t i = 0; i < pl.passes.size(); ++i) {
     PassPlan& ps = *pl.passes[i];
     const std::size_t M = std::size_t(ps.R) * ps.S;
@@ -233,18 +256,47 @@ void Engine::build_passes(PrimePlan& pl) {
       upload(ps.r3_hi_fwd, hf, stream_);
       upload(ps.r3_lo_inv, li, stream_);
       upload(ps.r3_hi_inv, hi, stream_);
-      ps.r3_r0_inv = shoup_pair(F, scale);
-      if (i == 0 && r3_full_tables(ps.S)) {
-        // rows 1, 2 of omega_N^{-f s} scale (N = M = 3 S), generated on the device. Inverse only:
-        // with them the fused pack turned HBM-bound (config 4: 4.17 -> 4.66 ms) while the
-        // carry split gained (3.29 -> 3.12 ms).
-        ps.r3_full_inv.ensure(2 * ps.S);
-        launch_gen_pass_table(ps.r3_full_inv.ptr, F.to_mont(wMi), F.to_mont(scale), 2, 0, ps.S, pl.p, recip, stream_, M,
-                              1);
-        cuda_check(cudaGetLastError(), "gen radix-3 table");
-        ps.r3_full_ok = true;
-      }
       cuda_check(cudaStreamSynchronize(stream_), "radix-3 tables");
+    } else if (i == 1 && pl.r3_merged) {
+      // pass 1 after a twiddle-free radix-3 pass: group g (radix-3 row g) uses
+      // omega_N^{(3 f1 + g) c} = omega_S^{f1 c} (its own twiddle) * omega_N^{g c} (the radix-3
+      // twiddle's part that commutes with the column DFT); one table (or lo / hi pair) per group
+      const std::size_t N = pl.N;
+      const u64 xi = pl.xi, xii = F.inv(pl.xi);
+      const std::size_t cnt = std::size_t(ps.R) * ps.S;
+      const u64 scale = int(i) == last_table ? pl.conv_scale : 1;
+      if (factor_all_ || factor_tables(3 * cnt)) {
+        const int lb = std::max(kTileLogW, (ps.logS + 1) / 2);
+        const std::size_t L = std::size_t(1) << lb, H = ps.S / L;
+        ps.tw_lbits = lb;
+        ps.tw_gstride = std::size_t(ps.R) * L;
+        ps.hi_gstride = std::size_t(ps.R) * H;
+        ps.tw_fwd.ensure(3 * ps.tw_gstride);
+        ps.tw_inv.ensure(3 * ps.tw_gstride);
+        ps.hi_fwd.ensure(3 * ps.hi_gstride);
+        ps.hi_inv.ensure(3 * ps.hi_gstride);
+        for (int g = 0; g < 3; ++g) {
+          launch_gen_pass_table(ps.tw_fwd.ptr + g * ps.tw_gstride, F.to_mont(xi), F.to_mont(1), ps.R, ps.logR, L, pl.p,
+                                recip, stream_, N, 0, 3, g);
+          launch_gen_pass_table(ps.tw_inv.ptr + g * ps.tw_gstride, F.to_mont(xii), F.to_mont(1), ps.R, ps.logR, L,
+                                pl.p, recip, stream_, N, 0, 3, g);
+          launch_gen_pass_table(ps.hi_fwd.ptr + g * ps.hi_gstride, F.to_mont(F.pow(xi, L)), F.to_mont(1), ps.R,
+                                ps.logR, H, pl.p, recip, stream_, N / L, 0, 3, g);
+          launch_gen_pass_table(ps.hi_inv.ptr + g * ps.hi_gstride, F.to_mont(F.pow(xii, L)), F.to_mont(scale), ps.R,
+                                ps.logR, H, pl.p, recip, stream_, N / L, 0, 3, g);
+        }
+      } else {
+        ps.tw_gstride = cnt;
+        ps.tw_fwd.ensure(3 * cnt);
+        ps.tw_inv.ensure(3 * cnt);
+        for (int g = 0; g < 3; ++g) {
+          launch_gen_pass_table(ps.tw_fwd.ptr + g * cnt, F.to_mont(xi), F.to_mont(1), ps.R, ps.logR, ps.S, pl.p, recip,
+                                stream_, N, 0, 3, g);
+          launch_gen_pass_table(ps.tw_inv.ptr + g * cnt, F.to_mont(xii), F.to_mont(scale), ps.R, ps.logR, ps.S, pl.p,
+                                recip, stream_, N, 0, 3, g);
+        }
+      }
+      cuda_check(cudaGetLastError(), "gen table");
     } else if (ps.S > 1) {
       const std::size_t cnt = std::size_t(ps.R) * ps.S;
       const u64 scale = int(i) == last_table ? pl.conv_scale : 1;
@@ -422,6 +474,7 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
         a.p[q] = pl[q]->p;
         a.lam[q] = pl[q]->lam;
       }
+      a.notw = pl[0]->r3_merged ? 1 : 0;
       a.S = L.S;
       a.lbits = pl[0]->passes[i]->r3_lbits;
       a.hrow = pl[0]->passes[i]->S >> a.lbits;
@@ -447,7 +500,10 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
           a.src_b[q] = first ? src_b[q] : dst_b[q];
           a.dst_b[q] = dst_b[q];
         }
+        a.pre[q] = (i == 1 && pl[q]->r3_merged) ? pl[q]->r3_pre.ptr : nullptr;
       }
+      a.tw_gstride = P.tw_gstride;
+      a.hi_gstride = P.hi_gstride;
       a.nops = src_b ? 2 : 1;
       a.tw_lbits = P.tw_lbits;
       a.S = L.S;
@@ -520,6 +576,11 @@ void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std:
         a.hi[q] = pl[q]->passes[ii]->r3_hi_inv.ptr;
         a.p[q] = pl[q]->p;
         a.lam[q] = pl[q]->lam_inv;
+        a.pinv[q] = pl[q]->r3_merged ? pl[q]->r3_pinv.ptr : nullptr;
+      }
+      if (pl[0]->r3_merged) {
+        a.pre_shift = pl[0]->passes[1]->logS;
+        a.pre_rows = pl[0]->passes[1]->R;
       }
       a.S = L.S;
       a.lbits = pl[0]->passes[ii]->r3_lbits;
@@ -552,6 +613,8 @@ void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std:
       a.has_final_scale = (!any_table && ii == 0) ? 1 : 0;
       a.lazy_out = inverse_lazy_ok(*pl[0], ii) ? 1 : 0;
       a.tw_lbits = P.tw_lbits;
+      a.tw_gstride = P.tw_gstride;
+      a.hi_gstride = P.hi_gstride;
       launch_pass_inv(P.logR, a, L.ncols, np, st);
       if (prof_on_) {
         char nm[64];
@@ -699,11 +762,10 @@ void Engine::pack_radix3(const PrimePlan* pl[2], const char* digits, std::size_t
     a.dst[q] = dst[q];
     a.lo[q] = pl[q]->passes[0]->r3_lo_fwd.ptr;
     a.hi[q] = pl[q]->passes[0]->r3_hi_fwd.ptr;
-    a.full[q] = nullptr;  // factorised forward twiddles (see build_passes)
     a.p[q] = pl[q]->p;
     a.lam[q] = pl[q]->lam;
   }
-  if (!a.full[0] || !a.full[1]) a.full[0] = a.full[1] = nullptr;
+  a.notw = pl[0]->r3_merged ? 1 : 0;
   a.S = P.S;
   a.lbits = P.r3_lbits;
   a.hrow = P.S >> a.lbits;
@@ -912,12 +974,14 @@ void Engine::run_product(const ProductPlan& pp, const char* dx, const char* dy, 
       r.dst[q] = nullptr;
       r.lo[q] = pl[q]->passes[0]->r3_lo_inv.ptr;
       r.hi[q] = pl[q]->passes[0]->r3_hi_inv.ptr;
-      r.full[q] = pl[q]->passes[0]->r3_full_ok ? pl[q]->passes[0]->r3_full_inv.ptr : nullptr;
-      r.r0[q] = pl[q]->passes[0]->r3_r0_inv;
       r.p[q] = pl[q]->p;
       r.lam[q] = pl[q]->lam_inv;
+      r.pinv[q] = pl[q]->r3_merged ? pl[q]->r3_pinv.ptr : nullptr;
     }
-    if (!r.full[0] || !r.full[1]) r.full[0] = r.full[1] = nullptr;
+    if (P1.r3_merged) {
+      r.pre_shift = P1.passes[1]->logS;
+      r.pre_rows = P1.passes[1]->R;
+    }
     r.S = P0.S;
     r.lbits = P0.r3_lbits;
     r.hrow = P0.S >> r.lbits;

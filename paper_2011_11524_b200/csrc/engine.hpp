@@ -60,11 +60,8 @@ struct PassPlan {
   // radix-3 passes: omega_N^{+-f s} = lo[f][s mod 2^lbits] * hi[f][s >> lbits]
   DevBuf<TwPair> r3_lo_fwd, r3_hi_fwd, r3_lo_inv, r3_hi_inv;
   int r3_lbits = 0;
-  // unfactorised inverse rows f = 1, 2 (2 S pairs, carrying the scale) for the fused carry
-  // kernel when they fit (r3_full_ok), and the inverse's row-0 factor (the scale)
-  DevBuf<TwPair> r3_full_inv;
-  bool r3_full_ok = false;
-  TwPair r3_r0_inv{};
+  // per-group twiddle tables (pass 1 after a merged radix-3 pass): group g at + g * stride
+  unsigned long long tw_gstride = 0, hi_gstride = 0;
 };
 
 // Transform plan for one prime and one length N = 2^k or 3*2^k (root chosen
@@ -79,6 +76,10 @@ struct PrimePlan {
   TwPair lam{}, lam_inv{};
   std::vector<std::unique_ptr<PassPlan>> passes;  // pass 0 first
   bool last_pow2 = false;  // last pass is a power-of-two pass with S == 1 (fusable)
+  // radix-3 twiddles merged into pass 1 (build_passes): pre = omega_{3 R1}^{f r} (forward, pass 1's
+  // column inputs), pinv = omega_{3 R1}^{-f r} scale (inverse radix-3), 3 x R1 Shoup pairs each
+  bool r3_merged = false;
+  DevBuf<TwPair> r3_pre, r3_pinv;
   // one-CTA kernel tables (N small): row length c = N / 3^three
   DevBuf<TwPair> small_fwd, small_inv, r3_fwd, r3_inv;
   bool small_ok = false;

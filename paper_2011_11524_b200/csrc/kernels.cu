@@ -207,9 +207,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   const u64 p = a.p[pr];
   const u64* src = blockIdx.y ? a.src_b[pr] : a.src[pr];  // blockIdx.y: the second operand
   u64* dst = blockIdx.y ? a.dst_b[pr] : a.dst[pr];
-  const TwPair* __restrict__ T = a.pass_tw[pr];
-  const TwPair* __restrict__ Hi = a.pass_hi[pr];
   const Geom<LOGR, ROWS, TW> G(a);
+  const unsigned long long grp = ROWS ? (blockIdx.x / a.np) % a.G : 0;  // group of a row tile
+  const TwPair* __restrict__ T = a.pass_tw[pr] + grp * a.tw_gstride;
+  const TwPair* __restrict__ Hi = a.pass_hi[pr] + grp * a.hi_gstride;
   if constexpr (ROWS && !FACT) {
     // The twiddles are applied in the epilogue, after the DIF; start pulling the tile's
     // rows T[f][s0 .. s0 + TW) (TW pairs = TW * 16 bytes each) into L2 now so those
@@ -225,6 +226,9 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_fwd[pr]);
   if constexpr (kStageFwd<ROWS, TW> && LOGR > E1) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  // merged radix-3 twiddles: column input r of radix-3 row g times omega_{3 R}^{g r}, in the
+  // first round (a separate shared-memory sweep cost config 4's two launches +1.1 ms)
+  const TwPair* pre = (ROWS && a.pre[pr] && grp) ? a.pre[pr] + grp * R : nullptr;
   if constexpr (LOGR == E1) {  // one round: HBM -> registers -> HBM
     for (int g = tid; g < (R >> E1) * TW; g += NTK) {
       int w, q, j0, base;
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
     return;
   } else {
     if constexpr (kStageFwd<ROWS, TW>) {
-      dif_rounds_smem<LOGR, LOGR, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK);
+      dif_rounds_smem<LOGR, LOGR, EL, TW>(sm, L, UniformField<kSwzTables<ROWS>>{p, tw}, tid, NTK, pre);
     } else {
       constexpr int ST1 = 1 << (LOGR - E1);
       for (int g = tid; g < (R >> E1) * TW; g += NTK) {
@@ -302,8 +306,9 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   const u64 p = a.p[pr];
   const u64* src = a.src[pr];
   u64* dst = a.dst[pr];
-  const TwPair* __restrict__ T = a.pass_tw[pr];
-  const TwPair* __restrict__ Hi = a.pass_hi[pr];
+  const unsigned long long grp = ROWS ? (blockIdx.x / a.np) % a.G : 0;  // group of a row tile
+  const TwPair* __restrict__ T = a.pass_tw[pr] + grp * a.tw_gstride;
+  const TwPair* __restrict__ Hi = a.pass_hi[pr] + grp * a.hi_gstride;
   const TwPair sc = a.final_scale[pr];
   const Geom<LOGR, ROWS, TW> G(a);
   const TileLayout<LOGR, ROWS, TW> L;
@@ -490,8 +495,13 @@ __global__ void k_radix3_fwd(Radix3Args a) {
     const u64 y1 = mod_add(mod_sub(x0, x2, p), t, p);
     const u64 y2 = mod_sub(mod_sub(x0, x1, p), t, p);
     dst[s] = y0;
-    dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hi[H + sh], p);
-    dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
+    if (a.notw) {  // the twiddles are pass 1's (merged)
+      dst[S + s] = y1;
+      dst[2 * S + s] = y2;
+    } else {
+      dst[S + s] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hi[H + sh], p);
+      dst[2 * S + s] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hi[2 * H + sh], p);
+    }
   }
 }
 
@@ -512,9 +522,17 @@ __global__ void k_radix3_inv(Radix3Args a) {
        s += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long sg = ((s >> a.cb) << a.sb) + a.off + (s & ((1ull << a.cb) - 1));  // global column
     const unsigned long long sl = sg & (L - 1), sh = sg >> a.lbits;
-    const u64 y0 = shoup_mul(src[s], hi[sh], p);  // lo[0][.] = 1
-    const u64 y1 = shoup_mul(shoup_mul(src[S + s], lo[L + sl], p), hi[H + sh], p);
-    const u64 y2 = shoup_mul(shoup_mul(src[2 * S + s], lo[2 * L + sl], p), hi[2 * H + sh], p);
+    u64 y0, y1, y2;
+    if (const TwPair* __restrict__ pv = pr ? a.pinv[1] : a.pinv[0]) {  // merged: omega_{3 R1}^{-f r} scale
+      const unsigned long long r = sg >> a.pre_shift;
+      y0 = shoup_mul(src[s], pv[r], p);
+      y1 = shoup_mul(src[S + s], pv[a.pre_rows + r], p);
+      y2 = shoup_mul(src[2 * S + s], pv[2 * a.pre_rows + r], p);
+    } else {
+      y0 = shoup_mul(src[s], hi[sh], p);  // lo[0][.] = 1
+      y1 = shoup_mul(shoup_mul(src[S + s], lo[L + sl], p), hi[H + sh], p);
+      y2 = shoup_mul(shoup_mul(src[2 * S + s], lo[2 * L + sl], p), hi[2 * H + sh], p);
+    }
     const u64 t = shoup_mul(mod_sub(y1, y2, p), lam, p);
     dst[s] = mod_add(mod_add(y0, y1, p), y2, p);
     dst[S + s] = mod_add(mod_sub(y0, y2, p), t, p);
@@ -540,7 +558,7 @@ struct GenArgs {
   u64 p, pp, d_norm, recip;
   unsigned shift;
   int R, f_off;
-  unsigned long long S, M;
+  unsigned long long S, M, f_mul, f_add;
 };
 
 __global__ void k_gen_table(GenArgs g) {
@@ -548,7 +566,8 @@ __global__ void k_gen_table(GenArgs g) {
   for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
     const unsigned long long f = i / g.S + g.f_off, s = i % g.S;
-    const unsigned long long e = (f * s) % g.M;  // exponent of omega_M (root_mont may be omega^-1)
+    const unsigned long long fe = (g.f_mul * f + g.f_add) % g.M;
+    const unsigned long long e = (unsigned long long)(((unsigned __int128)fe * s) % g.M);  // exponent of the root
     u64 w = mont_pow_dev(g.root_mont, e, g.one_mont, g.p, g.pp);
     w = mont_mul(w, g.scale_mont, g.p, g.pp);  // Montgomery form of omega^e * scale
     w = mont_mul(w, 1, g.p, g.pp);             // plain
@@ -763,8 +782,13 @@ __global__ void __launch_bounds__(kPackLimbs) k_pack_radix3(const char* __restri
         const u64 y1 = mod_add(mod_sub(x[h][0], x[h][2], p), t, p);
         const u64 y2 = mod_sub(mod_sub(x[h][0], x[h][1], p), t, p);
         dst[0] = y0;
-        dst[S] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hiw[H + sh], p);
-        dst[2 * S] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hiw[2 * H + sh], p);
+        if (a.notw) {  // the twiddles are pass 1's (merged)
+          dst[S] = y1;
+          dst[2 * S] = y2;
+        } else {
+          dst[S] = shoup_mul(shoup_mul(y1, lo[L + sl], p), hiw[H + sh], p);
+          dst[2 * S] = shoup_mul(shoup_mul(y2, lo[2 * L + sl], p), hiw[2 * H + sh], p);
+        }
       }
     }
   }
@@ -982,9 +1006,12 @@ void launch_radix3(bool inverse, const Radix3Args& a, int np, cudaStream_t st) {
 }
 
 void launch_gen_pass_table(TwPair* out, u64 root_mont, u64 scale_mont, int R, int /*logR*/, unsigned long long S,
-                           u64 p, u64 recip, cudaStream_t st, unsigned long long order, int f_off) {
+                           u64 p, u64 recip, cudaStream_t st, unsigned long long order, int f_off,
+                           unsigned long long f_mul, unsigned long long f_add) {
   GenArgs g;
   g.f_off = f_off;
+  g.f_mul = f_mul;
+  g.f_add = f_add;
   g.out = out;
   g.root_mont = root_mont;
   g.scale_mont = scale_mont;
@@ -998,7 +1025,7 @@ void launch_gen_pass_table(TwPair* out, u64 root_mont, u64 scale_mont, int R, in
   g.recip = recip;
   g.R = R;
   g.S = S;
-  g.M = order ? order : (unsigned long long)(R + f_off) * S;  // order of the root (exponents reduced mod M)
+  g.M = order ? order : (unsigned long long)(R + f_off) * S * f_mul;  // order of the root (exponents mod M)
   k_gen_table<<<grid_for((unsigned long long)R * S, 256), 256, 0, st>>>(g);
 }
 

@@ -80,6 +80,12 @@ struct PassArgs {
                            // inverse row pass, whose first step is a Shoup twiddle product)
   int two;                 // fused pass: other = the first operand before its last forward pass
   int nops;                // forward passes: 2 = a second operand in the same launch (blockIdx.y = 1)
+  // Pass 1 after a twiddle-free radix-3 pass (N = 3 S): group g of the pass is radix-3 row f = g.
+  // omega_N^{f s}, s = r S1 + c, splits into omega_{3 R}^{f r} (a pre-multiply of the column
+  // input r: pre[g R + r], g > 0) and omega_N^{f c}, which commutes with the column DFT and
+  // merges into the group's own twiddle table (tables per group: + g tw_gstride / hi_gstride).
+  const TwPair* pre[2];
+  unsigned long long tw_gstride, hi_gstride;
   const u64* src_b[2];     // the second operand's input / output (nops == 2)
   u64* dst_b[2];
 };
@@ -101,11 +107,14 @@ struct Radix3Args {
   // Unsharded: cb = sb = 0, off = 0 (s = l).
   int cb, sb;
   unsigned long long off;
-  // Unfactorised rows f = 1, 2 (full[(f - 1) S + s], the inverse's carrying the scale) and the
-  // inverse's row-0 factor (the scale): one Shoup product per twiddle instead of two. Only the
-  // fused pack / carry kernels use them (nullptr: the factorised lo * hi).
-  const TwPair* full[2];
-  TwPair r0[2];
+  // Merged twiddles (when the next power-of-two pass carries them, see PassArgs::pre):
+  //  * forward: notw = 1, the length-3 DFT alone (omega_N^{f s} moves to pass 1);
+  //  * inverse: pinv[f R1 + (s >> pre_shift)] = omega_{3 R1}^{-f r} replaces
+  //    lo * hi: one Shoup product per element (r = pass 1's row of global column s).
+  int notw;
+  const TwPair* pinv[2];
+  int pre_shift;
+  int pre_rows;  // R1
 };
 
 // Launchers (kernels.cu).
@@ -115,9 +124,11 @@ void launch_pass_fused(int logR, const PassArgs& a, unsigned long long ncols, in
 void launch_radix3(bool inverse, const Radix3Args& a, int nprimes, cudaStream_t st);
 
 // out[f][s] = root^(f s mod order) * scale (Shoup pairs), f < R, s < S; order 0 = R S.
-// f_off: rows f_off .. f_off + R - 1 (out[f - f_off][s]).
+// f_off: rows f_off .. f_off + R - 1 (out[f - f_off][s]). f_mul / f_add: the exponent of
+// entry [f][s] is (f_mul f + f_add) s (mod order).
 void launch_gen_pass_table(TwPair* out, u64 root_m, u64 scale, int R, int logR, unsigned long long S, u64 p,
-                           u64 recip, cudaStream_t st, unsigned long long order = 0, int f_off = 0);
+                           u64 recip, cudaStream_t st, unsigned long long order = 0, int f_off = 0,
+                           unsigned long long f_mul = 1, unsigned long long f_add = 0);
 // Local limb i is global limb ((i >> row_bits) * row_stride) + off + (i & (2^row_bits - 1)):
 // unsharded packs use row_bits = 63, off = 0 (limb i = i). Sharded packs need 2^row_bits >= 256.
 // lead_check false (unsharded map only): no leading-zero check (a rank's compacted digit slices).

@@ -177,8 +177,10 @@ __device__ __forceinline__ void group_of(int g, int& w, int& q) {
 }
 
 // ---- shared-memory rounds ----
+// pre (first round only, may be nullptr): input row r is multiplied by pre[r] first.
 template <int LOGR, int MLOG, int E, int W, class L, class F>
-__device__ __forceinline__ void dif_round_smem(u64* s, const L& idx, const F& fld, int tid, int nt) {
+__device__ __forceinline__ void dif_round_smem(u64* s, const L& idx, const F& fld, int tid, int nt,
+                                               const TwPair* pre = nullptr) {
   constexpr int NE = 1 << E, STRIDE = 1 << (MLOG - E), NQ = (1 << LOGR) >> E;
   for (int g = tid; g < NQ * W; g += nt) {
     int w, q, j0, base;
@@ -187,6 +189,10 @@ __device__ __forceinline__ void dif_round_smem(u64* s, const L& idx, const F& fl
     u64 v[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) v[i] = s[idx(base + i * STRIDE, w)];
+    if (pre) {
+#pragma unroll
+      for (int i = 0; i < NE; ++i) v[i] = shoup_mul(v[i], pre[base + i * STRIDE], fld.p(w));
+    }
     dif_regs<LOGR, MLOG, E, F::kSwz>(v, j0, fld.tw(w), fld.p(w));
 #pragma unroll
     for (int i = 0; i < NE; ++i) s[idx(base + i * STRIDE, w)] = v[i];
@@ -211,10 +217,11 @@ __device__ __forceinline__ void dit_round_smem(u64* s, const L& idx, const F& fl
 
 // DIF rounds whose first span is 2^MLOG, down to (but excluding) span 2^STOP.
 template <int LOGR, int MLOG, int STOP, int W, class L, class F>
-__device__ __forceinline__ void dif_rounds_smem(u64* s, const L& idx, const F& fld, int tid, int nt) {
+__device__ __forceinline__ void dif_rounds_smem(u64* s, const L& idx, const F& fld, int tid, int nt,
+                                                const TwPair* pre = nullptr) {
   if constexpr (MLOG > STOP) {
     constexpr int E = Sched<LOGR>::e_dif(MLOG);
-    dif_round_smem<LOGR, MLOG, E, W>(s, idx, fld, tid, nt);
+    dif_round_smem<LOGR, MLOG, E, W>(s, idx, fld, tid, nt, pre);
     __syncthreads();
     dif_rounds_smem<LOGR, MLOG - E, STOP, W>(s, idx, fld, tid, nt);
   }
