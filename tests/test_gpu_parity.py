@@ -145,58 +145,29 @@ def test_factorised_pass_tables(gpu, ref):
 
 
 def test_radix3_twiddle_tables_both_forms(ref):
-    """The fused pack / carry kernels with unfactorised radix-3 twiddle rows (config 4's plan)
-    and with the factorised lo * hi pair (config 5's), forced at small N = 3 2^k sizes
-    (multi-pass, the fused carry included), squaring and not, both prime pairs."""
-    for full in ("1", "0"):
-        os.environ["DECMUL_R3_FULL"] = full
-        try:
-            for large in (False, True):
-                if large:
-                    os.environ["DECMUL_FORCE_LARGE_PAIR"] = "1"
-                ctx = dm.Context(0)  # fresh plans under the knobs
-                for nx, ny in ((300001, 250000), (1400000, 1200000), (5000000, 4000001)):
-                    assert ctx.plan(nx, ny)["length"] % 3 == 0
-                    x, y = inputs.gen_digits(nx + 3, nx), inputs.gen_digits(ny + 4, ny)
-                    assert ctx.multiply_text(x, y) == ref.multiply(x, y), (full, large, nx, ny)
-                    assert ctx.multiply_text(x, None) == ref.multiply(x, None), (full, large, nx)
-                ctx.close()
-                os.environ.pop("DECMUL_FORCE_LARGE_PAIR", None)
-        finally:
-            os.environ.pop("DECMUL_R3_FULL", None)
-            os.environ.pop("DECMUL_FORCE_LARGE_PAIR", None)
-
-
-def test_block_convolution_fallback(ref):
-    """Products past the largest transform run as sums of block products (SURVEY §7 D1
-    fallback, blocked.cu), forced at small sizes with DECMUL_BLOCK_DIGITS: ragged blocks,
-    leading zeros and all-zero blocks inside an operand, squaring, one and two engines."""
-    def with_zeros(seed, n, runs):
-        d = bytearray(inputs.gen_digits(seed, n))
-        for start, length in runs:
-            d[start:start + length] = b"0" * length
-        return bytes(d)
-
-    os.environ["DECMUL_BLOCK_DIGITS"] = "7000"
-    try:
-        for devices in ([0], [0, 0]):
-            ctx = dm.Context(devices=devices)
-            cases = [(inputs.gen_digits(11, 30001), inputs.gen_digits(12, 17000)),
-                     (with_zeros(13, 50000, [(8000, 7000), (43000 - 5, 3000)]), with_zeros(14, 21001, [(1, 9000)])),
-                     (inputs.gen_digits(15, 6999), inputs.gen_digits(16, 70000)),
-                     (b"9" * 28000, b"9" * 28000)]
-            for x, y in cases:
-                assert ctx.multiply_text(x, y) == ref.multiply(x, y), (devices, len(x), len(y))
-            x = inputs.gen_digits(17, 40000)
-            assert ctx.multiply_text(x, None) == ref.multiply(x, None)
-            with pytest.raises(ValueError, match="non-digit"):
-                ctx.multiply_text(x[:30000] + b"/" + x[30001:], x)
-            with pytest.raises(ValueError, match="leading zero"):
-                ctx.multiply_text(b"0" + x[1:], x)
-            assert ctx.multiply_text(b"0", x) == b"0"
-            ctx.close()
-    finally:
-        os.environ.pop("DECMUL_BLOCK_DIGITS", None)
+    """N = 3 2^k with the radix-3 twiddles merged into pass 1 (pre-multiplied column inputs,
+    per-group pass-1 tables, a 3 x R1 inverse table) and with the factorised lo * hi pair in the
+    radix-3 passes (DECMUL_R3_MERGE=0), full and factorised pass tables, both prime pairs,
+    squaring and not, the fused pack and carry included."""
+    for merge in ("1", "0"):
+        for factor in ("0", "1"):
+            os.environ["DECMUL_R3_MERGE"] = merge
+            os.environ["DECMUL_FACTOR_TABLES"] = factor
+            try:
+                for large in (False, True):
+                    if large:
+                        os.environ["DECMUL_FORCE_LARGE_PAIR"] = "1"
+                    ctx = dm.Context(0)  # fresh plans under the knobs
+                    for nx, ny in ((300001, 250000), (1400000, 1200000), (5000000, 4000001)):
+                        assert ctx.plan(nx, ny)["length"] % 3 == 0
+                        x, y = inputs.gen_digits(nx + 3, nx), inputs.gen_digits(ny + 4, ny)
+                        assert ctx.multiply_text(x, y) == ref.multiply(x, y), (merge, factor, large, nx, ny)
+                        assert ctx.multiply_text(x, None) == ref.multiply(x, None), (merge, factor, large, nx)
+                    ctx.close()
+                    os.environ.pop("DECMUL_FORCE_LARGE_PAIR", None)
+            finally:
+                for k in ("DECMUL_R3_MERGE", "DECMUL_FACTOR_TABLES", "DECMUL_FORCE_LARGE_PAIR"):
+                    os.environ.pop(k, None)
 
 
 def test_errors_match_reference_types(gpu):
