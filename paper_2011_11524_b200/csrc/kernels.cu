@@ -187,6 +187,12 @@ __device__ __forceinline__ void group_coords(int g, int& w, int& q) {
 #ifndef DMG_FWD_MINB9
 #define DMG_FWD_MINB9 3
 #endif
+#ifndef DMG_GROUP_PREFETCH
+#define DMG_GROUP_PREFETCH 0
+#endif
+#ifndef DMG_INV_GROUP_PREFETCH
+#define DMG_INV_GROUP_PREFETCH 1
+#endif
 constexpr int pass_min_blocks(int logr, int tw) {
   return logr == 9 ? (tw == kTileW ? DMG_FWD_MINB9 : 3) : (logr == 8 ? 4 : 0);
 }
@@ -211,7 +217,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   const unsigned long long grp = ROWS ? (blockIdx.x / a.np) % a.G : 0;  // group of a row tile
   const TwPair* __restrict__ T = a.pass_tw[pr] + grp * a.tw_gstride;
   const TwPair* __restrict__ Hi = a.pass_hi[pr] + grp * a.hi_gstride;
-  if constexpr (ROWS && !FACT) {
+  if constexpr (ROWS && !FACT) if (DMG_GROUP_PREFETCH || a.tw_gstride == 0) {
     // The twiddles are applied in the epilogue, after the DIF; start pulling the tile's
     // rows T[f][s0 .. s0 + TW) (TW pairs = TW * 16 bytes each) into L2 now so those
     // loads hit L2 instead of DRAM (large-S passes stream a table of N / 3 .. N pairs).
@@ -312,6 +318,17 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   const TwPair sc = a.final_scale[pr];
   const Geom<LOGR, ROWS, TW> G(a);
   const TileLayout<LOGR, ROWS, TW> L;
+#if DMG_INV_GROUP_PREFETCH
+  if constexpr (ROWS && !FACT) if (a.tw_gstride != 0) {
+    // per-group tables (pass 1 after a merged radix-3 pass) stream from HBM with no reuse
+    // across tiles: start them towards L2 before the tile's own loads
+    constexpr int LINES = TW * 16 / 128 > 0 ? TW * 16 / 128 : 1;
+    for (int i = tid; i < R * LINES; i += NTK) {
+      const TwPair* row = &G.tw(T, i / LINES, 0) + (i % LINES) * 8;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+    }
+  }
+#endif
   constexpr bool STAGE = kStageInv<ROWS> && LOGR > E1;
   if constexpr (STAGE) stage_tile<LOGR, ROWS, TW, NTK>(sm, src, G, L, tid);
   load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_inv[pr]);
