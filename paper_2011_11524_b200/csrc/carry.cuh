@@ -16,12 +16,26 @@ namespace dmg {
 constexpr unsigned kIdentityMap = 0x24u;  // c -> c
 
 __device__ __forceinline__ unsigned map_apply(unsigned m, unsigned c) { return (m >> (2 * c)) & 3u; }
-// later o earlier
-__device__ __forceinline__ unsigned map_compose(unsigned later, unsigned earlier) {
+// Every map here is monotone (limb maps are, and composition keeps it), so out(0) == out(2)
+// means a constant map c -> k (0x15 k). Limb sums sit within 2 of a band edge (B or 2B) with
+// probability ~4/B, so nearly every limb map and every composed aggregate is constant:
+// DMG_MAP_FAST takes those through a short path and keeps the general bit-field code for
+// the rest (the branch is taken by whole warps almost always).
+#ifndef DMG_MAP_FAST
+#define DMG_MAP_FAST 1
+#endif
+__device__ __forceinline__ unsigned map_compose_full(unsigned later, unsigned earlier) {
   return map_apply(later, earlier & 3u) | (map_apply(later, (earlier >> 2) & 3u) << 2) |
          (map_apply(later, (earlier >> 4) & 3u) << 4);
 }
-__device__ __forceinline__ unsigned limb_map(u64 s, u64 B) {
+// later o earlier
+__device__ __forceinline__ unsigned map_compose(unsigned later, unsigned earlier) {
+#if DMG_MAP_FAST
+  if ((later & 3u) == (later >> 4)) return later;  // constant later map
+#endif
+  return map_compose_full(later, earlier);
+}
+__device__ __forceinline__ unsigned limb_map_full(u64 s, u64 B) {
   unsigned m = 0;
 #pragma unroll
   for (unsigned c = 0; c < 3; ++c) {
@@ -29,6 +43,13 @@ __device__ __forceinline__ unsigned limb_map(u64 s, u64 B) {
     m |= (unsigned(v >= B) + unsigned(v >= 2 * B)) << (2 * c);
   }
   return m;
+}
+__device__ __forceinline__ unsigned limb_map(u64 s, u64 B) {
+#if DMG_MAP_FAST
+  // s in [B - 2, B) or [2B - 2, 2B): the carry-in decides; else the constant map of s's band
+  if (s - (B - 2) >= 2 && s - (2 * B - 2) >= 2) return (unsigned(s >= B) + unsigned(s >= 2 * B)) * 0x15u;
+#endif
+  return limb_map_full(s, B);
 }
 
 // m = a1 + p1 * REDC_{p2}(r~, (a2 - a1) mod p2) < p1 p2.

@@ -38,7 +38,7 @@ __device__ unsigned long long g_phase_cycles[12];
 #endif
 
 #ifndef DMG_SMALL_TW_PREFETCH
-#define DMG_SMALL_TW_PREFETCH 0
+#define DMG_SMALL_TW_PREFETCH 1
 #endif
 constexpr int NT = 256;  // 8 warps, 3 CTAs/SM at <= 85 registers; measured fastest of 192/256/320/384(x3) and 512(x2)
 
