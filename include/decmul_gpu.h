@@ -150,6 +150,19 @@ int decmul_gpu_convolve_mod_p(decmul_gpu_ctx* ctx, uint64_t p, size_t n, const u
 int decmul_gpu_forward_transform(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint64_t* a);
 int decmul_gpu_inverse_transform(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint64_t* a);
 int decmul_gpu_pointwise_product(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint64_t* a, const uint64_t* b);
+/* The same hooks for a plan built with a non-default six-step threshold, build_conv_plan(ctx, n,
+ * six_step_threshold) (conv.hpp:59-60, conv.cpp:243-269; 0 = kDefaultSixStepThreshold = 2^15):
+ * the spectrum is stored in that plan's order (kDirect when n <= threshold, else kSixStep with
+ * n1 = 2^floor(k/2); the three-row shape hands the threshold to its row plan), as the
+ * reference's forced-shape checks need (test_conv.cpp:183-196, selftest.cpp:109-118).
+ * conv_plan_info reports the plan's shape (0 direct, 1 six-step, 2 three-row), its plain
+ * primitive root (primes.cpp:99-112) and the six-step factors; it needs no GPU. */
+int decmul_gpu_forward_transform_ex(decmul_gpu_ctx* ctx, uint64_t p, size_t n, size_t six_step_threshold,
+                                    uint64_t* a);
+int decmul_gpu_inverse_transform_ex(decmul_gpu_ctx* ctx, uint64_t p, size_t n, size_t six_step_threshold,
+                                    uint64_t* a);
+int decmul_gpu_conv_plan_info(uint64_t p, size_t n, size_t six_step_threshold, int* shape, uint64_t* root,
+                              size_t* n1, size_t* n2);
 
 /* ---- stage hooks ----
  * pack: decimal.cpp:102-118. recover_decimal: crt2 over the two residue vectors

@@ -29,7 +29,7 @@ __all__ = [
     "P1", "P2", "Q1", "Q2", "OperandTooLarge", "CudaError", "DecimalNumber", "MultiplyOptions", "BasePlan",
     "PackedOperand", "Context", "default_context", "multiply", "multiply_batch", "select_base_and_length",
     "smallest_supported_length", "pack", "to_decimal", "convolve_mod_p", "forward_transform",
-    "inverse_transform", "pointwise_product", "transpose_square_sub", "transpose_n_x_2n", "transpose_2n_x_n",
+    "inverse_transform", "build_conv_plan", "pointwise_product", "transpose_square_sub", "transpose_n_x_2n", "transpose_2n_x_n",
     "lib_path", "load_library", "EXPORTED_SYMBOLS",
 ]
 
@@ -60,7 +60,8 @@ EXPORTED_SYMBOLS = [
     "decmul_gpu_shard_carry_emit", "decmul_gpu_selftest", "decmul_gpu_multiply_batch_ptrs",
     "decmul_gpu_check_errors", "decmul_gpu_profile", "decmul_gpu_profile_report", "decmul_gpu_create_multi",
     "decmul_gpu_context_devices", "decmul_gpu_multiply_sharded", "decmul_gpu_multiply_ex",
-    "decmul_gpu_coalesce_stats",
+    "decmul_gpu_coalesce_stats", "decmul_gpu_forward_transform_ex", "decmul_gpu_inverse_transform_ex",
+    "decmul_gpu_conv_plan_info",
 ]
 
 
@@ -392,14 +393,18 @@ class Context:
                    _ptr(yy), C.c_size_t(yy.size), _ptr(out))
         return out[:n]
 
-    def forward_transform(self, p: int, a) -> np.ndarray:
+    def forward_transform(self, p: int, a, six_step_threshold: int = 0) -> np.ndarray:
+        """Spectrum in the storage order of build_conv_plan(ctx, n, six_step_threshold)
+        (reference conv.hpp:19-24, :59-60; 0 = the default 2^15)."""
         a = _u64arr(a).copy()
-        self._call("decmul_gpu_forward_transform", C.c_uint64(p), C.c_size_t(a.size), _ptr(a))
+        self._call("decmul_gpu_forward_transform_ex", C.c_uint64(p), C.c_size_t(a.size),
+                   C.c_size_t(six_step_threshold), _ptr(a))
         return a
 
-    def inverse_transform(self, p: int, a) -> np.ndarray:
+    def inverse_transform(self, p: int, a, six_step_threshold: int = 0) -> np.ndarray:
         a = _u64arr(a).copy()
-        self._call("decmul_gpu_inverse_transform", C.c_uint64(p), C.c_size_t(a.size), _ptr(a))
+        self._call("decmul_gpu_inverse_transform_ex", C.c_uint64(p), C.c_size_t(a.size),
+                   C.c_size_t(six_step_threshold), _ptr(a))
         return a
 
     def pointwise_product(self, p: int, a, b=None) -> np.ndarray:
@@ -474,6 +479,17 @@ def select_base_and_length(dx: int, dy: int, pair: tuple[int, int] | None = None
     return BasePlan(be.value, ln.value)
 
 
+def build_conv_plan(p: int, n: int, six_step_threshold: int = 0) -> dict:
+    """reference build_conv_plan (conv.hpp:59-60, conv.cpp:212-271): shape ("direct", "six_step",
+    "three_rows"), plain primitive root and six-step factors of the plan; needs no GPU. Raises
+    ValueError like the reference's invalid_argument."""
+    shape, root, n1, n2 = C.c_int(), C.c_uint64(), C.c_size_t(), C.c_size_t()
+    _raise(load_library().decmul_gpu_conv_plan_info(C.c_uint64(p), C.c_size_t(n), C.c_size_t(six_step_threshold),
+                                                   C.byref(shape), C.byref(root), C.byref(n1), C.byref(n2)), None)
+    return dict(p=p, n=n, six_step_threshold=six_step_threshold or 1 << 15,
+                shape=("direct", "six_step", "three_rows")[shape.value], root=root.value, n1=n1.value, n2=n2.value)
+
+
 def multiply(x: DecimalNumber, y: DecimalNumber, opt: MultiplyOptions | None = None,
              ctx: Context | None = None) -> DecimalNumber:
     """reference decimal.cpp:191-216: exact product; x is y takes the squaring path."""
@@ -521,12 +537,12 @@ def convolve_mod_p(p: int, n: int, x, y=None, ctx: Context | None = None) -> np.
     return (ctx or default_context()).convolve_mod_p(p, n, x, y)
 
 
-def forward_transform(p: int, a, ctx: Context | None = None) -> np.ndarray:
-    return (ctx or default_context()).forward_transform(p, a)
+def forward_transform(p: int, a, ctx: Context | None = None, six_step_threshold: int = 0) -> np.ndarray:
+    return (ctx or default_context()).forward_transform(p, a, six_step_threshold)
 
 
-def inverse_transform(p: int, a, ctx: Context | None = None) -> np.ndarray:
-    return (ctx or default_context()).inverse_transform(p, a)
+def inverse_transform(p: int, a, ctx: Context | None = None, six_step_threshold: int = 0) -> np.ndarray:
+    return (ctx or default_context()).inverse_transform(p, a, six_step_threshold)
 
 
 def pointwise_product(p: int, a, b=None, ctx: Context | None = None) -> np.ndarray:

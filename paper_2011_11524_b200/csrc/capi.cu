@@ -45,9 +45,9 @@ namespace {
 
 thread_local std::string g_create_err;
 
+// Runs f, mapping exceptions to error codes; the message goes to msg.
 template <class F>
-int guarded(decmul_gpu_ctx* ctx, F&& f) {
-  std::string msg;
+int guarded_msg(std::string& msg, F&& f) {
   int rc = DECMUL_OK;
   try {
     f();
@@ -77,6 +77,16 @@ int guarded(decmul_gpu_ctx* ctx, F&& f) {
     rc = DECMUL_ECUDA;
     msg = e.what();
   }
+  return rc;
+}
+
+// The same with the message stored in the context (the caller holds its lock) or, without a
+// context, in the thread's creation-error slot.
+template <class F>
+int guarded(decmul_gpu_ctx* ctx, F&& f) {
+  std::string msg;
+  const int rc = guarded_msg(msg, f);
+  if (rc == DECMUL_OK) return rc;
   if (ctx)
     ctx->err = msg;
   else
@@ -268,6 +278,28 @@ int multiply_coalesced(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char
   return req.rc;
 }
 
+// Large products from pinned buffers: the engine takes the context lock only around the
+// compute stage, so concurrent callers overlap one product's download with the next one's
+// upload and compute (Engine::multiply_host_overlapped). Returns false when the call does
+// not qualify (the caller then runs the ordinary locked path).
+bool multiply_overlapped(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
+                         size_t cap, size_t* out_len, unsigned forced, int alias, uint64_t p1, uint64_t p2, int* rc) {
+  if (!ctx || !out_len) return false;
+  DeviceGuard dev_(ctx->eng->device());
+  dmg::Engine* e = nullptr;
+  std::string msg;
+  if (guarded_msg(msg, [&] { e = ctx->multi->overlap_engine(x, nx, y, ny, out, forced, p1, p2); }) || !e)
+    return false;
+  *rc = guarded_msg(msg, [&] {
+    *out_len = e->multiply_host_overlapped(ctx->mu, x, nx, y, ny, out, cap, forced, alias != 0, p1, p2);
+  });
+  if (*rc) {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ctx->err = msg;
+  }
+  return true;
+}
+
 }  // namespace
 
 int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
@@ -276,6 +308,7 @@ int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const cha
     bool valid = cap >= nx + ny && x[0] != '0' && y[0] != '0';
     if (valid) return multiply_coalesced(ctx, x, nx, y, ny, out, cap, out_len);
   }
+  if (int rc = 0; multiply_overlapped(ctx, x, nx, y, ny, out, cap, out_len, forced, alias, 0, 0, &rc)) return rc;
   LOCKED(ctx, {
     if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
     const bool xz = nx == 1 && x[0] == '0', yz = ny == 1 && y[0] == '0';
@@ -296,6 +329,9 @@ int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const cha
 
 int decmul_gpu_multiply_ex(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
                            size_t cap, size_t* out_len, const decmul_gpu_multiply_options* opt) {
+  if (int rc = 0; multiply_overlapped(ctx, x, nx, y, ny, out, cap, out_len, opt ? opt->forced_base_exp : 0,
+                                      opt ? opt->alias : 0, opt ? opt->p1 : 0, opt ? opt->p2 : 0, &rc))
+    return rc;
   LOCKED(ctx, {
     const decmul_gpu_multiply_options o = opt ? *opt : decmul_gpu_multiply_options{0, 0, 0, 0};
     if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
@@ -373,6 +409,42 @@ int decmul_gpu_forward_transform(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint
 
 int decmul_gpu_inverse_transform(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint64_t* a) {
   LOCKED(ctx, ctx->eng->inverse_transform(p, n, reinterpret_cast<dmg::u64*>(a)));
+}
+
+int decmul_gpu_forward_transform_ex(decmul_gpu_ctx* ctx, uint64_t p, size_t n, size_t six_step_threshold,
+                                    uint64_t* a) {
+  LOCKED(ctx, ctx->eng->forward_transform(p, n, reinterpret_cast<dmg::u64*>(a), six_step_threshold));
+}
+
+int decmul_gpu_inverse_transform_ex(decmul_gpu_ctx* ctx, uint64_t p, size_t n, size_t six_step_threshold,
+                                    uint64_t* a) {
+  LOCKED(ctx, ctx->eng->inverse_transform(p, n, reinterpret_cast<dmg::u64*>(a), six_step_threshold));
+}
+
+int decmul_gpu_conv_plan_info(uint64_t p, size_t n, size_t six_step_threshold, int* shape, uint64_t* root,
+                              size_t* n1, size_t* n2) {
+  return guarded(nullptr, [&] {
+    const size_t c = n % 3 == 0 ? n / 3 : n;
+    const bool three = n % 3 == 0 && n > 0 && !(c & (c - 1));
+    const bool pow2 = n > 0 && !(n & (n - 1));
+    if (!pow2 && !three) throw std::invalid_argument("build_conv_plan: length must be 2^k or 3*2^k");
+    if (n > 1 && (p - 1) % n) throw std::invalid_argument("build_conv_plan: length does not divide p-1");
+    const size_t thr = six_step_threshold ? six_step_threshold : size_t(1) << 15;
+    dmg::HostField F(p);
+    if (root) *root = F.root_of_unity(n);
+    size_t a = 0, b = 0;
+    int sh = 0;
+    if (three) {
+      sh = 2;
+    } else if (n > thr) {
+      sh = 1;
+      a = size_t(1) << (__builtin_ctzll(n) / 2);
+      b = n / a;
+    }
+    if (shape) *shape = sh;
+    if (n1) *n1 = a;
+    if (n2) *n2 = b;
+  });
 }
 
 int decmul_gpu_pointwise_product(decmul_gpu_ctx* ctx, uint64_t p, size_t n, uint64_t* a, const uint64_t* b) {

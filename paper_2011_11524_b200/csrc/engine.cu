@@ -60,16 +60,17 @@ int bitrev_h(std::size_t x, int bits) {
   return int(r);
 }
 
-// The reference's storage -> spectrum map for its default plan (conv.hpp:19-24,
-// build_conv_plan threshold 2^15; checked by test_conv.cpp:18-32).
-std::size_t ref_order_of(std::size_t n, std::size_t k) {
+// The reference's storage -> spectrum map (conv.hpp:19-24) for a plan built with six-step
+// threshold thr (build_conv_plan, conv.cpp:243-269; default 2^15; checked by
+// test_conv.cpp:18-32). The three-row shape hands thr on to its row plan.
+std::size_t ref_order_of(std::size_t n, std::size_t k, std::size_t thr) {
   if (n <= 1) return 0;
   if (n % 3 == 0) {
     const std::size_t c = n / 3;
-    return k / c + 3 * ref_order_of(c, k % c);
+    return k / c + 3 * ref_order_of(c, k % c, thr);
   }
   const int lg = __builtin_ctzll(n);
-  if (n <= (std::size_t(1) << 15)) return std::size_t(bitrev_h(k, lg));
+  if (n <= thr) return std::size_t(bitrev_h(k, lg));
   const std::size_t n1 = std::size_t(1) << (lg / 2), n2 = n / n1;
   const std::size_t i = k / n2, j = k % n2;
   return i + n1 * std::size_t(bitrev_h(j, __builtin_ctzll(n2)));
@@ -144,6 +145,12 @@ Engine::~Engine() {
     cudaEventDestroy(done_ev_[i]);
   }
   if (host_lens_) cudaFreeHost(host_lens_);
+  if (ov_up_stream_) cudaStreamDestroy(ov_up_stream_);
+  for (OvSlot& s : ov_) {
+    if (s.dl_stream) cudaStreamDestroy(s.dl_stream);
+    if (s.ev_x) cudaEventDestroy(s.ev_x);
+    if (s.ev_y) cudaEventDestroy(s.ev_y);
+  }
   copy_pool_.reset();
   for (int k = 0; k < kStageSlots; ++k) {
     if (stage_[k]) cudaFreeHost(stage_[k]);
@@ -1347,7 +1354,8 @@ void Engine::convolve_mod_p(u64 p, std::size_t n, const u64* x, std::size_t nx, 
   cuda_check(cudaStreamSynchronize(st), "sync");
 }
 
-void Engine::forward_transform(u64 p, std::size_t n, u64* a) {
+void Engine::forward_transform(u64 p, std::size_t n, u64* a, std::size_t thr) {
+  if (thr == 0) thr = std::size_t(1) << 15;
   const PrimePlan& P = prime_plan(p, n);
   const std::size_t npad = padded_len(P);
   X_[0].ensure(npad);
@@ -1359,7 +1367,7 @@ void Engine::forward_transform(u64 p, std::size_t n, u64* a) {
   const u64* sx[2] = {X_[0].ptr, nullptr};
   transform_forward(pl, 1, sx, X, true, st);
   std::vector<unsigned long long> map(n);
-  for (std::size_t k = 0; k < n; ++k) map[k] = P.position_of(ref_order_of(n, k));
+  for (std::size_t k = 0; k < n; ++k) map[k] = P.position_of(ref_order_of(n, k, thr));
   DevBuf<unsigned long long> dmap;
   upload(dmap, map, st);
   launch_gather(X_[0].ptr, Y_[0].ptr, dmap.ptr, n, st);
@@ -1368,7 +1376,8 @@ void Engine::forward_transform(u64 p, std::size_t n, u64* a) {
   cuda_check(cudaStreamSynchronize(st), "sync");
 }
 
-void Engine::inverse_transform(u64 p, std::size_t n, u64* a) {
+void Engine::inverse_transform(u64 p, std::size_t n, u64* a, std::size_t thr) {
+  if (thr == 0) thr = std::size_t(1) << 15;
   const PrimePlan& P = prime_plan(p, n);
   const std::size_t npad = padded_len(P);
   X_[0].ensure(npad);
@@ -1377,7 +1386,7 @@ void Engine::inverse_transform(u64 p, std::size_t n, u64* a) {
   cuda_check(cudaMemcpyAsync(Y_[0].ptr, a, n * 8, cudaMemcpyHostToDevice, st), "h2d");
   // inverse of the forward gather: position_of(ref_order_of(k)) <- a[k]
   std::vector<unsigned long long> map(n);
-  for (std::size_t k = 0; k < n; ++k) map[P.position_of(ref_order_of(n, k))] = k;
+  for (std::size_t k = 0; k < n; ++k) map[P.position_of(ref_order_of(n, k, thr))] = k;
   DevBuf<unsigned long long> dmap;
   upload(dmap, map, st);
   launch_gather(Y_[0].ptr, X_[0].ptr, dmap.ptr, n, st);
@@ -1471,7 +1480,7 @@ void Engine::transpose(int kind, u64* a, std::size_t n, std::size_t stride) {
     total = 2 * n * n;
   if (total == 0) return;
   X_[0].ensure(total);
-  X_[1].ensure(total);
+  if (kind != 0) X_[1].ensure(std::max<std::size_t>(rho_scratch_words(n), 1));
   cudaStream_t st = stream_;
   cuda_check(cudaMemcpyAsync(X_[0].ptr, a, total * 8, cudaMemcpyHostToDevice, st), "h2d");
   if (kind == 0) {

@@ -184,6 +184,14 @@ class Engine {
   // Host strings -> host string (reference decmul::multiply semantics).
   std::size_t multiply_host(const char* x, std::size_t nx, const char* y, std::size_t ny, char* out,
                             std::size_t cap, unsigned forced_base_exp, bool alias, u64 p1 = 0, u64 p2 = 0);
+  // The same product for concurrent callers with large pinned buffers: the caller does NOT hold
+  // the context lock; uploads, compute (under ctx_mu) and the download are separate stages over
+  // two buffer slots, so one call's download overlaps the next call's upload and compute and the
+  // next upload starts while this product still computes (PCIe is full duplex; hostio.cu).
+  bool overlap_ok(const char* x, std::size_t nx, const char* y, std::size_t ny, const char* out) const;
+  std::size_t multiply_host_overlapped(std::mutex& ctx_mu, const char* x, std::size_t nx, const char* y,
+                                       std::size_t ny, char* out, std::size_t cap, unsigned forced_base_exp,
+                                       bool alias, u64 p1 = 0, u64 p2 = 0);
   // Device digits -> device digits; stream-ordered; *out_len written (host) after sync.
   std::size_t multiply_device(const char* dx, std::size_t nx, const char* dy, std::size_t ny, char* dout,
                               std::size_t cap, unsigned forced_base_exp, bool squaring, cudaStream_t st,
@@ -202,8 +210,10 @@ class Engine {
   // Parity hooks (reference conv.hpp:59-71), host arrays, one prime.
   void convolve_mod_p(u64 p, std::size_t n, const u64* x, std::size_t nx, const u64* y, std::size_t ny,
                       u64* out);
-  void forward_transform(u64 p, std::size_t n, u64* a);  // reference storage order (conv.hpp:19-24)
-  void inverse_transform(u64 p, std::size_t n, u64* a);
+  // reference storage order (conv.hpp:19-24) of a plan built with six-step threshold thr
+  // (0 = the default 2^15)
+  void forward_transform(u64 p, std::size_t n, u64* a, std::size_t thr = 0);
+  void inverse_transform(u64 p, std::size_t n, u64* a, std::size_t thr = 0);
   void pointwise_product(u64 p, std::size_t n, u64* a, const u64* b);
   // Stage hooks on the device path (decimal.cpp pack / crt2 + recover_digits + to_decimal).
   std::size_t pack(const char* digits, std::size_t nd, unsigned base_exp, u64* limbs, std::size_t cap);
@@ -346,6 +356,19 @@ class Engine {
   DevBuf<unsigned char> pm_;                         // per-limb prefix maps of the carry (split -> emit)
   DevBuf<unsigned long long> meta_, lens_;
   DevBuf<char> din_x_, din_y_, dout_;
+  // multiply_host_overlapped: two slots of digit buffers; ov_up_mu_ orders the uploads, the
+  // context lock the compute, a slot's dl_mu its output buffer (held from before the compute
+  // that fills it to the end of its download)
+  struct OvSlot {
+    DevBuf<char> dx, dy, dout;
+    std::mutex dl_mu;
+    cudaStream_t dl_stream = nullptr;
+    cudaEvent_t ev_x = nullptr, ev_y = nullptr;
+  };
+  OvSlot ov_[2];
+  std::mutex ov_up_mu_;
+  cudaStream_t ov_up_stream_ = nullptr;
+  int ov_slot_ = 0;
   int launches_ = 0;
   struct ProfRec {
     std::string name;

@@ -86,6 +86,70 @@ constexpr std::size_t kStageMin = std::size_t(4) << 20;  // below this the drive
 
 }  // namespace
 
+// ---- overlapped host products (concurrent callers, pinned buffers) ----
+// Below kOverlapMin digits the transfers are too short to matter; above kOverlapMax the four
+// extra digit buffers (2 slots x (inputs + output)) would not fit beside a config-5-size plan.
+constexpr std::size_t kOverlapMin = std::size_t(1) << 24;
+constexpr std::size_t kOverlapMax = std::size_t(4) << 30;
+
+bool Engine::overlap_ok(const char* x, std::size_t nx, const char* y, std::size_t ny, const char* out) const {
+  if (const char* e = std::getenv("DECMUL_OVERLAP"))
+    if (e[0] == '0') return false;
+  if (nx == 0 || ny == 0 || !x || !y || !out) return false;
+  const std::size_t n = nx + ny;
+  if (n < kOverlapMin || n > kOverlapMax) return false;
+  return is_pinned(x) && is_pinned(y) && is_pinned(out);
+}
+
+std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, std::size_t nx, const char* y,
+                                             std::size_t ny, char* out, std::size_t cap, unsigned forced,
+                                             bool alias, u64 p1, u64 p2) {
+  const bool squaring = alias || (nx == ny && (x == y || std::memcmp(x, y, nx) == 0));
+  const ProductPlan pp = plan_product(nx, ny, forced, p1, p2);
+  if (cap < nx + ny) throw std::length_error("multiply: output buffer too small");
+  // stage 1, uploads (in call order): x starts at once, also while the previous product computes
+  std::unique_lock<std::mutex> up(ov_up_mu_);
+  if (!ov_up_stream_) {
+    cuda_check(cudaStreamCreateWithFlags(&ov_up_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (OvSlot& s : ov_) {
+      cuda_check(cudaStreamCreateWithFlags(&s.dl_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      cuda_check(cudaEventCreateWithFlags(&s.ev_x, cudaEventDisableTiming), "cudaEventCreate");
+      cuda_check(cudaEventCreateWithFlags(&s.ev_y, cudaEventDisableTiming), "cudaEventCreate");
+    }
+  }
+  OvSlot& s = ov_[ov_slot_ ^= 1];
+  // the slot's inputs are free: its previous product finished computing before the product
+  // after it could take the context lock, and that one released ov_up_mu_ only later
+  s.dx.ensure(nx);
+  if (!squaring) s.dy.ensure(ny);
+  cuda_check(cudaMemcpyAsync(s.dx.ptr, x, nx, cudaMemcpyHostToDevice, ov_up_stream_), "h2d");
+  cuda_check(cudaEventRecord(s.ev_x, ov_up_stream_), "event");
+  // the slot's output buffer: wait out the download of the product that used it last
+  std::unique_lock<std::mutex> dl(s.dl_mu);
+  s.dout.ensure(nx + ny);
+  // stage 2, compute, under the context lock (workspace, plans, error word)
+  std::unique_lock<std::mutex> comp(ctx_mu);
+  cudaStream_t st = stream_;
+  cuda_check(cudaStreamWaitEvent(st, s.ev_x, 0), "wait");
+  run_product(pp, s.dx.ptr, squaring ? s.dx.ptr : s.dy.ptr, squaring, s.dout.ptr, st, err_.ptr, [&] {
+    if (squaring) return;
+    cuda_check(cudaMemcpyAsync(s.dy.ptr, y, ny, cudaMemcpyHostToDevice, ov_up_stream_), "h2d");
+    cuda_check(cudaEventRecord(s.ev_y, ov_up_stream_), "event");
+    cuda_check(cudaStreamWaitEvent(st, s.ev_y, 0), "wait");
+  });
+  unsigned long long len = 0;
+  cuda_check(cudaMemcpyAsync(&len, meta_.ptr + 2, sizeof len, cudaMemcpyDeviceToHost, st), "len");
+  cuda_check(cudaEventSynchronize(squaring ? s.ev_x : s.ev_y), "upload wait");
+  up.unlock();  // this product's digits are in HBM: the next call may upload
+  check_err(st);
+  if (len > cap) throw std::length_error("multiply: output buffer too small");
+  comp.unlock();
+  // stage 3, download, outside the context lock
+  cuda_check(cudaMemcpyAsync(out, s.dout.ptr, std::size_t(len), cudaMemcpyDeviceToHost, s.dl_stream), "d2h");
+  cuda_check(cudaStreamSynchronize(s.dl_stream), "sync");
+  return std::size_t(len);
+}
+
 void Engine::ensure_staging() {
   if (stage_[0]) return;
   for (int s = 0; s < kStageSlots; ++s) {

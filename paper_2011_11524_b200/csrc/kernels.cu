@@ -8,12 +8,18 @@
 // number of passes so every tile fits shared memory. Columns are read as
 // 128 B row segments (16 adjacent columns) so the reference's explicit
 // transpositions (conv.cpp:30-38) become strided addressing.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <string>
 #include <type_traits>
+
+#include <cuda.h>
 
 #include "kernels.cuh"
 #include "digits.cuh"
+#include "engine.hpp"
 #include "ntt_tile.cuh"
 
 namespace dmg {
@@ -139,6 +145,64 @@ constexpr bool kStageFwd = ROWS ? (DMG_STAGE_MASK & 1) != 0 : ((DMG_STAGE_MASK &
 template <bool ROWS>
 constexpr bool kStageInv = ROWS && (DMG_STAGE_MASK & 2) != 0;
 
+// Full-width row tiles (16 columns: R row segments of 128 B, dense [r][16] in shared memory)
+// are staged by the TMA unit instead: the array is a 2-D tensor {S, G R} of u64 (row pitch
+// 8 S bytes), the tile a box {16, min(R, 256)} at (s0, g R) -- one or two
+// cp.async.bulk.tensor.2d instructions from one thread per CTA (against 16 cp.async plus
+// index arithmetic from every thread), completion counted in bytes on an mbarrier that
+// every thread waits on. (Per-row cp.async.bulk copies are no substitute: UBLKCP takes
+// uniform-register addresses, so per-thread rows compile to a 32-step loop per warp.)
+// DMG_BULK_ROWS=0 keeps the cp.async burst (A/B).
+#ifndef DMG_BULK_ROWS
+#define DMG_BULK_ROWS 1
+#endif
+template <bool ROWS, int TW>
+constexpr bool kBulkRows = ROWS && TW == kTileW && DMG_BULK_ROWS != 0;
+constexpr int kBoxRows = 256;  // TMA box dimensions are at most 256
+
+__device__ __forceinline__ void mbar_init(u64* bar, unsigned count) {
+  const unsigned b = unsigned(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, unsigned bytes) {
+  const unsigned b = unsigned(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
+  const unsigned b = unsigned(__cvta_generic_to_shared(bar));
+  unsigned done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred ok;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 ok, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, ok;\n\t}"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// Thread 0 of the CTA: arm the barrier and issue the tile's TMA copies (rows row0 .. row0 + R
+// of the tensor, columns s0 .. s0 + 16). Everyone else meets it at the next __syncthreads and
+// then waits on the barrier's phase 0.
+template <int LOGR>
+__device__ __forceinline__ void stage_rows_tma(u64* sm, const void* map, unsigned long long s0,
+                                               unsigned long long row0, u64* bar) {
+  constexpr int R = 1 << LOGR, BR = R < kBoxRows ? R : kBoxRows;
+  mbar_init(bar, 1);
+  mbar_expect_tx(bar, unsigned(R * kTileW * sizeof(u64)));
+  const unsigned b = unsigned(__cvta_generic_to_shared(bar));
+#pragma unroll
+  for (int h = 0; h < R / BR; ++h) {
+    const unsigned sa = unsigned(__cvta_generic_to_shared(sm + h * BR * kTileW));
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(sa), "l"(map), "r"(int(s0)), "r"(int(row0) + h * BR), "r"(b)
+        : "memory");
+  }
+}
+
 // Issue the async copy of a tile into its shared layout: 16-byte chunks of the row segments
 // for row-major tiles; 8-byte words for swizzled columns (the swizzle may swap a 16-byte
 // pair), consecutive threads on consecutive rows of a column (coalesced). The caller waits
@@ -201,13 +265,13 @@ constexpr int pass_min_blocks(int logr, int tw) {
 // The first round reads HBM into registers and the last round writes HBM from
 // registers; shared memory carries only the rounds in between.
 template <int LOGR, bool ROWS, int TW, bool FACT = false>
-__global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_fwd(PassArgs a) {
+__global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_fwd(const __grid_constant__ PassArgs a, const __grid_constant__ TileMaps maps) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
   // first round's HBM loads above that barrier (config 5 +5%)
   pdl_wait();
   constexpr int R = 1 << LOGR, NTK = pass_threads(LOGR, TW);
   constexpr int E1 = Sched<LOGR>::e_dif(LOGR), EL = Sched<LOGR>::first_e;
-  extern __shared__ __align__(16) u64 sm[];
+  extern __shared__ __align__(128) u64 sm[];
   TwPair* tw = reinterpret_cast<TwPair*>(sm + R * TW);
   const int pr = int(blockIdx.x % a.np), tid = threadIdx.x;
   const u64 p = a.p[pr];
@@ -228,10 +292,18 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
     }
   }
   const TileLayout<LOGR, ROWS, TW> L;
-  if constexpr (kStageFwd<ROWS, TW> && LOGR > E1) stage_tile<LOGR, ROWS, TW, NTK>(sm, src, G, L, tid);
+  constexpr bool BULK = kBulkRows<ROWS, TW> && kStageFwd<ROWS, TW> && LOGR > E1;
+  u64* bar = sm + R * TW + R;  // after the tile and the R / 2 table pairs
+  if constexpr (BULK) {
+    if (tid == 0)
+      stage_rows_tma<LOGR>(sm, &maps.m[blockIdx.y * 2 + pr], G.s0, grp << LOGR, bar);
+  } else if constexpr (kStageFwd<ROWS, TW> && LOGR > E1) {
+    stage_tile<LOGR, ROWS, TW, NTK>(sm, src, G, L, tid);
+  }
   load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_fwd[pr]);
-  if constexpr (kStageFwd<ROWS, TW> && LOGR > E1) asm volatile("cp.async.wait_all;" ::: "memory");
+  if constexpr (!BULK && kStageFwd<ROWS, TW> && LOGR > E1) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  if constexpr (BULK) mbar_wait(bar, 0);
   // merged radix-3 twiddles: column input r of radix-3 row g times omega_{3 R}^{g r}, in the
   // first round (a separate shared-memory sweep cost config 4's two launches +1.1 ms)
   const TwPair* pre = (ROWS && a.pre[pr] && grp) ? a.pre[pr] + grp * R : nullptr;
@@ -298,7 +370,7 @@ constexpr int pass_inv_min_blocks(int logr, int tw) {
   return (logr == 9 && tw == kTileW) ? DMG_INV_MINB9 : pass_min_blocks(logr, tw);
 }
 template <int LOGR, bool ROWS, int TW, bool FACT = false, bool LZO = false>
-__global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LOGR, TW)) k_pass_inv(PassArgs a) {
+__global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LOGR, TW)) k_pass_inv(const __grid_constant__ PassArgs a, const __grid_constant__ TileMaps maps) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
   // first round's HBM loads above that barrier (config 5 +5%)
   pdl_wait();
@@ -306,7 +378,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   constexpr int E1 = Sched<LOGR>::first_e;
   constexpr int EL = Sched<LOGR>::rem ? Sched<LOGR>::rem : E1;  // last DIT round
   constexpr int AL = LOGR - EL;                                   // its starting stage
-  extern __shared__ __align__(16) u64 sm[];
+  extern __shared__ __align__(128) u64 sm[];
   TwPair* tw = reinterpret_cast<TwPair*>(sm + R * TW);
   const int pr = int(blockIdx.x % a.np), tid = threadIdx.x;
   const u64 p = a.p[pr];
@@ -330,10 +402,17 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   }
 #endif
   constexpr bool STAGE = kStageInv<ROWS> && LOGR > E1;
-  if constexpr (STAGE) stage_tile<LOGR, ROWS, TW, NTK>(sm, src, G, L, tid);
+  constexpr bool BULK = STAGE && kBulkRows<ROWS, TW>;
+  u64* bar = sm + R * TW + R;  // after the tile and the R / 2 table pairs
+  if constexpr (BULK) {
+    if (tid == 0) stage_rows_tma<LOGR>(sm, &maps.m[pr], G.s0, grp << LOGR, bar);
+  } else if constexpr (STAGE) {
+    stage_tile<LOGR, ROWS, TW, NTK>(sm, src, G, L, tid);
+  }
   load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_inv[pr]);
-  if constexpr (STAGE) asm volatile("cp.async.wait_all;" ::: "memory");
+  if constexpr (STAGE && !BULK) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  if constexpr (BULK) mbar_wait(bar, 0);
   for (int g = tid; g < (R >> E1) * TW; g += NTK) {
     int w, q, j0, base;
     group_coords<LOGR, ROWS, E1, TW>(g, w, q);
@@ -404,7 +483,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), fused_min_blocks(LOGR,
   constexpr int E1 = Sched<LOGR>::e_dif(LOGR), EM = Sched<LOGR>::first_e;
   constexpr int EL = Sched<LOGR>::rem ? Sched<LOGR>::rem : EM;
   constexpr int AL = LOGR - EL;
-  extern __shared__ __align__(16) u64 sm[];
+  extern __shared__ __align__(128) u64 sm[];
   u64* smx = sm + R * TW;  // TWO: the first operand's tile
   TwPair* twf = reinterpret_cast<TwPair*>(sm + (TWO ? 2 : 1) * R * TW);
   TwPair* twi = twf + R / 2;
@@ -917,6 +996,59 @@ void launch_pass_kernel(const PassArgs& a, unsigned long long ncols, int np, int
   launch_pdl(FN, dim3(unsigned((ncols + TW - 1) / TW * np), a.nops > 1 ? 2 : 1), dim3(NTK), size_t(smem), st, b);
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link against libcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// The {S, rows} u64 tensor over base with the row-tile box {16, min(R, 256)}.
+void encode_row_map(unsigned char (&out)[128], const u64* base, unsigned long long S, unsigned long long rows,
+                    int logR) {
+  static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
+  EncodeTiledFn fn = encode_tiled_fn();
+  if (!fn) throw CudaError("cuTensorMapEncodeTiled: driver entry point not found");
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {S, rows};
+  const cuuint64_t strides[1] = {S * sizeof(u64)};
+  const cuuint32_t box[2] = {cuuint32_t(kTileW), cuuint32_t(std::min(1 << logR, kBoxRows))};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult rc = fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<u64*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(rc)) + ")");
+  std::memcpy(out, &m, sizeof m);
+}
+
+// Forward / inverse passes: the same launch plus the tiles' tensor maps (full-width row tiles
+// of multi-round radices are staged by TMA; other shapes ignore the maps).
+template <auto FN, int TW, int NTK>
+void launch_pass_kernel_maps(const PassArgs& a, unsigned long long ncols, int np, int smem, bool tma, int logR,
+                             cudaStream_t st) {
+  set_smem<FN>(smem);
+  PassArgs b = a;
+  b.np = np;
+  TileMaps maps;
+  if (tma) {
+    const unsigned long long rows = a.G << logR;
+    for (int pr = 0; pr < np; ++pr) {
+      encode_row_map(maps.m[pr], a.src[pr], a.S, rows, logR);
+      if (a.nops > 1) encode_row_map(maps.m[2 + pr], a.src_b[pr], a.S, rows, logR);
+    }
+  }
+  launch_pdl(FN, dim3(unsigned((ncols + TW - 1) / TW * np), a.nops > 1 ? 2 : 1), dim3(NTK), size_t(smem), st, b, maps);
+}
+
 // Tile width: 16 columns (128 B row segments) normally; 4 when a pass would otherwise
 // launch fewer than two CTAs per SM (small transforms, e.g. config 1's N = 2^17 has
 // 16 tiles of 512 x 16 per prime), trading segment length for parallelism.
@@ -928,28 +1060,30 @@ inline bool narrow_tiles(int logR, unsigned long long ncols, int np) {
 template <int LOGR, int TW>
 void pass_fwd_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
-  const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) / 2 * 16;
+  const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) / 2 * 16 + 16;  // tile, table, mbarrier
+  constexpr bool TMA = kBulkRows<true, TW> && kStageFwd<true, TW> && LOGR > Sched<LOGR>::e_dif(LOGR);
   if (a.S > 1 && a.tw_lbits)
-    launch_pass_kernel<k_pass_fwd<LOGR, true, TW, true>, TW, NTK>(a, ncols, np, sm, st);
+    launch_pass_kernel_maps<k_pass_fwd<LOGR, true, TW, true>, TW, NTK>(a, ncols, np, sm, TMA, LOGR, st);
   else if (a.S > 1)
-    launch_pass_kernel<k_pass_fwd<LOGR, true, TW>, TW, NTK>(a, ncols, np, sm, st);
+    launch_pass_kernel_maps<k_pass_fwd<LOGR, true, TW>, TW, NTK>(a, ncols, np, sm, TMA, LOGR, st);
   else
-    launch_pass_kernel<k_pass_fwd<LOGR, false, TW>, TW, NTK>(a, ncols, np, sm, st);
+    launch_pass_kernel_maps<k_pass_fwd<LOGR, false, TW>, TW, NTK>(a, ncols, np, sm, false, LOGR, st);
 }
 template <int LOGR, int TW>
 void pass_inv_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
-  const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) / 2 * 16;
+  const int sm = (1 << LOGR) * TW * 8 + (1 << LOGR) / 2 * 16 + 16;  // tile, table, mbarrier
+  constexpr bool TMA = kBulkRows<true, TW> && kStageInv<true> && LOGR > Sched<LOGR>::first_e;
   if (a.S > 1 && a.tw_lbits && a.lazy_out)
-    launch_pass_kernel<k_pass_inv<LOGR, true, TW, true, true>, TW, NTK>(a, ncols, np, sm, st);
+    launch_pass_kernel_maps<k_pass_inv<LOGR, true, TW, true, true>, TW, NTK>(a, ncols, np, sm, TMA, LOGR, st);
   else if (a.S > 1 && a.tw_lbits)
-    launch_pass_kernel<k_pass_inv<LOGR, true, TW, true>, TW, NTK>(a, ncols, np, sm, st);
+    launch_pass_kernel_maps<k_pass_inv<LOGR, true, TW, true>, TW, NTK>(a, ncols, np, sm, TMA, LOGR, st);
   else if (a.S > 1 && a.lazy_out)
-    launch_pass_kernel<k_pass_inv<LOGR, true, TW, false, true>, TW, NTK>(a, ncols, np, sm, st);
+    launch_pass_kernel_maps<k_pass_inv<LOGR, true, TW, false, true>, TW, NTK>(a, ncols, np, sm, TMA, LOGR, st);
   else if (a.S > 1)
-    launch_pass_kernel<k_pass_inv<LOGR, true, TW>, TW, NTK>(a, ncols, np, sm, st);
+    launch_pass_kernel_maps<k_pass_inv<LOGR, true, TW>, TW, NTK>(a, ncols, np, sm, TMA, LOGR, st);
   else
-    launch_pass_kernel<k_pass_inv<LOGR, false, TW>, TW, NTK>(a, ncols, np, sm, st);
+    launch_pass_kernel_maps<k_pass_inv<LOGR, false, TW>, TW, NTK>(a, ncols, np, sm, false, LOGR, st);
 }
 template <int LOGR, int TW>
 void pass_fused_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {

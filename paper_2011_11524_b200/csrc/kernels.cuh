@@ -90,6 +90,12 @@ struct PassArgs {
   u64* dst_b[2];
 };
 
+// Tensor maps (CUtensorMap, opaque 128 bytes each) of the source arrays of a forward / inverse
+// row pass: [operand * 2 + prime]; the tiles are fetched by TMA (kernels.cu stage_rows_tma).
+struct alignas(64) TileMaps {
+  unsigned char m[4][128];
+};
+
 // Radix-3 pass over N = 3 S. The twiddle omega_N^{+-f s} (times the convolution
 // scale on the inverse) is factorised as lo[f][s mod L] * hi[f][s / L], L = 2^lbits,
 // so the tables are 3 (L + S / L) pairs instead of 3 S (both stay L2-resident).
@@ -240,6 +246,9 @@ double measure_modmul_rate(int variant, cudaStream_t st);
 // In-place transposes (reference transpose.cpp) on device memory.
 void launch_transpose_square_sub(u64* a, unsigned long long n, unsigned long long stride, cudaStream_t st);
 // rho per row of 2n words (n rows), through scratch (>= 2 n^2 words); inverse = unpermute_rho.
+// rho permutation of every 2n-word row, in place; scratch holds rho_scratch_words(n) words
+// (0 when a row fits shared memory, else 2n per resident CTA)
+std::size_t rho_scratch_words(unsigned long long n);
 void launch_rho(u64* a, u64* scratch, unsigned long long n, bool inverse, cudaStream_t st);
 
 }  // namespace dmg

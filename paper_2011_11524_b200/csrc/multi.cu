@@ -133,6 +133,15 @@ std::size_t MultiEngine::multiply_host(const char* x, std::size_t nx, const char
   return eng_[0]->multiply_host(x, nx, y, ny, out, cap, forced, alias, p1, p2);
 }
 
+Engine* MultiEngine::overlap_engine(const char* x, std::size_t nx, const char* y, std::size_t ny, const char* out,
+                                    unsigned forced, u64 p1, u64 p2) {
+  Engine& e = *eng_[0];
+  if (!e.overlap_ok(x, nx, y, ny, out)) return nullptr;
+  if ((nx == 1 && x[0] == '0') || (ny == 1 && y[0] == '0')) return nullptr;
+  if (!p1 && !p2 && (block_digits(nx, ny, forced) || shards(nx, ny, forced))) return nullptr;
+  return &e;
+}
+
 void MultiEngine::multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
                                       const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
                                       std::size_t out_stride, std::size_t* lens) {

@@ -25,6 +25,11 @@ class MultiEngine {
   // enough (shards()), else on the first device
   std::size_t multiply_host(const char* x, std::size_t nx, const char* y, std::size_t ny, char* out,
                             std::size_t cap, unsigned forced_base_exp, bool alias, u64 p1 = 0, u64 p2 = 0);
+  // The engine that would run this product alone on one device with overlappable transfers
+  // (Engine::overlap_ok: large, pinned buffers; not sharded, not block-convolved), else nullptr.
+  // Its multiply_host_overlapped is called WITHOUT the context lock held.
+  Engine* overlap_engine(const char* x, std::size_t nx, const char* y, std::size_t ny, const char* out,
+                         unsigned forced_base_exp, u64 p1 = 0, u64 p2 = 0);
   // batches: contiguous ranges of products per device, one host thread per device
   void multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
                            const char* ys, std::size_t y_stride, std::size_t ny, char* outs,

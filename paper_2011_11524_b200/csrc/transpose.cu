@@ -6,6 +6,8 @@
 //  stride `stride`, swapped as 32 x 32 tile pairs staged through shared memory:
 //  one CTA owns one (i <= j) tile pair, so the swap is race-free in place.
 //  permute_rho / unpermute_rho (transpose.cpp:27-41) per row of 2n words.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace dmg {
@@ -42,18 +44,29 @@ __global__ void k_transpose_square(u64* a, unsigned long long n, unsigned long l
   }
 }
 
-__global__ void k_rho(const u64* a, u64* s, unsigned long long n, int inverse) {
-  const unsigned long long total = 2 * n * n;
-  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < total;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long row = i / (2 * n), j = i % (2 * n);
-    // destination index j of the permuted row
-    unsigned long long from;
-    if (!inverse)
-      from = j < n ? 2 * j : 2 * (j - n) + 1;  // row[j] = old[2j], row[n+j] = old[2j+1]
-    else
-      from = (j & 1) ? n + j / 2 : j / 2;      // row[2i] = old[i], row[2i+1] = old[n+i]
-    s[i] = a[row * 2 * n + from];
+// permute_rho / unpermute_rho in place, one row of 2n words at a time per CTA: the row is
+// staged in shared memory (2n <= kRhoSmemWords) or in this CTA's own 2n-word slice of a small
+// global scratch, like the reference's 2n words of scratch per row (transpose.cpp:27-47).
+constexpr unsigned long long kRhoSmemWords = 16384;  // 128 KiB
+
+template <bool SMEM>
+__global__ void k_rho_rows(u64* a, u64* scratch, unsigned long long n, int inverse) {
+  extern __shared__ u64 rho_stage[];
+  const unsigned long long w = 2 * n;
+  u64* s = SMEM ? rho_stage : scratch + blockIdx.x * w;
+  for (unsigned long long row = blockIdx.x; row < n; row += gridDim.x) {
+    u64* r = a + row * w;
+    for (unsigned long long j = threadIdx.x; j < w; j += blockDim.x) s[j] = r[j];
+    __syncthreads();
+    for (unsigned long long j = threadIdx.x; j < w; j += blockDim.x) {
+      unsigned long long from;
+      if (!inverse)
+        from = j < n ? 2 * j : 2 * (j - n) + 1;  // row[j] = old[2j], row[n+j] = old[2j+1]
+      else
+        from = (j & 1) ? n + j / 2 : j / 2;      // row[2i] = old[i], row[2i+1] = old[n+i]
+      r[j] = s[from];
+    }
+    __syncthreads();
   }
 }
 
@@ -66,13 +79,28 @@ void launch_transpose_square_sub(u64* a, unsigned long long n, unsigned long lon
   k_transpose_square<<<unsigned(pairs), dim3(T, 8), 0, st>>>(a, n, stride, nt);
 }
 
+unsigned rho_ctas(unsigned long long n) { return unsigned(n < 148 * 2 ? n : 148 * 2); }
+
+// DECMUL_RHO_GLOBAL=1 forces the global-scratch variant at small n (tests)
+bool rho_in_smem(unsigned long long n) {
+  const char* e = std::getenv("DECMUL_RHO_GLOBAL");
+  return 2 * n <= kRhoSmemWords && !(e && e[0] == '1');
+}
+
+std::size_t rho_scratch_words(unsigned long long n) {
+  return rho_in_smem(n) ? 0 : std::size_t(rho_ctas(n)) * 2 * n;
+}
+
 void launch_rho(u64* a, u64* scratch, unsigned long long n, bool inverse, cudaStream_t st) {
   if (n == 0) return;
-  const unsigned long long total = 2 * n * n;
-  unsigned long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  k_rho<<<unsigned(blocks), 256, 0, st>>>(a, scratch, n, inverse ? 1 : 0);
-  cudaMemcpyAsync(a, scratch, total * sizeof(u64), cudaMemcpyDeviceToDevice, st);
+  const unsigned ctas = rho_ctas(n);
+  if (rho_in_smem(n)) {
+    const std::size_t smem = 2 * n * sizeof(u64);
+    cudaFuncSetAttribute(k_rho_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_rho_rows<true><<<ctas, 256, smem, st>>>(a, nullptr, n, inverse ? 1 : 0);
+  } else {
+    k_rho_rows<false><<<ctas, 256, 0, st>>>(a, scratch, n, inverse ? 1 : 0);
+  }
 }
 
 }  // namespace dmg

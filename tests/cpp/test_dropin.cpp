@@ -137,6 +137,32 @@ int main() {
       CHECK(a == x);
     }
   }
+  // non-default plans (test_conv.cpp:183-196 "all shapes agree", selftest.cpp:109-118 forced shapes)
+  for (Word p : {kProductionP1, kProductionP2}) {
+    const MontCtx c = make_ctx(p);
+    for (size_t n : {size_t(64), size_t(96), size_t(192)}) {
+      std::vector<Word> x(n), y(n);
+      or_gen_residues(n + 7, n, p, x.data());
+      or_gen_residues(n + 8, n, p, y.data());
+      const ConvPlan direct = build_conv_plan(c, n);
+      CHECK(direct.shape == (n % 3 == 0 ? ConvShape::kFourStepThreeRows : ConvShape::kDirect));
+      const std::vector<Word> ref = convolve_mod_p(direct, x, y);
+      for (size_t thr : {size_t(32), size_t(8), size_t(4), size_t(2)}) {
+        const ConvPlan alt = build_conv_plan(c, n, thr);
+        if (n % 3) CHECK(alt.shape == ConvShape::kSixStep && alt.n1 * alt.n2 == n);
+        CHECK(alt.root == direct.root);
+        CHECK(convolve_mod_p(alt, x, y) == ref);
+        std::vector<Word> a = x, r = x;
+        forward_transform(alt, a);
+        or_forward_transform(p, n, thr, r.data());
+        CHECK(a == r);
+        inverse_transform(alt, a);
+        CHECK(a == x);
+      }
+    }
+    CHECK_THROWS_AS(build_conv_plan(c, 5), std::invalid_argument);
+    CHECK_THROWS_AS(build_conv_plan(c, size_t(1) << 40), std::invalid_argument);
+  }
   // transposes (test_transpose.cpp:93-129)
   {
     std::vector<Word> a{1, 2, 3, 4, 5, 6, 7, 8};

@@ -227,6 +227,20 @@ def test_convolution_hook_vs_reference(gpu, ref, golden):
         assert np.array_equal(gpu.inverse_transform(p, fwd), x), key
 
 
+def test_forced_six_step_threshold_orders(gpu, port):
+    """Non-default plans (reference build_conv_plan(ctx, n, six_step_threshold), test_conv.cpp:183-196,
+    selftest.cpp:109-118): the forward hook returns the spectrum in the forced plan's storage
+    order (conv.hpp:19-24), the inverse hook consumes it, for every shape the threshold selects."""
+    for p in (P1, P2, dm.Q1):
+        for n in (64, 96, 192, 1024, 3 << 9, 1 << 13, 3 << 12):
+            x = port.gen_residues(n + 5, n, p)
+            for thr in (2, 4, 8, 32, 1 << 10, 0):
+                fwd = gpu.forward_transform(p, x, thr)
+                assert np.array_equal(fwd, port.forward_transform(p, x, thr)), (p, n, thr)
+                assert np.array_equal(gpu.inverse_transform(p, fwd, thr), x), (p, n, thr)
+                assert np.array_equal(gpu.inverse_transform(p, port.forward_transform(p, x, thr), thr), x)
+
+
 def test_convolution_hook_shorter_inputs_and_squaring(gpu, port):
     for p in (P1, P2, dm.Q1, dm.Q2):
         for n in (6, 64, 1536, 1 << 14, 3 << 13):
@@ -288,6 +302,20 @@ def test_transpose_hooks(gpu, port, golden):
     for n, stride in ((3, 3), (31, 31), (33, 64), (100, 100), (128, 200)):
         m = rng.integers(0, 2**63, n * stride, dtype=np.uint64)
         assert np.array_equal(gpu.transpose_square_sub(m, n, stride), port.transpose_square_sub(m, n, stride))
+
+
+def test_transpose_rho_in_place_variants(gpu, port, monkeypatch):
+    """The rho permutation runs in place row by row (reference transpose.cpp:27-47: 2n words of
+    scratch): rows staged in shared memory, or -- past 128 KiB per row, forced here at small n --
+    in a per-CTA 2n-word global slice; more rows than CTAs (n = 700 > 296)."""
+    rng = np.random.default_rng(31)
+    for force in ("0", "1"):
+        monkeypatch.setenv("DECMUL_RHO_GLOBAL", force)
+        for n in (1, 7, 300, 700):
+            m = rng.integers(0, 2**63, 2 * n * n, dtype=np.uint64)
+            t = gpu.transpose_n_x_2n(m, n)
+            assert np.array_equal(t, port.transpose_n_x_2n(m, n)), (force, n)
+            assert np.array_equal(gpu.transpose_2n_x_n(t, n), m), (force, n)
 
 
 def test_device_api_and_generator(gpu, port):

@@ -99,6 +99,27 @@ def test_planner_random_sizes_vs_port(port):
         assert dm.smallest_supported_length(need) == port.smallest_supported_length(need)
 
 
+def test_build_conv_plan_matches_reference_plan(port):
+    """build_conv_plan(ctx, n, six_step_threshold) through the C ABI (no GPU): shape, root and
+    six-step factors equal the reference restatement's plan (conv.cpp:212-271), default and
+    forced thresholds (test_conv.cpp:183-196, selftest.cpp:109-118)."""
+    names = ("direct", "six_step", "three_rows")
+    for p in (dm.P1, dm.P2, dm.Q1, dm.Q2):
+        for n in (1, 2, 3, 4, 6, 16, 48, 64, 96, 192, 768, 1 << 15, 1 << 16, 3 << 15, 1 << 20):
+            for thr in (0, 2, 4, 8, 32, 1 << 10):
+                got = dm.build_conv_plan(p, n, thr)
+                want = port.conv_plan_info(p, n, thr)
+                assert got["shape"] == names[want["shape"]], (p, n, thr)
+                assert got["root"] == want["root"], (p, n, thr)
+                if got["shape"] == "six_step":
+                    assert (got["n1"], got["n2"]) == (want["n1"], want["n2"]), (p, n, thr)
+    for bad in (0, 5, 12 * 5, 7):
+        with pytest.raises(ValueError, match="length must be 2\\^k or 3\\*2\\^k"):
+            dm.build_conv_plan(dm.P1, bad)
+    with pytest.raises(ValueError, match="does not divide p-1"):
+        dm.build_conv_plan(dm.P1, 1 << 40)
+
+
 def test_decimal_number_parse_errors():
     assert dm.DecimalNumber().text() == b"0" and dm.DecimalNumber().is_zero()
     assert dm.DecimalNumber.parse("1000").digit_count() == 4
