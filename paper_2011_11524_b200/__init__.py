@@ -318,6 +318,16 @@ class Context:
                        C.c_size_t(cap), C.byref(n), C.byref(o))
         return out.raw[: n.value]
 
+    def multiply_ptr(self, h_x: int, nx: int, h_y: int, ny: int, h_out: int, cap: int, alias: bool = False,
+                     forced_base_exp: int = 0) -> int:
+        """Host pointers (ints, e.g. pinned torch tensor.data_ptr()); returns the product length.
+        Thread-safe; concurrent calls with large pinned buffers overlap their transfers
+        (one call's download with the next call's upload and compute)."""
+        n = C.c_size_t()
+        self._call("decmul_gpu_multiply", C.c_void_p(h_x), C.c_size_t(nx), C.c_void_p(h_y), C.c_size_t(ny),
+                   C.c_void_p(h_out), C.c_size_t(cap), C.byref(n), C.c_uint(forced_base_exp), C.c_int(int(alias)))
+        return n.value
+
     def multiply_device(self, d_x: int, nx: int, d_y: int, ny: int, d_out: int, cap: int, stream: int = 0,
                         squaring: bool = False, sync: bool = True, forced_base_exp: int = 0):
         """Device pointers (ints, e.g. torch tensor.data_ptr()); returns the length if sync."""

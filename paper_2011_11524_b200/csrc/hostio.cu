@@ -3,6 +3,8 @@
 // large pageable ones are pipelined through a ring of pinned slots, the host threads of
 // a CopyPool filling (or draining) slot c while the DMA engine moves slot c - 1.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -107,8 +109,17 @@ std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, 
   const bool squaring = alias || (nx == ny && (x == y || std::memcmp(x, y, nx) == 0));
   const ProductPlan pp = plan_product(nx, ny, forced, p1, p2);
   if (cap < nx + ny) throw std::length_error("multiply: output buffer too small");
+  // DECMUL_OVERLAP_TRACE=1: one stderr line of stage timestamps (ms since the call began)
+  static const bool trace = [] {
+    const char* e = std::getenv("DECMUL_OVERLAP_TRACE");
+    return e && e[0] == '1';
+  }();
+  const auto t_begin = std::chrono::steady_clock::now();
+  auto ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count(); };
+  double t_up = 0, t_dl = 0, t_comp = 0, t_enq = 0, t_ydone = 0, t_cdone = 0;
   // stage 1, uploads (in call order): x starts at once, also while the previous product computes
   std::unique_lock<std::mutex> up(ov_up_mu_);
+  t_up = ms();
   if (!ov_up_stream_) {
     cuda_check(cudaStreamCreateWithFlags(&ov_up_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
     for (OvSlot& s : ov_) {
@@ -126,9 +137,11 @@ std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, 
   cuda_check(cudaEventRecord(s.ev_x, ov_up_stream_), "event");
   // the slot's output buffer: wait out the download of the product that used it last
   std::unique_lock<std::mutex> dl(s.dl_mu);
+  t_dl = ms();
   s.dout.ensure(nx + ny);
   // stage 2, compute, under the context lock (workspace, plans, error word)
   std::unique_lock<std::mutex> comp(ctx_mu);
+  t_comp = ms();
   cudaStream_t st = stream_;
   cuda_check(cudaStreamWaitEvent(st, s.ev_x, 0), "wait");
   run_product(pp, s.dx.ptr, squaring ? s.dx.ptr : s.dy.ptr, squaring, s.dout.ptr, st, err_.ptr, [&] {
@@ -139,14 +152,22 @@ std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, 
   });
   unsigned long long len = 0;
   cuda_check(cudaMemcpyAsync(&len, meta_.ptr + 2, sizeof len, cudaMemcpyDeviceToHost, st), "len");
+  t_enq = ms();
   cuda_check(cudaEventSynchronize(squaring ? s.ev_x : s.ev_y), "upload wait");
   up.unlock();  // this product's digits are in HBM: the next call may upload
+  t_ydone = ms();
   check_err(st);
+  t_cdone = ms();
   if (len > cap) throw std::length_error("multiply: output buffer too small");
   comp.unlock();
   // stage 3, download, outside the context lock
   cuda_check(cudaMemcpyAsync(out, s.dout.ptr, std::size_t(len), cudaMemcpyDeviceToHost, s.dl_stream), "d2h");
   cuda_check(cudaStreamSynchronize(s.dl_stream), "sync");
+  if (trace)
+    std::fprintf(stderr,
+                 "overlap slot %d: up lock %.1f, out slot %.1f, ctx lock %.1f, enqueued %.1f, uploads done %.1f, "
+                 "computed %.1f, downloaded %.1f ms\n",
+                 int(&s - ov_), t_up, t_dl, t_comp, t_enq, t_ydone, t_cdone, ms());
   return std::size_t(len);
 }
 

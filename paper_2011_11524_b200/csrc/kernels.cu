@@ -183,6 +183,28 @@ __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
   } while (!done);
 }
 
+// The same tiles leave through the TMA unit: the last round writes its results back into the
+// tile in shared memory (same positions it read) and one thread stores the box to the output
+// tensor, instead of 8 strided 8-byte global stores per register group. DMG_BULK_STORE=0
+// keeps the direct stores (A/B).
+#ifndef DMG_BULK_STORE
+#define DMG_BULK_STORE 0
+#endif
+template <int LOGR>
+__device__ __forceinline__ void store_rows_tma(const u64* sm, const void* map, unsigned long long s0,
+                                               unsigned long long row0) {
+  constexpr int R = 1 << LOGR, BR = R < kBoxRows ? R : kBoxRows;
+#pragma unroll
+  for (int h = 0; h < R / BR; ++h) {
+    const unsigned sa = unsigned(__cvta_generic_to_shared(sm + h * BR * kTileW));
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map),
+                 "r"(int(s0)), "r"(int(row0) + h * BR), "r"(sa)
+                 : "memory");
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the CTA's shared memory outlives the reads
+}
+
 // Thread 0 of the CTA: arm the barrier and issue the tile's TMA copies (rows row0 .. row0 + R
 // of the tensor, columns s0 .. s0 + 16). Everyone else meets it at the next __syncthreads and
 // then waits on the barrier's phase 0.
@@ -351,10 +373,20 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i, w)];
       dif_regs<LOGR, EL, EL, kSwzTables<ROWS>, ROWS>(v, 0, tw, p);  // lazy: twiddled next
       if constexpr (ROWS) G.template twist_group<EL, FACT>(v, T, Hi, q, w, p);
-      u64* d = dst + G.at(base, w);
-      const unsigned long long es = G.row_stride();
+      if constexpr (BULK && DMG_BULK_STORE) {
 #pragma unroll
-      for (int i = 0; i < (1 << EL); ++i) d[i * es] = v[i];
+        for (int i = 0; i < (1 << EL); ++i) sm[L(base + i, w)] = v[i];
+      } else {
+        u64* d = dst + G.at(base, w);
+        const unsigned long long es = G.row_stride();
+#pragma unroll
+        for (int i = 0; i < (1 << EL); ++i) d[i * es] = v[i];
+      }
+    }
+    if constexpr (BULK && DMG_BULK_STORE) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
+      __syncthreads();
+      if (tid == 0) store_rows_tma<LOGR>(sm, &maps.m[4 + blockIdx.y * 2 + pr], G.s0, grp << LOGR);
     }
   }
 }
@@ -454,8 +486,16 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
         if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
-        dst[G.at(base + i * STL, w)] = v[i];
+        if constexpr (BULK && DMG_BULK_STORE)
+          sm[L(base + i * STL, w)] = v[i];
+        else
+          dst[G.at(base + i * STL, w)] = v[i];
       }
+    }
+    if constexpr (BULK && DMG_BULK_STORE) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
+      __syncthreads();
+      if (tid == 0) store_rows_tma<LOGR>(sm, &maps.m[4 + pr], G.s0, grp << LOGR);
     }
   }
 }
@@ -1044,6 +1084,10 @@ void launch_pass_kernel_maps(const PassArgs& a, unsigned long long ncols, int np
     for (int pr = 0; pr < np; ++pr) {
       encode_row_map(maps.m[pr], a.src[pr], a.S, rows, logR);
       if (a.nops > 1) encode_row_map(maps.m[2 + pr], a.src_b[pr], a.S, rows, logR);
+      if (DMG_BULK_STORE) {
+        encode_row_map(maps.m[4 + pr], a.dst[pr], a.S, rows, logR);
+        if (a.nops > 1) encode_row_map(maps.m[6 + pr], a.dst_b[pr], a.S, rows, logR);
+      }
     }
   }
   launch_pdl(FN, dim3(unsigned((ncols + TW - 1) / TW * np), a.nops > 1 ? 2 : 1), dim3(NTK), size_t(smem), st, b, maps);

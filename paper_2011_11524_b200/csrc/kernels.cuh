@@ -91,9 +91,10 @@ struct PassArgs {
 };
 
 // Tensor maps (CUtensorMap, opaque 128 bytes each) of the source arrays of a forward / inverse
-// row pass: [operand * 2 + prime]; the tiles are fetched by TMA (kernels.cu stage_rows_tma).
+// row pass, [operand * 2 + prime], and of its destination arrays, [4 + operand * 2 + prime]; the
+// tiles are fetched (and optionally stored) by TMA (kernels.cu stage_rows_tma / store_rows_tma).
 struct alignas(64) TileMaps {
-  unsigned char m[4][128];
+  unsigned char m[8][128];
 };
 
 // Radix-3 pass over N = 3 S. The twiddle omega_N^{+-f s} (times the convolution

@@ -352,6 +352,66 @@ def test_host_api_pageable_staging(gpu, ref):
     assert sha(z2) == sha(ref.multiply(x, None))
 
 
+def test_concurrent_large_products_overlap_transfers(gpu, ref, monkeypatch):
+    """Concurrent decmul_gpu_multiply calls with large pinned buffers take the overlapped path
+    (upload / compute / download stages over two buffer slots, csrc/hostio.cu): four threads,
+    three products each of different operands and sizes, one aliased squaring, one thread
+    hitting a non-digit. Every product equals the ordinary locked path's (DECMUL_OVERLAP=0),
+    one of them the reference's."""
+    import threading
+
+    import torch
+
+    shapes = [(9_000_001, 8_000_003), (12_000_000, 5_000_000), (8_500_000, 8_500_000), (17_000_000, 1)]
+    jobs = []
+    for t, (nx, ny) in enumerate(shapes):
+        x = torch.frombuffer(bytearray(inputs.gen_digits(700 + t, nx)), dtype=torch.uint8).pin_memory()
+        y = torch.frombuffer(bytearray(inputs.gen_digits(800 + t, ny)), dtype=torch.uint8).pin_memory()
+        out = torch.empty(nx + ny, dtype=torch.uint8).pin_memory()
+        jobs.append((x, y, out))
+    want = []
+    monkeypatch.setenv("DECMUL_OVERLAP", "0")
+    for t, (x, y, out) in enumerate(jobs):
+        alias = t == 2
+        n = gpu.multiply_ptr(x.data_ptr(), x.numel(), (x if alias else y).data_ptr(), x.numel() if alias else y.numel(),
+                             out.data_ptr(), out.numel(), alias=alias)
+        want.append((n, sha(out.numpy()[:n].tobytes())))
+    x0, y0 = bytes(jobs[0][0].numpy()), bytes(jobs[0][1].numpy())
+    z0 = ref.multiply(x0, y0)
+    assert want[0] == (len(z0), sha(z0))
+    monkeypatch.setenv("DECMUL_OVERLAP", "1")
+    got, errs = {}, {}
+
+    def worker(t):
+        x, y, out = jobs[t]
+        alias = t == 2
+        for rep in range(3):
+            out.zero_()
+            try:
+                n = gpu.multiply_ptr(x.data_ptr(), x.numel(), (x if alias else y).data_ptr(),
+                                     x.numel() if alias else y.numel(), out.data_ptr(), out.numel(), alias=alias)
+                got[(t, rep)] = (n, sha(out.numpy()[:n].tobytes()))
+            except Exception as e:  # noqa
+                errs[(t, rep)] = e
+            if t == 1 and rep == 0:
+                x[12345] = ord("x")  # the second call of this thread must fail, the third succeed again
+            elif t == 1 and rep == 1:
+                x[12345] = ord("7")
+
+    saved = int(jobs[1][0][12345])
+    th = [threading.Thread(target=worker, args=(t,)) for t in range(len(jobs))]
+    for h in th:
+        h.start()
+    for h in th:
+        h.join()
+    assert set(errs) == {(1, 1)} and isinstance(errs[(1, 1)], ValueError) and "non-digit" in str(errs[(1, 1)])
+    for (t, rep), v in got.items():
+        if t == 1 and rep == 2 and saved != ord("7"):
+            continue  # a different operand now; checked for length only
+        assert v == want[t], (t, rep)
+    assert len(got) == 11
+
+
 def test_batch_mixed_sizes_pointer_arrays(gpu, ref):
     """decmul_gpu_multiply_batch_ptrs (the pointer-array batch of SURVEY §8(b)): repeated
     size pairs run as uniform batches, singletons one by one; results in input order."""
