@@ -150,6 +150,7 @@ Engine::~Engine() {
     if (s.dl_stream) cudaStreamDestroy(s.dl_stream);
     if (s.ev_x) cudaEventDestroy(s.ev_x);
     if (s.ev_y) cudaEventDestroy(s.ev_y);
+    if (s.h_len) cudaFreeHost(s.h_len);
   }
   copy_pool_.reset();
   for (int k = 0; k < kStageSlots; ++k) {

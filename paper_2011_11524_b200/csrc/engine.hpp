@@ -364,6 +364,7 @@ class Engine {
     std::mutex dl_mu;
     cudaStream_t dl_stream = nullptr;
     cudaEvent_t ev_x = nullptr, ev_y = nullptr;
+    unsigned long long* h_len = nullptr;  // pinned: the product length, read back without blocking
   };
   OvSlot ov_[2];
   std::mutex ov_up_mu_;

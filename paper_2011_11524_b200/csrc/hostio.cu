@@ -126,6 +126,7 @@ std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, 
       cuda_check(cudaStreamCreateWithFlags(&s.dl_stream, cudaStreamNonBlocking), "cudaStreamCreate");
       cuda_check(cudaEventCreateWithFlags(&s.ev_x, cudaEventDisableTiming), "cudaEventCreate");
       cuda_check(cudaEventCreateWithFlags(&s.ev_y, cudaEventDisableTiming), "cudaEventCreate");
+      cuda_check(cudaMallocHost(&s.h_len, sizeof *s.h_len), "cudaMallocHost");
     }
   }
   OvSlot& s = ov_[ov_slot_ ^= 1];
@@ -150,14 +151,16 @@ std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, 
     cuda_check(cudaEventRecord(s.ev_y, ov_up_stream_), "event");
     cuda_check(cudaStreamWaitEvent(st, s.ev_y, 0), "wait");
   });
-  unsigned long long len = 0;
-  cuda_check(cudaMemcpyAsync(&len, meta_.ptr + 2, sizeof len, cudaMemcpyDeviceToHost, st), "len");
+  // (into pinned memory: a copy to pageable memory would block this thread, and with it the
+  // upload lock, until the whole product has been computed)
+  cuda_check(cudaMemcpyAsync(s.h_len, meta_.ptr + 2, sizeof *s.h_len, cudaMemcpyDeviceToHost, st), "len");
   t_enq = ms();
   cuda_check(cudaEventSynchronize(squaring ? s.ev_x : s.ev_y), "upload wait");
   up.unlock();  // this product's digits are in HBM: the next call may upload
   t_ydone = ms();
   check_err(st);
   t_cdone = ms();
+  const unsigned long long len = *s.h_len;
   if (len > cap) throw std::length_error("multiply: output buffer too small");
   comp.unlock();
   // stage 3, download, outside the context lock
