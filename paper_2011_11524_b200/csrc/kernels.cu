@@ -156,8 +156,12 @@ constexpr bool kStageInv = ROWS && (DMG_STAGE_MASK & 2) != 0;
 #ifndef DMG_BULK_ROWS
 #define DMG_BULK_ROWS 1
 #endif
+// DMG_BULK_NARROW=1: the 4-column tiles of small transforms too (32-byte box rows)
+#ifndef DMG_BULK_NARROW
+#define DMG_BULK_NARROW 0
+#endif
 template <bool ROWS, int TW>
-constexpr bool kBulkRows = ROWS && TW == kTileW && DMG_BULK_ROWS != 0;
+constexpr bool kBulkRows = ROWS && (TW == kTileW || DMG_BULK_NARROW != 0) && DMG_BULK_ROWS != 0;
 constexpr int kBoxRows = 256;  // TMA box dimensions are at most 256
 
 __device__ __forceinline__ void mbar_init(u64* bar, unsigned count) {
@@ -190,13 +194,13 @@ __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
 #ifndef DMG_BULK_STORE
 #define DMG_BULK_STORE 1
 #endif
-template <int LOGR>
+template <int LOGR, int TW>
 __device__ __forceinline__ void store_rows_tma(const u64* sm, const void* map, unsigned long long s0,
                                                unsigned long long row0) {
   constexpr int R = 1 << LOGR, BR = R < kBoxRows ? R : kBoxRows;
 #pragma unroll
   for (int h = 0; h < R / BR; ++h) {
-    const unsigned sa = unsigned(__cvta_generic_to_shared(sm + h * BR * kTileW));
+    const unsigned sa = unsigned(__cvta_generic_to_shared(sm + h * BR * TW));
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map),
                  "r"(int(s0)), "r"(int(row0) + h * BR), "r"(sa)
                  : "memory");
@@ -208,16 +212,16 @@ __device__ __forceinline__ void store_rows_tma(const u64* sm, const void* map, u
 // Thread 0 of the CTA: arm the barrier and issue the tile's TMA copies (rows row0 .. row0 + R
 // of the tensor, columns s0 .. s0 + 16). Everyone else meets it at the next __syncthreads and
 // then waits on the barrier's phase 0.
-template <int LOGR>
+template <int LOGR, int TW>
 __device__ __forceinline__ void stage_rows_tma(u64* sm, const void* map, unsigned long long s0,
                                                unsigned long long row0, u64* bar) {
   constexpr int R = 1 << LOGR, BR = R < kBoxRows ? R : kBoxRows;
   mbar_init(bar, 1);
-  mbar_expect_tx(bar, unsigned(R * kTileW * sizeof(u64)));
+  mbar_expect_tx(bar, unsigned(R * TW * sizeof(u64)));
   const unsigned b = unsigned(__cvta_generic_to_shared(bar));
 #pragma unroll
   for (int h = 0; h < R / BR; ++h) {
-    const unsigned sa = unsigned(__cvta_generic_to_shared(sm + h * BR * kTileW));
+    const unsigned sa = unsigned(__cvta_generic_to_shared(sm + h * BR * TW));
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
             "r"(sa), "l"(map), "r"(int(s0)), "r"(int(row0) + h * BR), "r"(b)
@@ -318,7 +322,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   u64* bar = sm + R * TW + R;  // after the tile and the R / 2 table pairs
   if constexpr (BULK) {
     if (tid == 0)
-      stage_rows_tma<LOGR>(sm, &maps.m[blockIdx.y * 2 + pr], G.s0, grp << LOGR, bar);
+      stage_rows_tma<LOGR, TW>(sm, &maps.m[blockIdx.y * 2 + pr], G.s0, grp << LOGR, bar);
   } else if constexpr (kStageFwd<ROWS, TW> && LOGR > E1) {
     stage_tile<LOGR, ROWS, TW, NTK>(sm, src, G, L, tid);
   }
@@ -326,6 +330,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   if constexpr (!BULK && kStageFwd<ROWS, TW> && LOGR > E1) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if constexpr (BULK) mbar_wait(bar, 0);
+  pdl_trigger_mid();
   // merged radix-3 twiddles: column input r of radix-3 row g times omega_{3 R}^{g r}, in the
   // first round (a separate shared-memory sweep cost config 4's two launches +1.1 ms)
   const TwPair* pre = (ROWS && a.pre[pr] && grp) ? a.pre[pr] + grp * R : nullptr;
@@ -386,7 +391,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
     if constexpr (BULK && DMG_BULK_STORE) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
       __syncthreads();
-      if (tid == 0) store_rows_tma<LOGR>(sm, &maps.m[4 + blockIdx.y * 2 + pr], G.s0, grp << LOGR);
+      if (tid == 0) store_rows_tma<LOGR, TW>(sm, &maps.m[4 + blockIdx.y * 2 + pr], G.s0, grp << LOGR);
     }
   }
 }
@@ -437,7 +442,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   constexpr bool BULK = STAGE && kBulkRows<ROWS, TW>;
   u64* bar = sm + R * TW + R;  // after the tile and the R / 2 table pairs
   if constexpr (BULK) {
-    if (tid == 0) stage_rows_tma<LOGR>(sm, &maps.m[pr], G.s0, grp << LOGR, bar);
+    if (tid == 0) stage_rows_tma<LOGR, TW>(sm, &maps.m[pr], G.s0, grp << LOGR, bar);
   } else if constexpr (STAGE) {
     stage_tile<LOGR, ROWS, TW, NTK>(sm, src, G, L, tid);
   }
@@ -445,6 +450,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   if constexpr (STAGE && !BULK) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if constexpr (BULK) mbar_wait(bar, 0);
+  pdl_trigger_mid();
   for (int g = tid; g < (R >> E1) * TW; g += NTK) {
     int w, q, j0, base;
     group_coords<LOGR, ROWS, E1, TW>(g, w, q);
@@ -495,7 +501,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
     if constexpr (BULK && DMG_BULK_STORE) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
       __syncthreads();
-      if (tid == 0) store_rows_tma<LOGR>(sm, &maps.m[4 + pr], G.s0, grp << LOGR);
+      if (tid == 0) store_rows_tma<LOGR, TW>(sm, &maps.m[4 + pr], G.s0, grp << LOGR);
     }
   }
 }
@@ -542,6 +548,7 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), fused_min_blocks(LOGR,
   load_table<LOGR, NTK, kSwzTables<false>>(twi, a.dft_inv[pr]);
   if constexpr (STAGE || TWO) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  pdl_trigger_mid();
   if constexpr (TWO) tile_dif<LOGR, TW>(smx, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
   if constexpr (STAGE) {
     dif_rounds_smem<LOGR, LOGR, EM, TW>(sm, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
@@ -1054,14 +1061,14 @@ EncodeTiledFn encode_tiled_fn() {
 
 // The {S, rows} u64 tensor over base with the row-tile box {16, min(R, 256)}.
 void encode_row_map(unsigned char (&out)[128], const u64* base, unsigned long long S, unsigned long long rows,
-                    int logR) {
+                    int logR, int tw) {
   static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
   EncodeTiledFn fn = encode_tiled_fn();
   if (!fn) throw CudaError("cuTensorMapEncodeTiled: driver entry point not found");
   CUtensorMap m;
   const cuuint64_t dims[2] = {S, rows};
   const cuuint64_t strides[1] = {S * sizeof(u64)};
-  const cuuint32_t box[2] = {cuuint32_t(kTileW), cuuint32_t(std::min(1 << logR, kBoxRows))};
+  const cuuint32_t box[2] = {cuuint32_t(tw), cuuint32_t(std::min(1 << logR, kBoxRows))};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult rc = fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<u64*>(base), dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1082,11 +1089,11 @@ void launch_pass_kernel_maps(const PassArgs& a, unsigned long long ncols, int np
   if (tma) {
     const unsigned long long rows = a.G << logR;
     for (int pr = 0; pr < np; ++pr) {
-      encode_row_map(maps.m[pr], a.src[pr], a.S, rows, logR);
-      if (a.nops > 1) encode_row_map(maps.m[2 + pr], a.src_b[pr], a.S, rows, logR);
+      encode_row_map(maps.m[pr], a.src[pr], a.S, rows, logR, TW);
+      if (a.nops > 1) encode_row_map(maps.m[2 + pr], a.src_b[pr], a.S, rows, logR, TW);
       if (DMG_BULK_STORE) {
-        encode_row_map(maps.m[4 + pr], a.dst[pr], a.S, rows, logR);
-        if (a.nops > 1) encode_row_map(maps.m[6 + pr], a.dst_b[pr], a.S, rows, logR);
+        encode_row_map(maps.m[4 + pr], a.dst[pr], a.S, rows, logR, TW);
+        if (a.nops > 1) encode_row_map(maps.m[6 + pr], a.dst_b[pr], a.S, rows, logR, TW);
       }
     }
   }

@@ -23,6 +23,16 @@ constexpr int kMaxPassLog = 9;  // radix of one pass <= 512 (64 KiB tile)
 // griddepcontrol.wait is a no-op for kernels launched without the attribute;
 // DECMUL_PDL=0 disables the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// DMG_PDL_MID=1 (A/B): chain kernels signal launch_dependents once their inputs are staged, so
+// the next grid is scheduled (and parks in its wait) while this one still computes.
+#ifndef DMG_PDL_MID
+#define DMG_PDL_MID 0
+#endif
+__device__ __forceinline__ void pdl_trigger_mid() {
+#if DMG_PDL_MID
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
