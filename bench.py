@@ -329,7 +329,10 @@ def kernel_roofline(rep: list, steps: int, rmm: float, hbm_peak: float, config: 
         out.update({"bound": "hbm", "unit": "GB/s", "achieved": a_bw, "peak": hbm_peak, "frac": f_hbm,
                     "int": {"achieved": a_mm / 1e9, "peak": rmm / 1e9, "unit": "Gmodmul/s", "frac": f_int}})
     out["traffic"] = ncu_traffic(config, name)
-    out["algorithmic_per_launch"] = {"modmuls": mm / n, "hbm_bytes": by / n}
+    out["algorithmic_per_launch"] = {
+        "modmuls": mm / n, "hbm_bytes": by / n,
+        "note": "mean over the kernel's launches in a step; pass bytes = 16 B per element and prime in and out, plus "
+                "the inter-pass twiddle table where it is streamed (pass 1 of N = 3 * 2^k: one table per radix-3 row)"}
     out["all_kernels"] = kernels
     return out
 

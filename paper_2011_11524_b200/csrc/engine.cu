@@ -524,7 +524,11 @@ void Engine::passes_fwd(const PrimePlan* pl[2], int np, const u64* const src[2],
         char nm[64];
         std::snprintf(nm, sizeof nm, "k_pass_fwd<%d,%s>", P.logR, L.S > 1 ? "rows" : "cols");
         const double n = double(L.ncols) * P.R;
-        prof_mark(nm, st, a.nops * np * (n / 2 * P.logR + (L.S > 1 ? n : 0)), a.nops * np * 16 * n);
+        // algorithmic HBM bytes: the data once in, once out, plus the inter-pass twiddle table
+        // (one 16-byte pair per element; shared by the pass's groups unless pass 1 carries a
+        // table per radix-3 row; factorised tables are small)
+        const double tb = (L.S > 1 && !P.tw_lbits) ? np * 16.0 * n / (P.tw_gstride ? 1.0 : double(L.groups)) : 0.0;
+        prof_mark(nm, st, a.nops * np * (n / 2 * P.logR + (L.S > 1 ? n : 0)), a.nops * np * 16 * n + tb);
       }
     }
     ++launches_;
@@ -628,7 +632,8 @@ void Engine::passes_inv(const PrimePlan* pl[2], int np, u64* const data[2], std:
         char nm[64];
         std::snprintf(nm, sizeof nm, "k_pass_inv<%d,%s>", P.logR, L.S > 1 ? "rows" : "cols");
         const double n = double(L.ncols) * P.R;
-        prof_mark(nm, st, np * (n / 2 * P.logR + (L.S > 1 ? n : 0) + (a.has_final_scale ? n : 0)), np * 16 * n);
+        const double tb = (L.S > 1 && !P.tw_lbits) ? np * 16.0 * n / (P.tw_gstride ? 1.0 : double(L.groups)) : 0.0;
+        prof_mark(nm, st, np * (n / 2 * P.logR + (L.S > 1 ? n : 0) + (a.has_final_scale ? n : 0)), np * 16 * n + tb);
       }
     }
     ++launches_;

@@ -412,6 +412,62 @@ def test_concurrent_large_products_overlap_transfers(gpu, ref, monkeypatch):
     assert len(got) == 11
 
 
+def test_mixed_concurrent_traffic(gpu, ref):
+    """One context shared by threads doing different things at once: two threads of overlapped
+    large pinned products, two of small (coalesced) products, one of uniform batches, one of the
+    convolution hook. Every result is checked; nothing deadlocks (lock orders: upload -> output
+    slot -> context for the overlapped path, context -> queue for the coalesced one)."""
+    import threading
+
+    import torch
+
+    nbig = 9_000_000
+    bx = torch.frombuffer(bytearray(inputs.gen_digits(901, nbig)), dtype=torch.uint8).pin_memory()
+    by = torch.frombuffer(bytearray(inputs.gen_digits(902, nbig)), dtype=torch.uint8).pin_memory()
+    zbig = ref.multiply(bytes(bx.numpy()), bytes(by.numpy()))
+    want_big = (len(zbig), sha(zbig))
+    small = [(inputs.gen_digits(1000 + k, 9000 + k), inputs.gen_digits(2000 + k, 7000 + 3 * k)) for k in range(6)]
+    want_small = [ref.multiply(a, b) for a, b in small]
+    bxs = [inputs.gen_digits(3000 + k, 5000) for k in range(64)]
+    bys = [inputs.gen_digits(4000 + k, 5000) for k in range(64)]
+    want_batch = [ref.multiply(a, b) for a, b in zip(bxs, bys)]
+    p, n = P1, 3 << 10
+    cx, cy = ref.random_residues(5, n, p), ref.random_residues(6, n, p)
+    want_conv = gpu.convolve_mod_p(p, n, cx, cy)
+    fails = []
+
+    def big():
+        out = torch.empty(2 * nbig, dtype=torch.uint8).pin_memory()
+        for _ in range(4):
+            m = gpu.multiply_ptr(bx.data_ptr(), nbig, by.data_ptr(), nbig, out.data_ptr(), out.numel())
+            if (m, sha(out.numpy()[:m].tobytes())) != want_big:
+                fails.append("big")
+
+    def smalls():
+        for rep in range(12):
+            for (a, b), w in zip(small, want_small):
+                if gpu.multiply_text(a, b) != w:
+                    fails.append("small")
+
+    def batches():
+        for _ in range(6):
+            if gpu.multiply_batch(b"".join(bxs), b"".join(bys), 64, 5000, 5000) != want_batch:
+                fails.append("batch")
+
+    def hooks():
+        for _ in range(10):
+            if not np.array_equal(gpu.convolve_mod_p(p, n, cx, cy), want_conv):
+                fails.append("conv")
+
+    th = [threading.Thread(target=f) for f in (big, big, smalls, smalls, batches, hooks)]
+    for h in th:
+        h.start()
+    for h in th:
+        h.join(timeout=300)
+    assert not any(h.is_alive() for h in th), "deadlock"
+    assert not fails, fails
+
+
 def test_batch_mixed_sizes_pointer_arrays(gpu, ref):
     """decmul_gpu_multiply_batch_ptrs (the pointer-array batch of SURVEY §8(b)): repeated
     size pairs run as uniform batches, singletons one by one; results in input order."""
