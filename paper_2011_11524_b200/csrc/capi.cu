@@ -329,8 +329,13 @@ int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const cha
 
 int decmul_gpu_multiply_ex(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
                            size_t cap, size_t* out_len, const decmul_gpu_multiply_options* opt) {
-  if (int rc = 0; multiply_overlapped(ctx, x, nx, y, ny, out, cap, out_len, opt ? opt->forced_base_exp : 0,
-                                      opt ? opt->alias : 0, opt ? opt->p1 : 0, opt ? opt->p2 : 0, &rc))
+  // no options that change the plan: the same path as decmul_gpu_multiply (coalescing of
+  // concurrent small products, overlapped transfers of concurrent large ones). The C++
+  // drop-in's decmul::multiply always calls this entry point.
+  if (!opt || (!opt->forced_base_exp && !opt->p1 && !opt->p2))
+    return decmul_gpu_multiply(ctx, x, nx, y, ny, out, cap, out_len, 0, opt ? opt->alias : 0);
+  if (int rc = 0; multiply_overlapped(ctx, x, nx, y, ny, out, cap, out_len, opt->forced_base_exp, opt->alias, opt->p1,
+                                      opt->p2, &rc))
     return rc;
   LOCKED(ctx, {
     const decmul_gpu_multiply_options o = opt ? *opt : decmul_gpu_multiply_options{0, 0, 0, 0};

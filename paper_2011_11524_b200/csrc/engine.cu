@@ -152,11 +152,6 @@ Engine::~Engine() {
     if (s.ev_y) cudaEventDestroy(s.ev_y);
     if (s.h_len) cudaFreeHost(s.h_len);
   }
-  copy_pool_.reset();
-  for (int k = 0; k < kStageSlots; ++k) {
-    if (stage_[k]) cudaFreeHost(stage_[k]);
-    if (stage_ev_[k]) cudaEventDestroy(stage_ev_[k]);
-  }
   cudaStreamDestroy(stream_);
 }
 
@@ -1162,9 +1157,18 @@ void Engine::multiply_batch_host(std::size_t count, const char* xs, std::size_t 
   if (count == 0) return;
   if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
   const ProductPlan pp = plan_product(nx, ny, 0);
-  if (prime_plan(pp.p1, pp.N).small_ok && prime_plan(pp.p2, pp.N).small_ok && count >= 2 * kPipe) {
-    batch_host_pipelined(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, lens);
-    return;
+  // the chunked upload / compute / download pipeline pays from two waves of one-CTA products
+  // up; a smaller batch (e.g. a handful of coalesced concurrent calls) is one partial wave:
+  // one copy in, one launch, one copy out
+  const PrimePlan& Pb = prime_plan(pp.p1, pp.N);
+  if (Pb.small_ok && prime_plan(pp.p2, pp.N).small_ok) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_);
+    const std::size_t wave = std::size_t(sms) * std::max(1, small_resident_ctas(Pb.k, Pb.three, 0));
+    if (count >= 2 * wave) {
+      batch_host_pipelined(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, lens);
+      return;
+    }
   }
   const std::size_t xb = (count - 1) * x_stride + nx, yb = (count - 1) * y_stride + ny;
   const std::size_t ob = count * out_stride;
@@ -1283,7 +1287,7 @@ void Engine::multiply_batch_ptrs(std::size_t count, const char* const* xs, const
     if (caps[i] < nxs[i] + nys[i]) throw std::length_error("multiply: output buffer too small");
   std::map<std::pair<std::size_t, std::size_t>, std::vector<std::size_t>> groups;
   for (std::size_t i = 0; i < count; ++i) groups[{nxs[i], nys[i]}].push_back(i);
-  std::vector<char> bx, by, bo;
+  std::vector<char> vx, vy, vo;
   std::vector<std::size_t> bl;
   for (const auto& [shape, idx] : groups) {
     const auto [nx, ny] = shape;
@@ -1292,17 +1296,31 @@ void Engine::multiply_batch_ptrs(std::size_t count, const char* const* xs, const
       continue;
     }
     const std::size_t m = idx.size(), ostride = nx + ny;
-    bx.resize(m * nx);
-    by.resize(m * ny);
-    bo.resize(m * ostride);
+    // the group's operands gathered into one buffer each -- pinned while the group is small
+    // (coalesced concurrent calls: a few products), so the batch moves by DMA in three copies
+    // instead of the driver's staged pageable path
+    char *bx, *by, *bo;
+    if (2 * m * ostride <= kGatherMax) {
+      gather_.ensure(2 * m * ostride);
+      bx = gather_.ptr;
+      by = bx + m * nx;
+      bo = bx + m * ostride;
+    } else {
+      vx.resize(m * nx);
+      vy.resize(m * ny);
+      vo.resize(m * ostride);
+      bx = vx.data();
+      by = vy.data();
+      bo = vo.data();
+    }
     bl.resize(m);
     for (std::size_t j = 0; j < m; ++j) {
-      std::memcpy(&bx[j * nx], xs[idx[j]], nx);
-      std::memcpy(&by[j * ny], ys[idx[j]], ny);
+      std::memcpy(bx + j * nx, xs[idx[j]], nx);
+      std::memcpy(by + j * ny, ys[idx[j]], ny);
     }
-    multiply_batch_host(m, bx.data(), nx, nx, by.data(), ny, ny, bo.data(), ostride, bl.data());
+    multiply_batch_host(m, bx, nx, nx, by, ny, ny, bo, ostride, bl.data());
     for (std::size_t j = 0; j < m; ++j) {
-      std::memcpy(outs[idx[j]], &bo[j * ostride], bl[j]);
+      std::memcpy(outs[idx[j]], bo + j * ostride, bl[j]);
       lens[idx[j]] = bl[j];
     }
   }

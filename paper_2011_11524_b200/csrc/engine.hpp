@@ -27,6 +27,19 @@ struct CorruptionError : std::runtime_error {
 
 void cuda_check(cudaError_t e, const char* what);
 
+// Pinned host scratch that only grows.
+struct PinnedBuf {
+  char* ptr = nullptr;
+  size_t n = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  ~PinnedBuf() {
+    if (ptr) cudaFreeHost(ptr);
+  }
+  void ensure(size_t count);
+};
+
 template <class T>
 struct DevBuf {
   T* ptr = nullptr;
@@ -160,6 +173,21 @@ class CopyPool {
   unsigned long long gen_ = 0;
   int pending_ = 0;
   bool stop_ = false;
+};
+
+// A ring of pinned staging slots with its own copy threads: large pageable host buffers are
+// moved slot by slot, the host threads filling (or draining) one slot while the DMA engine
+// moves another (hostio.cu). Pinned buffers and small ones go straight to cudaMemcpyAsync.
+struct StageRing {
+  static constexpr int kSlots = 4;
+  static constexpr std::size_t kSlot = std::size_t(16) << 20;
+  char* slot[kSlots] = {};
+  cudaEvent_t ev[kSlots] = {};
+  std::unique_ptr<CopyPool> pool;
+  ~StageRing();
+  void ensure();
+  void h2d(void* dst, const void* src, std::size_t n, cudaStream_t st);  // asynchronous for pinned src
+  void d2h(void* dst, const void* src, std::size_t n, cudaStream_t st);  // returns with dst complete
 };
 
 // One rank's device buffers of a sharded product driven inside the library (multi.cu).
@@ -303,7 +331,6 @@ class Engine {
   // the data.
   void stage_h2d(void* dst, const void* src, std::size_t n, cudaStream_t st);
   void stage_d2h(void* dst, const void* src, std::size_t n, cudaStream_t st);
-  void ensure_staging();
   void transform_forward(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2],
                          bool include_last, cudaStream_t st);
   void transform_forward_packed(const PrimePlan* pl[2], u64* const data[2], bool include_last, cudaStream_t st);
@@ -344,11 +371,10 @@ class Engine {
   cudaEvent_t up_ev_[kMaxChunks] = {}, done_ev_[kMaxChunks] = {};
   unsigned long long* host_lens_ = nullptr;  // pinned
   std::size_t host_lens_n_ = 0;
-  static constexpr int kStageSlots = 4;
-  static constexpr std::size_t kStageSlot = std::size_t(16) << 20;
-  char* stage_[kStageSlots] = {};
-  cudaEvent_t stage_ev_[kStageSlots] = {};
-  std::unique_ptr<CopyPool> copy_pool_;
+  static constexpr std::size_t kGatherMax = std::size_t(64) << 20;
+  PinnedBuf gather_;                // multiply_batch_ptrs: operands / products of a small group
+  StageRing ring_;                  // the locked host path (under the context lock)
+  StageRing ov_up_ring_;            // the overlapped path's upload stage (under ov_up_mu_)
   std::mutex mu_;
   std::map<std::pair<u64, std::size_t>, std::unique_ptr<PrimePlan>> plans_;
   DevBuf<u64> X_[2], Y_[2], Px_, Py_, S_, S2_;
@@ -365,6 +391,7 @@ class Engine {
     cudaStream_t dl_stream = nullptr;
     cudaEvent_t ev_x = nullptr, ev_y = nullptr;
     unsigned long long* h_len = nullptr;  // pinned: the product length, read back without blocking
+    StageRing dl_ring;  // pageable outputs: the two slots' downloads may run at the same time
   };
   OvSlot ov_[2];
   std::mutex ov_up_mu_;

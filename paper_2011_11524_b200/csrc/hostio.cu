@@ -100,7 +100,7 @@ bool Engine::overlap_ok(const char* x, std::size_t nx, const char* y, std::size_
   if (nx == 0 || ny == 0 || !x || !y || !out) return false;
   const std::size_t n = nx + ny;
   if (n < kOverlapMin || n > kOverlapMax) return false;
-  return is_pinned(x) && is_pinned(y) && is_pinned(out);
+  return true;  // pinned buffers go straight to DMA, pageable ones through the stage's own ring
 }
 
 std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, std::size_t nx, const char* y,
@@ -134,7 +134,7 @@ std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, 
   // after it could take the context lock, and that one released ov_up_mu_ only later
   s.dx.ensure(nx);
   if (!squaring) s.dy.ensure(ny);
-  cuda_check(cudaMemcpyAsync(s.dx.ptr, x, nx, cudaMemcpyHostToDevice, ov_up_stream_), "h2d");
+  ov_up_ring_.h2d(s.dx.ptr, x, nx, ov_up_stream_);
   cuda_check(cudaEventRecord(s.ev_x, ov_up_stream_), "event");
   // the slot's output buffer: wait out the download of the product that used it last
   std::unique_lock<std::mutex> dl(s.dl_mu);
@@ -147,7 +147,7 @@ std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, 
   cuda_check(cudaStreamWaitEvent(st, s.ev_x, 0), "wait");
   run_product(pp, s.dx.ptr, squaring ? s.dx.ptr : s.dy.ptr, squaring, s.dout.ptr, st, err_.ptr, [&] {
     if (squaring) return;
-    cuda_check(cudaMemcpyAsync(s.dy.ptr, y, ny, cudaMemcpyHostToDevice, ov_up_stream_), "h2d");
+    ov_up_ring_.h2d(s.dy.ptr, y, ny, ov_up_stream_);
     cuda_check(cudaEventRecord(s.ev_y, ov_up_stream_), "event");
     cuda_check(cudaStreamWaitEvent(st, s.ev_y, 0), "wait");
   });
@@ -164,8 +164,7 @@ std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, 
   if (len > cap) throw std::length_error("multiply: output buffer too small");
   comp.unlock();
   // stage 3, download, outside the context lock
-  cuda_check(cudaMemcpyAsync(out, s.dout.ptr, std::size_t(len), cudaMemcpyDeviceToHost, s.dl_stream), "d2h");
-  cuda_check(cudaStreamSynchronize(s.dl_stream), "sync");
+  s.dl_ring.d2h(out, s.dout.ptr, std::size_t(len), s.dl_stream);
   if (trace)
     std::fprintf(stderr,
                  "overlap slot %d: up lock %.1f, out slot %.1f, ctx lock %.1f, enqueued %.1f, uploads done %.1f, "
@@ -174,60 +173,81 @@ std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, 
   return std::size_t(len);
 }
 
-void Engine::ensure_staging() {
-  if (stage_[0]) return;
-  for (int s = 0; s < kStageSlots; ++s) {
-    cuda_check(cudaMallocHost(&stage_[s], kStageSlot), "cudaMallocHost");
-    cuda_check(cudaEventCreateWithFlags(&stage_ev_[s], cudaEventDisableTiming), "cudaEventCreate");
+void PinnedBuf::ensure(size_t count) {
+  if (count <= n) return;
+  if (ptr) cudaFreeHost(ptr);
+  ptr = nullptr;
+  n = 0;
+  const size_t want = std::max<size_t>(count + count / 2, size_t(1) << 20);
+  cuda_check(cudaMallocHost(&ptr, want), "cudaMallocHost");
+  n = want;
+}
+
+StageRing::~StageRing() {
+  pool.reset();
+  for (int k = 0; k < kSlots; ++k) {
+    if (slot[k]) cudaFreeHost(slot[k]);
+    if (ev[k]) cudaEventDestroy(ev[k]);
+  }
+}
+
+void StageRing::ensure() {
+  if (slot[0]) return;
+  for (int k = 0; k < kSlots; ++k) {
+    cuda_check(cudaMallocHost(&slot[k], kSlot), "cudaMallocHost");
+    cuda_check(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming), "cudaEventCreate");
   }
   int threads = 4;
   if (const char* e = std::getenv("DECMUL_COPY_THREADS")) threads = std::max(0, std::atoi(e));
   threads = std::min<int>(threads, std::max(1u, std::thread::hardware_concurrency()) - 1);
-  copy_pool_ = std::make_unique<CopyPool>(std::max(0, threads));
+  pool = std::make_unique<CopyPool>(std::max(0, threads));
 }
 
-void Engine::stage_h2d(void* dst, const void* src, std::size_t n, cudaStream_t st) {
+void StageRing::h2d(void* dst, const void* src, std::size_t n, cudaStream_t st) {
   if (n < kStageMin || is_pinned(src)) {
     cuda_check(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st), "h2d");
     return;
   }
-  ensure_staging();
+  ensure();
   char* d = static_cast<char*>(dst);
   const char* s = static_cast<const char*>(src);
-  for (std::size_t off = 0, c = 0; off < n; off += kStageSlot, ++c) {
-    const int k = int(c % kStageSlots);
-    const std::size_t len = std::min(kStageSlot, n - off);
-    cuda_check(cudaEventSynchronize(stage_ev_[k]), "stage wait");  // the slot's previous DMA is done
-    copy_pool_->copy(stage_[k], s + off, len);
-    cuda_check(cudaMemcpyAsync(d + off, stage_[k], len, cudaMemcpyHostToDevice, st), "h2d");
-    cuda_check(cudaEventRecord(stage_ev_[k], st), "event");
+  for (std::size_t off = 0, c = 0; off < n; off += kSlot, ++c) {
+    const int k = int(c % kSlots);
+    const std::size_t len = std::min(kSlot, n - off);
+    cuda_check(cudaEventSynchronize(ev[k]), "stage wait");  // the slot's previous DMA is done
+    pool->copy(slot[k], s + off, len);
+    cuda_check(cudaMemcpyAsync(d + off, slot[k], len, cudaMemcpyHostToDevice, st), "h2d");
+    cuda_check(cudaEventRecord(ev[k], st), "event");
   }
 }
 
-void Engine::stage_d2h(void* dst, const void* src, std::size_t n, cudaStream_t st) {
+void StageRing::d2h(void* dst, const void* src, std::size_t n, cudaStream_t st) {
   if (n < kStageMin || is_pinned(dst)) {
     cuda_check(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, st), "d2h");
     cuda_check(cudaStreamSynchronize(st), "sync");
     return;
   }
-  ensure_staging();
+  ensure();
   char* d = static_cast<char*>(dst);
   const char* s = static_cast<const char*>(src);
-  const std::size_t nch = (n + kStageSlot - 1) / kStageSlot;
-  auto len = [&](std::size_t c) { return std::min(kStageSlot, n - c * kStageSlot); };
+  const std::size_t nch = (n + kSlot - 1) / kSlot;
+  auto len = [&](std::size_t c) { return std::min(kSlot, n - c * kSlot); };
   auto issue = [&](std::size_t c) {
-    const int k = int(c % kStageSlots);
-    cuda_check(cudaMemcpyAsync(stage_[k], s + c * kStageSlot, len(c), cudaMemcpyDeviceToHost, st), "d2h");
-    cuda_check(cudaEventRecord(stage_ev_[k], st), "event");
+    const int k = int(c % kSlots);
+    cuda_check(cudaMemcpyAsync(slot[k], s + c * kSlot, len(c), cudaMemcpyDeviceToHost, st), "d2h");
+    cuda_check(cudaEventRecord(ev[k], st), "event");
   };
   std::size_t issued = 0;
-  for (; issued < std::min<std::size_t>(kStageSlots, nch); ++issued) issue(issued);
+  for (; issued < std::min<std::size_t>(kSlots, nch); ++issued) issue(issued);
   for (std::size_t c = 0; c < nch; ++c) {
-    const int k = int(c % kStageSlots);
-    cuda_check(cudaEventSynchronize(stage_ev_[k]), "stage wait");
-    copy_pool_->copy(d + c * kStageSlot, stage_[k], len(c));
+    const int k = int(c % kSlots);
+    cuda_check(cudaEventSynchronize(ev[k]), "stage wait");
+    pool->copy(d + c * kSlot, slot[k], len(c));
     if (issued < nch) issue(issued++);  // refills slot k, whose data has just been copied out
   }
 }
+
+void Engine::stage_h2d(void* dst, const void* src, std::size_t n, cudaStream_t st) { ring_.h2d(dst, src, n, st); }
+void Engine::stage_d2h(void* dst, const void* src, std::size_t n, cudaStream_t st) { ring_.d2h(dst, src, n, st); }
 
 }  // namespace dmg

@@ -414,8 +414,8 @@ def test_concurrent_large_products_overlap_transfers(gpu, ref, monkeypatch):
 
 def test_mixed_concurrent_traffic(gpu, ref):
     """One context shared by threads doing different things at once: two threads of overlapped
-    large pinned products, two of small (coalesced) products, one of uniform batches, one of the
-    convolution hook. Every result is checked; nothing deadlocks (lock orders: upload -> output
+    large pinned products, two of large pageable ones, two of small (coalesced) products, one of
+    uniform batches, one of the convolution hook. Every result is checked; nothing deadlocks (lock orders: upload -> output
     slot -> context for the overlapped path, context -> queue for the coalesced one)."""
     import threading
 
@@ -443,6 +443,13 @@ def test_mixed_concurrent_traffic(gpu, ref):
             if (m, sha(out.numpy()[:m].tobytes())) != want_big:
                 fails.append("big")
 
+    xb, yb = bytes(bx.numpy()), bytes(by.numpy())
+
+    def big_pageable():  # pageable operands: the overlapped path's own staging rings
+        for _ in range(3):
+            if gpu.multiply_text(xb, yb) != zbig:
+                fails.append("big pageable")
+
     def smalls():
         for rep in range(12):
             for (a, b), w in zip(small, want_small):
@@ -459,7 +466,7 @@ def test_mixed_concurrent_traffic(gpu, ref):
             if not np.array_equal(gpu.convolve_mod_p(p, n, cx, cy), want_conv):
                 fails.append("conv")
 
-    th = [threading.Thread(target=f) for f in (big, big, smalls, smalls, batches, hooks)]
+    th = [threading.Thread(target=f) for f in (big, big, big_pageable, big_pageable, smalls, smalls, batches, hooks)]
     for h in th:
         h.start()
     for h in th:
