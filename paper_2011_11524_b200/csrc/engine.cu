@@ -1067,11 +1067,21 @@ std::size_t Engine::multiply_host(const char* x, std::size_t nx, const char* y, 
     cuda_check(cudaEventRecord(up_ev_[1], cs), "event");
     cuda_check(cudaStreamWaitEvent(st, up_ev_[1], 0), "wait");
   });
-  unsigned long long len = 0;
-  cuda_check(cudaMemcpyAsync(&len, meta_.ptr + 2, sizeof len, cudaMemcpyDeviceToHost, st), "len");
+  // The length comes back through pinned memory and, when the output goes straight to DMA
+  // (pinned or small), the product's nx + ny bytes are copied behind it before the error word
+  // is read: one synchronisation instead of three (a product is nx + ny or nx + ny - 1 digits
+  // long; cap >= nx + ny was checked above).
+  if (host_lens_n_ < 1) {
+    cuda_check(cudaMallocHost(&host_lens_, 1024 * sizeof(unsigned long long)), "cudaMallocHost");
+    host_lens_n_ = 1024;
+  }
+  cuda_check(cudaMemcpyAsync(host_lens_, meta_.ptr + 2, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "len");
+  const bool direct = stage_direct(out, nx + ny);
+  if (direct) cuda_check(cudaMemcpyAsync(out, dout_.ptr, nx + ny, cudaMemcpyDeviceToHost, st), "d2h");
   check_err(st);
+  const unsigned long long len = host_lens_[0];
   if (len > cap) throw std::length_error("multiply: output buffer too small");
-  stage_d2h(out, dout_.ptr, std::size_t(len), st);
+  if (!direct) stage_d2h(out, dout_.ptr, std::size_t(len), st);
   return std::size_t(len);
 }
 
@@ -1180,12 +1190,21 @@ void Engine::multiply_batch_host(std::size_t count, const char* xs, std::size_t 
   cuda_check(cudaMemcpyAsync(din_y_.ptr, ys, yb, cudaMemcpyHostToDevice, stream_), "h2d");
   batch_device(count, din_x_.ptr, x_stride, nx, din_y_.ptr, y_stride, ny, dout_.ptr, out_stride, lens_.ptr,
                stream_, err_.ptr);
-  std::vector<unsigned long long> l(count);
-  cuda_check(cudaMemcpyAsync(l.data(), lens_.ptr, count * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream_),
-             "d2h");
+  // lengths into pinned memory: a pageable destination would block here until the kernel is done,
+  // and the product copy behind it
+  if (host_lens_n_ < count) {
+    if (host_lens_) cudaFreeHost(host_lens_);
+    host_lens_ = nullptr;
+    host_lens_n_ = 0;
+    const std::size_t want = std::max<std::size_t>(count, 1024);
+    cuda_check(cudaMallocHost(&host_lens_, want * sizeof(unsigned long long)), "cudaMallocHost");
+    host_lens_n_ = want;
+  }
+  cuda_check(cudaMemcpyAsync(host_lens_, lens_.ptr, count * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             stream_), "d2h");
   cuda_check(cudaMemcpyAsync(outs, dout_.ptr, ob, cudaMemcpyDeviceToHost, stream_), "d2h");
   check_err(stream_);
-  for (std::size_t i = 0; i < count; ++i) lens[i] = std::size_t(l[i]);
+  for (std::size_t i = 0; i < count; ++i) lens[i] = std::size_t(host_lens_[i]);
 }
 
 // Chunks of products flow through three streams — upload, compute, download — linked by
@@ -1291,7 +1310,21 @@ void Engine::multiply_batch_ptrs(std::size_t count, const char* const* xs, const
   std::vector<std::size_t> bl;
   for (const auto& [shape, idx] : groups) {
     const auto [nx, ny] = shape;
-    if (idx.size() < 2 || nx == 0 || ny == 0) {  // singletons (and empty operands: the error path)
+    // singletons go one by one unless they are one-CTA products (then the gathered pinned
+    // path below is the cheaper one: three DMA copies and one launch); so do empty and zero
+    // operands (the error path and the zero short-circuit)
+    bool single = nx == 0 || ny == 0;
+    if (!single && idx.size() < 2) {
+      single = true;
+      if (!(nx == 1 && xs[idx[0]][0] == '0') && !(ny == 1 && ys[idx[0]][0] == '0')) {
+        try {
+          const ProductPlan pp = plan_product(nx, ny, 0);
+          single = !(prime_plan(pp.p1, pp.N).small_ok && prime_plan(pp.p2, pp.N).small_ok);
+        } catch (const std::exception&) {
+        }
+      }
+    }
+    if (single) {
       for (std::size_t i : idx) lens[i] = multiply_host(xs[i], nx, ys[i], ny, outs[i], caps[i], 0, false);
       continue;
     }

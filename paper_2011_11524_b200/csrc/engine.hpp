@@ -330,6 +330,7 @@ class Engine {
   // source may be reused (copies stream-ordered on st); stage_d2h returns when dst holds
   // the data.
   void stage_h2d(void* dst, const void* src, std::size_t n, cudaStream_t st);
+  bool stage_direct(const void* host, std::size_t n) const;  // no staging ring: pinned or small
   void stage_d2h(void* dst, const void* src, std::size_t n, cudaStream_t st);
   void transform_forward(const PrimePlan* pl[2], int np, const u64* const src[2], u64* const dst[2],
                          bool include_last, cudaStream_t st);
