@@ -1,4 +1,5 @@
 // extern "C" implementation of include/decmul_gpu.h over dmg::Engine.
+#include <atomic>
 #include <condition_variable>
 #include <cstring>
 #include <memory>
@@ -39,6 +40,7 @@ struct decmul_gpu_ctx {
   std::vector<CoalescedReq*> queue;
   bool leader = false;
   unsigned long long coalesced_batches = 0, coalesced_products = 0;
+  std::atomic<int> large_active{0};  // large host products inside decmul_gpu_multiply[_ex] right now
 };
 
 namespace {
@@ -278,17 +280,33 @@ int multiply_coalesced(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char
   return req.rc;
 }
 
+// Counts the large host products in flight on a context (Engine::overlap_ok's `concurrent`).
+struct LargeCall {
+  std::atomic<int>* c = nullptr;
+  int before = 0;
+  LargeCall(decmul_gpu_ctx* ctx, size_t nx, size_t ny) {
+    if (ctx && nx + ny >= (size_t(1) << 24)) {
+      c = &ctx->large_active;
+      before = c->fetch_add(1);
+    }
+  }
+  ~LargeCall() {
+    if (c) c->fetch_sub(1);
+  }
+};
+
 // Large products from pinned buffers: the engine takes the context lock only around the
 // compute stage, so concurrent callers overlap one product's download with the next one's
 // upload and compute (Engine::multiply_host_overlapped). Returns false when the call does
 // not qualify (the caller then runs the ordinary locked path).
 bool multiply_overlapped(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char* y, size_t ny, char* out,
-                         size_t cap, size_t* out_len, unsigned forced, int alias, uint64_t p1, uint64_t p2, int* rc) {
+                         size_t cap, size_t* out_len, unsigned forced, int alias, uint64_t p1, uint64_t p2,
+                         bool concurrent, int* rc) {
   if (!ctx || !out_len) return false;
   DeviceGuard dev_(ctx->eng->device());
   dmg::Engine* e = nullptr;
   std::string msg;
-  if (guarded_msg(msg, [&] { e = ctx->multi->overlap_engine(x, nx, y, ny, out, forced, p1, p2); }) || !e)
+  if (guarded_msg(msg, [&] { e = ctx->multi->overlap_engine(x, nx, y, ny, out, forced, concurrent, p1, p2); }) || !e)
     return false;
   *rc = guarded_msg(msg, [&] {
     *out_len = e->multiply_host_overlapped(ctx->mu, x, nx, y, ny, out, cap, forced, alias != 0, p1, p2);
@@ -308,7 +326,9 @@ int decmul_gpu_multiply(decmul_gpu_ctx* ctx, const char* x, size_t nx, const cha
     bool valid = cap >= nx + ny && x[0] != '0' && y[0] != '0';
     if (valid) return multiply_coalesced(ctx, x, nx, y, ny, out, cap, out_len);
   }
-  if (int rc = 0; multiply_overlapped(ctx, x, nx, y, ny, out, cap, out_len, forced, alias, 0, 0, &rc)) return rc;
+  LargeCall large(ctx, nx, ny);
+  if (int rc = 0; multiply_overlapped(ctx, x, nx, y, ny, out, cap, out_len, forced, alias, 0, 0, large.before > 0, &rc))
+    return rc;
   LOCKED(ctx, {
     if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
     const bool xz = nx == 1 && x[0] == '0', yz = ny == 1 && y[0] == '0';
@@ -334,8 +354,9 @@ int decmul_gpu_multiply_ex(decmul_gpu_ctx* ctx, const char* x, size_t nx, const 
   // drop-in's decmul::multiply always calls this entry point.
   if (!opt || (!opt->forced_base_exp && !opt->p1 && !opt->p2))
     return decmul_gpu_multiply(ctx, x, nx, y, ny, out, cap, out_len, 0, opt ? opt->alias : 0);
+  LargeCall large(ctx, nx, ny);
   if (int rc = 0; multiply_overlapped(ctx, x, nx, y, ny, out, cap, out_len, opt->forced_base_exp, opt->alias, opt->p1,
-                                      opt->p2, &rc))
+                                      opt->p2, large.before > 0, &rc))
     return rc;
   LOCKED(ctx, {
     const decmul_gpu_multiply_options o = opt ? *opt : decmul_gpu_multiply_options{0, 0, 0, 0};

@@ -216,7 +216,9 @@ class Engine {
   // the context lock; uploads, compute (under ctx_mu) and the download are separate stages over
   // two buffer slots, so one call's download overlaps the next call's upload and compute and the
   // next upload starts while this product still computes (PCIe is full duplex; hostio.cu).
-  bool overlap_ok(const char* x, std::size_t nx, const char* y, std::size_t ny, const char* out) const;
+  // concurrent: another large host product is in flight on the context
+  bool overlap_ok(const char* x, std::size_t nx, const char* y, std::size_t ny, const char* out,
+                  bool concurrent) const;
   std::size_t multiply_host_overlapped(std::mutex& ctx_mu, const char* x, std::size_t nx, const char* y,
                                        std::size_t ny, char* out, std::size_t cap, unsigned forced_base_exp,
                                        bool alias, u64 p1 = 0, u64 p2 = 0);

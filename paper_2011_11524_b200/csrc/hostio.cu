@@ -94,13 +94,17 @@ constexpr std::size_t kStageMin = std::size_t(4) << 20;  // below this the drive
 constexpr std::size_t kOverlapMin = std::size_t(1) << 24;
 constexpr std::size_t kOverlapMax = std::size_t(4) << 30;
 
-bool Engine::overlap_ok(const char* x, std::size_t nx, const char* y, std::size_t ny, const char* out) const {
+bool Engine::overlap_ok(const char* x, std::size_t nx, const char* y, std::size_t ny, const char* out,
+                        bool concurrent) const {
   if (const char* e = std::getenv("DECMUL_OVERLAP"))
     if (e[0] == '0') return false;
   if (nx == 0 || ny == 0 || !x || !y || !out) return false;
   const std::size_t n = nx + ny;
   if (n < kOverlapMin || n > kOverlapMax) return false;
-  return true;  // pinned buffers go straight to DMA, pageable ones through the stage's own ring
+  // pinned buffers go straight to DMA. Pageable ones move through the stages' own staging rings
+  // (192 MB of pinned memory, ~45 ms to set up), so they take this path only while another
+  // large call is in flight on the context; a lone caller keeps the locked path and its one ring.
+  return concurrent || (is_pinned(x) && is_pinned(y) && is_pinned(out));
 }
 
 std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, std::size_t nx, const char* y,

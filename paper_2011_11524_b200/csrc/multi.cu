@@ -134,9 +134,9 @@ std::size_t MultiEngine::multiply_host(const char* x, std::size_t nx, const char
 }
 
 Engine* MultiEngine::overlap_engine(const char* x, std::size_t nx, const char* y, std::size_t ny, const char* out,
-                                    unsigned forced, u64 p1, u64 p2) {
+                                    unsigned forced, bool concurrent, u64 p1, u64 p2) {
   Engine& e = *eng_[0];
-  if (!e.overlap_ok(x, nx, y, ny, out)) return nullptr;
+  if (!e.overlap_ok(x, nx, y, ny, out, concurrent)) return nullptr;
   if ((nx == 1 && x[0] == '0') || (ny == 1 && y[0] == '0')) return nullptr;
   if (!p1 && !p2 && (block_digits(nx, ny, forced) || shards(nx, ny, forced))) return nullptr;
   return &e;

@@ -29,7 +29,7 @@ class MultiEngine {
   // (Engine::overlap_ok: large, pinned buffers; not sharded, not block-convolved), else nullptr.
   // Its multiply_host_overlapped is called WITHOUT the context lock held.
   Engine* overlap_engine(const char* x, std::size_t nx, const char* y, std::size_t ny, const char* out,
-                         unsigned forced_base_exp, u64 p1 = 0, u64 p2 = 0);
+                         unsigned forced_base_exp, bool concurrent, u64 p1 = 0, u64 p2 = 0);
   // batches: contiguous ranges of products per device, one host thread per device
   void multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
                            const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
