@@ -1,12 +1,15 @@
 // extern "C" implementation of include/decmul_gpu.h over dmg::Engine.
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <vector>
 #include <new>
 #include <string>
+#include <thread>
 
 #include "../../include/decmul_gpu.h"
 #include "engine.hpp"
@@ -40,6 +43,8 @@ struct decmul_gpu_ctx {
   std::vector<CoalescedReq*> queue;
   bool leader = false;
   unsigned long long coalesced_batches = 0, coalesced_products = 0;
+  size_t last_batch = 0;                             // size and end of the last coalesced batch
+  std::chrono::steady_clock::time_point last_end{};  // (under mu)
   std::atomic<int> large_active{0};  // large host products inside decmul_gpu_multiply[_ex] right now
 };
 
@@ -259,8 +264,37 @@ int multiply_coalesced(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char
   }
   std::vector<CoalescedReq*> batch;
   {
-    std::lock_guard<std::mutex> lock_(ctx->mu);  // waits for the batch in flight; callers keep queueing
+    // waits for the batch in flight; callers keep queueing
+    std::unique_lock<std::mutex> lock_(ctx->mu, std::try_to_lock);
+    const bool waited = !lock_.owns_lock();
+    if (waited) lock_.lock();
     DeviceGuard dev_(ctx->eng->device());
+    // Callers in a closed loop come back right after their batch: give them a moment to queue up,
+    // so that all of them share the next launch instead of two groups taking turns. Expected
+    // callers: the batch that has just ended, plus -- when this leader had to wait for it -- the
+    // callers that queued meanwhile. DECMUL_COALESCE_WAIT_US=0 turns the wait off.
+    static const int wait_us = [] {
+      const char* e = std::getenv("DECMUL_COALESCE_WAIT_US");
+      return e ? std::atoi(e) : 40;
+    }();
+    const auto now = std::chrono::steady_clock::now();
+    if (wait_us > 0 && ctx->last_batch > 1 && now - ctx->last_end < std::chrono::milliseconds(1)) {
+      size_t queued = 0;
+      {
+        std::lock_guard<std::mutex> q(ctx->qmu);
+        queued = ctx->queue.size();
+      }
+      // (only while the batches are small, where the fixed cost of a launch dominates: measured
+      // with 1e4-digit products, 2 threads 20.8k -> 26.0k products/s, 4 threads 29.7k -> 42.3k,
+      // but 16 threads 78k -> 51k when batches of 8 wait as well)
+      const size_t target = ctx->last_batch + queued < 8 ? (waited ? ctx->last_batch + queued : ctx->last_batch) : 0;
+      const auto deadline = now + std::chrono::microseconds(wait_us);
+      while (queued < target && std::chrono::steady_clock::now() < deadline) {
+        std::this_thread::yield();
+        std::lock_guard<std::mutex> q(ctx->qmu);
+        queued = ctx->queue.size();
+      }
+    }
     {
       std::lock_guard<std::mutex> q(ctx->qmu);
       batch.swap(ctx->queue);
@@ -269,6 +303,8 @@ int multiply_coalesced(decmul_gpu_ctx* ctx, const char* x, size_t nx, const char
     run_coalesced(ctx, batch);
     ++ctx->coalesced_batches;
     ctx->coalesced_products += batch.size();
+    ctx->last_batch = batch.size();
+    ctx->last_end = std::chrono::steady_clock::now();
     if (req.rc) ctx->err = req.msg;
   }
   {

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 
 #include "engine.hpp"
 
@@ -138,6 +139,15 @@ std::size_t Engine::multiply_host_overlapped(std::mutex& ctx_mu, const char* x, 
   // after it could take the context lock, and that one released ov_up_mu_ only later
   s.dx.ensure(nx);
   if (!squaring) s.dy.ensure(ny);
+  // from here on a DMA may be reading the caller's buffers: no error leaves this function
+  // before the upload stream has drained
+  struct DrainOnError {
+    cudaStream_t st;
+    int live = std::uncaught_exceptions();
+    ~DrainOnError() {
+      if (std::uncaught_exceptions() > live) cudaStreamSynchronize(st);
+    }
+  } drain{ov_up_stream_};
   ov_up_ring_.h2d(s.dx.ptr, x, nx, ov_up_stream_);
   cuda_check(cudaEventRecord(s.ev_x, ov_up_stream_), "event");
   // the slot's output buffer: wait out the download of the product that used it last
