@@ -241,6 +241,22 @@ def test_forced_six_step_threshold_orders(gpu, port):
                 assert np.array_equal(gpu.inverse_transform(p, port.forward_transform(p, x, thr), thr), x)
 
 
+def test_tma_tile_shapes_single_prime_and_paired_operands(gpu, port, ref):
+    """Full-width row tiles moved by TMA in the launches the other tests do not reach: one prime
+    per launch (the convolution hook at N = 2^21 and 3 * 2^20, maps of prime 0 only) and both
+    operands in one launch (products with N = 2^21 and 3 * 2^19: maps of the second operand)."""
+    for p, n in ((P1, 1 << 21), (dm.Q1, 3 << 20)):
+        x = port.gen_residues(n + 1, n, p)
+        y = port.gen_residues(n + 2, n - 5, p)
+        assert np.array_equal(gpu.convolve_mod_p(p, n, x, y), port.convolve_mod_p(p, n, x, y)), (p, n)
+        assert np.array_equal(gpu.inverse_transform(p, gpu.forward_transform(p, x)), x), (p, n)
+    for (nx, ny), length in (((16_000_000, 15_000_000), 1 << 21), ((12_000_000, 9_000_001), 3 << 19)):
+        x, y = inputs.gen_digits(71, nx), inputs.gen_digits(72, ny)
+        assert gpu.plan(nx, ny)["length"] == length
+        z, want = gpu.multiply_text(x, y), ref.multiply(x, y)
+        assert len(z) == len(want) and sha(z) == sha(want), (nx, ny)
+
+
 def test_convolution_hook_shorter_inputs_and_squaring(gpu, port):
     for p in (P1, P2, dm.Q1, dm.Q2):
         for n in (6, 64, 1536, 1 << 14, 3 << 13):
