@@ -81,3 +81,29 @@ def test_multi_context_batch_fan_out(multi, golden):
     single = dm.Context(0)
     assert ctx.multiply_batch_mixed(mixed_x, mixed_y) == single.multiply_batch_mixed(mixed_x, mixed_y)
     single.close()
+
+
+def test_block_convolution_fallback(multi, ref, monkeypatch):
+    """Products past the largest transform run as a block convolution (csrc/blocked.cu; SURVEY §7
+    D1; the reference throws OperandTooLarge, decimal.cpp:94-96). DECMUL_BLOCK_DIGITS forces it
+    at small sizes: ragged last blocks, all-zero blocks, blocks with inner leading zeros,
+    squaring by equal text, one block against many, on a one-engine and a two-engine context;
+    operands are validated as a whole with the reference's messages."""
+    one = dm.Context(0)
+    x = bytearray(inputs.gen_digits(91, 25_013))
+    y = bytearray(inputs.gen_digits(92, 9_001))
+    x[5_000:12_500] = b"0" * 7_500      # whole zero blocks and leading zeros inside blocks
+    y[1:3_000] = b"0" * 2_999
+    x, y = bytes(x), bytes(y)
+    cases = [(x, y), (y, x), (x, x), (x, b"7"), (b"9" * 10_000, b"9" * 10_000), (x, inputs.gen_digits(93, 2_999))]
+    for K in ("3000", "4096", "10007"):
+        monkeypatch.setenv("DECMUL_BLOCK_DIGITS", K)
+        for ctx in (one, multi[2]):
+            for a, b in cases:
+                assert ctx.multiply_text(a, b) == ref.multiply(a, b), (K, len(a), len(b))
+            assert ctx.multiply_text(x, b"0") == b"0"
+            with pytest.raises(ValueError, match="non-digit"):
+                ctx.multiply_text(x[:20_000] + b"x" + x[20_001:], y)
+            with pytest.raises(ValueError, match="leading zero"):
+                ctx.multiply_text(b"0" + x, y)
+    one.close()
