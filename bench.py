@@ -644,9 +644,15 @@ def run_ours(args, cfg, rank, world, local_rank):
     # (The reference arm's steps are concurrent multiply() calls too.)
     single_ms = None
     T = 1
-    if count == 1 and (1 << 24) <= nx + ny <= (4 << 30) and os.environ.get("DECMUL_OVERLAP", "1") != "0":
+    overlap_on = os.environ.get("DECMUL_OVERLAP", "1") != "0"
+    if count == 1 and (1 << 24) <= nx + ny <= (4 << 30) and overlap_on:
+        T = max(1, min(args.e2e_threads, args.steps))
+    elif count > 1 and overlap_on and not dist:
+        # batches of one-CTA products: concurrent calls overlap one batch's pipeline drain with
+        # the next one's fill (Engine::batch_host_pipelined)
         T = max(1, min(args.e2e_threads, args.steps))
     if T > 1:
+        import ctypes as C
         import threading
         t0 = time.perf_counter()
         call()
@@ -654,13 +660,13 @@ def run_ours(args, cfg, rank, world, local_rank):
         bufs = [(hx, hy, ho)]
         try:
             for _ in range(T - 1):
-                bx = torch.empty(nx, dtype=torch.uint8, pin_memory=True)
+                bx = torch.empty(hx.numel(), dtype=torch.uint8, pin_memory=True)
                 bx.copy_(hx)
                 by = None
-                if not squaring:
-                    by = torch.empty(ny, dtype=torch.uint8, pin_memory=True)
+                if hy is not None:
+                    by = torch.empty(hy.numel(), dtype=torch.uint8, pin_memory=True)
                     by.copy_(hy)
-                bufs.append((bx, by, torch.empty(out_stride, dtype=torch.uint8, pin_memory=True)))
+                bufs.append((bx, by, torch.empty(ho.numel(), dtype=torch.uint8, pin_memory=True)))
         except RuntimeError:  # not enough pinned host memory for every thread: use what there is
             pass
         T = len(bufs)
@@ -671,16 +677,21 @@ def run_ours(args, cfg, rank, world, local_rank):
         def worker(k, limit):
             bx, by, bo = bufs[k]
             ol = C.c_size_t()
+            bl = torch.zeros(max(count, 1), dtype=torch.int64)
             try:
                 while True:
                     with lock:
                         if todo[0] >= limit:
                             return
                         todo[0] += 1
-                    ctx._call("decmul_gpu_multiply", C.c_void_p(bx.data_ptr()), C.c_size_t(nx),
-                              C.c_void_p((bx if squaring else by).data_ptr()), C.c_size_t(ny),
-                              C.c_void_p(bo.data_ptr()), C.c_size_t(out_stride), C.byref(ol), C.c_uint(0),
-                              C.c_int(int(squaring)))
+                    if count > 1:
+                        ctx.multiply_batch_ptr(count, bx.data_ptr(), nx, by.data_ptr(), ny, bo.data_ptr(), out_stride,
+                                               bl.data_ptr())
+                    else:
+                        ctx._call("decmul_gpu_multiply", C.c_void_p(bx.data_ptr()), C.c_size_t(nx),
+                                  C.c_void_p((bx if squaring else by).data_ptr()), C.c_size_t(ny),
+                                  C.c_void_p(bo.data_ptr()), C.c_size_t(out_stride), C.byref(ol), C.c_uint(0),
+                                  C.c_int(int(squaring)))
             except Exception as e:  # noqa
                 errs.append(e)
 
@@ -721,7 +732,14 @@ def run_ours(args, cfg, rank, world, local_rank):
     e2e = {"value": world * digits_step * args.steps / (e2e_ms * 1e-3), "unit": "digits/s",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
            "api": "decmul_gpu_multiply_batch" if count > 1 else "decmul_gpu_multiply", "host_buffers": "pinned"}
-    if T > 1:
+    if T > 1 and count > 1:
+        # every thread's last batch must be the same digits as the single-call batch's
+        same = all(torch.equal(bufs[0][2], b[2]) for b in bufs[1:])
+        e2e.update({"host_threads": T, "single_call_ms": single_ms, "threads_agree": bool(same),
+                    "note": f"{args.steps} batches issued by {T} host threads calling decmul_gpu_multiply_batch "
+                            "concurrently (own pinned buffers each); the library overlaps one batch's pipeline drain "
+                            "with the next one's fill; single_call_ms = one synchronous call alone"})
+    elif T > 1:
         # every thread's last product must be the same digits (thread 0's are checked below)
         same = all(torch.equal(bufs[0][2][:olen.value], b[2][:olen.value]) for b in bufs[1:])
         e2e.update({"host_threads": T, "single_call_ms": single_ms, "threads_agree": bool(same),

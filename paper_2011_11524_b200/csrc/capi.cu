@@ -443,7 +443,20 @@ int decmul_gpu_result_length(decmul_gpu_ctx* ctx, size_t* out_len) {
 int decmul_gpu_multiply_batch(decmul_gpu_ctx* ctx, size_t count, const char* xs, size_t x_stride, size_t nx,
                               const char* ys, size_t y_stride, size_t ny, char* outs, size_t out_stride,
                               size_t* out_lens) {
-  LOCKED(ctx, ctx->multi->multiply_batch_host(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, out_lens));
+  // the engine may release the context lock once a large pinned batch is enqueued, so that
+  // batches from several threads overlap (Engine::batch_host_pipelined)
+  if (!ctx) return DECMUL_EINVAL;
+  std::unique_lock<std::mutex> lock_(ctx->mu);
+  DeviceGuard dev_(ctx->eng->device());
+  std::string msg;
+  const int rc = guarded_msg(msg, [&] {
+    ctx->multi->multiply_batch_host(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, out_lens, &lock_);
+  });
+  if (rc) {
+    if (!lock_.owns_lock()) lock_.lock();
+    ctx->err = msg;
+  }
+  return rc;
 }
 
 int decmul_gpu_multiply_batch_ptrs(decmul_gpu_ctx* ctx, size_t count, const char* const* xs, const size_t* nxs,

@@ -145,6 +145,10 @@ Engine::~Engine() {
     cudaEventDestroy(done_ev_[i]);
   }
   if (host_lens_) cudaFreeHost(host_lens_);
+  for (BatchSet& b : bsets_) {
+    if (b.done) cudaEventDestroy(b.done);
+    if (b.h_err) cudaFreeHost(b.h_err);
+  }
   if (ov_up_stream_) cudaStreamDestroy(ov_up_stream_);
   for (OvSlot& s : ov_) {
     if (s.dl_stream) cudaStreamDestroy(s.dl_stream);
@@ -683,6 +687,10 @@ void Engine::check_word(unsigned* word, cudaStream_t st) {
     cuda_check(cudaMemsetAsync(word, 0, sizeof(unsigned), st), "memset");
     cuda_check(cudaStreamSynchronize(st), "sync");
   }
+  throw_err_bits(e);
+}
+
+void Engine::throw_err_bits(unsigned e) {
   if (e & kErrBadDigit) throw std::invalid_argument("decimal: non-digit character");
   if (e & kErrLeadingZero) throw std::invalid_argument("decimal: leading zero");
   if (e & kErrCoeffBound)
@@ -1163,7 +1171,7 @@ void Engine::batch_device(std::size_t count, const char* dxs, std::size_t x_stri
 
 void Engine::multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
                                  const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
-                                 std::size_t out_stride, std::size_t* lens) {
+                                 std::size_t out_stride, std::size_t* lens, std::unique_lock<std::mutex>* ctx_lock) {
   if (count == 0) return;
   if (nx == 0 || ny == 0) throw std::invalid_argument("decimal: empty string");
   const ProductPlan pp = plan_product(nx, ny, 0);
@@ -1176,7 +1184,7 @@ void Engine::multiply_batch_host(std::size_t count, const char* xs, std::size_t 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_);
     const std::size_t wave = std::size_t(sms) * std::max(1, small_resident_ctas(Pb.k, Pb.three, 0));
     if (count >= 2 * wave) {
-      batch_host_pipelined(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, lens);
+      batch_host_pipelined(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, lens, ctx_lock);
       return;
     }
   }
@@ -1213,7 +1221,7 @@ void Engine::multiply_batch_host(std::size_t count, const char* xs, std::size_t 
 // workspace, so the chunks are independent.
 void Engine::batch_host_pipelined(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
                                   const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
-                                  std::size_t out_stride, std::size_t* lens) {
+                                  std::size_t out_stride, std::size_t* lens, std::unique_lock<std::mutex>* ctx_lock) {
   // whole waves of the one-CTA kernel per chunk (a partial wave costs a full one)
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_);
@@ -1233,17 +1241,49 @@ void Engine::batch_host_pipelined(std::size_t count, const char* xs, std::size_t
   std::vector<std::size_t> bounds{0};
   for (std::size_t c = per; c < count; c += per) bounds.push_back(c);
   bounds.push_back(count);
-  din_x_.ensure((count - 1) * x_stride + nx);
-  din_y_.ensure((count - 1) * y_stride + ny);
-  lens_.ensure(count);
-  dout_.ensure(count * out_stride);
-  if (host_lens_n_ < count) {
-    if (host_lens_) cudaFreeHost(host_lens_);
-    host_lens_ = nullptr;
-    host_lens_n_ = 0;
-    cuda_check(cudaMallocHost(&host_lens_, count * sizeof(unsigned long long)), "cudaMallocHost");
-    host_lens_n_ = count;
+  // Calls from several threads overlap (pinned buffers, the caller's context lock handed in):
+  // the lock is held only while the chunks are enqueued; each call works in one of two buffer
+  // sets (digits, lengths, error word), so the next call's uploads follow this call's on the
+  // upload stream while this one still computes and downloads -- a call's pipeline fill and
+  // drain disappear behind its neighbours'. The set's own lock is held until the lengths have
+  // been copied out.
+  const bool overlap = ctx_lock && ctx_lock->owns_lock() && host_pinned(xs) && host_pinned(ys) && host_pinned(outs) &&
+                       !(std::getenv("DECMUL_OVERLAP") && std::getenv("DECMUL_OVERLAP")[0] == '0');
+  BatchSet* B = nullptr;
+  std::unique_lock<std::mutex> set_lock;
+  if (overlap) {
+    B = &bsets_[bset_ ^= 1];
+    set_lock = std::unique_lock<std::mutex>(B->mu);  // waits for the call that used this set last
+    if (!B->done) {
+      cuda_check(cudaEventCreateWithFlags(&B->done, cudaEventDisableTiming), "cudaEventCreate");
+      cuda_check(cudaMallocHost(&B->h_err, sizeof(unsigned)), "cudaMallocHost");
+      B->err.ensure(1);
+      cuda_check(cudaMemsetAsync(B->err.ptr, 0, sizeof(unsigned), stream_), "memset");
+    }
+    B->dx.ensure((count - 1) * x_stride + nx);
+    B->dy.ensure((count - 1) * y_stride + ny);
+    B->lens.ensure(count);
+    B->dout.ensure(count * out_stride);
+    B->h_lens.ensure(count * sizeof(unsigned long long));
+  } else {
+    din_x_.ensure((count - 1) * x_stride + nx);
+    din_y_.ensure((count - 1) * y_stride + ny);
+    lens_.ensure(count);
+    dout_.ensure(count * out_stride);
+    if (host_lens_n_ < count) {
+      if (host_lens_) cudaFreeHost(host_lens_);
+      host_lens_ = nullptr;
+      host_lens_n_ = 0;
+      cuda_check(cudaMallocHost(&host_lens_, count * sizeof(unsigned long long)), "cudaMallocHost");
+      host_lens_n_ = count;
+    }
   }
+  char* const d_x = overlap ? B->dx.ptr : din_x_.ptr;
+  char* const d_y = overlap ? B->dy.ptr : din_y_.ptr;
+  char* const d_o = overlap ? B->dout.ptr : dout_.ptr;
+  unsigned long long* const d_l = overlap ? B->lens.ptr : lens_.ptr;
+  unsigned long long* const h_l = overlap ? reinterpret_cast<unsigned long long*>(B->h_lens.ptr) : host_lens_;
+  unsigned* const d_err = overlap ? B->err.ptr : err_.ptr;
   cuda_check(cudaEventRecord(pipe_ev_, stream_), "event");  // after any earlier work of this context
   for (auto s : pipe_) cuda_check(cudaStreamWaitEvent(s, pipe_ev_, 0), "wait");
   // DECMUL_PIPE_TRACE=1: per-chunk stage timestamps on stderr (debugging the overlap)
@@ -1262,24 +1302,41 @@ void Engine::batch_host_pipelined(std::size_t count, const char* xs, std::size_t
     const std::size_t c0 = bounds[c], n = bounds[c + 1] - c0;
     if (n == 0) continue;
     cudaStream_t up = pipe_[0], comp = pipe_[1], down = pipe_[2];
-    cuda_check(cudaMemcpyAsync(din_x_.ptr + c0 * x_stride, xs + c0 * x_stride, (n - 1) * x_stride + nx,
+    cuda_check(cudaMemcpyAsync(d_x + c0 * x_stride, xs + c0 * x_stride, (n - 1) * x_stride + nx,
                                cudaMemcpyHostToDevice, up), "h2d");
-    cuda_check(cudaMemcpyAsync(din_y_.ptr + c0 * y_stride, ys + c0 * y_stride, (n - 1) * y_stride + ny,
+    cuda_check(cudaMemcpyAsync(d_y + c0 * y_stride, ys + c0 * y_stride, (n - 1) * y_stride + ny,
                                cudaMemcpyHostToDevice, up), "h2d");
     mark(up);
     cuda_check(cudaEventRecord(up_ev_[c], up), "event");
     cuda_check(cudaStreamWaitEvent(comp, up_ev_[c], 0), "wait");
-    batch_device(n, din_x_.ptr + c0 * x_stride, x_stride, nx, din_y_.ptr + c0 * y_stride, y_stride, ny,
-                 dout_.ptr + c0 * out_stride, out_stride, lens_.ptr + c0, comp, err_.ptr);
+    batch_device(n, d_x + c0 * x_stride, x_stride, nx, d_y + c0 * y_stride, y_stride, ny, d_o + c0 * out_stride,
+                 out_stride, d_l + c0, comp, d_err);
     launched += launches_;
     mark(comp);
     cuda_check(cudaEventRecord(done_ev_[c], comp), "event");
     cuda_check(cudaStreamWaitEvent(down, done_ev_[c], 0), "wait");
-    cuda_check(cudaMemcpyAsync(outs + c0 * out_stride, dout_.ptr + c0 * out_stride, n * out_stride,
-                               cudaMemcpyDeviceToHost, down), "d2h");
-    cuda_check(cudaMemcpyAsync(host_lens_ + c0, lens_.ptr + c0, n * sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, down), "d2h");
+    cuda_check(cudaMemcpyAsync(outs + c0 * out_stride, d_o + c0 * out_stride, n * out_stride, cudaMemcpyDeviceToHost,
+                               down), "d2h");
+    cuda_check(cudaMemcpyAsync(h_l + c0, d_l + c0, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, down),
+               "d2h");
     mark(down);
+  }
+  if (overlap) {
+    // the download stream is ordered after every chunk's kernel: the set's error word and the
+    // completion event go there, the context lock is released, and only this caller waits
+    cudaStream_t down = pipe_[2];
+    cuda_check(cudaMemcpyAsync(B->h_err, B->err.ptr, sizeof(unsigned), cudaMemcpyDeviceToHost, down), "err");
+    cuda_check(cudaEventRecord(B->done, down), "event");
+    launches_ = launched;
+    ctx_lock->unlock();
+    cuda_check(cudaEventSynchronize(B->done), "batch wait");
+    if (const unsigned e = *B->h_err) {
+      cuda_check(cudaMemsetAsync(B->err.ptr, 0, sizeof(unsigned), down), "memset");
+      cuda_check(cudaStreamSynchronize(down), "sync");
+      throw_err_bits(e);
+    }
+    for (std::size_t i = 0; i < count; ++i) lens[i] = std::size_t(h_l[i]);
+    return;
   }
   for (auto s : pipe_) {
     cuda_check(cudaEventRecord(pipe_ev_, s), "event");

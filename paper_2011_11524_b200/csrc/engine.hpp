@@ -233,9 +233,12 @@ class Engine {
   // Mixed sizes from host pointers: equal (nx, ny) groups through multiply_batch_host.
   void multiply_batch_ptrs(std::size_t count, const char* const* xs, const std::size_t* nxs, const char* const* ys,
                            const std::size_t* nys, char* const* outs, const std::size_t* caps, std::size_t* lens);
+  // ctx_lock: the caller's (held) context lock; a large batch from pinned buffers releases it
+  // once its chunks are enqueued, so batches from several threads overlap (batch_host_pipelined)
   void multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
                            const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
-                           std::size_t out_stride, std::size_t* lens);
+                           std::size_t out_stride, std::size_t* lens,
+                           std::unique_lock<std::mutex>* ctx_lock = nullptr);
 
   // Parity hooks (reference conv.hpp:59-71), host arrays, one prime.
   void convolve_mod_p(u64 p, std::size_t n, const u64* x, std::size_t nx, const u64* y, std::size_t ny,
@@ -363,7 +366,9 @@ class Engine {
   // H2D / compute / D2H pipeline of multiply_batch_host (one-CTA products)
   void batch_host_pipelined(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx, const char* ys,
                             std::size_t y_stride, std::size_t ny, char* outs, std::size_t out_stride,
-                            std::size_t* lens);
+                            std::size_t* lens, std::unique_lock<std::mutex>* ctx_lock);
+  static bool host_pinned(const void* p);
+  static void throw_err_bits(unsigned e);
 
   int device_ = 0;
   cudaStream_t stream_ = nullptr;
@@ -396,6 +401,18 @@ class Engine {
     unsigned long long* h_len = nullptr;  // pinned: the product length, read back without blocking
     StageRing dl_ring;  // pageable outputs: the two slots' downloads may run at the same time
   };
+  // batch_host_pipelined in overlap mode: two sets of batch buffers
+  struct BatchSet {
+    DevBuf<char> dx, dy, dout;
+    DevBuf<unsigned long long> lens;
+    DevBuf<unsigned> err;
+    PinnedBuf h_lens;
+    unsigned* h_err = nullptr;
+    cudaEvent_t done = nullptr;
+    std::mutex mu;
+  };
+  BatchSet bsets_[2];
+  int bset_ = 0;
   OvSlot ov_[2];
   std::mutex ov_up_mu_;
   cudaStream_t ov_up_stream_ = nullptr;

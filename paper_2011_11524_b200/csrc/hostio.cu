@@ -261,6 +261,7 @@ void StageRing::d2h(void* dst, const void* src, std::size_t n, cudaStream_t st) 
   }
 }
 
+bool Engine::host_pinned(const void* p) { return is_pinned(p); }
 bool Engine::stage_direct(const void* host, std::size_t n) const { return n < kStageMin || is_pinned(host); }
 void Engine::stage_h2d(void* dst, const void* src, std::size_t n, cudaStream_t st) { ring_.h2d(dst, src, n, st); }
 void Engine::stage_d2h(void* dst, const void* src, std::size_t n, cudaStream_t st) { ring_.d2h(dst, src, n, st); }

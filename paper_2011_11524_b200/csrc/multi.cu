@@ -144,10 +144,11 @@ Engine* MultiEngine::overlap_engine(const char* x, std::size_t nx, const char* y
 
 void MultiEngine::multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
                                       const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
-                                      std::size_t out_stride, std::size_t* lens) {
+                                      std::size_t out_stride, std::size_t* lens,
+                                      std::unique_lock<std::mutex>* ctx_lock) {
   if (eng_.size() == 1 || count < 2 * eng_.size()) {
     cudaSetDevice(eng_[0]->device());
-    eng_[0]->multiply_batch_host(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, lens);
+    eng_[0]->multiply_batch_host(count, xs, x_stride, nx, ys, y_stride, ny, outs, out_stride, lens, ctx_lock);
     return;
   }
   fan_out(count, [&](Engine& e, std::size_t b, std::size_t end) {

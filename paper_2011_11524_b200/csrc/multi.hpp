@@ -33,7 +33,8 @@ class MultiEngine {
   // batches: contiguous ranges of products per device, one host thread per device
   void multiply_batch_host(std::size_t count, const char* xs, std::size_t x_stride, std::size_t nx,
                            const char* ys, std::size_t y_stride, std::size_t ny, char* outs,
-                           std::size_t out_stride, std::size_t* lens);
+                           std::size_t out_stride, std::size_t* lens,
+                           std::unique_lock<std::mutex>* ctx_lock = nullptr);
   void multiply_batch_ptrs(std::size_t count, const char* const* xs, const std::size_t* nxs, const char* const* ys,
                            const std::size_t* nys, char* const* outs, const std::size_t* caps, std::size_t* lens);
   // whether multiply_host shards this product (G > 1, N >= 2^22, a valid shard shape)

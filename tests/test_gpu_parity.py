@@ -428,6 +428,58 @@ def test_concurrent_large_products_overlap_transfers(gpu, ref, monkeypatch):
     assert len(got) == 11
 
 
+def test_concurrent_batches_overlap(gpu, ref):
+    """decmul_gpu_multiply_batch from three threads with pinned buffers (1024 one-CTA products per
+    call: more than two waves, so the chunked pipeline; the context lock is released once a
+    batch is enqueued and the calls alternate between two buffer sets). Every call's products
+    equal the reference's; a bad digit fails only its own call."""
+    import threading
+
+    import torch
+
+    count, nx, ny = 1024, 3000, 2500
+    stride = nx + ny
+    jobs, want = [], []
+    for t in range(3):
+        xs = b"".join(inputs.gen_digits(9000 + 2 * (t * count + k), nx) for k in range(count))
+        ys = b"".join(inputs.gen_digits(9001 + 2 * (t * count + k), ny) for k in range(count))
+        hx = torch.frombuffer(bytearray(xs), dtype=torch.uint8).pin_memory()
+        hy = torch.frombuffer(bytearray(ys), dtype=torch.uint8).pin_memory()
+        ho = torch.empty(count * stride, dtype=torch.uint8).pin_memory()
+        hl = torch.zeros(count, dtype=torch.int64)
+        jobs.append((hx, hy, ho, hl))
+        want.append([ref.multiply(xs[k * nx:(k + 1) * nx], ys[k * ny:(k + 1) * ny]) for k in range(0, count, 97)])
+    fails, errs = [], {}
+
+    def worker(t):
+        hx, hy, ho, hl = jobs[t]
+        for rep in range(6):
+            bad = t == 1 and rep == 2
+            if bad:
+                hx[500 * nx + 7] = ord("x")
+            try:
+                ho.zero_()
+                gpu.multiply_batch_ptr(count, hx.data_ptr(), nx, hy.data_ptr(), ny, ho.data_ptr(), stride, hl.data_ptr())
+                o = ho.numpy()
+                got = [bytes(o[k * stride:k * stride + int(hl[k])]) for k in range(0, count, 97)]
+                if got != want[t]:
+                    fails.append((t, rep))
+            except ValueError as e:
+                errs[(t, rep)] = str(e)
+            if bad:
+                hx[500 * nx + 7] = jobs_saved[0]
+
+    jobs_saved = [int(jobs[1][0][500 * nx + 7])]
+    th = [threading.Thread(target=worker, args=(t,)) for t in range(3)]
+    for h in th:
+        h.start()
+    for h in th:
+        h.join(timeout=300)
+    assert not any(h.is_alive() for h in th), "deadlock"
+    assert not fails, fails
+    assert list(errs) == [(1, 2)] and "non-digit" in errs[(1, 2)]
+
+
 def test_mixed_concurrent_traffic(gpu, ref):
     """One context shared by threads doing different things at once: two threads of overlapped
     large pinned products, two of large pageable ones, two of small (coalesced) products, one of
