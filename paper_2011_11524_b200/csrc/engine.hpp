@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <condition_variable>
 #include <functional>
 #include <map>
@@ -413,6 +414,7 @@ class Engine {
   };
   BatchSet bsets_[2];
   int bset_ = 0;
+  std::atomic<int> batch_active_{0};  // batch_host_pipelined calls in flight
   OvSlot ov_[2];
   std::mutex ov_up_mu_;
   cudaStream_t ov_up_stream_ = nullptr;
