@@ -156,7 +156,8 @@ constexpr bool kStageInv = ROWS && (DMG_STAGE_MASK & 2) != 0;
 #ifndef DMG_BULK_ROWS
 #define DMG_BULK_ROWS 1
 #endif
-// DMG_BULK_NARROW=1: the 4-column tiles of small transforms too (32-byte box rows)
+// DMG_BULK_NARROW=1: the 4-column tiles of small transforms too (32-byte box rows); measured
+// neutral (config 1 39 us either way), so they keep the cp.async burst
 #ifndef DMG_BULK_NARROW
 #define DMG_BULK_NARROW 0
 #endif
@@ -288,8 +289,9 @@ constexpr int pass_min_blocks(int logr, int tw) {
 }
 
 // Forward pass: column DIFs, then the inter-pass twiddle omega_M^{f s} (row passes).
-// The first round reads HBM into registers and the last round writes HBM from
-// registers; shared memory carries only the rounds in between.
+// Full-width row tiles arrive and leave by TMA (stage_rows_tma / store_rows_tma); narrow
+// tiles are staged by cp.async; column tiles read HBM into the first round's registers. All
+// but the TMA-stored tiles write HBM from the last round's registers.
 template <int LOGR, bool ROWS, int TW, bool FACT = false>
 __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, TW)) k_pass_fwd(const __grid_constant__ PassArgs a, const __grid_constant__ TileMaps maps) {
   // at entry: a wait placed after the table loads kept the compiler from hoisting the
