@@ -195,6 +195,12 @@ __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
 #ifndef DMG_BULK_STORE
 #define DMG_BULK_STORE 1
 #endif
+#ifndef DMG_FUSED_BULK_X
+#define DMG_FUSED_BULK_X 1
+#endif
+#ifndef DMG_FUSED_BULK_Y
+#define DMG_FUSED_BULK_Y 1
+#endif
 template <int LOGR, int TW>
 __device__ __forceinline__ void store_rows_tma(const u64* sm, const void* map, unsigned long long s0,
                                                unsigned long long row0) {
@@ -544,16 +550,88 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), fused_min_blocks(LOGR,
   const Geom<LOGR, false, TW> G(a);
   const ContigColumns<LOGR> L;
   constexpr bool STAGE = kStageFwd<false, TW> && LOGR > EM;
+  // TWO, full-width tiles: the first operand's tile (one contiguous run of R * TW words) comes
+  // in by a single bulk copy into the still unused y region, unswizzled; its first DIF round
+  // reads it from there and writes the swizzled layout into smx (DMG_FUSED_BULK_X=0: the
+  // 8-byte cp.async burst straight into the swizzled layout).
+  constexpr bool XBULK = TWO && !STAGE && LOGR > E1 && DMG_FUSED_BULK_X != 0;
+  // The operand's own tile the same way (DMG_FUSED_BULK_Y): copied unswizzled into its region
+  // -- for TWO once the first operand's first round has left it, so the copy runs under that
+  // operand's remaining rounds -- and re-laid out in place by the first round (all reads,
+  // a barrier, then the swizzled writes) instead of that round reading HBM into registers.
+  constexpr bool YBULK = !STAGE && LOGR > E1 && TW == kTileW && DMG_FUSED_BULK_Y != 0 && (!TWO || XBULK) &&
+                         ((R >> E1) % 32) == 0 && (1 << (LOGR - E1)) >= 16;  // (the re-layout's hazard analysis)
+  u64* bar = sm + (TWO ? 2 : 1) * R * TW + 2 * R;  // after the tiles and both tables
+  auto bulk_tile = [&](const u64* g) {  // thread 0: one bulk copy of the contiguous tile into sm
+    mbar_expect_tx(bar, unsigned(R * TW * sizeof(u64)));
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     unsigned(__cvta_generic_to_shared(sm))),
+                 "l"(g + G.at(0, 0)), "r"(unsigned(R * TW * sizeof(u64))), "r"(unsigned(__cvta_generic_to_shared(bar)))
+                 : "memory");
+  };
   if constexpr (STAGE) stage_tile<LOGR, false, TW, NTK>(sm, src, G, L, tid);
-  if constexpr (TWO) stage_tile<LOGR, false, TW, NTK>(smx, oth, G, L, tid);
+  if constexpr (XBULK || YBULK) {
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      bulk_tile(XBULK ? oth : src);
+    }
+  }
+  if constexpr (TWO && !XBULK) stage_tile<LOGR, false, TW, NTK>(smx, oth, G, L, tid);
   load_table<LOGR, NTK, kSwzTables<false>>(twf, a.dft_fwd[pr]);
   load_table<LOGR, NTK, kSwzTables<false>>(twi, a.dft_inv[pr]);
-  if constexpr (STAGE || TWO) asm volatile("cp.async.wait_all;" ::: "memory");
+  if constexpr (STAGE || (TWO && !XBULK)) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  if constexpr (XBULK || YBULK) mbar_wait(bar, 0);
   pdl_trigger_mid();
-  if constexpr (TWO) tile_dif<LOGR, TW>(smx, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
+  if constexpr (XBULK) {
+    constexpr int ST1 = 1 << (LOGR - E1);
+    for (int g = tid; g < (R >> E1) * TW; g += NTK) {
+      int w, q, j0, base;
+      group_coords<LOGR, false, E1, TW>(g, w, q);
+      dif_group<LOGR, E1>(q, j0, base);
+      u64 v[1 << E1];
+#pragma unroll
+      for (int i = 0; i < (1 << E1); ++i) v[i] = sm[(w << LOGR) + base + i * ST1];
+      dif_regs<LOGR, LOGR, E1, kSwzTables<false>>(v, j0, twf, p);
+#pragma unroll
+      for (int i = 0; i < (1 << E1); ++i) smx[L(base + i * ST1, w)] = v[i];
+    }
+    __syncthreads();
+    if constexpr (YBULK) {
+      if (tid == 0) {  // the y region is free again: its tile comes in under the rounds below
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_tile(src);
+      }
+    }
+    dif_rounds_smem<LOGR, LOGR - E1, 0, TW>(smx, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
+  } else if constexpr (TWO) {
+    tile_dif<LOGR, TW>(smx, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
+  }
   if constexpr (STAGE) {
     dif_rounds_smem<LOGR, LOGR, EM, TW>(sm, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
+  } else if constexpr (YBULK) {
+    // In-place re-layout: the swizzle permutes positions inside aligned 16-element blocks of a
+    // column; a group's elements are >= 32 apart (one per block), and the 16 groups that share
+    // a set of blocks are 16 adjacent lanes of one warp in the same iteration (lanes run along
+    // the column, (R >> E1) is a multiple of 32). So a warp-level barrier between a group's
+    // reads and its writes is enough.
+    static_assert(((R >> E1) % 32) == 0 && (1 << (LOGR - E1)) >= 16, "re-layout hazard analysis");
+    constexpr int ST1 = 1 << (LOGR - E1);
+    if constexpr (TWO) mbar_wait(bar, 1);
+    for (int g = tid; g < (R >> E1) * TW; g += NTK) {
+      int w, q, j0, base;
+      group_coords<LOGR, false, E1, TW>(g, w, q);
+      dif_group<LOGR, E1>(q, j0, base);
+      u64 v[1 << E1];
+#pragma unroll
+      for (int i = 0; i < (1 << E1); ++i) v[i] = sm[(w << LOGR) + base + i * ST1];
+      __syncwarp();
+      dif_regs<LOGR, LOGR, E1, kSwzTables<false>>(v, j0, twf, p);
+#pragma unroll
+      for (int i = 0; i < (1 << E1); ++i) sm[L(base + i * ST1, w)] = v[i];
+    }
+    __syncthreads();
+    dif_rounds_smem<LOGR, LOGR - E1, EM, TW>(sm, L, UniformField<kSwzTables<false>>{p, twf}, tid, NTK);
   } else if constexpr (LOGR > EM) {
     constexpr int ST1 = 1 << (LOGR - E1);
     for (int g = tid; g < (R >> E1) * TW; g += NTK) {
@@ -1141,7 +1219,7 @@ void pass_inv_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_
 template <int LOGR, int TW>
 void pass_fused_w(const PassArgs& a, unsigned long long ncols, int np, cudaStream_t st) {
   constexpr int NTK = pass_threads(LOGR, TW);
-  const int sm = (1 << LOGR) * TW * 8 * (a.two ? 2 : 1) + (1 << LOGR) * 16;
+  const int sm = (1 << LOGR) * TW * 8 * (a.two ? 2 : 1) + (1 << LOGR) * 16 + 16;  // tiles, tables, mbarrier
   if (a.two) {
     if (a.lazy_out)
       launch_pass_kernel<k_pass_fused<LOGR, TW, true, true>, TW, NTK>(a, ncols, np, sm, st);
