@@ -201,6 +201,9 @@ __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
 #ifndef DMG_FUSED_BULK_Y
 #define DMG_FUSED_BULK_Y 1
 #endif
+#ifndef DMG_FUSED_BULK_OUT
+#define DMG_FUSED_BULK_OUT 1
+#endif
 template <int LOGR, int TW>
 __device__ __forceinline__ void store_rows_tma(const u64* sm, const void* map, unsigned long long s0,
                                                unsigned long long row0) {
@@ -561,6 +564,10 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), fused_min_blocks(LOGR,
   // a barrier, then the swizzled writes) instead of that round reading HBM into registers.
   constexpr bool YBULK = !STAGE && LOGR > E1 && TW == kTileW && DMG_FUSED_BULK_Y != 0 && (!TWO || XBULK) &&
                          ((R >> E1) % 32) == 0 && (1 << (LOGR - E1)) >= 16;  // (the re-layout's hazard analysis)
+  // ... and the results leave the same way (DMG_FUSED_BULK_OUT): the last DIT round writes
+  // them unswizzled into the tile's region (same hazard analysis, its stride is 2^AL) and one
+  // thread stores the contiguous run.
+  constexpr bool OBULK = YBULK && DMG_FUSED_BULK_OUT != 0 && LOGR > EM && (((R >> EL) % 32) == 0) && (1 << AL) >= 16;
   u64* bar = sm + (TWO ? 2 : 1) * R * TW + 2 * R;  // after the tiles and both tables
   auto bulk_tile = [&](const u64* g) {  // thread 0: one bulk copy of the contiguous tile into sm
     mbar_expect_tx(bar, unsigned(R * TW * sizeof(u64)));
@@ -686,10 +693,26 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), fused_min_blocks(LOGR,
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) v[i] = sm[L(base + i * STL, w)];
       dit_regs<LOGR, AL, EL, kSwzTables<false>, LZO>(v, j0, twi, p);
+      if constexpr (OBULK) __syncwarp();  // every lane has read its group: un-swizzle in place
 #pragma unroll
       for (int i = 0; i < (1 << EL); ++i) {
         if (a.has_final_scale) v[i] = shoup_mul(v[i], sc, p);
-        dst[G.at(base + i * STL, w)] = v[i];
+        if constexpr (OBULK)
+          sm[(w << LOGR) + base + i * STL] = v[i];
+        else
+          dst[G.at(base + i * STL, w)] = v[i];
+      }
+    }
+    if constexpr (OBULK) {
+      // the tile is one contiguous run of R * TW words in the output too: one bulk store
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + G.at(0, 0)),
+                     "r"(unsigned(__cvta_generic_to_shared(sm))), "r"(unsigned(R * TW * sizeof(u64)))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       }
     }
   }
