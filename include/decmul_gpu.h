@@ -13,10 +13,13 @@
  *    wrapper rethrows the same type with the same text.
  *  - Buffers are caller-owned. "d_" parameters are device pointers on the
  *    context's GPU; all others are host pointers.
- *  - A context is internally locked: one context may be shared by threads
- *    (calls serialise), or use one context per thread — matching the
- *    reference's reentrant multiply and its single plan-cache
- *    mutex (conv.cpp:311-322).
+ *  - A context is internally locked: one context may be shared by threads,
+ *    or use one context per thread — matching the reference's reentrant
+ *    multiply and its single plan-cache mutex
+ *    (conv.cpp:311-322). Concurrent calls on one context do not simply
+ *    serialise: small products are coalesced into batch launches, large
+ *    products and batches from pinned buffers overlap their transfers (see
+ *    "Concurrency" below).
  */
 #ifndef DECMUL_GPU_H
 #define DECMUL_GPU_H
@@ -105,7 +108,13 @@ int decmul_gpu_multiply_sharded(decmul_gpu_ctx* ctx, const char* x, size_t nx, c
  * coalesced: the first caller leads, waits for the context, and runs every product queued by
  * then as one batch launch; the others sleep until their result is in. Results and errors are
  * per call (a failing batch is rerun product by product). DECMUL_COALESCE=0 disables it.
- * decmul_gpu_coalesce_stats reports the batches and products run that way. */
+ * decmul_gpu_coalesce_stats reports the batches and products run that way.
+ * decmul_gpu_multiply[_ex] calls with >= 2^24 digits in all (pinned buffers always; pageable ones
+ * while another such call is in flight) run upload, compute and download as separate stages over
+ * two sets of digit buffers, the context lock held only around the compute, so one call's
+ * download overlaps the next call's upload and compute; decmul_gpu_multiply_batch calls from
+ * pinned buffers (two waves of one-CTA products or more) release the context once their chunks
+ * are enqueued and alternate between two buffer sets. DECMUL_OVERLAP=0 disables both. */
 int decmul_gpu_coalesce_stats(decmul_gpu_ctx* ctx, unsigned long long* batches, unsigned long long* products);
 
 /* Device-resident variant: digits in and out stay in HBM. stream = cudaStream_t (NULL = the
