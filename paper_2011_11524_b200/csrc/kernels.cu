@@ -219,6 +219,28 @@ __device__ __forceinline__ void store_rows_tma(const u64* sm, const void* map, u
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the CTA's shared memory outlives the reads
 }
 
+// The tile's inter-pass twiddle rows T[f][s0 .. s0 + 16) (16 pairs = 256 bytes per row, all R
+// rows) pulled towards L2 by the TMA unit: the table is a 2-D tensor {2 S' u64, rows}, the
+// rows a box {32, min(R, 256)} -- one or two prefetch instructions from one thread instead of
+// four prefetch.global.L2 per thread (DMG_TMA_TWPF=0 keeps those). DMG_TMA_TWPF_FWD_GROUP: the
+// forward pass over per-group tables (pass 1 of N = 3 * 2^k), which the per-thread loop did
+// not pay for: 0 none, 1 at kernel entry, 2 after the first round.
+#ifndef DMG_TMA_TWPF
+#define DMG_TMA_TWPF 1
+#endif
+#ifndef DMG_TMA_TWPF_FWD_GROUP
+#define DMG_TMA_TWPF_FWD_GROUP 0
+#endif
+template <int LOGR>
+__device__ __forceinline__ void prefetch_tw_rows_tma(const void* map, unsigned long long col, unsigned long long row0) {
+  constexpr int R = 1 << LOGR, BR = R < kBoxRows ? R : kBoxRows;
+#pragma unroll
+  for (int h = 0; h < R / BR; ++h)
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(int(2 * col)),
+                 "r"(int(row0) + h * BR)
+                 : "memory");
+}
+
 // Thread 0 of the CTA: arm the barrier and issue the tile's TMA copies (rows row0 .. row0 + R
 // of the tensor, columns s0 .. s0 + 16). Everyone else meets it at the next __syncthreads and
 // then waits on the barrier's phase 0.
@@ -318,16 +340,24 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   const unsigned long long grp = ROWS ? (blockIdx.x / a.np) % a.G : 0;  // group of a row tile
   const TwPair* __restrict__ T = a.pass_tw[pr] + grp * a.tw_gstride;
   const TwPair* __restrict__ Hi = a.pass_hi[pr] + grp * a.hi_gstride;
+  // (the launcher encodes the table maps for the launches whose tiles move by TMA)
+  constexpr bool TWPF = ROWS && !FACT && DMG_TMA_TWPF != 0 && kBulkRows<ROWS, TW> && kStageFwd<ROWS, TW> && LOGR > E1;
   if constexpr (ROWS && !FACT) if (DMG_GROUP_PREFETCH || a.tw_gstride == 0) {
     // The twiddles are applied in the epilogue, after the DIF; start pulling the tile's
     // rows T[f][s0 .. s0 + TW) (TW pairs = TW * 16 bytes each) into L2 now so those
     // loads hit L2 instead of DRAM (large-S passes stream a table of N / 3 .. N pairs).
-    constexpr int LINES = TW * 16 / 128 > 0 ? TW * 16 / 128 : 1;
-    for (int i = tid; i < R * LINES; i += NTK) {
-      const TwPair* row = &G.tw(T, i / LINES, 0) + (i % LINES) * 8;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+    if constexpr (TWPF) {
+      if (tid == 0) prefetch_tw_rows_tma<LOGR>(&maps.m[8 + pr], G.tw_col, a.tw_gstride ? grp << LOGR : 0);
+    } else {
+      constexpr int LINES = TW * 16 / 128 > 0 ? TW * 16 / 128 : 1;
+      for (int i = tid; i < R * LINES; i += NTK) {
+        const TwPair* row = &G.tw(T, i / LINES, 0) + (i % LINES) * 8;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+      }
     }
   }
+  if constexpr (TWPF && DMG_TMA_TWPF_FWD_GROUP == 1)
+    if (a.tw_gstride != 0 && tid == 0) prefetch_tw_rows_tma<LOGR>(&maps.m[8 + pr], G.tw_col, grp << LOGR);
   const TileLayout<LOGR, ROWS, TW> L;
   constexpr bool BULK = kBulkRows<ROWS, TW> && kStageFwd<ROWS, TW> && LOGR > E1;
   u64* bar = sm + R * TW + R;  // after the tile and the R / 2 table pairs
@@ -342,6 +372,8 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   __syncthreads();
   if constexpr (BULK) mbar_wait(bar, 0);
   pdl_trigger_mid();
+  if constexpr (TWPF && DMG_TMA_TWPF_FWD_GROUP == 2)  // once the tile has arrived
+    if (a.tw_gstride != 0 && tid == 0) prefetch_tw_rows_tma<LOGR>(&maps.m[8 + pr], G.tw_col, grp << LOGR);
   // merged radix-3 twiddles: column input r of radix-3 row g times omega_{3 R}^{g r}, in the
   // first round (a separate shared-memory sweep cost config 4's two launches +1.1 ms)
   const TwPair* pre = (ROWS && a.pre[pr] && grp) ? a.pre[pr] + grp * R : nullptr;
@@ -442,10 +474,14 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   if constexpr (ROWS && !FACT) if (a.tw_gstride != 0) {
     // per-group tables (pass 1 after a merged radix-3 pass) stream from HBM with no reuse
     // across tiles: start them towards L2 before the tile's own loads
-    constexpr int LINES = TW * 16 / 128 > 0 ? TW * 16 / 128 : 1;
-    for (int i = tid; i < R * LINES; i += NTK) {
-      const TwPair* row = &G.tw(T, i / LINES, 0) + (i % LINES) * 8;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+    if constexpr (DMG_TMA_TWPF != 0 && kBulkRows<ROWS, TW> && kStageInv<ROWS> && LOGR > E1) {
+      if (tid == 0) prefetch_tw_rows_tma<LOGR>(&maps.m[8 + pr], G.tw_col, grp << LOGR);
+    } else {
+      constexpr int LINES = TW * 16 / 128 > 0 ? TW * 16 / 128 : 1;
+      for (int i = tid; i < R * LINES; i += NTK) {
+        const TwPair* row = &G.tw(T, i / LINES, 0) + (i % LINES) * 8;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(row));
+      }
     }
   }
 #endif
@@ -1164,6 +1200,16 @@ EncodeTiledFn encode_tiled_fn() {
 
 // The {S, rows} u64 tensor over base with the row-tile box {16, min(R, 256)}.
 void encode_row_map(unsigned char (&out)[128], const u64* base, unsigned long long S, unsigned long long rows,
+                    int logR, int tw);
+
+// The twiddle table of a row pass as a {2 S' u64, rows} tensor with the box {32, min(R, 256)}
+// (16 pairs of one row): Sp = pairs per table row, rows = R times the number of per-group tables.
+void encode_table_map(unsigned char (&out)[128], const TwPair* table, unsigned long long Sp, unsigned long long rows,
+                      int logR) {
+  encode_row_map(out, reinterpret_cast<const u64*>(table), 2 * Sp, rows, logR, 2 * kTileW);
+}
+
+void encode_row_map(unsigned char (&out)[128], const u64* base, unsigned long long S, unsigned long long rows,
                     int logR, int tw) {
   static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
   EncodeTiledFn fn = encode_tiled_fn();
@@ -1198,6 +1244,9 @@ void launch_pass_kernel_maps(const PassArgs& a, unsigned long long ncols, int np
         encode_row_map(maps.m[4 + pr], a.dst[pr], a.S, rows, logR, TW);
         if (a.nops > 1) encode_row_map(maps.m[6 + pr], a.dst_b[pr], a.S, rows, logR, TW);
       }
+      if (DMG_TMA_TWPF && TW == kTileW && a.pass_tw[pr] && !a.tw_lbits)
+        encode_table_map(maps.m[8 + pr], a.pass_tw[pr], 1ull << a.tw_logS,
+                         (a.tw_gstride ? a.G : 1ull) << logR, logR);
     }
   }
   launch_pdl(FN, dim3(unsigned((ncols + TW - 1) / TW * np), a.nops > 1 ? 2 : 1), dim3(NTK), size_t(smem), st, b, maps);

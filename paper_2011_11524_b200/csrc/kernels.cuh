@@ -104,7 +104,7 @@ struct PassArgs {
 // row pass, [operand * 2 + prime], and of its destination arrays, [4 + operand * 2 + prime]; the
 // tiles are fetched (and optionally stored) by TMA (kernels.cu stage_rows_tma / store_rows_tma).
 struct alignas(64) TileMaps {
-  unsigned char m[8][128];
+  unsigned char m[10][128];  // [8 + prime]: the pass's inter-pass twiddle table (L2 prefetch of its rows)
 };
 
 // Radix-3 pass over N = 3 S. The twiddle omega_N^{+-f s} (times the convolution
