@@ -231,6 +231,9 @@ __device__ __forceinline__ void store_rows_tma(const u64* sm, const void* map, u
 #ifndef DMG_TMA_TWPF_FWD_GROUP
 #define DMG_TMA_TWPF_FWD_GROUP 0
 #endif
+#ifndef DMG_TMA_TWPF_INV_SHARED
+#define DMG_TMA_TWPF_INV_SHARED 0
+#endif
 template <int LOGR>
 __device__ __forceinline__ void prefetch_tw_rows_tma(const void* map, unsigned long long col, unsigned long long row0) {
   constexpr int R = 1 << LOGR, BR = R < kBoxRows ? R : kBoxRows;
@@ -470,6 +473,12 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   const TwPair sc = a.final_scale[pr];
   const Geom<LOGR, ROWS, TW> G(a);
   const TileLayout<LOGR, ROWS, TW> L;
+#if DMG_TMA_TWPF_INV_SHARED
+  // tables shared by the pass's groups too, now that the prefetch costs one thread two
+  // instructions (as a per-thread loop it lost on configs 3 and 5)
+  if constexpr (ROWS && !FACT && DMG_TMA_TWPF != 0 && kBulkRows<ROWS, TW> && kStageInv<ROWS> && LOGR > E1)
+    if (a.tw_gstride == 0 && tid == 0) prefetch_tw_rows_tma<LOGR>(&maps.m[8 + pr], G.tw_col, 0);
+#endif
 #if DMG_INV_GROUP_PREFETCH
   if constexpr (ROWS && !FACT) if (a.tw_gstride != 0) {
     // per-group tables (pass 1 after a merged radix-3 pass) stream from HBM with no reuse
