@@ -247,13 +247,26 @@ __device__ __forceinline__ void prefetch_tw_rows_tma(const void* map, unsigned l
 // Thread 0 of the CTA: arm the barrier and issue the tile's TMA copies (rows row0 .. row0 + R
 // of the tensor, columns s0 .. s0 + 16). Everyone else meets it at the next __syncthreads and
 // then waits on the barrier's phase 0.
+// table != nullptr (DMG_BULK_TABLE): the pass's butterfly table (R / 2 pairs, stored linearly
+// for row-major tiles) rides on the same barrier as one more bulk copy, instead of a load and a
+// shared store per thread.
+#ifndef DMG_BULK_TABLE
+#define DMG_BULK_TABLE 1
+#endif
 template <int LOGR, int TW>
 __device__ __forceinline__ void stage_rows_tma(u64* sm, const void* map, unsigned long long s0,
-                                               unsigned long long row0, u64* bar) {
+                                               unsigned long long row0, u64* bar, TwPair* tw_dst = nullptr,
+                                               const TwPair* table = nullptr) {
   constexpr int R = 1 << LOGR, BR = R < kBoxRows ? R : kBoxRows;
+  constexpr unsigned kTableBytes = unsigned((R / 2) * sizeof(TwPair));
   mbar_init(bar, 1);
-  mbar_expect_tx(bar, unsigned(R * TW * sizeof(u64)));
+  mbar_expect_tx(bar, unsigned(R * TW * sizeof(u64)) + (table ? kTableBytes : 0u));
   const unsigned b = unsigned(__cvta_generic_to_shared(bar));
+  if (table)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     unsigned(__cvta_generic_to_shared(tw_dst))),
+                 "l"(table), "r"(kTableBytes), "r"(b)
+                 : "memory");
 #pragma unroll
   for (int h = 0; h < R / BR; ++h) {
     const unsigned sa = unsigned(__cvta_generic_to_shared(sm + h * BR * TW));
@@ -365,12 +378,15 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_min_blocks(LOGR, 
   constexpr bool BULK = kBulkRows<ROWS, TW> && kStageFwd<ROWS, TW> && LOGR > E1;
   u64* bar = sm + R * TW + R;  // after the tile and the R / 2 table pairs
   if constexpr (BULK) {
+    constexpr bool TBL = false;  // forward passes: neutral at R = 512, +2.7% at R = 256
     if (tid == 0)
-      stage_rows_tma<LOGR, TW>(sm, &maps.m[blockIdx.y * 2 + pr], G.s0, grp << LOGR, bar);
+      stage_rows_tma<LOGR, TW>(sm, &maps.m[blockIdx.y * 2 + pr], G.s0, grp << LOGR, bar, tw,
+                               TBL ? a.dft_fwd[pr] : nullptr);
+    if constexpr (!TBL) load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_fwd[pr]);
   } else if constexpr (kStageFwd<ROWS, TW> && LOGR > E1) {
     stage_tile<LOGR, ROWS, TW, NTK>(sm, src, G, L, tid);
   }
-  load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_fwd[pr]);
+  if constexpr (!BULK) load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_fwd[pr]);
   if constexpr (!BULK && kStageFwd<ROWS, TW> && LOGR > E1) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if constexpr (BULK) mbar_wait(bar, 0);
@@ -498,11 +514,15 @@ __global__ void __launch_bounds__(pass_threads(LOGR, TW), pass_inv_min_blocks(LO
   constexpr bool BULK = STAGE && kBulkRows<ROWS, TW>;
   u64* bar = sm + R * TW + R;  // after the tile and the R / 2 table pairs
   if constexpr (BULK) {
-    if (tid == 0) stage_rows_tma<LOGR, TW>(sm, &maps.m[pr], G.s0, grp << LOGR, bar);
+    // R = 512 only: the inverse pass 5.83 -> 5.62 ms on config 4; R = 256 passes lose 3%
+    constexpr bool TBL = DMG_BULK_TABLE != 0 && !kSwzTables<ROWS> && LOGR >= 9;
+    if (tid == 0)
+      stage_rows_tma<LOGR, TW>(sm, &maps.m[pr], G.s0, grp << LOGR, bar, tw, TBL ? a.dft_inv[pr] : nullptr);
+    if constexpr (!TBL) load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_inv[pr]);
   } else if constexpr (STAGE) {
     stage_tile<LOGR, ROWS, TW, NTK>(sm, src, G, L, tid);
   }
-  load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_inv[pr]);
+  if constexpr (!BULK) load_table<LOGR, NTK, kSwzTables<ROWS>>(tw, a.dft_inv[pr]);
   if constexpr (STAGE && !BULK) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if constexpr (BULK) mbar_wait(bar, 0);
