@@ -2,7 +2,7 @@
 # Round-2 evidence on one GPU box: all GPU tests, smoke, bench lines of every config (and the
 # reference arm), launch lists, and ncu --set full captures exported as CSV (the .ncu-rep files
 # stay on the box: they exceed the copy-back cap).
-cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out /tmp/ncu
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out /tmp/ncu; rm -f /tmp/ncu/f2_*.ncu-rep
 part=${1:-a}
 if [ "$part" = a ]; then
   timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider --timeout=600 > gpurun_out/f2_tests.log 2>&1; echo "rc=$?" >> gpurun_out/f2_tests.log
